@@ -1,0 +1,181 @@
+"""Pins for oracle.ftk / oracle.brute / oracle.closed_form (no GPU).
+
+FTK (Steps 1-3) is pinned to the brute-force definition (no Bessel/SVD/FFT), which is pinned to
+the exact Gaussian inner products; plus special cases that reduce to textbook quantities.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import brute, closed_form, fb, ftk, kernel_svd as ks
+import synth
+
+
+def _plan(cfg, eps=None, shifts=None):
+    sh = synth.shift_list(cfg) if shifts is None else shifts
+    return ks.build_plan(cfg.n, cfg.K, synth.delta_max(cfg), sh, cfg.eps if eps is None else eps, cfg.n_k, cfg.n_psi)
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    cfg = synth.config("tiny")
+    plan = _plan(cfg)
+    imgs, pi = synth.draw_items(cfg, "images", range(4), plan.k, "planted")
+    tpls, pt = synth.draw_items(cfg, "templates", range(4), plan.k)
+    return cfg, plan, imgs, tpls, pi, pt
+
+
+def test_tiny_plan_shape(tiny):
+    cfg, plan, *_ = tiny
+    assert plan.H == 27 and plan.H_plus == 15          # SURVEY Sec. 8 table [calc], strict Sigma > eps
+    assert abs(plan.W - 0.75 * math.sqrt(2) / 2) < 1e-15
+
+
+def test_ftk_vs_brute_force_tiny(tiny):
+    """|X^FTK - X^bf| <= 4 eps ||A|| ||B|| per inner product (north star), full landscapes."""
+    cfg, plan, imgs, tpls, *_ = tiny
+    X = ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), plan)
+    na, nb = fb.discrete_norm(imgs, plan.w), fb.discrete_norm(tpls, plan.w)
+    for i in range(4):
+        for j in range(4):
+            Xb = brute.brute_landscape(imgs[i], tpls[j], plan.k, plan.w, plan.shifts)
+            assert np.max(np.abs(X[i, j] - Xb)) <= 4 * cfg.eps * na[i] * nb[j]
+    assert np.max(np.abs(X.imag)) < 1e-12 * np.max(np.abs(X.real))   # real images -> Im X = 0
+
+
+def test_ftk_tends_to_brute_force_as_eps_shrinks(tiny):
+    cfg, _, imgs, tpls, *_ = tiny
+    plan = _plan(cfg, eps=1e-9)
+    X = ftk.ftk_landscapes(fb.fb_coeffs(imgs[:1]), fb.fb_coeffs(tpls[:2]), plan)
+    for j in range(2):
+        Xb = brute.brute_landscape(imgs[0], tpls[j], plan.k, plan.w, plan.shifts)
+        assert np.max(np.abs(X[0, j] - Xb)) < 1e-7 * np.max(np.abs(Xb))
+
+
+def test_brute_force_vs_closed_form(tiny):
+    """Brute force vs (2 pi)^2 <R T A, B> in closed form: quadrature-limited at tiny (n_k = 16)."""
+    cfg, plan, imgs, tpls, pi, pt = tiny
+    na, nb = fb.discrete_norm(imgs, plan.w), fb.discrete_norm(tpls, plan.w)
+    for i, j in [(0, 0), (1, 3), (3, 2)]:
+        Xb = brute.brute_landscape(imgs[i], tpls[j], plan.k, plan.w, plan.shifts)
+        for t, r in [(0, 0), (24, 0), (13, 17), (48, 63)]:
+            cf = closed_form.gaussian_ip(pi, pt, i, j, plan.shifts[t], 2 * math.pi * r / cfg.n_psi)
+            assert abs(Xb[t, r] - cf) < 3e-3 * na[i] * nb[j]
+
+
+@pytest.mark.parametrize("name,tol", [("c2", 1e-4), ("c3", 1e-6)])
+def test_brute_force_vs_closed_form_configs(name, tol):
+    cfg = synth.config(name)
+    plan = _plan(cfg, shifts=synth.shift_list(cfg)[:3])
+    x, px = synth.draw_items(cfg, "images", [0, 1], plan.k, noise=False)
+    y, py = synth.draw_items(cfg, "templates", [0], plan.k, noise=False)
+    for i in range(2):
+        for t, r in [(0, 0), (2, 5)]:
+            v = brute.brute_points(x[i], y[0], plan.k, plan.w, plan.shifts, [t], [r])[0]
+            cf = closed_form.gaussian_ip(px, py, i, 0, plan.shifts[t], 2 * math.pi * r / cfg.n_psi)
+            assert abs(v - cf) < tol * (2 * math.pi) ** 2
+
+
+def test_zero_shift_is_rotational_correlation_and_plain_ip(tiny):
+    """delta = 0: U(0; l != 0) = 0 so X(0, gamma) = 2 pi sum_m w_m sum_q a conj(b) e^{-i q gamma}
+    (P:583-589 with L = 0); at gamma = 0 the plain discrete inner product (no transform at all)."""
+    cfg, _, imgs, tpls, *_ = tiny
+    plan = _plan(cfg, shifts=np.zeros((1, 2)))
+    a, b = fb.fb_coeffs(imgs[:2]), fb.fb_coeffs(tpls[:2])
+    X = ftk.ftk_landscapes(a, b, plan)
+    n = cfg.n_psi
+    q = np.arange(n)
+    for i in range(2):
+        for j in range(2):
+            for r in (0, 7, 40):
+                ref = 2 * math.pi * np.sum(plan.w[:, None] * a[i] * np.conj(b[j]) * np.exp(-2j * math.pi * q * r / n)[None, :])
+                assert abs(X[i, j, 0, r] - ref) < 1.5 * cfg.eps * 40
+            plain = (2 * math.pi / n) * np.sum(plan.w[:, None] * imgs[i].astype(complex) * np.conj(tpls[j].astype(complex)))
+            assert abs(X[i, j, 0, 0] - plain) <= cfg.eps * 40
+
+
+def test_template_rotation_is_cyclic_shift(tiny):
+    """Template rotated by 2 pi j/n_psi (samples rolled by j) -> X'(t, r) = X(t, r - j), exactly."""
+    cfg, plan, imgs, tpls, *_ = tiny
+    a = fb.fb_coeffs(imgs[:1])
+    b = fb.fb_coeffs(tpls[:1])
+    b_rot = fb.fb_coeffs(np.roll(tpls[:1], 5, axis=-1))
+    X = ftk.ftk_landscapes(a, b, plan)[0, 0]
+    Xr = ftk.ftk_landscapes(a, b_rot, plan)[0, 0]
+    assert np.max(np.abs(Xr - np.roll(X, 5, axis=-1))) < 1e-12 * np.max(np.abs(X))
+
+
+def test_image_rotation_by_quarter_turn(tiny):
+    """Image rotated by alpha = pi/2 (roll n/4): X'(delta, gamma) = X(R_{-alpha} delta, gamma + alpha);
+    the square lattice maps to itself, so one plan serves both sides (F^SVD is rotation-covariant)."""
+    cfg, plan, imgs, tpls, *_ = tiny
+    n = cfg.n_psi
+    a = fb.fb_coeffs(imgs[:1])
+    a_rot = fb.fb_coeffs(np.roll(imgs[:1], n // 4, axis=-1))
+    b = fb.fb_coeffs(tpls[1:2])
+    X = ftk.ftk_landscapes(a, b, plan)[0, 0]
+    Xr = ftk.ftk_landscapes(a_rot, b, plan)[0, 0]
+    sh = plan.shifts
+    rot = np.stack([sh[:, 1], -sh[:, 0]], 1)          # R_{-pi/2} delta
+    idx = [int(np.argmin(np.hypot(*(sh - p).T))) for p in rot]
+    for t in range(sh.shape[0]):
+        assert np.max(np.abs(Xr[t] - np.roll(X[idx[t]], -n // 4))) < 1e-12 * np.max(np.abs(X))
+
+
+def test_linearity_and_scale(tiny):
+    cfg, plan, imgs, tpls, *_ = tiny
+    a, b = fb.fb_coeffs(imgs[:2]), fb.fb_coeffs(tpls[:1])
+    X = ftk.ftk_landscapes(a, b, plan)
+    Xc = ftk.ftk_landscapes(2.0 * a[:1] - 0.5 * a[1:2], b, plan)
+    assert np.max(np.abs(Xc[0] - (2.0 * X[0] - 0.5 * X[1]))) < 1e-12 * np.max(np.abs(X))
+    v, j, t, r, _ = ftk.best_per_image(X)
+    v2, j2, t2, r2, _ = ftk.best_per_image(3.0 * X)
+    assert np.array_equal(np.stack([j, t, r]), np.stack([j2, t2, r2]))
+
+
+def test_planted_recovery_noiseless(tiny):
+    """P:1324 consistency check: argmax = (j0, -delta0, -gamma0) (reading R12)."""
+    cfg, plan, imgs, tpls, *_ = tiny
+    X = ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), plan)
+    v, j, t, r, _ = ftk.best_per_image(X)
+    sh = plan.shifts
+    for i in range(4):
+        j0, t0, r0 = synth.planted_truth(cfg, i, sh.shape[0])
+        assert j[i] == j0
+        assert np.allclose(sh[t[i]], -sh[t0])
+        assert r[i] == (-r0) % cfg.n_psi
+
+
+def test_argmax_tie_break():
+    X = np.zeros((1, 2, 3, 4))
+    X[0, 1, 0, 0] = 1.0
+    X[0, 0, 2, 3] = 1.0
+    v, j, t, r, gap = ftk.best_per_image(X)
+    assert (j[0], t[0], r[0]) == (0, 2, 3) and gap[0] == 0.0
+
+
+def test_ftk_best_blocked_equals_full(tiny):
+    cfg, plan, imgs, tpls, *_ = tiny
+    a, b = fb.fb_coeffs(imgs), fb.fb_coeffs(tpls)
+    v, j, t, r, _ = ftk.best_per_image(ftk.ftk_landscapes(a, b, plan))
+    bv, bi = ftk.ftk_best(a, b, plan, chunk_i=3, chunk_j=3)
+    assert np.allclose(bv, v, rtol=1e-13) and np.all(bi[:, 0] == j) and np.all(bi[:, 1] == t) and np.all(bi[:, 2] == r)
+
+
+def test_c2_ftk_vs_brute_sampled():
+    """c2 (W=1, eps=1e-2, SNR 1), sampled inner products."""
+    cfg = synth.config("c2")
+    plan = _plan(cfg)
+    assert plan.H == 36 and plan.H_plus == 20
+    x, _ = synth.draw_items(cfg, "images", [0, 1], plan.k)
+    y, _ = synth.draw_items(cfg, "templates", [0, 1], plan.k)
+    X = ftk.ftk_landscapes(fb.fb_coeffs(x), fb.fb_coeffs(y), plan)
+    na, nb = fb.discrete_norm(x, plan.w), fb.discrete_norm(y, plan.w)
+    rng = np.random.default_rng(3)
+    T = rng.integers(0, plan.shifts.shape[0], 25)
+    R = rng.integers(0, cfg.n_psi, 25)
+    for i in range(2):
+        for j in range(2):
+            v = brute.brute_points(x[i], y[j], plan.k, plan.w, plan.shifts, T, R)
+            assert np.max(np.abs(X[i, j][T, R] - v)) <= 4 * cfg.eps * na[i] * nb[j]
