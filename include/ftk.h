@@ -1,0 +1,164 @@
+/*
+ * ftk.h -- C ABI of the B200-native FTK alignment hot path.
+ *
+ * Method: Rangan, Spivak, Andén, Barnett, "Factorization of the translation kernel for
+ * fast rigid image alignment" (arXiv:1905.12317).  "P:n" = line n of the paper text
+ * with its section / equation label.
+ *
+ * What is computed (Eq. Xtrunc P:492-496 evaluated by Eq. fbk3): for every image A_i
+ * and template B_j, the bandlimited inner products
+ *     X_ij(delta_t, gamma_r) = < R_gamma T_delta A_i , B_j >_{Omega_K}      (Eq. Xdg)
+ * over all N_t user shifts delta_t and all n_psi rotations gamma_r = 2 pi r / n_psi, using the
+ * Fourier-Bessel representation (Eq. aqkcalc) and the eps-truncated operator SVD of the
+ * translation kernel (Eqs. Jsvd/svdtrunc).  Per image the library returns the maximal
+ * value and its (template, shift, rotation) (the consistency check of P:1324); small cases may
+ * also request every per-pair maximum or the full landscape.
+ *
+ * Units and conventions
+ *   - Lengths in pixels, frequencies in rad/px.  K is given in cycles per image width (the
+ *     BASELINE.json configs use K = n/2, i.e. Nyquist): k_max = 2 pi K / n.
+ *   - Input images/templates are polar Fourier samples  Ahat(k_m, psi_p)  with the sign convention
+ *     Ahat(k) = int A(x) exp(-i k.x) dx (Eq. Ahat), k_m from ftk_plan_radial(),
+ *     psi_p = 2 pi p / n_psi.  Layout: complex64 (re, im float pairs), [N][n_k][n_psi], psi fastest.
+ *   - Images are assumed REAL (Hermitian samples: Ahat(k, psi + pi) = conj Ahat(k, psi)); the
+ *     library uses the exact symmetry of DESIGN.md reading R13 to evaluate only ell >= 0 terms.
+ *   - Shift index t = position in the caller's shift list; rotation index r <-> gamma_r.
+ *     X(delta, gamma) rotates/translates the IMAGE: a planted image T_d0 R_g0 B peaks at
+ *     (-d0, -g0).  Values are Re X in the bandlimited convention (no (2 pi)^-2 prefactor).
+ *   - Ties in the argmax resolve to the smallest (template, shift, rotation) (lexicographic).
+ *
+ * Ownership: load calls COPY the caller's buffers; outputs go to caller-allocated buffers; the plan
+ * owns its plan factors, Fourier-Bessel arrays and workspace.  A plan is not thread-safe; distinct
+ * plans are independent.  Nothing throws across the ABI: every call returns an ftk_status_t and a
+ * message is kept in ftk_last_error(plan).
+ *
+ * Multi-GPU: every rank creates a plan with opts.rank/opts.world and calls the same sequence with
+ * the same arguments.  Rank r keeps templates [floor(r N/W), floor((r+1) N/W)); ftk_align reports
+ * GLOBAL template indices; the caller all-gathers the per-image records (NCCL over NVLink through
+ * torch.distributed in the Python binding) and reduces them with ftk_merge_bests().
+ */
+#ifndef FTK_H_
+#define FTK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ftk_plan_s* ftk_plan_t;   /* opaque */
+
+typedef enum {
+  FTK_OK = 0,
+  FTK_EINVAL = 1,      /* bad argument (null pointer, non-positive size, unsupported n_psi, ...) */
+  FTK_ERANGE = 2,      /* a shift lies outside the disc ||delta|| <= delta_max (Omega_D) */
+  FTK_ENUMERIC = 3,    /* plan construction failed a numerical self-check (quadrature, SVD, energy) */
+  FTK_ENOMEM = 4,      /* host or device allocation failed */
+  FTK_ECUDA = 5,       /* CUDA runtime error (message holds cudaGetErrorString) */
+  FTK_ESTATE = 6,      /* wrong call order (e.g. ftk_align before both loads; host-only plan) */
+  FTK_ECAPACITY = 7,   /* an optional output buffer is too small, or an index does not fit */
+  FTK_ENODEV = 8       /* no CUDA device / device ordinal invalid */
+} ftk_status_t;
+
+typedef struct {
+  int n_k;              /* radial quadrature nodes; 0 -> round(K)  (configs: n_k = K) */
+  int n_psi;            /* angles per ring = number of rotations; 0 -> 4 round(K); power of two, 16..1024 */
+  int radial_rule;      /* 0 = Gauss-Legendre x k dk (configs), 1 = Gauss-Jacobi(0,1) (paper P:483-490) */
+  int device;           /* CUDA ordinal; -1 = host-only plan: plan math + queries, no device memory */
+  int rank, world;      /* template shard of this process; world <= 0 is treated as 1 */
+  int engine;           /* 0 = tcgen05 3xTF32 tensor-core path (default), 1 = SIMT fp32 reference kernels */
+  int svd_nodes;        /* Nystrom nodes per axis for the operator SVD; 0 -> 96 */
+  size_t workspace_bytes;  /* pair-block workspace; 0 -> 1 GiB */
+} ftk_plan_opts_t;
+
+/* One per-image (or per-pair) result, 16 bytes. */
+typedef struct {
+  float value;               /* Re X at the maximum */
+  int32_t template_idx;      /* GLOBAL template index (-1 if no template was seen) */
+  int32_t shift_idx;         /* index into the caller's shift list */
+  int32_t rot_idx;           /* r, gamma_r = 2 pi r / n_psi */
+} ftk_best_t;
+
+typedef struct {
+  int n, n_k, n_psi, N_t;
+  int H;                     /* total retained terms, both signs of ell */
+  int H_plus;                /* retained terms with ell >= 0 (the ones the device evaluates) */
+  int H0;                    /* retained terms with ell = 0 */
+  int K3;                    /* Step-3 contraction length 2 H_plus - H0 (reading R13) */
+  int ell_max;               /* largest |ell| with a retained term */
+  double K_cycles, k_max, delta_max, W, eps;
+  double certificate;        /* max |F - F^SVD| over (sampled shifts) x (k_m) x (psi_p) */
+  int64_t n_images, n_templates_total, n_templates_local, template_offset;
+  int engine, device, rank, world;
+} ftk_plan_info_t;
+
+/* Build the plan (host, double precision, untimed per P:1321): radial rule, per-ell operator SVD of
+ * J_ell(delta k) (Nystrom on Gauss-Jacobi(0,1) nodes with a one-sided Jacobi SVD), eps truncation
+ * Sigma > eps, global relabel, G_zeta(k_m) and Y_zeta(delta_t) (Eq. svdtrunc), and their
+ * device copies.  shifts_xy_px: host [N_t][2] doubles.  Errors: FTK_EINVAL, FTK_ERANGE (any
+ * ||delta_t|| > delta_max_px * (1 + 1e-12)), FTK_ENUMERIC, FTK_ENODEV, FTK_ENOMEM, FTK_ECUDA.
+ * On error *out is NULL. */
+ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double* shifts_xy_px,
+                             int N_t, double eps, const ftk_plan_opts_t* opts, ftk_plan_t* out);
+
+void ftk_plan_destroy(ftk_plan_t plan);
+
+ftk_status_t ftk_plan_query(ftk_plan_t plan, ftk_plan_info_t* info);
+
+/* Host copies of plan quantities (caller-allocated host arrays).
+ *   radial: k[n_k], w[n_k]                       (sum_m w_m g(k_m) ~ int_0^K g(k) k dk)
+ *   terms : ell[H], eta[H] (0-based), sigma[H]   (zeta order: Sigma desc, |ell| asc, ell>0 first, eta asc)
+ *   factors: G[H][n_k] = Sigma_zeta V_zeta(k_m) ; Y[N_t][H][2] = (re, im) of Y_zeta(delta_t)   (px units) */
+ftk_status_t ftk_plan_radial(ftk_plan_t plan, double* k, double* w);
+ftk_status_t ftk_plan_terms(ftk_plan_t plan, int32_t* ell, int32_t* eta, double* sigma);
+ftk_status_t ftk_plan_factors(ftk_plan_t plan, double* G, double* Y);
+
+/* Load polar samples and compute their Fourier-Bessel coefficients on the device (ring FFT kernel,
+ * Eq. aqkcalc).  polar_c64: [N][n_k][n_psi] complex64, host (is_device = 0; any host memory,
+ * pinned is faster) or device (is_device = 1).  stream: cudaStream_t or NULL.  Images: all N are
+ * kept.  Templates: N_total is the global count; this rank keeps its shard.  Re-loading replaces the
+ * previous set.  Errors: FTK_ESTATE on a host-only plan, FTK_EINVAL, FTK_ENOMEM, FTK_ECUDA. */
+ftk_status_t ftk_load_images(ftk_plan_t plan, const void* polar_c64, int64_t N, int is_device, void* stream);
+ftk_status_t ftk_load_templates(ftk_plan_t plan, const void* polar_c64, int64_t N_total, int is_device, void* stream);
+
+/* Copy Fourier-Bessel coefficients a(k_m; q) of loaded items [first, first+count) to out_c64
+ * (device, [count][n_k][n_psi] complex64, q fastest, q cyclic).  which: 0 images, 1 local templates. */
+ftk_status_t ftk_fb_coeffs(ftk_plan_t plan, int which, int64_t first, int64_t count, void* out_c64, void* stream);
+
+/* The hot path: Steps 1-3 over all (image, local template) pairs, fused max/argmax.
+ *   best      : [N_im] per-image best over this rank's templates (global indices); host or device
+ *               pointer (detected); required.
+ *   pair_best : nullable, device, [N_im][N_tm_local] per-pair maxima (template_idx global).
+ *   landscape : nullable, device, float [N_im][N_tm_local][N_t][n_psi] = Re X; landscape_capacity is its
+ *               element count (FTK_ECAPACITY if smaller).
+ * The call is asynchronous on `stream` for device outputs; it synchronizes `stream` when `best` is
+ * a host pointer.  Errors: FTK_ESTATE (missing load / host-only plan), FTK_ECAPACITY, FTK_ECUDA. */
+ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best, float* landscape,
+                       int64_t landscape_capacity, void* stream);
+
+/* Full landscapes for selected pairs (sampled parity at large configs).  img_idx / tpl_idx:
+ * device int32 [n_pairs] (template index LOCAL to this rank); out: device float [n_pairs][N_t][n_psi]. */
+ftk_status_t ftk_landscape_pairs(ftk_plan_t plan, const int32_t* img_idx, const int32_t* tpl_idx, int n_pairs,
+                                 float* out, void* stream);
+
+/* Deterministic merge of per-rank results: out[i] = best of gathered[r][i] over r (max value, ties ->
+ * smallest (template, shift, rot)).  Device pointers; gathered: [world][N_im].  The _host variant
+ * does the same on host arrays (no device needed). */
+ftk_status_t ftk_merge_bests(const ftk_best_t* gathered, int world, int64_t N_im, ftk_best_t* out, void* stream);
+ftk_status_t ftk_merge_bests_host(const ftk_best_t* gathered, int world, int64_t N_im, ftk_best_t* out);
+
+/* Kernel timing hooks for bench.py: when enabled, ftk_align records CUDA events on its stream around
+ * each kernel launch; ftk_kernel_times returns, per kernel class (0 load-FFT, 1 step1, 2 step2, 3 step3,
+ * 4 finalize), the summed milliseconds and launch counts of the last ftk_align/ftk_load_* calls. */
+ftk_status_t ftk_set_profiling(ftk_plan_t plan, int enabled);
+ftk_status_t ftk_kernel_times(ftk_plan_t plan, double* ms /*[5]*/, int64_t* launches /*[5]*/);
+
+const char* ftk_last_error(ftk_plan_t plan);   /* never NULL; "" when no error */
+const char* ftk_status_string(ftk_status_t s);
+int ftk_version(void);                          /* 100 * major + minor */
+
+#ifdef __cplusplus
+}
+#endif
+#endif  /* FTK_H_ */

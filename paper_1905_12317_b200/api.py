@@ -1,0 +1,205 @@
+"""Thin Python binding over the C ABI (include/ftk.h).  Argument marshalling only: every step of the
+hot path runs in libftk.so's CUDA kernels; torch is used for device memory, streams and
+torch.distributed (NCCL) plumbing."""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _ffi
+
+ENGINE_TC = 0     # tcgen05 bf16x3 tensor-core path
+ENGINE_SIMT = 1   # CUDA-core fp32 reference kernels
+KERNEL_CLASSES = ("load_fft", "step1", "step2", "step3", "finalize")
+
+
+class FTKError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        super().__init__(f"{_ffi.lib().ftk_status_string(status).decode()}: {msg}")
+
+
+def _check(st: int, plan_ptr=None):
+    if st != 0:
+        msg = _ffi.lib().ftk_last_error(plan_ptr).decode() if plan_ptr else ""
+        raise FTKError(st, msg)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except ImportError:
+            pass
+        return C.c_void_p(0)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+BEST_DTYPE = np.dtype([("value", "<f4"), ("template_idx", "<i4"), ("shift_idx", "<i4"), ("rot_idx", "<i4")])
+
+
+def best_to_numpy(t) -> np.ndarray:
+    """Device/host int32 [N, 4] record tensor -> structured numpy array (value, template, shift, rot)."""
+    a = t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
+    return np.ascontiguousarray(a).view(BEST_DTYPE).reshape(-1)
+
+
+class FTKPlan:
+    """One FTK plan (ftk_plan_create) bound to one CUDA device (or host-only with device=-1)."""
+
+    def __init__(self, n: int, K: float, delta_max: float, shifts, eps: float, *, n_k: int = 0, n_psi: int = 0,
+                 radial_rule: int = 0, device: int = 0, rank: int = 0, world: int = 1, engine: int = ENGINE_TC,
+                 svd_nodes: int = 0, workspace_bytes: int = 0):
+        self._L = _ffi.lib()
+        sh = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(-1, 2))
+        opts = _ffi.PlanOpts(n_k, n_psi, radial_rule, device, rank, world, engine, svd_nodes, workspace_bytes)
+        out = C.c_void_p()
+        st = self._L.ftk_plan_create(n, float(K), float(delta_max), sh.ctypes.data_as(C.c_void_p), sh.shape[0],
+                                     float(eps), C.byref(opts), C.byref(out))
+        if st != 0:
+            raise FTKError(st, "ftk_plan_create failed")
+        self._p = out
+        self.shifts = sh
+        self.device = device
+        self._refresh()
+
+    def _refresh(self):
+        info = _ffi.PlanInfo()
+        _check(self._L.ftk_plan_query(self._p, C.byref(info)), self._p)
+        self.info = {f: getattr(info, f) for f, _ in info._fields_}
+
+    def __del__(self):
+        p = getattr(self, "_p", None)
+        if p:
+            self._L.ftk_plan_destroy(p)
+            self._p = None
+
+    # ---------------- plan queries (host)
+    def radial(self):
+        nk = self.info["n_k"]
+        k, w = np.empty(nk), np.empty(nk)
+        _check(self._L.ftk_plan_radial(self._p, k.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p)), self._p)
+        return k, w
+
+    def terms(self):
+        H = self.info["H"]
+        ell, eta, sig = np.empty(H, np.int32), np.empty(H, np.int32), np.empty(H)
+        _check(self._L.ftk_plan_terms(self._p, ell.ctypes.data_as(C.c_void_p), eta.ctypes.data_as(C.c_void_p),
+                                      sig.ctypes.data_as(C.c_void_p)), self._p)
+        return ell, eta, sig
+
+    def factors(self):
+        H, nk, Nt = self.info["H"], self.info["n_k"], self.info["N_t"]
+        G, Y = np.empty((H, nk)), np.empty((Nt, H, 2))
+        _check(self._L.ftk_plan_factors(self._p, G.ctypes.data_as(C.c_void_p), Y.ctypes.data_as(C.c_void_p)), self._p)
+        return G, Y[..., 0] + 1j * Y[..., 1]
+
+    # ---------------- loads
+    def _load(self, fn, x, stream):
+        import torch
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(np.ascontiguousarray(x.astype(np.complex64, copy=False)))
+        assert x.dtype == torch.complex64 and x.dim() == 3, "polar samples must be complex64 [N][n_k][n_psi]"
+        assert x.shape[1] == self.info["n_k"] and x.shape[2] == self.info["n_psi"], (tuple(x.shape), self.info)
+        x = x.contiguous()
+        _check(fn(self._p, C.c_void_p(x.data_ptr()), x.shape[0], 1 if x.is_cuda else 0, _stream_ptr(stream)), self._p)
+        self._refresh()
+
+    def load_images(self, polar, stream=None):
+        self._load(self._L.ftk_load_images, polar, stream)
+
+    def load_templates(self, polar, stream=None):
+        self._load(self._L.ftk_load_templates, polar, stream)
+
+    def fb_coeffs(self, which: int, first: int, count: int, stream=None):
+        import torch
+        out = torch.empty((count, self.info["n_k"], self.info["n_psi"]), dtype=torch.complex64,
+                          device=f"cuda:{self.device}")
+        _check(self._L.ftk_fb_coeffs(self._p, which, first, count, C.c_void_p(out.data_ptr()), _stream_ptr(stream)),
+               self._p)
+        return out
+
+    # ---------------- hot path
+    def align(self, pair_best: bool = False, landscape: bool = False, stream=None, out=None):
+        """Returns dict with 'best' (int32 [N_im,4] device tensor of ftk_best_t), optionally 'pair_best'
+        [N_im, N_tm_local, 4] and 'landscape' float [N_im, N_tm_local, N_t, n_psi]."""
+        import torch
+        dev = f"cuda:{self.device}"
+        NI, NJ = self.info["n_images"], self.info["n_templates_local"]
+        best = out if out is not None else torch.empty((NI, 4), dtype=torch.int32, device=dev)
+        pb = torch.empty((NI, NJ, 4), dtype=torch.int32, device=dev) if pair_best else None
+        land = torch.empty((NI, NJ, self.info["N_t"], self.info["n_psi"]), dtype=torch.float32, device=dev) \
+            if landscape else None
+        _check(self._L.ftk_align(self._p, C.c_void_p(best.data_ptr()),
+                                 C.c_void_p(pb.data_ptr() if pb is not None else 0),
+                                 C.c_void_p(land.data_ptr() if land is not None else 0),
+                                 land.numel() if land is not None else 0, _stream_ptr(stream)), self._p)
+        res = {"best": best}
+        if pb is not None:
+            res["pair_best"] = pb
+        if land is not None:
+            res["landscape"] = land
+        return res
+
+    def align_host(self, stream=None) -> np.ndarray:
+        """ftk_align with a HOST output buffer (the call copies back and synchronizes)."""
+        out = np.empty(self.info["n_images"], dtype=BEST_DTYPE)
+        _check(self._L.ftk_align(self._p, C.c_void_p(out.ctypes.data), C.c_void_p(0), C.c_void_p(0), 0,
+                                 _stream_ptr(stream)), self._p)
+        return out
+
+    def landscape_pairs(self, img_idx, tpl_idx, stream=None):
+        import torch
+        dev = f"cuda:{self.device}"
+        ii = torch.as_tensor(np.asarray(img_idx, dtype=np.int32), device=dev)
+        jj = torch.as_tensor(np.asarray(tpl_idx, dtype=np.int32), device=dev)
+        out = torch.empty((ii.numel(), self.info["N_t"], self.info["n_psi"]), dtype=torch.float32, device=dev)
+        _check(self._L.ftk_landscape_pairs(self._p, C.c_void_p(ii.data_ptr()), C.c_void_p(jj.data_ptr()), ii.numel(),
+                                           C.c_void_p(out.data_ptr()), _stream_ptr(stream)), self._p)
+        return out
+
+    # ---------------- profiling
+    def set_profiling(self, on: bool):
+        _check(self._L.ftk_set_profiling(self._p, 1 if on else 0), self._p)
+
+    def kernel_times(self):
+        ms = np.zeros(5)
+        cnt = np.zeros(5, dtype=np.int64)
+        _check(self._L.ftk_kernel_times(self._p, ms.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p)), self._p)
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}
+
+
+def merge_bests(gathered, world: int, n_im: int, out=None, stream=None):
+    """Deterministic cross-rank merge (ftk_merge_bests on device tensors, _host on numpy/CPU tensors)."""
+    L = _ffi.lib()
+    if isinstance(gathered, np.ndarray) or not getattr(gathered, "is_cuda", False):
+        g = gathered.numpy() if hasattr(gathered, "numpy") else gathered
+        g = np.ascontiguousarray(g, dtype=np.int32).reshape(world * n_im, 4)
+        o = np.empty((n_im, 4), dtype=np.int32)
+        _check(L.ftk_merge_bests_host(C.c_void_p(g.ctypes.data), world, n_im, C.c_void_p(o.ctypes.data)))
+        return o
+    import torch
+    o = out if out is not None else torch.empty((n_im, 4), dtype=torch.int32, device=gathered.device)
+    _check(L.ftk_merge_bests(C.c_void_p(gathered.data_ptr()), world, n_im, C.c_void_p(o.data_ptr()),
+                             _stream_ptr(stream)))
+    return o
+
+
+def distributed_align(plan: FTKPlan, group=None, stream=None):
+    """Template-sharded alignment: local ftk_align on this rank's shard, all-gather of the per-image
+    records through torch.distributed (NCCL on GPUs, gloo on CPU), deterministic merge."""
+    import torch
+    import torch.distributed as dist
+    local = plan.align(stream=stream)["best"]
+    world = dist.get_world_size(group)
+    if world == 1:
+        return local
+    gathered = torch.empty((world * local.shape[0], 4), dtype=torch.int32, device=local.device)
+    dist.all_gather_into_tensor(gathered, local, group=group)
+    return merge_bests(gathered, world, local.shape[0], stream=stream)

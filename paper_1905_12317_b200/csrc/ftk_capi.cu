@@ -1,0 +1,612 @@
+// C ABI of the FTK hot path: plan lifetime, loads, the pair-block scheduler behind ftk_align,
+// merge and profiling hooks.  See include/ftk.h for the contracts.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ftk_internal.cuh"
+#include "ftk_plan_math.h"
+#include "ftk_tc.cuh"
+
+using namespace ftk;
+
+struct ftk_plan_s {
+  PlanMath pm;
+  int device = -1, rank = 0, world = 1, engine = 0;
+  size_t ws_bytes = (size_t)1 << 30;
+  std::string err;
+  // device constants
+  float* d_g = nullptr;
+  int* d_ell = nullptr;
+  int* d_col = nullptr;
+  float* d_Y3 = nullptr;
+  float2* d_tw = nullptr;
+  int K3p = 0, log2_psi = 0;
+  TcPlan tc;  // tensor-core engine constants (ftk_tc.cu)
+  // data
+  float2* d_A = nullptr;
+  int64_t n_im = 0;
+  float2* d_B = nullptr;
+  int64_t n_tm_total = 0, n_tm_local = 0, tm_off = 0;
+  bool have_images = false, have_templates = false;
+  // workspace
+  void* d_ws = nullptr;
+  size_t ws_size = 0;
+  unsigned long long* d_keys = nullptr;
+  int64_t keys_cap = 0;
+  ftk_best_t* d_best_tmp = nullptr;
+  int64_t best_tmp_cap = 0;
+  void* d_stage = nullptr;
+  size_t stage_bytes = 0;
+  // profiling
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[5];
+  size_t ev_used[5] = {0, 0, 0, 0, 0};
+};
+
+namespace {
+
+const char* kStatusStr[] = {"FTK_OK",     "FTK_EINVAL", "FTK_ERANGE", "FTK_ENUMERIC", "FTK_ENOMEM",
+                            "FTK_ECUDA",  "FTK_ESTATE", "FTK_ECAPACITY", "FTK_ENODEV"};
+
+ftk_status_t fail(ftk_plan_t p, ftk_status_t s, const std::string& msg) {
+  if (p) p->err = msg;
+  return s;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      return fail(plan, e_ == cudaErrorMemoryAllocation ? FTK_ENOMEM : FTK_ECUDA,            \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+    }                                                                                         \
+  } while (0)
+
+DevPlan devplan(ftk_plan_t p) {
+  DevPlan d;
+  d.n_k = p->pm.n_k;
+  d.n_psi = p->pm.n_psi;
+  d.log2_psi = p->log2_psi;
+  d.N_t = p->pm.N_t;
+  d.H_plus = p->pm.H_plus;
+  d.K3 = p->pm.K3;
+  d.K3p = p->K3p;
+  int lm = 0;
+  for (const auto& t : p->pm.terms)
+    if (t.ell >= 0) lm = std::max(lm, t.ell);
+  d.ell_max = lm;
+  d.g = p->d_g;
+  d.ell = p->d_ell;
+  d.col = p->d_col;
+  d.Y3 = p->d_Y3;
+  d.tw = p->d_tw;
+  return d;
+}
+
+void prof_begin(ftk_plan_t p, int c, cudaStream_t s) {
+  if (!p->prof) return;
+  if (p->ev_used[c] == p->ev[c].size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    p->ev[c].push_back({a, b});
+  }
+  cudaEventRecord(p->ev[c][p->ev_used[c]].first, s);
+}
+void prof_end(ftk_plan_t p, int c, cudaStream_t s) {
+  if (!p->prof) return;
+  cudaEventRecord(p->ev[c][p->ev_used[c]].second, s);
+  p->ev_used[c]++;
+}
+void prof_reset(ftk_plan_t p) {
+  for (int c = 0; c < 5; ++c) p->ev_used[c] = 0;
+}
+
+bool is_device_ptr(const void* ptr) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+ftk_status_t upload(ftk_plan_t plan, T** dst, const std::vector<T>& src) {
+  if (*dst) cudaFree(*dst);
+  *dst = nullptr;
+  if (src.empty()) return FTK_OK;
+  CK(cudaMalloc((void**)dst, src.size() * sizeof(T)));
+  CK(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return FTK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ftk_status_string(ftk_status_t s) {
+  int i = (int)s;
+  return (i >= 0 && i <= 8) ? kStatusStr[i] : "FTK_UNKNOWN";
+}
+
+int ftk_version(void) { return 100; }
+
+const char* ftk_last_error(ftk_plan_t plan) { return plan ? plan->err.c_str() : ""; }
+
+ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double* shifts_xy_px, int N_t, double eps,
+                             const ftk_plan_opts_t* opts, ftk_plan_t* out) {
+  if (!out) return FTK_EINVAL;
+  *out = nullptr;
+  if (!shifts_xy_px || N_t <= 0) return FTK_EINVAL;
+  ftk_plan_t plan = new (std::nothrow) ftk_plan_s();
+  if (!plan) return FTK_ENOMEM;
+  ftk_plan_opts_t o;
+  std::memset(&o, 0, sizeof o);
+  if (opts) o = *opts;
+  PlanMath& pm = plan->pm;
+  pm.n = n;
+  pm.K_cycles = K;
+  pm.delta_max = delta_max_px;
+  pm.eps = eps;
+  pm.N_t = N_t;
+  pm.n_k = o.n_k > 0 ? o.n_k : (int)std::lround(K);
+  pm.n_psi = o.n_psi > 0 ? o.n_psi : 4 * (int)std::lround(K);
+  pm.rule = o.radial_rule;
+  pm.svd_nodes = o.svd_nodes > 0 ? o.svd_nodes : 96;
+  pm.shifts.assign(shifts_xy_px, shifts_xy_px + 2 * (size_t)N_t);
+  plan->device = o.device;
+  plan->world = o.world > 0 ? o.world : 1;
+  plan->rank = o.rank;
+  plan->engine = o.engine;
+  plan->ws_bytes = o.workspace_bytes ? o.workspace_bytes : ((size_t)1 << 30);
+  auto bail = [&](ftk_status_t s) {
+    ftk_plan_destroy(plan);
+    return s;
+  };
+  if (plan->rank < 0 || plan->rank >= plan->world || (plan->engine != 0 && plan->engine != 1) ||
+      (pm.rule != 0 && pm.rule != 1))
+    return bail(FTK_EINVAL);
+  const int np = pm.n_psi;
+  if (np < 64 || np > 1024 || (np & (np - 1)) != 0) return bail(FTK_EINVAL);
+  if (pm.n_k > 1024) return bail(FTK_EINVAL);
+  int st = pm.build();
+  if (st != FTK_OK) {
+    fprintf(stderr, "ftk_plan_create: %s\n", pm.error.c_str());
+    return bail((ftk_status_t)st);
+  }
+  plan->log2_psi = 0;
+  while ((1 << plan->log2_psi) < np) plan->log2_psi++;
+  plan->K3p = (pm.K3 + 7) / 8 * 8;
+  if (plan->device < 0) {
+    *out = plan;
+    return FTK_OK;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || plan->device >= ndev) {
+    cudaGetLastError();
+    return bail(FTK_ENODEV);
+  }
+  if (cudaSetDevice(plan->device) != cudaSuccess) return bail(FTK_ECUDA);
+  // ---- device constants: ell >= 0 terms in zeta order
+  std::vector<float> g, Y3((size_t)N_t * plan->K3p, 0.f);
+  std::vector<int> ell, col;
+  std::vector<int> zplus;
+  for (int z = 0; z < pm.H; ++z)
+    if (pm.terms[z].ell >= 0) zplus.push_back(z);
+  int c = 0;
+  for (int z : zplus) {
+    const int l = pm.terms[z].ell;
+    ell.push_back(l);
+    col.push_back(c);
+    for (int m = 0; m < pm.n_k; ++m) g.push_back((float)(2.0 * M_PI * pm.w[m] * pm.G[(size_t)z * pm.n_k + m]));
+    for (int t = 0; t < N_t; ++t) {
+      const std::complex<double> y = pm.Y[(size_t)t * pm.H + z];
+      if (l == 0) {
+        Y3[(size_t)t * plan->K3p + c] = (float)y.real();
+      } else {
+        Y3[(size_t)t * plan->K3p + c] = (float)(2.0 * y.real());
+        Y3[(size_t)t * plan->K3p + c + 1] = (float)(-2.0 * y.imag());
+      }
+    }
+    c += (l == 0) ? 1 : 2;
+  }
+  std::vector<float2> tw(np / 2);
+  for (int j = 0; j < np / 2; ++j) {
+    const double ph = -2.0 * M_PI * j / np;
+    tw[j] = make_float2((float)std::cos(ph), (float)std::sin(ph));
+  }
+  ftk_status_t s;
+  if ((s = upload(plan, &plan->d_g, g)) != FTK_OK) return bail(s);
+  if ((s = upload(plan, &plan->d_ell, ell)) != FTK_OK) return bail(s);
+  if ((s = upload(plan, &plan->d_col, col)) != FTK_OK) return bail(s);
+  if ((s = upload(plan, &plan->d_Y3, Y3)) != FTK_OK) return bail(s);
+  if ((s = upload(plan, &plan->d_tw, tw)) != FTK_OK) return bail(s);
+  if (plan->engine == 0) {
+    std::string msg;
+    int ts = tc_plan_init(plan->tc, pm, g, ell, Y3, plan->K3p, msg);
+    if (ts != FTK_OK) {
+      plan->err = msg;
+      fprintf(stderr, "ftk_plan_create: %s\n", msg.c_str());
+      return bail((ftk_status_t)ts);
+    }
+  }
+  *out = plan;
+  return FTK_OK;
+}
+
+void ftk_plan_destroy(ftk_plan_t plan) {
+  if (!plan) return;
+  if (plan->device >= 0) {
+    cudaSetDevice(plan->device);
+    cudaFree(plan->d_g);
+    cudaFree(plan->d_ell);
+    cudaFree(plan->d_col);
+    cudaFree(plan->d_Y3);
+    cudaFree(plan->d_tw);
+    cudaFree(plan->d_A);
+    cudaFree(plan->d_B);
+    cudaFree(plan->d_ws);
+    cudaFree(plan->d_keys);
+    cudaFree(plan->d_best_tmp);
+    cudaFree(plan->d_stage);
+    tc_plan_free(plan->tc);
+    for (int c = 0; c < 5; ++c)
+      for (auto& e : plan->ev[c]) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
+  }
+  delete plan;
+}
+
+ftk_status_t ftk_plan_query(ftk_plan_t plan, ftk_plan_info_t* info) {
+  if (!plan || !info) return FTK_EINVAL;
+  const PlanMath& pm = plan->pm;
+  std::memset(info, 0, sizeof *info);
+  info->n = pm.n;
+  info->n_k = pm.n_k;
+  info->n_psi = pm.n_psi;
+  info->N_t = pm.N_t;
+  info->H = pm.H;
+  info->H_plus = pm.H_plus;
+  info->H0 = pm.H0;
+  info->K3 = pm.K3;
+  info->ell_max = pm.ell_max;
+  info->K_cycles = pm.K_cycles;
+  info->k_max = pm.k_max;
+  info->delta_max = pm.delta_max;
+  info->W = pm.W;
+  info->eps = pm.eps;
+  info->certificate = pm.certificate;
+  info->n_images = plan->n_im;
+  info->n_templates_total = plan->n_tm_total;
+  info->n_templates_local = plan->n_tm_local;
+  info->template_offset = plan->tm_off;
+  info->engine = plan->engine;
+  info->device = plan->device;
+  info->rank = plan->rank;
+  info->world = plan->world;
+  return FTK_OK;
+}
+
+ftk_status_t ftk_plan_radial(ftk_plan_t plan, double* k, double* w) {
+  if (!plan || !k || !w) return FTK_EINVAL;
+  std::copy(plan->pm.k.begin(), plan->pm.k.end(), k);
+  std::copy(plan->pm.w.begin(), plan->pm.w.end(), w);
+  return FTK_OK;
+}
+
+ftk_status_t ftk_plan_terms(ftk_plan_t plan, int32_t* ell, int32_t* eta, double* sigma) {
+  if (!plan || !ell || !eta || !sigma) return FTK_EINVAL;
+  for (int z = 0; z < plan->pm.H; ++z) {
+    ell[z] = plan->pm.terms[z].ell;
+    eta[z] = plan->pm.terms[z].eta;
+    sigma[z] = plan->pm.terms[z].sigma;
+  }
+  return FTK_OK;
+}
+
+ftk_status_t ftk_plan_factors(ftk_plan_t plan, double* G, double* Y) {
+  if (!plan || !G || !Y) return FTK_EINVAL;
+  std::copy(plan->pm.G.begin(), plan->pm.G.end(), G);
+  for (size_t i = 0; i < plan->pm.Y.size(); ++i) {
+    Y[2 * i] = plan->pm.Y[i].real();
+    Y[2 * i + 1] = plan->pm.Y[i].imag();
+  }
+  return FTK_OK;
+}
+
+static ftk_status_t load_set(ftk_plan_t plan, const void* polar, int64_t first, int64_t count, int is_device,
+                             float2* dst, cudaStream_t s) {
+  const DevPlan P = devplan(plan);
+  const size_t item_bytes = (size_t)P.n_k * P.n_psi * sizeof(float2);
+  const float2* src = reinterpret_cast<const float2*>(polar) + first * (int64_t)P.n_k * P.n_psi;
+  if (is_device) {
+    prof_begin(plan, 0, s);
+    launch_ring_fft(src, dst, count, P, s);
+    prof_end(plan, 0, s);
+    CK(cudaGetLastError());
+    return FTK_OK;
+  }
+  if (!plan->d_stage) {
+    plan->stage_bytes = std::max(item_bytes, (size_t)256 << 20);
+    CK(cudaMalloc(&plan->d_stage, plan->stage_bytes));
+  }
+  const int64_t chunk = std::max<int64_t>(1, plan->stage_bytes / item_bytes);
+  for (int64_t c0 = 0; c0 < count; c0 += chunk) {
+    const int64_t nc = std::min(chunk, count - c0);
+    CK(cudaMemcpyAsync(plan->d_stage, src + c0 * (int64_t)P.n_k * P.n_psi, nc * item_bytes, cudaMemcpyHostToDevice, s));
+    prof_begin(plan, 0, s);
+    launch_ring_fft(reinterpret_cast<float2*>(plan->d_stage), dst + c0 * (int64_t)P.n_k * P.n_psi, nc, P, s);
+    prof_end(plan, 0, s);
+    CK(cudaGetLastError());
+  }
+  return FTK_OK;
+}
+
+ftk_status_t ftk_load_images(ftk_plan_t plan, const void* polar_c64, int64_t N, int is_device, void* stream) {
+  if (!plan) return FTK_EINVAL;
+  if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
+  if (!polar_c64 || N <= 0) return fail(plan, FTK_EINVAL, "ftk_load_images: null pointer or N <= 0");
+  CK(cudaSetDevice(plan->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)N * plan->pm.n_k * plan->pm.n_psi * sizeof(float2);
+  if (N != plan->n_im) {
+    cudaFree(plan->d_A);
+    plan->d_A = nullptr;
+    CK(cudaMalloc(&plan->d_A, bytes));
+  }
+  plan->n_im = N;
+  prof_reset(plan);
+  ftk_status_t st = load_set(plan, polar_c64, 0, N, is_device, plan->d_A, s);
+  if (st != FTK_OK) return st;
+  if (plan->engine == 0) {
+    std::string msg;
+    int ts = tc_prepare_images(plan->tc, plan->d_A, N, devplan(plan), s, msg);
+    if (ts != FTK_OK) return fail(plan, (ftk_status_t)ts, msg);
+  }
+  plan->have_images = true;
+  return FTK_OK;
+}
+
+ftk_status_t ftk_load_templates(ftk_plan_t plan, const void* polar_c64, int64_t N_total, int is_device, void* stream) {
+  if (!plan) return FTK_EINVAL;
+  if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
+  if (!polar_c64 || N_total <= 0) return fail(plan, FTK_EINVAL, "ftk_load_templates: null pointer or N <= 0");
+  CK(cudaSetDevice(plan->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t lo = (int64_t)plan->rank * N_total / plan->world;
+  const int64_t hi = (int64_t)(plan->rank + 1) * N_total / plan->world;
+  const int64_t nl = hi - lo;
+  const double flat_max = (double)N_total * plan->pm.N_t * plan->pm.n_psi;
+  if (flat_max > 4294967295.0)
+    return fail(plan, FTK_ECAPACITY, "N_templates * N_t * n_psi exceeds the 32-bit argmax index");
+  if (nl != plan->n_tm_local) {
+    cudaFree(plan->d_B);
+    plan->d_B = nullptr;
+    if (nl > 0) CK(cudaMalloc(&plan->d_B, (size_t)nl * plan->pm.n_k * plan->pm.n_psi * sizeof(float2)));
+  }
+  plan->n_tm_total = N_total;
+  plan->n_tm_local = nl;
+  plan->tm_off = lo;
+  prof_reset(plan);
+  if (nl > 0) {
+    ftk_status_t st = load_set(plan, polar_c64, lo, nl, is_device, plan->d_B, s);
+    if (st != FTK_OK) return st;
+    if (plan->engine == 0) {
+      std::string msg;
+      int ts = tc_prepare_templates(plan->tc, plan->d_B, nl, devplan(plan), s, msg);
+      if (ts != FTK_OK) return fail(plan, (ftk_status_t)ts, msg);
+    }
+  }
+  plan->have_templates = true;
+  return FTK_OK;
+}
+
+ftk_status_t ftk_fb_coeffs(ftk_plan_t plan, int which, int64_t first, int64_t count, void* out_c64, void* stream) {
+  if (!plan || !out_c64) return FTK_EINVAL;
+  const float2* src = which == 0 ? plan->d_A : plan->d_B;
+  const int64_t n = which == 0 ? plan->n_im : plan->n_tm_local;
+  if (!src || first < 0 || count < 0 || first + count > n) return fail(plan, FTK_EINVAL, "ftk_fb_coeffs: range");
+  CK(cudaSetDevice(plan->device));
+  launch_fb_export(src, first, count, plan->pm.n_k, plan->pm.n_psi, reinterpret_cast<float2*>(out_c64),
+                   (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return FTK_OK;
+}
+
+static ftk_status_t ensure_ws(ftk_plan_t plan, size_t bytes) {
+  if (plan->ws_size >= bytes) return FTK_OK;
+  cudaFree(plan->d_ws);
+  plan->d_ws = nullptr;
+  plan->ws_size = 0;
+  CK(cudaMalloc(&plan->d_ws, bytes));
+  CK(cudaMemset(plan->d_ws, 0, bytes));
+  plan->ws_size = bytes;
+  return FTK_OK;
+}
+
+// Run Steps 1-3 on one pair block with the selected engine.
+static ftk_status_t run_block(ftk_plan_t plan, const PairBlock& pb, unsigned long long* img_keys,
+                              unsigned long long* pair_keys, float* land, cudaStream_t s) {
+  const DevPlan P = devplan(plan);
+  if (plan->engine == 1) {
+    float2* Zhat = reinterpret_cast<float2*>(plan->d_ws);
+    float* Z3 = reinterpret_cast<float*>(Zhat + (size_t)pb.count * P.H_plus * P.n_psi);
+    prof_begin(plan, 1, s);
+    launch_step1_simt(plan->d_A, plan->d_B, Zhat, pb, P, s);
+    prof_end(plan, 1, s);
+    prof_begin(plan, 2, s);
+    launch_step2_simt(Zhat, Z3, pb, P, s);
+    prof_end(plan, 2, s);
+    prof_begin(plan, 3, s);
+    launch_step3_simt(Z3, pb, P, (int)plan->tm_off, img_keys, pair_keys, (int)plan->n_tm_local, land, s);
+    prof_end(plan, 3, s);
+  } else {
+    std::string msg;
+    int ts = tc_run_block(plan->tc, pb, P, plan->d_ws, plan->ws_size, (int)plan->tm_off, img_keys, pair_keys,
+                          (int)plan->n_tm_local, land, s, plan->prof ? &prof_begin_tc : nullptr, plan, msg);
+    if (ts != FTK_OK) return fail(plan, (ftk_status_t)ts, msg);
+  }
+  CK(cudaGetLastError());
+  return FTK_OK;
+}
+
+static size_t bytes_per_pair(ftk_plan_t plan) {
+  const DevPlan P = devplan(plan);
+  if (plan->engine == 1) return (size_t)P.H_plus * P.n_psi * sizeof(float2) + (size_t)P.K3p * P.n_psi * sizeof(float);
+  return tc_bytes_per_pair(plan->tc, P);
+}
+
+ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best, float* landscape,
+                       int64_t landscape_capacity, void* stream) {
+  if (!plan || !best) return FTK_EINVAL;
+  if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
+  if (!plan->have_images || !plan->have_templates)
+    return fail(plan, FTK_ESTATE, "ftk_align called before ftk_load_images and ftk_load_templates");
+  CK(cudaSetDevice(plan->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevPlan P = devplan(plan);
+  const int64_t NI = plan->n_im, NJ = plan->n_tm_local;
+  if (landscape && landscape_capacity < NI * NJ * P.N_t * (int64_t)P.n_psi)
+    return fail(plan, FTK_ECAPACITY, "landscape buffer too small");
+  if (plan->keys_cap < NI * (pair_best ? NJ + 1 : 1)) {
+    cudaFree(plan->d_keys);
+    plan->d_keys = nullptr;
+    plan->keys_cap = NI * (NJ + 1);
+    CK(cudaMalloc(&plan->d_keys, plan->keys_cap * sizeof(unsigned long long)));
+  }
+  unsigned long long* img_keys = plan->d_keys;
+  unsigned long long* pair_keys = pair_best ? plan->d_keys + NI : nullptr;
+  CK(cudaMemsetAsync(plan->d_keys, 0, NI * (pair_best ? NJ + 1 : 1) * sizeof(unsigned long long), s));
+  prof_reset(plan);
+  if (NJ > 0) {
+    const size_t per = bytes_per_pair(plan);
+    int64_t cap = (int64_t)(plan->ws_bytes / per);
+    if (cap < 1) cap = 1;
+    if (cap > (1 << 24)) cap = 1 << 24;
+    int64_t nj = std::min<int64_t>(NJ, cap);
+    if (landscape && nj < NJ) return fail(plan, FTK_ECAPACITY, "landscape output needs workspace for a full template row");
+    int64_t ni = std::max<int64_t>(1, std::min<int64_t>(NI, cap / nj));
+    ftk_status_t st = tc_block_shape(plan->tc, P, plan->engine, NI, NJ, cap, ni, nj);
+    if (st != FTK_OK) return fail(plan, st, "block shape");
+    st = ensure_ws(plan, (size_t)(ni * nj) * per + 4096);
+    if (st != FTK_OK) return st;
+    for (int64_t i0 = 0; i0 < NI; i0 += ni) {
+      for (int64_t j0 = 0; j0 < NJ; j0 += nj) {
+        PairBlock pb;
+        pb.i0 = (int)i0;
+        pb.ni = (int)std::min(ni, NI - i0);
+        pb.j0 = (int)j0;
+        pb.nj = (int)std::min(nj, NJ - j0);
+        pb.li = pb.lj = nullptr;
+        pb.count = pb.ni * pb.nj;
+        float* land = landscape ? landscape + (size_t)i0 * NJ * P.N_t * P.n_psi : nullptr;
+        st = run_block(plan, pb, img_keys, pair_keys, land, s);
+        if (st != FTK_OK) return st;
+      }
+    }
+  }
+  const bool host_out = !is_device_ptr(best);
+  if (plan->best_tmp_cap < NI) {
+    cudaFree(plan->d_best_tmp);
+    plan->d_best_tmp = nullptr;
+    CK(cudaMalloc(&plan->d_best_tmp, NI * sizeof(ftk_best_t)));
+    plan->best_tmp_cap = NI;
+  }
+  prof_begin(plan, 4, s);
+  launch_finalize(img_keys, NI, P.N_t, P.n_psi, host_out ? plan->d_best_tmp : best, s);
+  if (pair_best) launch_finalize(pair_keys, NI * NJ, P.N_t, P.n_psi, pair_best, s);
+  prof_end(plan, 4, s);
+  CK(cudaGetLastError());
+  if (host_out) {
+    CK(cudaMemcpyAsync(best, plan->d_best_tmp, NI * sizeof(ftk_best_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return FTK_OK;
+}
+
+ftk_status_t ftk_landscape_pairs(ftk_plan_t plan, const int32_t* img_idx, const int32_t* tpl_idx, int n_pairs,
+                                 float* out, void* stream) {
+  if (!plan || !img_idx || !tpl_idx || !out || n_pairs <= 0) return FTK_EINVAL;
+  if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
+  if (!plan->have_images || !plan->have_templates) return fail(plan, FTK_ESTATE, "load images and templates first");
+  CK(cudaSetDevice(plan->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevPlan P = devplan(plan);
+  const size_t per = bytes_per_pair(plan);
+  int64_t cap = std::max<int64_t>(1, (int64_t)(plan->ws_bytes / per));
+  const int64_t chunk = std::min<int64_t>(cap, n_pairs);
+  ftk_status_t st = ensure_ws(plan, (size_t)chunk * per + 4096);
+  if (st != FTK_OK) return st;
+  for (int64_t p0 = 0; p0 < n_pairs; p0 += chunk) {
+    PairBlock pb;
+    pb.i0 = pb.j0 = 0;
+    pb.ni = pb.nj = 1;
+    pb.li = img_idx + p0;
+    pb.lj = tpl_idx + p0;
+    pb.count = (int)std::min<int64_t>(chunk, n_pairs - p0);
+    st = run_block(plan, pb, nullptr, nullptr, out + p0 * (int64_t)P.N_t * P.n_psi, s);
+    if (st != FTK_OK) return st;
+  }
+  return FTK_OK;
+}
+
+ftk_status_t ftk_merge_bests(const ftk_best_t* gathered, int world, int64_t N_im, ftk_best_t* out, void* stream) {
+  if (!gathered || !out || world <= 0 || N_im < 0) return FTK_EINVAL;
+  launch_merge(gathered, world, N_im, out, (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? FTK_OK : FTK_ECUDA;
+}
+
+ftk_status_t ftk_merge_bests_host(const ftk_best_t* gathered, int world, int64_t N_im, ftk_best_t* out) {
+  if (!gathered || !out || world <= 0 || N_im < 0) return FTK_EINVAL;
+  for (int64_t i = 0; i < N_im; ++i) {
+    ftk_best_t b = gathered[i];
+    for (int r = 1; r < world; ++r)
+      if (best_better(gathered[(int64_t)r * N_im + i], b)) b = gathered[(int64_t)r * N_im + i];
+    out[i] = b;
+  }
+  return FTK_OK;
+}
+
+ftk_status_t ftk_set_profiling(ftk_plan_t plan, int enabled) {
+  if (!plan) return FTK_EINVAL;
+  plan->prof = enabled != 0;
+  prof_reset(plan);
+  return FTK_OK;
+}
+
+ftk_status_t ftk_kernel_times(ftk_plan_t plan, double* ms, int64_t* launches) {
+  if (!plan || !ms || !launches) return FTK_EINVAL;
+  if (plan->device >= 0) CK(cudaSetDevice(plan->device));
+  for (int c = 0; c < 5; ++c) {
+    double tot = 0;
+    for (size_t k = 0; k < plan->ev_used[c]; ++k) {
+      float v = 0;
+      CK(cudaEventSynchronize(plan->ev[c][k].second));
+      CK(cudaEventElapsedTime(&v, plan->ev[c][k].first, plan->ev[c][k].second));
+      tot += v;
+    }
+    ms[c] = tot;
+    launches[c] = (int64_t)plan->ev_used[c];
+  }
+  return FTK_OK;
+}
+
+}  // extern "C"
+
+// profiling callback used by the tensor-core engine (class c, begin/end)
+void prof_begin_tc(void* plan_v, int cls, int end, cudaStream_t s) {
+  ftk_plan_t p = reinterpret_cast<ftk_plan_t>(plan_v);
+  if (end)
+    prof_end(p, cls, s);
+  else
+    prof_begin(p, cls, s);
+}

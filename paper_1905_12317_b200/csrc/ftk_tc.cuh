@@ -1,0 +1,41 @@
+// Tensor-core (tcgen05, bf16x3 split) engine of the FTK hot path.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "ftk_internal.cuh"
+#include "ftk_plan_math.h"
+
+namespace ftk {
+
+struct TcPlan {
+  bool ready = false;
+  int K3p = 0;          // Step-3 contraction length padded to a multiple of 16
+  int n_ttiles = 0;     // ceil(N_t / 128)
+  uint32_t* d_Yh = nullptr;  // [n_ttiles*128][K3p/2] packed bf16x2, hi part
+  uint32_t* d_Yl = nullptr;  // lo part
+  // Step 1 operands
+  uint32_t* d_Bop = nullptr;   // templates, split, Step-1 operand layout
+  int64_t n_tm = 0;
+  int num_sms = 148;
+};
+
+typedef void (*prof_cb_t)(void* plan, int cls, int end, cudaStream_t s);
+
+int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, const std::vector<int>& ell,
+                 const std::vector<float>& Y3, int K3p_simt, std::string& msg);
+void tc_plan_free(TcPlan& tc);
+int tc_prepare_images(TcPlan& tc, const float2* fb, int64_t n, const DevPlan& P, cudaStream_t s, std::string& msg);
+int tc_prepare_templates(TcPlan& tc, const float2* fb, int64_t n, const DevPlan& P, cudaStream_t s, std::string& msg);
+size_t tc_bytes_per_pair(const TcPlan& tc, const DevPlan& P);
+ftk_status_t tc_block_shape(const TcPlan& tc, const DevPlan& P, int engine, int64_t NI, int64_t NJ, int64_t cap,
+                            int64_t& ni, int64_t& nj);
+int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, void* ws, size_t ws_size, int tm_off,
+                 unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
+                 cudaStream_t s, prof_cb_t prof, void* plan, std::string& msg);
+
+}  // namespace ftk
+
+void prof_begin_tc(void* plan_v, int cls, int end, cudaStream_t s);

@@ -1,0 +1,94 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/ftk.h declares,
+and the host-side plan (ftk_plan_create with device = -1, untimed plan math) agrees with the oracle."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import kernel_svd as ks, quadrature
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ftk():
+    import __graft_entry__ as g
+    g.build()
+    import paper_1905_12317_b200 as p
+    return p
+
+
+def test_exports_every_declared_symbol(ftk):
+    hdr = open(os.path.join(ROOT, "include", "ftk.h")).read()
+    declared = set(re.findall(r"^\s*(?:ftk_status_t|void|const char\*|int)\s+(ftk_\w+)\s*\(", hdr, re.M))
+    assert len(declared) >= 18
+    L = ftk.lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    assert set(declared) == set(ftk._ffi.SYMBOLS), set(declared) ^ set(ftk._ffi.SYMBOLS)
+    assert L.ftk_version() >= 100
+
+
+def _host_plan(ftk, name, **kw):
+    cfg = synth.config(name)
+    return cfg, ftk.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), synth.shift_list(cfg), cfg.eps, n_k=cfg.n_k,
+                            n_psi=cfg.n_psi, device=-1, **kw)
+
+
+@pytest.mark.parametrize("name,H,Hp", [("tiny", 27, 15), ("c2", 36, 20), ("c3", 63, 34), ("c5", 94, 50)])
+def test_host_plan_matches_oracle(ftk, name, H, Hp):
+    cfg, p = _host_plan(ftk, name)
+    assert p.info["H"] == H and p.info["H_plus"] == Hp
+    k, w = p.radial()
+    ko, wo = quadrature.radial_rule(cfg.n_k, cfg.k_max)
+    assert np.max(np.abs(k - ko)) < 1e-13 and np.max(np.abs(w - wo)) < 1e-12 * np.max(wo)
+    ell, eta, sig = p.terms()
+    op = ks.build_plan(cfg.n, cfg.K, synth.delta_max(cfg), synth.shift_list(cfg), cfg.eps, cfg.n_k, cfg.n_psi,
+                       n_nodes=96 if name != "tiny" else 64)
+    assert list(ell) == [t.ell for t in op.terms] and list(eta) == [t.eta for t in op.terms]
+    assert np.max(np.abs(sig - np.array([t.sigma for t in op.terms]))) < 1e-10
+    G, Y = p.factors()
+    # products Y_zeta(t) G_zeta(k_m) are sign-invariant; compare the assembled per-term rank-1 factors
+    for z in range(H):
+        P1 = np.outer(Y[:, z], G[z])
+        P2 = np.outer(op.Y[:, z], op.G[z])
+        assert np.max(np.abs(P1 - P2)) < 1e-8 * max(1.0, np.max(np.abs(P2)))
+    assert p.info["certificate"] < 13 * cfg.eps
+
+
+def test_host_plan_errors(ftk):
+    cfg = synth.config("tiny")
+    sh = synth.shift_list(cfg)
+    with pytest.raises(ftk.FTKError) as e:
+        ftk.FTKPlan(cfg.n, cfg.K, 0.5, sh, cfg.eps, n_k=16, n_psi=64, device=-1)    # shifts outside Omega_D
+    assert e.value.status == 2
+    with pytest.raises(ftk.FTKError) as e:
+        ftk.FTKPlan(cfg.n, cfg.K, 1.1, sh, cfg.eps, n_k=16, n_psi=48, device=-1)    # n_psi not a power of two
+    assert e.value.status == 1
+    cfg2, p = _host_plan(ftk, "tiny")
+    with pytest.raises(ftk.FTKError) as e:
+        p.align_host()                     # host-only plan: FTK_ESTATE, no device touched
+    assert e.value.status == 6
+
+
+def test_gauss_jacobi_rule_option(ftk):
+    cfg, p = _host_plan(ftk, "c2", radial_rule=1)
+    k, w = p.radial()
+    ko, wo = quadrature.gauss_jacobi_01(cfg.n_k, cfg.k_max)
+    assert np.max(np.abs(k - ko)) < 1e-12 and np.max(np.abs(w - wo)) < 1e-12 * np.max(wo)
+
+
+def test_merge_host_tie_break(ftk):
+    # records: value, template, shift, rot (value stored as float32 bits)
+    def rec(v, j, t, r):
+        return [np.float32(v).view(np.int32), j, t, r]
+    g = np.array([rec(1.0, 5, 0, 0), rec(2.0, 9, 1, 1), rec(-np.inf, -1, -1, -1),
+                  rec(1.0, 3, 7, 7), rec(2.0, 9, 0, 5), rec(0.5, 1, 1, 1)], dtype=np.int32)
+    out = ftk.merge_bests(g, 2, 3)
+    vals = out[:, 0].view(np.float32)
+    assert vals[0] == 1.0 and out[0, 1] == 3          # equal values -> smaller template
+    assert vals[1] == 2.0 and tuple(out[1, 1:]) == (9, 0, 5)   # equal template -> smaller shift
+    assert vals[2] == 0.5 and out[2, 1] == 1          # missing record (-1) loses
