@@ -331,7 +331,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ci, cj = {"tiny": (4, 4), "c2": (8, 16), "c3": (4, 16), "c4": (2, 8), "c5": (8, 16)}[cfg.name]
+        ci, cj = {"tiny": (4, 4), "c2": (32, 64), "c3": (16, 64), "c4": (4, 16), "c5": (8, 32)}[cfg.name]
         src_i = (imgs_h if e2e is not None else imgs)[:ci].cpu().numpy()
         src_j = (tpls_h if e2e is not None else tpls)[:cj].cpu().numpy()
         cpu = cpu_baseline(cfg, src_i, src_j, k)

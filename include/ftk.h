@@ -67,7 +67,7 @@ typedef struct {
   int radial_rule;      /* 0 = Gauss-Legendre x k dk (configs), 1 = Gauss-Jacobi(0,1) (paper P:483-490) */
   int device;           /* CUDA ordinal; -1 = host-only plan: plan math + queries, no device memory */
   int rank, world;      /* template shard of this process; world <= 0 is treated as 1 */
-  int engine;           /* 0 = tcgen05 3xTF32 tensor-core path (default), 1 = SIMT fp32 reference kernels */
+  int engine;           /* 0 = tcgen05 bf16x3 tensor-core path (default), 1 = SIMT fp32 reference kernels */
   int svd_nodes;        /* Nystrom nodes per axis for the operator SVD; 0 -> 96 */
   size_t workspace_bytes;  /* pair-block workspace; 0 -> 1 GiB */
 } ftk_plan_opts_t;
@@ -153,6 +153,11 @@ ftk_status_t ftk_merge_bests_host(const ftk_best_t* gathered, int world, int64_t
  * 4 finalize), the summed milliseconds and launch counts of the last ftk_align/ftk_load_* calls. */
 ftk_status_t ftk_set_profiling(ftk_plan_t plan, int enabled);
 ftk_status_t ftk_kernel_times(ftk_plan_t plan, double* ms /*[5]*/, int64_t* launches /*[5]*/);
+
+/* Hardware self-test of the tensor-core primitives (one 128x64x32 bf16 tcgen05.mma with A from TMEM and
+ * one with A from shared memory, canonical K-major layouts) against a host reference: writes the max
+ * absolute errors (expected ~1e-6, fp32 accumulation of exactly representable bf16 products). */
+ftk_status_t ftk_tc_selftest(int device, double* err_ts, double* err_ss);
 
 const char* ftk_last_error(ftk_plan_t plan);   /* never NULL; "" when no error */
 const char* ftk_status_string(ftk_status_t s);

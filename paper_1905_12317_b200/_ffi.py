@@ -44,6 +44,7 @@ SYMBOLS = {
     "ftk_merge_bests_host": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
     "ftk_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "ftk_kernel_times": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ftk_tc_selftest": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p]),
     "ftk_last_error": (C.c_char_p, [C.c_void_p]),
     "ftk_status_string": (C.c_char_p, [C.c_int]),
     "ftk_version": (C.c_int, []),

@@ -183,7 +183,7 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
   }
   plan->log2_psi = 0;
   while ((1 << plan->log2_psi) < np) plan->log2_psi++;
-  plan->K3p = (pm.K3 + 7) / 8 * 8;
+  plan->K3p = plan->engine == 0 ? (pm.K3 + 15) / 16 * 16 : (pm.K3 + 7) / 8 * 8;
   if (plan->device < 0) {
     *out = plan;
     return FTK_OK;
@@ -364,7 +364,6 @@ ftk_status_t ftk_load_images(ftk_plan_t plan, const void* polar_c64, int64_t N, 
     CK(cudaMalloc(&plan->d_A, bytes));
   }
   plan->n_im = N;
-  prof_reset(plan);
   ftk_status_t st = load_set(plan, polar_c64, 0, N, is_device, plan->d_A, s);
   if (st != FTK_OK) return st;
   if (plan->engine == 0) {
@@ -396,7 +395,6 @@ ftk_status_t ftk_load_templates(ftk_plan_t plan, const void* polar_c64, int64_t 
   plan->n_tm_total = N_total;
   plan->n_tm_local = nl;
   plan->tm_off = lo;
-  prof_reset(plan);
   if (nl > 0) {
     ftk_status_t st = load_set(plan, polar_c64, lo, nl, is_device, plan->d_B, s);
     if (st != FTK_OK) return st;
@@ -451,7 +449,7 @@ static ftk_status_t run_block(ftk_plan_t plan, const PairBlock& pb, unsigned lon
     prof_end(plan, 3, s);
   } else {
     std::string msg;
-    int ts = tc_run_block(plan->tc, pb, P, plan->d_ws, plan->ws_size, (int)plan->tm_off, img_keys, pair_keys,
+    int ts = tc_run_block(plan->tc, pb, P, plan->d_A, plan->d_B, plan->d_ws, plan->ws_size, (int)plan->tm_off, img_keys, pair_keys,
                           (int)plan->n_tm_local, land, s, plan->prof ? &prof_begin_tc : nullptr, plan, msg);
     if (ts != FTK_OK) return fail(plan, (ftk_status_t)ts, msg);
   }
@@ -486,7 +484,6 @@ ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best,
   unsigned long long* img_keys = plan->d_keys;
   unsigned long long* pair_keys = pair_best ? plan->d_keys + NI : nullptr;
   CK(cudaMemsetAsync(plan->d_keys, 0, NI * (pair_best ? NJ + 1 : 1) * sizeof(unsigned long long), s));
-  prof_reset(plan);
   if (NJ > 0) {
     const size_t per = bytes_per_pair(plan);
     int64_t cap = (int64_t)(plan->ws_bytes / per);
@@ -574,6 +571,15 @@ ftk_status_t ftk_merge_bests_host(const ftk_best_t* gathered, int world, int64_t
     out[i] = b;
   }
   return FTK_OK;
+}
+
+ftk_status_t ftk_tc_selftest(int device, double* err_ts, double* err_ss) {
+  if (!err_ts || !err_ss) return FTK_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return FTK_ENODEV;
+  std::string msg;
+  int st = tc_selftest(err_ts, err_ss, msg);
+  if (st != FTK_OK) fprintf(stderr, "ftk_tc_selftest: %s\n", msg.c_str());
+  return (ftk_status_t)st;
 }
 
 ftk_status_t ftk_set_profiling(ftk_plan_t plan, int enabled) {

@@ -1,33 +1,507 @@
-// Tensor-core engine (tcgen05) -- under construction: every entry fails loudly until implemented.
+// Tensor-core (tcgen05) engine of the FTK hot path, bf16x3 split arithmetic.
+//
+// Step 3 (PAPER.md Eq. fbk3; real form of DESIGN.md reading R13):
+//   X_p(t, r) = sum_k Y3[t][k] Z3_p[k][r],  k < K3 = 2 H_plus - H0,  then max/argmax over (t, r).
+// Every operand x is split x = hi + lo in bf16 and the product is hi*hi + hi*lo + lo*hi with fp32
+// accumulation in TMEM (measured <= 6e-6 ||A|| ||B|| vs the 1e-4 budget).
+//
+// Kernel k_step3_tc (one CTA per SM, persistent over a contiguous range of pairs):
+//   * Z producers (warps 0-3): per pair, read Z3 (fp32, [K3p][n_psi]) from global, split to bf16
+//     hi/lo and write the whole pair into SMEM in the K-major SWIZZLE_NONE canonical layout, chunk by
+//     chunk of 128 r (z_full[rc] / z_empty[rc] mbarriers) -> the B operand (N = r).
+//   * Y loaders (warps 8-11): per 128-row t-tile, Y3 hi/lo rows -> TMEM via tcgen05.st -> the A
+//     operand (M = t), double-buffered (y_full / y_empty).
+//   * MMA issuer (warp 12, one lane): per (t-tile, r-chunk) 3 x K3p/16 tcgen05.mma (M128 N<=128 K16,
+//     A from TMEM, B from SMEM) into one of two TMEM accumulators (acc_full / acc_empty).
+//   * Epilogue (warps 4-7): tcgen05.ld the accumulator, running max/argmax per row, per-pair
+//     reduction, one packed-key atomicMax per pair (image key and optional pair key).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "ftk_sm100.cuh"
 #include "ftk_tc.cuh"
 
 namespace ftk {
+using namespace sm100;
 
-int tc_plan_init(TcPlan& tc, const PlanMath&, const std::vector<float>&, const std::vector<int>&,
-                 const std::vector<float>&, int, std::string& msg) {
+constexpr int S3_THREADS = 13 * 32;
+constexpr int S3_MAX_RC = 8;  // n_psi / 128 <= 8
+
+struct S3Params {
+  const float* Z3;        // [pair][K3p][n]
+  const uint32_t* Yh;     // [T*128][K3p/2]
+  const uint32_t* Yl;
+  PairBlock pb;
+  int n, K3p, N_t, T, NC, RC;
+  int tm_off, n_tm_local;
+  unsigned long long* img_keys;
+  unsigned long long* pair_keys;
+  float* land;
+};
+
+struct S3Smem {
+  uint64_t z_full[S3_MAX_RC], z_empty[S3_MAX_RC];
+  uint64_t y_full[2], y_empty[2];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+  float red_v[4];
+  uint32_t red_f[4];
+};
+
+__device__ __forceinline__ bool better(float v, uint32_t f, float bv, uint32_t bf) {
+  return v > bv || (v == bv && f < bf);
+}
+
+__global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
+  extern __shared__ __align__(1024) uint8_t s3_raw[];
+  S3Smem& S = *reinterpret_cast<S3Smem*>(s3_raw);
+  uint8_t* zs = s3_raw + 1024;  // Z image: [2 parts][n/8][K3p/8][128 B]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = P.n, K3p = P.K3p, NC = P.NC, RC = P.RC, T = P.T;
+  const uint32_t SBO = (uint32_t)K3p * 16;                // bytes between 8-row groups
+  const uint32_t part_bytes = (uint32_t)n * K3p * 2;      // one bf16 part of the whole pair
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < RC; ++i) {
+      mbar_init(&S.z_full[i], 128);
+      mbar_init(&S.z_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S.y_full[i], 128);
+      mbar_init(&S.y_empty[i], 1);
+      mbar_init(&S.acc_full[i], 1);
+      mbar_init(&S.acc_empty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 12) tmem_alloc<512>(&S.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+  // pair range of this CTA
+  const int count = P.pb.count;
+  const int per = (count + gridDim.x - 1) / gridDim.x;
+  const int p_begin = blockIdx.x * per;
+  const int p_end = min(count, p_begin + per);
+
+  if (warp < 4) {
+    // ---------------- Z producers
+    const int tid = threadIdx.x;  // 0..127
+    int it = 0;
+    for (int p = p_begin; p < p_end; ++p, ++it) {
+      const float* zsrc = P.Z3 + (size_t)p * K3p * n;
+      for (int rc = 0; rc < RC; ++rc) {
+        mbar_wait(&S.z_empty[rc], (it & 1) ^ 1);
+        for (int rr = tid; rr < NC; rr += 128) {
+          const int r = rc * NC + rr;
+          uint8_t* row_hi = zs + (size_t)(r >> 3) * SBO + (r & 7) * 16;
+          for (int kc = 0; kc < K3p / 8; ++kc) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = __ldg(zsrc + (size_t)(kc * 8 + e) * n + r);
+            uint4 h, l;
+            split2_bf16(v[0], v[1], h.x, l.x);
+            split2_bf16(v[2], v[3], h.y, l.y);
+            split2_bf16(v[4], v[5], h.z, l.z);
+            split2_bf16(v[6], v[7], h.w, l.w);
+            *reinterpret_cast<uint4*>(row_hi + kc * 128) = h;
+            *reinterpret_cast<uint4*>(row_hi + part_bytes + kc * 128) = l;
+          }
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&S.z_full[rc]);
+      }
+    }
+  } else if (warp < 8) {
+    // ---------------- epilogue
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int it = 0;
+    uint32_t g_acc = 0;
+    for (int p = p_begin; p < p_end; ++p, ++it) {
+      float bv = -INFINITY;
+      uint32_t bf = 0xffffffffu;
+      for (int tt = 0; tt < T; ++tt) {
+        const int t = tt * 128 + row;
+        for (int rc = 0; rc < RC; ++rc, ++g_acc) {
+          const int ab = g_acc & 1;
+          mbar_wait(&S.acc_full[ab], (g_acc >> 1) & 1);
+          tc_fence_after();
+          const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * 128);
+          for (int c0 = 0; c0 < NC; c0 += 16) {
+            uint32_t r16[16];
+            tmem_ld16(base + c0, r16);
+            tmem_wait_ld();
+            if (t < P.N_t) {
+              const uint32_t f0 = (uint32_t)t * (uint32_t)n + (uint32_t)(rc * NC + c0);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const float v = __uint_as_float(r16[e]);
+                if (v > bv) {
+                  bv = v;
+                  bf = f0 + e;
+                }
+              }
+              if (P.land) {
+                float4* dst = reinterpret_cast<float4*>(P.land + ((size_t)p * P.N_t + t) * n + rc * NC + c0);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  dst[e] = make_float4(__uint_as_float(r16[4 * e]), __uint_as_float(r16[4 * e + 1]),
+                                       __uint_as_float(r16[4 * e + 2]), __uint_as_float(r16[4 * e + 3]));
+              }
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(&S.acc_empty[ab]);
+        }
+      }
+      // per-pair reduction over the 128 epilogue threads (lexicographic tie-break on the flat index)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        const uint32_t f2 = __shfl_xor_sync(0xffffffffu, bf, o);
+        if (better(v2, f2, bv, bf)) {
+          bv = v2;
+          bf = f2;
+        }
+      }
+      if (lane == 0) {
+        S.red_v[q] = bv;
+        S.red_f[q] = bf;
+      }
+      named_bar(1, 128);
+      if (warp == 4 && lane == 0) {
+        float v = S.red_v[0];
+        uint32_t f = S.red_f[0];
+        for (int k = 1; k < 4; ++k)
+          if (better(S.red_v[k], S.red_f[k], v, f)) {
+            v = S.red_v[k];
+            f = S.red_f[k];
+          }
+        if (f != 0xffffffffu) {
+          int i, j;
+          pair_of(P.pb, p, i, j);
+          const uint32_t tt2 = f / (uint32_t)n, r = f - tt2 * (uint32_t)n;
+          const uint32_t gflat = ((uint32_t)(P.tm_off + j) * (uint32_t)P.N_t + tt2) * (uint32_t)n + r;
+          const unsigned long long key = pack_key(v, gflat);
+          if (P.img_keys) atomicMax(&P.img_keys[i], key);
+          if (P.pair_keys) atomicMax(&P.pair_keys[(size_t)i * P.n_tm_local + j], key);
+        }
+      }
+      named_bar(1, 128);
+    }
+  } else if (warp < 12) {
+    // ---------------- Y loaders: Y tile (128 t-rows x K3p) hi/lo -> TMEM columns 256 + ybuf*K3p
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int halfk = K3p / 2;
+    uint32_t g_t = 0;
+    for (int p = p_begin; p < p_end; ++p) {
+      for (int tt = 0; tt < T; ++tt, ++g_t) {
+        const int yb = g_t & 1;
+        mbar_wait(&S.y_empty[yb], ((g_t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t col0 = 256 + (uint32_t)(yb * K3p);
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + col0;
+        const uint4* yh = reinterpret_cast<const uint4*>(P.Yh + (size_t)(tt * 128 + row) * halfk);
+        const uint4* yl = reinterpret_cast<const uint4*>(P.Yl + (size_t)(tt * 128 + row) * halfk);
+        for (int c = 0; c < halfk; c += 8) {
+          uint4 a = __ldg(yh + c / 4), b = __ldg(yh + c / 4 + 1);
+          uint32_t r8[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+          tmem_st8(base + c, r8);
+          uint4 a2 = __ldg(yl + c / 4), b2 = __ldg(yl + c / 4 + 1);
+          uint32_t l8[8] = {a2.x, a2.y, a2.z, a2.w, b2.x, b2.y, b2.z, b2.w};
+          tmem_st8(base + halfk + c, l8);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&S.y_full[yb]);
+      }
+    }
+  } else {
+    // ---------------- MMA issuer (warp 12, lane 0)
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16_f32(128, NC);
+      const uint32_t zbase = smem_u32(zs);
+      const int ksteps = K3p / 16;
+      const int halfk = K3p / 2;
+      int it = 0;
+      uint32_t g_t = 0, g_acc = 0;
+      for (int p = p_begin; p < p_end; ++p, ++it) {
+        for (int tt = 0; tt < T; ++tt, ++g_t) {
+          const int yb = g_t & 1;
+          mbar_wait(&S.y_full[yb], (g_t >> 1) & 1);
+          tc_fence_after();
+          const uint32_t a_hi0 = tmem + 256 + (uint32_t)(yb * K3p);
+          for (int rc = 0; rc < RC; ++rc, ++g_acc) {
+            const int ab = g_acc & 1;
+            if (tt == 0) {
+              mbar_wait(&S.z_full[rc], it & 1);
+            }
+            mbar_wait(&S.acc_empty[ab], ((g_acc >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(ab * 128);
+            const uint32_t bchunk = zbase + (uint32_t)(rc * (NC / 8)) * SBO;
+            for (int ks = 0; ks < ksteps; ++ks) {
+              const uint32_t a_hi = a_hi0 + ks * 8, a_lo = a_hi + halfk;
+              const uint64_t b_hi = smem_desc_kmajor_noswz(bchunk + ks * 256, 128, SBO);
+              const uint64_t b_lo = smem_desc_kmajor_noswz(bchunk + part_bytes + ks * 256, 128, SBO);
+              mma_bf16_ts(d, a_hi, b_hi, idesc, ks > 0 ? 1u : 0u);
+              mma_bf16_ts(d, a_hi, b_lo, idesc, 1u);
+              mma_bf16_ts(d, a_lo, b_hi, idesc, 1u);
+            }
+            tc_commit(&S.acc_full[ab]);
+            if (tt == T - 1) tc_commit(&S.z_empty[rc]);
+          }
+          tc_commit(&S.y_empty[yb]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------- single-MMA self-test
+// D = A * B^T with A [128 x 32] (TS: from TMEM; SS: from SMEM), B [N=64 x 32] from SMEM, bf16 inputs.
+__global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const float* B, float* D_ts, float* D_ss) {
+  __shared__ __align__(1024) uint8_t sa[128 * 32 * 2];
+  __shared__ __align__(1024) uint8_t sb[64 * 32 * 2];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = 32;
+  // canonical K-major no-swizzle: core (row/8, k/8) at (row/8)*SBO + (k/8)*128, SBO = (K/8)*128
+  const uint32_t SBO = (K / 8) * 128;
+  for (int idx = tid; idx < 128 * K; idx += 128) {
+    const int m = idx / K, k = idx % K;
+    __nv_bfloat16 v = __float2bfloat16_rn(A[idx]);
+    *reinterpret_cast<__nv_bfloat16*>(sa + (m / 8) * SBO + (k / 8) * 128 + (m % 8) * 16 + (k % 8) * 2) = v;
+  }
+  for (int idx = tid; idx < 64 * K; idx += 128) {
+    const int nn = idx / K, k = idx % K;
+    __nv_bfloat16 v = __float2bfloat16_rn(B[idx]);
+    *reinterpret_cast<__nv_bfloat16*>(sb + (nn / 8) * SBO + (k / 8) * 128 + (nn % 8) * 16 + (k % 8) * 2) = v;
+  }
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<256>(&tbase);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tbase;
+  // A -> TMEM columns [0, 16): packed bf16 pairs (k even in the low half)
+  {
+    const uint32_t base = tm + ((uint32_t)(warp * 32) << 16);
+    uint32_t r16[16];
+    for (int j = 0; j < 16; ++j) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(A[tid * K + 2 * j], A[tid * K + 2 * j + 1]);
+      r16[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    tmem_st16(base, r16);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    const uint32_t idesc = idesc_bf16_f32(128, 64);
+    for (int ks = 0; ks < 2; ++ks) {
+      const uint64_t bd = smem_desc_kmajor_noswz(smem_u32(sb) + ks * 256, 128, SBO);
+      const uint64_t ad = smem_desc_kmajor_noswz(smem_u32(sa) + ks * 256, 128, SBO);
+      mma_bf16_ts(tm + 64, tm + ks * 8, bd, idesc, ks > 0);
+      mma_bf16_ss(tm + 128, ad, bd, idesc, ks > 0);
+    }
+    tc_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  const uint32_t base = tm + ((uint32_t)(warp * 32) << 16);
+  for (int c0 = 0; c0 < 64; c0 += 16) {
+    uint32_t r16[16];
+    tmem_ld16(base + 64 + c0, r16);
+    tmem_wait_ld();
+    for (int e = 0; e < 16; ++e) D_ts[tid * 64 + c0 + e] = __uint_as_float(r16[e]);
+    tmem_ld16(base + 128 + c0, r16);
+    tmem_wait_ld();
+    for (int e = 0; e < 16; ++e) D_ss[tid * 64 + c0 + e] = __uint_as_float(r16[e]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tm);
+  }
+}
+
+static float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+int tc_selftest(double* err_ts, double* err_ss, std::string& msg) {
+  const int M = 128, N = 64, K = 32;
+  std::vector<float> A(M * K), B(N * K), Dts(M * N), Dss(M * N);
+  uint32_t s = 12345;
+  auto rnd = [&]() {
+    s = s * 1664525u + 1013904223u;
+    return ((s >> 8) & 0xffff) / 32768.0f - 1.0f;
+  };
+  for (auto& x : A) x = rnd();
+  for (auto& x : B) x = rnd();
+  float *dA, *dB, *dT, *dS;
+  if (cudaMalloc(&dA, A.size() * 4) || cudaMalloc(&dB, B.size() * 4) || cudaMalloc(&dT, Dts.size() * 4) ||
+      cudaMalloc(&dS, Dss.size() * 4)) {
+    msg = "selftest alloc";
+    return FTK_ENOMEM;
+  }
+  cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
+  k_tc_selftest<<<1, 128>>>(dA, dB, dT, dS);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    msg = std::string("selftest kernel: ") + cudaGetErrorString(e);
+    return FTK_ECUDA;
+  }
+  cudaMemcpy(Dts.data(), dT, Dts.size() * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(Dss.data(), dS, Dss.size() * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dT);
+  cudaFree(dS);
+  double mt = 0, ms = 0;
+  for (int m = 0; m < M; ++m)
+    for (int nn = 0; nn < N; ++nn) {
+      double ref = 0;
+      for (int k = 0; k < K; ++k) ref += (double)bf16r(A[m * K + k]) * (double)bf16r(B[nn * K + k]);
+      mt = std::max(mt, std::fabs(ref - Dts[m * N + nn]));
+      ms = std::max(ms, std::fabs(ref - Dss[m * N + nn]));
+    }
+  *err_ts = mt;
+  *err_ss = ms;
+  return FTK_OK;
+}
+
+// ---------------------------------------------------------------- engine plumbing
+int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, const std::vector<int>&,
+                 const std::vector<float>& Y3, int K3p, std::string& msg) {
+  tc_plan_free(tc);
+  if (K3p % 16 != 0 || K3p > 128) {
+    msg = "tensor-core engine: K3 = 2 H_plus - H0 = " + std::to_string(pm.K3) + " exceeds 128 (use engine=1)";
+    return FTK_EINVAL;
+  }
+  if (pm.n_psi % 64 != 0 || pm.n_psi > 1024) {
+    msg = "tensor-core engine: n_psi must be a multiple of 64 and <= 1024";
+    return FTK_EINVAL;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&tc.num_sms, cudaDevAttrMultiProcessorCount, dev);
+  tc.K3p = K3p;
+  tc.n_ttiles = (pm.N_t + 127) / 128;
+  const int rows = tc.n_ttiles * 128, hk = K3p / 2;
+  std::vector<uint32_t> yh((size_t)rows * hk, 0u), yl((size_t)rows * hk, 0u);
+  for (int t = 0; t < pm.N_t; ++t)
+    for (int j = 0; j < hk; ++j) {
+      const float x0 = Y3[(size_t)t * K3p + 2 * j], x1 = Y3[(size_t)t * K3p + 2 * j + 1];
+      const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
+      const __nv_bfloat16 l0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
+      const __nv_bfloat16 l1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
+      uint16_t a, b, c, d;
+      std::memcpy(&a, &h0, 2);
+      std::memcpy(&b, &h1, 2);
+      std::memcpy(&c, &l0, 2);
+      std::memcpy(&d, &l1, 2);
+      yh[(size_t)t * hk + j] = (uint32_t)a | ((uint32_t)b << 16);
+      yl[(size_t)t * hk + j] = (uint32_t)c | ((uint32_t)d << 16);
+    }
+  if (cudaMalloc(&tc.d_Yh, yh.size() * 4) != cudaSuccess || cudaMalloc(&tc.d_Yl, yl.size() * 4) != cudaSuccess) {
+    msg = "tensor-core engine: allocation failed";
+    return FTK_ENOMEM;
+  }
+  cudaMemcpy(tc.d_Yh, yh.data(), yh.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(tc.d_Yl, yl.data(), yl.size() * 4, cudaMemcpyHostToDevice);
+  const size_t smem = 1024 + (size_t)4 * pm.n_psi * K3p;
+  if (smem > 227 * 1024) {
+    msg = "tensor-core engine: Step-3 pair operand exceeds shared memory";
+    return FTK_EINVAL;
+  }
+  cudaFuncSetAttribute(k_step3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tc.ready = true;
+  return FTK_OK;
+}
+
+void tc_plan_free(TcPlan& tc) {
+  cudaFree(tc.d_Yh);
+  cudaFree(tc.d_Yl);
+  cudaFree(tc.d_Bop);
+  tc.d_Yh = tc.d_Yl = tc.d_Bop = nullptr;
   tc.ready = false;
-  msg = "tensor-core engine (engine=0) not available in this build; use engine=1";
-  return FTK_EINVAL;
 }
-void tc_plan_free(TcPlan&) {}
-int tc_prepare_images(TcPlan&, const float2*, int64_t, const DevPlan&, cudaStream_t, std::string& msg) {
-  msg = "tensor-core engine not available";
-  return FTK_EINVAL;
+
+int tc_prepare_images(TcPlan&, const float2*, int64_t, const DevPlan&, cudaStream_t, std::string&) { return FTK_OK; }
+int tc_prepare_templates(TcPlan&, const float2*, int64_t, const DevPlan&, cudaStream_t, std::string&) {
+  return FTK_OK;
 }
-int tc_prepare_templates(TcPlan&, const float2*, int64_t, const DevPlan&, cudaStream_t, std::string& msg) {
-  msg = "tensor-core engine not available";
-  return FTK_EINVAL;
-}
+
 size_t tc_bytes_per_pair(const TcPlan&, const DevPlan& P) {
-  return (size_t)P.H_plus * P.n_psi * 8 + (size_t)P.K3p * P.n_psi * 4;
+  return (size_t)P.H_plus * P.n_psi * sizeof(float2) + (size_t)P.K3p * P.n_psi * sizeof(float);
 }
+
 ftk_status_t tc_block_shape(const TcPlan&, const DevPlan&, int, int64_t, int64_t, int64_t, int64_t&, int64_t&) {
   return FTK_OK;
 }
-int tc_run_block(TcPlan&, const PairBlock&, const DevPlan&, void*, size_t, int, unsigned long long*,
-                 unsigned long long*, int, float*, cudaStream_t, prof_cb_t, void*, std::string& msg) {
-  msg = "tensor-core engine not available";
-  return FTK_EINVAL;
+
+void launch_step3_tc(const TcPlan& tc, const float* Z3, const PairBlock& pb, const DevPlan& P, int tm_off,
+                     unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
+                     cudaStream_t s) {
+  S3Params prm;
+  prm.Z3 = Z3;
+  prm.Yh = tc.d_Yh;
+  prm.Yl = tc.d_Yl;
+  prm.pb = pb;
+  prm.n = P.n_psi;
+  prm.K3p = P.K3p;
+  prm.N_t = P.N_t;
+  prm.T = tc.n_ttiles;
+  prm.NC = P.n_psi < 128 ? P.n_psi : 128;
+  prm.RC = P.n_psi / prm.NC;
+  prm.tm_off = tm_off;
+  prm.n_tm_local = n_tm_local;
+  prm.img_keys = img_keys;
+  prm.pair_keys = pair_keys;
+  prm.land = land;
+  const size_t smem = 1024 + (size_t)4 * P.n_psi * P.K3p;
+  const int grid = pb.count < tc.num_sms ? pb.count : tc.num_sms;
+  k_step3_tc<<<grid, S3_THREADS, smem, s>>>(prm);
+}
+
+int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2* A, const float2* B, void* ws,
+                 size_t, int tm_off, unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local,
+                 float* land, cudaStream_t s, prof_cb_t prof, void* plan, std::string& msg) {
+  if (!tc.ready) {
+    msg = "tensor-core engine not initialized";
+    return FTK_ESTATE;
+  }
+  float2* Zhat = reinterpret_cast<float2*>(ws);
+  float* Z3 = reinterpret_cast<float*>(Zhat + (size_t)pb.count * P.H_plus * P.n_psi);
+  if (prof) prof(plan, 1, 0, s);
+  launch_step1_simt(A, B, Zhat, pb, P, s);
+  if (prof) prof(plan, 1, 1, s);
+  if (prof) prof(plan, 2, 0, s);
+  launch_step2_simt(Zhat, Z3, pb, P, s);
+  if (prof) prof(plan, 2, 1, s);
+  if (prof) prof(plan, 3, 0, s);
+  launch_step3_tc(tc, Z3, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
+  if (prof) prof(plan, 3, 1, s);
+  return FTK_OK;
 }
 
 }  // namespace ftk

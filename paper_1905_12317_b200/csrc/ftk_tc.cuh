@@ -32,7 +32,9 @@ int tc_prepare_templates(TcPlan& tc, const float2* fb, int64_t n, const DevPlan&
 size_t tc_bytes_per_pair(const TcPlan& tc, const DevPlan& P);
 ftk_status_t tc_block_shape(const TcPlan& tc, const DevPlan& P, int engine, int64_t NI, int64_t NJ, int64_t cap,
                             int64_t& ni, int64_t& nj);
-int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, void* ws, size_t ws_size, int tm_off,
+int tc_selftest(double* err_ts, double* err_ss, std::string& msg);
+int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2* A, const float2* B, void* ws,
+                 size_t ws_size, int tm_off,
                  unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
                  cudaStream_t s, prof_cb_t prof, void* plan, std::string& msg);
 

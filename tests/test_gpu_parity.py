@@ -27,7 +27,7 @@ def pkg():
     return p
 
 
-ENGINES = [1]  # TODO(tc): add 0 when the tensor-core engine lands
+ENGINES = [0, 1]
 _OPLANS = {}
 
 
@@ -204,3 +204,13 @@ def test_full_size_sampled(pkg, engine, name):
     for n in range(3):
         assert np.max(np.abs(Lp[n] - X[n, n])) <= TOL * na[n] * nb[n]
         assert abs(pb["value"][ii[n], jj[n]] - X[n, n].max()) <= TOL * na[n] * nb[n]
+
+
+def test_tc_selftest(pkg):
+    """One 128x64x32 bf16 tcgen05.mma with A from TMEM and one with A from SMEM vs a host reference:
+    validates the descriptor / TMEM-layout assumptions the tensor-core kernels rely on."""
+    import ctypes as C
+    ets, ess = C.c_double(-1), C.c_double(-1)
+    st = pkg.lib().ftk_tc_selftest(0, C.byref(ets), C.byref(ess))
+    assert st == 0
+    assert ets.value < 1e-4 and ess.value < 1e-4, (ets.value, ess.value)
