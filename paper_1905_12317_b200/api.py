@@ -191,15 +191,33 @@ def merge_bests(gathered, world: int, n_im: int, out=None, stream=None):
     return o
 
 
+def shard_range(rank: int, world: int, n_total: int):
+    """Templates kept by `rank` (mirrors ftk_load_templates): [floor(r N / W), floor((r+1) N / W))."""
+    return rank * n_total // world, (rank + 1) * n_total // world
+
+
+def gather_and_merge(local, group=None, stream=None):
+    """All-gather per-rank int32 [N_im, 4] records (NCCL for CUDA tensors, gloo for CPU) and merge them."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if world == 1:
+        return local
+    if local.is_cuda:
+        gathered = torch.empty((world * local.shape[0], 4), dtype=torch.int32, device=local.device)
+        dist.all_gather_into_tensor(gathered, local.contiguous(), group=group)
+    else:
+        parts = [torch.empty_like(local) for _ in range(world)]
+        dist.all_gather(parts, local.contiguous(), group=group)
+        gathered = torch.cat(parts)
+    out = merge_bests(gathered, world, local.shape[0], stream=stream)
+    return out if hasattr(out, "device") else torch.from_numpy(out)
+
+
 def distributed_align(plan: FTKPlan, group=None, stream=None):
     """Template-sharded alignment: local ftk_align on this rank's shard, all-gather of the per-image
     records through torch.distributed (NCCL on GPUs, gloo on CPU), deterministic merge."""
     import torch
     import torch.distributed as dist
     local = plan.align(stream=stream)["best"]
-    world = dist.get_world_size(group)
-    if world == 1:
-        return local
-    gathered = torch.empty((world * local.shape[0], 4), dtype=torch.int32, device=local.device)
-    dist.all_gather_into_tensor(gathered, local, group=group)
-    return merge_bests(gathered, world, local.shape[0], stream=stream)
+    return gather_and_merge(local, group=group, stream=stream)

@@ -19,6 +19,7 @@ struct ftk_plan_s {
   PlanMath pm;
   int device = -1, rank = 0, world = 1, engine = 0;
   size_t ws_bytes = (size_t)1 << 30;
+  bool ws_user = false;
   std::string err;
   // device constants
   float* d_g = nullptr;
@@ -166,6 +167,7 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
   plan->rank = o.rank;
   plan->engine = o.engine;
   plan->ws_bytes = o.workspace_bytes ? o.workspace_bytes : ((size_t)1 << 30);
+  plan->ws_user = o.workspace_bytes != 0;
   auto bail = [&](ftk_status_t s) {
     ftk_plan_destroy(plan);
     return s;
@@ -486,7 +488,16 @@ ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best,
   CK(cudaMemsetAsync(plan->d_keys, 0, NI * (pair_best ? NJ + 1 : 1) * sizeof(unsigned long long), s));
   if (NJ > 0) {
     const size_t per = bytes_per_pair(plan);
-    int64_t cap = (int64_t)(plan->ws_bytes / per);
+    size_t wsb = plan->ws_bytes;
+    if (!plan->ws_user && plan->engine == 0) {
+      // tensor-core engine: large pair blocks amortize the generated Step-1 operand; take up to half of
+      // the free device memory, at most 24 GiB
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      wsb = std::min<size_t>((size_t)24 << 30, (fr + plan->ws_size) / 2);
+      wsb = std::max<size_t>(wsb, (size_t)1 << 30);
+    }
+    int64_t cap = (int64_t)(wsb / per);
     if (cap < 1) cap = 1;
     if (cap > (1 << 24)) cap = 1 << 24;
     int64_t nj = std::min<int64_t>(NJ, cap);

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstring>
 
+#include "ftk_fft.cuh"
 #include "ftk_sm100.cuh"
 #include "ftk_tc.cuh"
 
@@ -130,26 +131,36 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           mbar_wait(&S.acc_full[ab], (g_acc >> 1) & 1);
           tc_fence_after();
           const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * 128);
-          for (int c0 = 0; c0 < NC; c0 += 16) {
-            uint32_t r16[16];
-            tmem_ld16(base + c0, r16);
+          for (int c0 = 0; c0 < NC; c0 += 64) {
+            uint32_t r[4][16];
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+              if (c0 + 16 * h < NC) tmem_ld16(base + c0 + 16 * h, r[h]);
             tmem_wait_ld();
             if (t < P.N_t) {
-              const uint32_t f0 = (uint32_t)t * (uint32_t)n + (uint32_t)(rc * NC + c0);
 #pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                const float v = __uint_as_float(r16[e]);
-                if (v > bv) {
-                  bv = v;
-                  bf = f0 + e;
+              for (int h = 0; h < 4; ++h) {
+                if (c0 + 16 * h >= NC) break;
+                // max first (1 FMNMX per value); locate the column only when the running best improves
+                float m = __uint_as_float(r[h][0]);
+#pragma unroll
+                for (int e = 1; e < 16; ++e) m = fmaxf(m, __uint_as_float(r[h][e]));
+                if (m > bv) {
+                  int e0 = 0;
+#pragma unroll
+                  for (int e = 15; e >= 0; --e)
+                    if (__uint_as_float(r[h][e]) == m) e0 = e;
+                  bv = m;
+                  bf = (uint32_t)t * (uint32_t)n + (uint32_t)(rc * NC + c0 + 16 * h + e0);
                 }
-              }
-              if (P.land) {
-                float4* dst = reinterpret_cast<float4*>(P.land + ((size_t)p * P.N_t + t) * n + rc * NC + c0);
+                if (P.land) {
+                  float4* dst =
+                      reinterpret_cast<float4*>(P.land + ((size_t)p * P.N_t + t) * n + rc * NC + c0 + 16 * h);
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  dst[e] = make_float4(__uint_as_float(r16[4 * e]), __uint_as_float(r16[4 * e + 1]),
-                                       __uint_as_float(r16[4 * e + 2]), __uint_as_float(r16[4 * e + 3]));
+                  for (int e = 0; e < 4; ++e)
+                    dst[e] = make_float4(__uint_as_float(r[h][4 * e]), __uint_as_float(r[h][4 * e + 1]),
+                                         __uint_as_float(r[h][4 * e + 2]), __uint_as_float(r[h][4 * e + 3]));
+                }
               }
             }
           }
@@ -269,6 +280,296 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   }
 }
 
+// ---------------------------------------------------------------- Step 1 (tensor cores)
+// Form B of Eq. (fbk3) Step 1 (P:836 with p = q - ell): for each image mode p
+//   Zhat'_{ij,zeta}(p) = sum_m a_i(m, p) c_{j zeta}(m),  c = g_zeta(m) conj b_j(m, p + ell_zeta),  g = 2 pi w G,
+// so that Zhat_zeta(q) = Zhat'_zeta(q - ell) and Step 2 applies e^{-i ell gamma_r} after the FFT.
+// Real GEMM per p with K' = 2 n_k:  rows (j, zeta, part) of the GENERATED operand c (A, in TMEM):
+//   Re-row = [c_r | -c_i],  Im-row = [c_i | c_r];  columns = images, B = [a_r | a_i] (pre-split, SMEM).
+// Output Zhat' [p][pair][zeta] complex (pair = il * nj + jl within the block).
+constexpr int S1_THREADS = 10 * 32;
+constexpr int S1_STAGES = 4;
+
+struct S1Params {
+  const uint8_t* Aop;   // image operand: [p][image tile][kchunk][part][16][KCH/8][128 B]
+  const float2* B;      // template FB coefficients [j][q][m] (local templates)
+  const float* g;       // [H_plus][n_k]
+  const int* ell;       // [H_plus]
+  float2* Zhat;         // [p][pairs][H_plus]
+  int i0, ni, j0, nj;   // block (i0 multiple of 128)
+  int n, n_k, Hp, KCH, NKCH, NIT;  // NIT = image tiles per mode in Aop
+  int F, NCT;           // F = nj * Hp flattened (j, zeta) columns, NCT = ceil(F / 64)
+};
+
+struct S1Smem {
+  uint64_t st_full[S1_STAGES], st_empty[S1_STAGES];
+  uint64_t a_full, a_empty;
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
+  extern __shared__ __align__(1024) uint8_t s1_raw[];
+  S1Smem& S = *reinterpret_cast<S1Smem*>(s1_raw);
+  uint8_t* stages = s1_raw + 1024;                                   // S1_STAGES x stage_bytes
+  const uint32_t stage_bytes = 128u * P.KCH * 4u;                    // hi + lo
+  float* stg = reinterpret_cast<float*>(stages + S1_STAGES * stage_bytes);  // [128 img][128 rows]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = P.n, nk = P.n_k;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S1_STAGES; ++i) {
+      mbar_init(&S.st_full[i], 1);
+      mbar_init(&S.st_empty[i], 1);
+    }
+    mbar_init(&S.a_full, 128);
+    mbar_init(&S.a_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S.acc_full[i], 1);
+      mbar_init(&S.acc_empty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&S.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+  const int units = n * P.NCT;
+  const int it0 = P.i0 / 128;
+  const int nit = (P.ni + 127) / 128;
+
+  if (warp == 0) {
+    // ---------------- bulk-copy producer of image operand stages
+    if (lane == 0) {
+      uint32_t g_st = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int p = u / P.NCT;
+        for (int t = 0; t < nit; ++t) {
+          for (int kc = 0; kc < P.NKCH; ++kc, ++g_st) {
+            const int s = g_st % S1_STAGES;
+            mbar_wait(&S.st_empty[s], ((g_st / S1_STAGES) & 1) ^ 1);
+            mbar_arrive_expect_tx(&S.st_full[s], stage_bytes);
+            const uint8_t* src = P.Aop + (((size_t)p * P.NIT + it0 + t) * P.NKCH + kc) * stage_bytes;
+            bulk_g2s(stages + s * stage_bytes, src, stage_bytes, &S.st_full[s]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16_f32(128, 128);
+      const uint32_t sbase = smem_u32(stages);
+      const uint32_t part_bytes = 128u * P.KCH * 2u;
+      const uint32_t SBO = (uint32_t)(P.KCH / 8) * 128u;
+      uint32_t g_st = 0, g_acc = 0, g_u = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++g_u) {
+        mbar_wait(&S.a_full, g_u & 1);
+        tc_fence_after();
+        for (int t = 0; t < nit; ++t, ++g_acc) {
+          const int ab = g_acc & 1;
+          mbar_wait(&S.acc_empty[ab], ((g_acc >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + 256 + (uint32_t)(ab * 128);
+          for (int kc = 0; kc < P.NKCH; ++kc, ++g_st) {
+            const int s = g_st % S1_STAGES;
+            mbar_wait(&S.st_full[s], (g_st / S1_STAGES) & 1);
+            tc_fence_after();
+            const uint32_t st = sbase + s * stage_bytes;
+            for (int ks = 0; ks < P.KCH / 16; ++ks) {
+              const uint32_t a_hi = tmem + (uint32_t)(kc * (P.KCH / 2) + ks * 8);
+              const uint32_t a_lo = a_hi + (uint32_t)nk;
+              const uint64_t b_hi = smem_desc_kmajor_noswz(st + ks * 256, 128, SBO);
+              const uint64_t b_lo = smem_desc_kmajor_noswz(st + part_bytes + ks * 256, 128, SBO);
+              const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+              mma_bf16_ts(d, a_hi, b_hi, idesc, acc);
+              mma_bf16_ts(d, a_hi, b_lo, idesc, 1u);
+              mma_bf16_ts(d, a_lo, b_hi, idesc, 1u);
+            }
+            tc_commit(&S.st_empty[s]);
+          }
+          tc_commit(&S.acc_full[ab]);
+        }
+        tc_commit(&S.a_empty);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 6) {
+    // ---------------- generators of the template x G operand (A, TMEM columns [0, 2 n_k))
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int c = row >> 1, part = row & 1;
+    const uint32_t base = tmem + ((uint32_t)(q * 32) << 16);
+    const int half = nk / 2;  // u32 columns per K' half
+    uint32_t g_u = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++g_u) {
+      const int p = u / P.NCT, ct = u - p * P.NCT;
+      const int f = ct * 64 + c;
+      mbar_wait(&S.a_empty, (g_u & 1) ^ 1);
+      tc_fence_after();
+      const bool valid = f < P.F;
+      int jl = 0, z = 0;
+      if (valid) {
+        jl = f / P.Hp;
+        z = f - jl * P.Hp;
+      }
+      const int qt = valid ? ((p + __ldg(P.ell + z)) & (n - 1)) : 0;
+      const float2* brow = P.B + ((size_t)(P.j0 + jl) * n + qt) * nk;
+      const float* grow = P.g + (size_t)z * nk;
+      for (int m0 = 0; m0 < nk; m0 += 16) {
+        uint32_t h1[8], l1[8], h2[8], l2[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float cr0 = 0.f, ci0 = 0.f, cr1 = 0.f, ci1 = 0.f;
+          if (valid) {
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(brow + m0 + 2 * e));
+            const float2 gg = __ldg(reinterpret_cast<const float2*>(grow + m0 + 2 * e));
+            cr0 = gg.x * bb.x;
+            ci0 = -gg.x * bb.y;
+            cr1 = gg.y * bb.z;
+            ci1 = -gg.y * bb.w;
+          }
+          if (part == 0) {  // Re-row: [c_r | -c_i]
+            split2_bf16(cr0, cr1, h1[e], l1[e]);
+            split2_bf16(-ci0, -ci1, h2[e], l2[e]);
+          } else {          // Im-row: [c_i | c_r]
+            split2_bf16(ci0, ci1, h1[e], l1[e]);
+            split2_bf16(cr0, cr1, h2[e], l2[e]);
+          }
+        }
+        const uint32_t col = (uint32_t)(m0 / 2);
+        tmem_st8(base + col, h1);
+        tmem_st8(base + half + col, h2);
+        tmem_st8(base + nk + col, l1);
+        tmem_st8(base + nk + half + col, l2);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&S.a_full);
+    }
+  } else {
+    // ---------------- epilogue: accumulator [128 rows (j,zeta,part)] x [128 images] -> Zhat'
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int ew = warp - 6;  // 0..3
+    uint32_t g_acc = 0;
+    const size_t npair = (size_t)P.ni * P.nj;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int p = u / P.NCT, ct = u - p * P.NCT;
+      const int nvalid = min(128, 2 * (P.F - ct * 64));
+      for (int t = 0; t < nit; ++t, ++g_acc) {
+        const int ab = g_acc & 1;
+        mbar_wait(&S.acc_full[ab], (g_acc >> 1) & 1);
+        tc_fence_after();
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + 256 + (uint32_t)(ab * 128);
+        for (int c0 = 0; c0 < 128; c0 += 16) {
+          uint32_t r16[16];
+          tmem_ld16(base + c0, r16);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) stg[(c0 + e) * 128 + row] = __uint_as_float(r16[e]);
+        }
+        tc_fence_before();
+        mbar_arrive(&S.acc_empty[ab]);
+        named_bar(2, 128);
+        // coalesced write-out: image ii -> 128 consecutive floats (rows) at pair (il, ct*64 ...)
+        for (int ii = ew; ii < 128; ii += 4) {
+          const int il = t * 128 + ii;  // local image index within the block
+          if (il >= P.ni) continue;
+          float2* dst = P.Zhat + ((size_t)p * npair + (size_t)il * P.nj) * P.Hp + (size_t)ct * 64;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cc = lane + 32 * h;  // complex column within the tile
+            if (2 * cc < nvalid) dst[cc] = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * cc);
+          }
+        }
+        named_bar(2, 128);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+static size_t s1_smem_bytes(const TcPlan& tc) {
+  return 1024 + (size_t)S1_STAGES * 128 * tc.KCH * 4 + (size_t)128 * 128 * 4;
+}
+
+// Image operand prep: FB a[i][q][m] -> split bf16 canonical K-major tiles (B operand of Step 1).
+__global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restrict__ Aop, int NI, int NIT, int n,
+                                int nk, int KCH, int NKCH) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int groups = (2 * nk) / 8;  // 8-element k' groups per row
+  const int64_t total = (int64_t)NIT * 128 * n * groups;
+  if (tid >= total) return;
+  const int gk = (int)(tid % groups);
+  int64_t rest = tid / groups;
+  const int i = (int)(rest % (NIT * 128));
+  const int p = (int)(rest / (NIT * 128));
+  const int k0 = gk * 8;
+  float v[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int kp = k0 + e;
+    float x = 0.f;
+    if (i < NI) {
+      const float2 a = fb[((size_t)i * n + p) * nk + (kp < nk ? kp : kp - nk)];
+      x = kp < nk ? a.x : a.y;
+    }
+    v[e] = x;
+  }
+  uint4 h, l;
+  split2_bf16(v[0], v[1], h.x, l.x);
+  split2_bf16(v[2], v[3], h.y, l.y);
+  split2_bf16(v[4], v[5], h.z, l.z);
+  split2_bf16(v[6], v[7], h.w, l.w);
+  const int it = i / 128, ii = i % 128, kch = k0 / KCH, kk = k0 % KCH;
+  const size_t stage_bytes = 128u * KCH * 4u;
+  uint8_t* st = Aop + (((size_t)p * NIT + it) * NKCH + kch) * stage_bytes;
+  const size_t off = (size_t)(ii / 8) * (KCH / 8) * 128 + (kk / 8) * 128 + (ii % 8) * 16;
+  *reinterpret_cast<uint4*>(st + off) = h;
+  *reinterpret_cast<uint4*>(st + 128u * KCH * 2u + off) = l;
+}
+
+// Step 2 for the tensor-core engine: FFT over the image mode p of Zhat' [p][pair][zeta], then the
+// Form-B twiddle e^{-2 pi i ell r / n} (Z_zeta(r) = sum_q Zhat_zeta(q) e^{-2 pi i q r/n}, q = p + ell),
+// written as Z3 [pair][K3p][n] real rows (reading R13).
+constexpr int S2T_ZB = 16;
+
+__global__ void __launch_bounds__(256) k_step2_tc(const float2* __restrict__ Zhat, float* __restrict__ Z3, int npair,
+                                                  DevPlan P) {
+  extern __shared__ float2 sm2t[];
+  const int n = P.n_psi, Hp = P.H_plus;
+  float2* tws = sm2t + S2T_ZB * n;
+  const int pr = blockIdx.x, z0 = blockIdx.y * S2T_ZB;
+  const int nz = min(S2T_ZB, Hp - z0);
+  for (int i = threadIdx.x; i < n / 2; i += blockDim.x) tws[i] = P.tw[i];
+  for (int idx = threadIdx.x; idx < nz * n; idx += blockDim.x) {
+    const int p = idx / nz, z = idx - p * nz;
+    sm2t[z * n + p] = Zhat[((size_t)p * npair + pr) * Hp + z0 + z];
+  }
+  __syncthreads();
+  smem_fft_rows(sm2t, nz, n, P.log2_psi, tws);
+  float* dst = Z3 + (size_t)pr * P.K3p * n;
+  for (int idx = threadIdx.x; idx < nz * n; idx += blockDim.x) {
+    const int z = idx / n, r = idx - z * n;
+    const int l = P.ell[z0 + z];
+    const int c = P.col[z0 + z];
+    const int j = (l * r) & (n - 1);
+    float2 w = tws[j & (n / 2 - 1)];
+    if (j >= n / 2) w = make_float2(-w.x, -w.y);
+    const float2 v = sm2t[idx];
+    const float re = v.x * w.x - v.y * w.y, im = v.x * w.y + v.y * w.x;
+    dst[(size_t)c * n + r] = re;
+    if (l > 0) dst[(size_t)(c + 1) * n + r] = im;
+  }
+}
+
 // ---------------------------------------------------------------- single-MMA self-test
 // D = A * B^T with A [128 x 32] (TS: from TMEM; SS: from SMEM), B [N=64 x 32] from SMEM, bf16 inputs.
 __global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const float* B, float* D_ts, float* D_ss) {
@@ -276,7 +577,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const fl
   __shared__ __align__(1024) uint8_t sb[64 * 32 * 2];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int K = 32;
   // canonical K-major no-swizzle: core (row/8, k/8) at (row/8)*SBO + (k/8)*128, SBO = (K/8)*128
   const uint32_t SBO = (K / 8) * 128;
@@ -434,6 +735,14 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
     return FTK_EINVAL;
   }
   cudaFuncSetAttribute(k_step3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (pm.n_k % 16 != 0 || pm.n_k > 128) {
+    msg = "tensor-core engine: n_k must be a multiple of 16 and <= 128";
+    return FTK_EINVAL;
+  }
+  tc.KCH = (2 * pm.n_k) % 64 == 0 ? 64 : 32;
+  tc.NKCH = 2 * pm.n_k / tc.KCH;
+  cudaFuncSetAttribute(k_step1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
+  cudaFuncSetAttribute(k_step2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   tc.ready = true;
   return FTK_OK;
 }
@@ -442,11 +751,32 @@ void tc_plan_free(TcPlan& tc) {
   cudaFree(tc.d_Yh);
   cudaFree(tc.d_Yl);
   cudaFree(tc.d_Bop);
+  cudaFree(tc.d_Aop);
   tc.d_Yh = tc.d_Yl = tc.d_Bop = nullptr;
+  tc.d_Aop = nullptr;
+  tc.aop_bytes = 0;
   tc.ready = false;
 }
 
-int tc_prepare_images(TcPlan&, const float2*, int64_t, const DevPlan&, cudaStream_t, std::string&) { return FTK_OK; }
+int tc_prepare_images(TcPlan& tc, const float2* fb, int64_t n_im, const DevPlan& P, cudaStream_t s, std::string& msg) {
+  tc.NIT = (int)((n_im + 127) / 128);
+  const size_t bytes = (size_t)P.n_psi * tc.NIT * 128 * (2 * P.n_k) * 4;
+  if (bytes != tc.aop_bytes) {
+    cudaFree(tc.d_Aop);
+    tc.d_Aop = nullptr;
+    tc.aop_bytes = 0;
+    if (cudaMalloc(&tc.d_Aop, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      msg = "tensor-core engine: image operand allocation failed";
+      return FTK_ENOMEM;
+    }
+    tc.aop_bytes = bytes;
+  }
+  const int64_t total = (int64_t)tc.NIT * 128 * P.n_psi * (2 * P.n_k / 8);
+  k_prep_image_op<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(fb, tc.d_Aop, (int)n_im, tc.NIT, P.n_psi, P.n_k,
+                                                                   tc.KCH, tc.NKCH);
+  return cudaGetLastError() == cudaSuccess ? FTK_OK : FTK_ECUDA;
+}
 int tc_prepare_templates(TcPlan&, const float2*, int64_t, const DevPlan&, cudaStream_t, std::string&) {
   return FTK_OK;
 }
@@ -455,7 +785,16 @@ size_t tc_bytes_per_pair(const TcPlan&, const DevPlan& P) {
   return (size_t)P.H_plus * P.n_psi * sizeof(float2) + (size_t)P.K3p * P.n_psi * sizeof(float);
 }
 
-ftk_status_t tc_block_shape(const TcPlan&, const DevPlan&, int, int64_t, int64_t, int64_t, int64_t&, int64_t&) {
+ftk_status_t tc_block_shape(const TcPlan&, const DevPlan&, int engine, int64_t NI, int64_t NJ, int64_t cap,
+                            int64_t& ni, int64_t& nj) {
+  if (engine != 0) return FTK_OK;
+  // image rows in multiples of 128 (Step-1 N tiles); as many as the workspace allows, up to 2048
+  int64_t ni_t = std::min<int64_t>((NI + 127) / 128 * 128, 2048);
+  while (ni_t > 128 && ni_t * 1 > cap) ni_t -= 128;
+  if (NI <= 128) ni_t = NI;
+  ni = std::min<int64_t>(ni_t, NI);
+  nj = std::max<int64_t>(1, std::min<int64_t>(NJ, cap / std::max<int64_t>(ni_t, 1)));
+  if (ni < NI && ni % 128 != 0) return FTK_EINVAL;
   return FTK_OK;
 }
 
@@ -483,6 +822,31 @@ void launch_step3_tc(const TcPlan& tc, const float* Z3, const PairBlock& pb, con
   k_step3_tc<<<grid, S3_THREADS, smem, s>>>(prm);
 }
 
+void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const PairBlock& pb, const DevPlan& P,
+                     cudaStream_t s) {
+  S1Params prm;
+  prm.Aop = tc.d_Aop;
+  prm.B = B;
+  prm.g = P.g;
+  prm.ell = P.ell;
+  prm.Zhat = Zhat;
+  prm.i0 = pb.i0;
+  prm.ni = pb.ni;
+  prm.j0 = pb.j0;
+  prm.nj = pb.nj;
+  prm.n = P.n_psi;
+  prm.n_k = P.n_k;
+  prm.Hp = P.H_plus;
+  prm.KCH = tc.KCH;
+  prm.NKCH = tc.NKCH;
+  prm.NIT = tc.NIT;
+  prm.F = pb.nj * P.H_plus;
+  prm.NCT = (prm.F + 63) / 64;
+  const int units = P.n_psi * prm.NCT;
+  const int grid = units < tc.num_sms ? units : tc.num_sms;
+  k_step1_tc<<<grid, S1_THREADS, s1_smem_bytes(tc), s>>>(prm);
+}
+
 int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2* A, const float2* B, void* ws,
                  size_t, int tm_off, unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local,
                  float* land, cudaStream_t s, prof_cb_t prof, void* plan, std::string& msg) {
@@ -492,12 +856,24 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
   }
   float2* Zhat = reinterpret_cast<float2*>(ws);
   float* Z3 = reinterpret_cast<float*>(Zhat + (size_t)pb.count * P.H_plus * P.n_psi);
-  if (prof) prof(plan, 1, 0, s);
-  launch_step1_simt(A, B, Zhat, pb, P, s);
-  if (prof) prof(plan, 1, 1, s);
-  if (prof) prof(plan, 2, 0, s);
-  launch_step2_simt(Zhat, Z3, pb, P, s);
-  if (prof) prof(plan, 2, 1, s);
+  if (pb.li) {
+    // explicit pair list (ftk_landscape_pairs): per-pair Steps 1-2 on CUDA cores, Step 3 on tensor cores
+    if (prof) prof(plan, 1, 0, s);
+    launch_step1_simt(A, B, Zhat, pb, P, s);
+    if (prof) prof(plan, 1, 1, s);
+    if (prof) prof(plan, 2, 0, s);
+    launch_step2_simt(Zhat, Z3, pb, P, s);
+    if (prof) prof(plan, 2, 1, s);
+  } else {
+    if (prof) prof(plan, 1, 0, s);
+    launch_step1_tc(tc, B, Zhat, pb, P, s);
+    if (prof) prof(plan, 1, 1, s);
+    if (prof) prof(plan, 2, 0, s);
+    const size_t smem = ((size_t)S2T_ZB * P.n_psi + P.n_psi / 2) * sizeof(float2);
+    dim3 grid(pb.count, (P.H_plus + S2T_ZB - 1) / S2T_ZB);
+    k_step2_tc<<<grid, 256, smem, s>>>(Zhat, Z3, pb.count, P);
+    if (prof) prof(plan, 2, 1, s);
+  }
   if (prof) prof(plan, 3, 0, s);
   launch_step3_tc(tc, Z3, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
   if (prof) prof(plan, 3, 1, s);

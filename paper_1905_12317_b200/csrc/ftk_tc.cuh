@@ -17,7 +17,10 @@ struct TcPlan {
   uint32_t* d_Yh = nullptr;  // [n_ttiles*128][K3p/2] packed bf16x2, hi part
   uint32_t* d_Yl = nullptr;  // lo part
   // Step 1 operands
-  uint32_t* d_Bop = nullptr;   // templates, split, Step-1 operand layout
+  uint32_t* d_Bop = nullptr;   // (unused; templates are generated in-kernel)
+  uint8_t* d_Aop = nullptr;    // images, bf16 hi/lo split, Step-1 K-major tiles [p][tile][kchunk][part]...
+  size_t aop_bytes = 0;
+  int NIT = 0, KCH = 64, NKCH = 0;
   int64_t n_tm = 0;
   int num_sms = 148;
 };
