@@ -155,7 +155,7 @@ ftk_status_t ftk_set_profiling(ftk_plan_t plan, int enabled);
 ftk_status_t ftk_kernel_times(ftk_plan_t plan, double* ms /*[5]*/, int64_t* launches /*[5]*/);
 
 /* Hardware self-test of the tensor-core primitives (one 128x64x32 bf16 tcgen05.mma with A from TMEM and
- * one with A from shared memory, canonical K-major layouts) against a host reference: writes the max
+ * one with A from shared memory, K-major, plus one with an MN-major B operand) against a host reference: writes the max
  * absolute errors (expected ~1e-6, fp32 accumulation of exactly representable bf16 products). */
 ftk_status_t ftk_tc_selftest(int device, double* err_ts, double* err_ss);
 

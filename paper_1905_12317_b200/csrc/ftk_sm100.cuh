@@ -102,6 +102,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// Same with B MN-major (bit 16): B stored with N contiguous inside 16-byte core rows
+// (INTERLEAVE canonical: core matrix = 8 K-rows x 8 N-elements, 128 B; SBO = N-direction core stride,
+// LBO = K-direction core stride).
+__host__ __device__ constexpr uint32_t idesc_bf16_f32_bmn(int M, int N) { return idesc_bf16_f32(M, N) | (1u << 16); }
+
 // D[tmem] (+)= A[tmem] * B[smem]^T  (A from TMEM: "TS" form), cta_group::1, kind::f16
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {

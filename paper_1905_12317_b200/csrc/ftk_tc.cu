@@ -6,8 +6,8 @@
 // accumulation in TMEM (measured <= 6e-6 ||A|| ||B|| vs the 1e-4 budget).
 //
 // Kernel k_step3_tc (one CTA per SM, persistent over a contiguous range of pairs):
-//   * Z producers (warps 0-3): per pair, read Z3 (fp32, [K3p][n_psi]) from global, split to bf16
-//     hi/lo and write the whole pair into SMEM in the K-major SWIZZLE_NONE canonical layout, chunk by
+//   * Z producer (warp 0, one lane): per pair, bulk-copies (cp.async.bulk) the pair's operand image
+//     written by Step 2 -- bf16 hi/lo, MN-major SWIZZLE_NONE canonical layout -- into SMEM, chunk by
 //     chunk of 128 r (z_full[rc] / z_empty[rc] mbarriers) -> the B operand (N = r).
 //   * Y loaders (warps 8-11): per 128-row t-tile, Y3 hi/lo rows -> TMEM via tcgen05.st -> the A
 //     operand (M = t), double-buffered (y_full / y_empty).
@@ -31,7 +31,7 @@ constexpr int S3_THREADS = 13 * 32;
 constexpr int S3_MAX_RC = 8;  // n_psi / 128 <= 8
 
 struct S3Params {
-  const float* Z3;        // [pair][K3p][n]
+  const uint8_t* Zop;     // per pair: bf16 hi/lo MN-major operand image (see k_step2_fft)
   const uint32_t* Yh;     // [T*128][K3p/2]
   const uint32_t* Yl;
   PairBlock pb;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   const uint32_t part_bytes = (uint32_t)n * K3p * 2;      // one bf16 part of the whole pair
   if (threadIdx.x == 0) {
     for (int i = 0; i < RC; ++i) {
-      mbar_init(&S.z_full[i], 128);
+      mbar_init(&S.z_full[i], 1);
       mbar_init(&S.z_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -88,33 +88,22 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   const int p_end = min(count, p_begin + per);
 
   if (warp < 4) {
-    // ---------------- Z producers
-    const int tid = threadIdx.x;  // 0..127
-    int it = 0;
-    for (int p = p_begin; p < p_end; ++p, ++it) {
-      const float* zsrc = P.Z3 + (size_t)p * K3p * n;
-      for (int rc = 0; rc < RC; ++rc) {
-        mbar_wait(&S.z_empty[rc], (it & 1) ^ 1);
-        for (int rr = tid; rr < NC; rr += 128) {
-          const int r = rc * NC + rr;
-          uint8_t* row_hi = zs + (size_t)(r >> 3) * SBO + (r & 7) * 16;
-          for (int kc = 0; kc < K3p / 8; ++kc) {
-            float v[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = __ldg(zsrc + (size_t)(kc * 8 + e) * n + r);
-            uint4 h, l;
-            split2_bf16(v[0], v[1], h.x, l.x);
-            split2_bf16(v[2], v[3], h.y, l.y);
-            split2_bf16(v[4], v[5], h.z, l.z);
-            split2_bf16(v[6], v[7], h.w, l.w);
-            *reinterpret_cast<uint4*>(row_hi + kc * 128) = h;
-            *reinterpret_cast<uint4*>(row_hi + part_bytes + kc * 128) = l;
-          }
+    // ---------------- Z producer: the pair's operand image chunk by chunk (hi and lo) via bulk copies
+    if (warp == 0 && lane == 0) {
+      const uint32_t chunk_bytes = (uint32_t)(NC / 8) * SBO;
+      int it = 0;
+      for (int p = p_begin; p < p_end; ++p, ++it) {
+        const uint8_t* zsrc = P.Zop + (size_t)p * 2 * part_bytes;
+        for (int rc = 0; rc < RC; ++rc) {
+          mbar_wait(&S.z_empty[rc], (it & 1) ^ 1);
+          mbar_arrive_expect_tx(&S.z_full[rc], 2 * chunk_bytes);
+          bulk_g2s(zs + rc * chunk_bytes, zsrc + rc * chunk_bytes, chunk_bytes, &S.z_full[rc]);
+          bulk_g2s(zs + part_bytes + rc * chunk_bytes, zsrc + part_bytes + rc * chunk_bytes, chunk_bytes,
+                   &S.z_full[rc]);
         }
-        fence_proxy_async_smem();
-        mbar_arrive(&S.z_full[rc]);
       }
     }
+    __syncwarp();
   } else if (warp < 8) {
     // ---------------- epilogue
     const int q = warp & 3;
@@ -234,7 +223,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   } else {
     // ---------------- MMA issuer (warp 12, lane 0)
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(128, NC);
+      const uint32_t idesc = idesc_bf16_f32_bmn(128, NC);  // B (Z) is MN-major
       const uint32_t zbase = smem_u32(zs);
       const int ksteps = K3p / 16;
       const int halfk = K3p / 2;
@@ -536,45 +525,195 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
   *reinterpret_cast<uint4*>(st + 128u * KCH * 2u + off) = l;
 }
 
-// Step 2 for the tensor-core engine: FFT over the image mode p of Zhat' [p][pair][zeta], then the
-// Form-B twiddle e^{-2 pi i ell r / n} (Z_zeta(r) = sum_q Zhat_zeta(q) e^{-2 pi i q r/n}, q = p + ell),
-// written as Z3 [pair][K3p][n] real rows (reading R13).
-constexpr int S2T_ZB = 16;
+// Step 2 for the tensor-core engine (Eq. fbk3 Step 2, Form B):
+//   Z_zeta(r) = e^{-2 pi i ell r / n} sum_p Zhat'_zeta(p) e^{-2 pi i p r / n},   (q = p + ell)
+// read from Zhat' [p][pair][zeta]; written as the Step-3 B-operand image (real rows of reading R13).
+// FFT: four-step decomposition n = 32 E, p = a + 32 b (a = lane), r = c + E d:
+//   (A) per lane an E-point DFT over b in registers, (B) twiddle w_n^{a c}, (C) a 32-point radix-2
+//   DIF across the warp with shfl_xor (output index d lands on lane bitrev5(d)).
+template <int E>
+__device__ __forceinline__ void dft_regs(float2 (&x)[E], const float2* tw, int n) {
+  // radix-2 DIT on bit-reversed register order -> natural-order output; w_E^j = tw[j n / E]
+  float2 y[E];
+  constexpr int LOG = (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    int r = 0;
+#pragma unroll
+    for (int bb = 0; bb < LOG; ++bb) r |= ((i >> bb) & 1) << (LOG - 1 - bb);
+    y[i] = x[r];
+  }
+#pragma unroll
+  for (int s = 1; s < E; s *= 2) {
+#pragma unroll
+    for (int blk = 0; blk < E; blk += 2 * s) {
+#pragma unroll
+      for (int j = 0; j < s; ++j) {
+        const float2 w = tw[j * (n / (2 * s))];
+        const float2 u = y[blk + j], v0 = y[blk + j + s];
+        const float2 v = make_float2(v0.x * w.x - v0.y * w.y, v0.x * w.y + v0.y * w.x);
+        y[blk + j] = make_float2(u.x + v.x, u.y + v.y);
+        y[blk + j + s] = make_float2(u.x - v.x, u.y - v.y);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < E; ++i) x[i] = y[i];
+}
 
-__global__ void __launch_bounds__(256) k_step2_tc(const float2* __restrict__ Zhat, float* __restrict__ Z3, int npair,
-                                                  DevPlan P) {
-  extern __shared__ float2 sm2t[];
-  const int n = P.n_psi, Hp = P.H_plus;
-  float2* tws = sm2t + S2T_ZB * n;
-  const int pr = blockIdx.x, z0 = blockIdx.y * S2T_ZB;
-  const int nz = min(S2T_ZB, Hp - z0);
-  for (int i = threadIdx.x; i < n / 2; i += blockDim.x) tws[i] = P.tw[i];
-  for (int idx = threadIdx.x; idx < nz * n; idx += blockDim.x) {
-    const int p = idx / nz, z = idx - p * nz;
-    sm2t[z * n + p] = Zhat[((size_t)p * npair + pr) * Hp + z0 + z];
+template <int E>
+__global__ void __launch_bounds__(E >= 16 ? 256 : 512) k_step2_fft(const float2* __restrict__ Zhat,
+                                                                   uint8_t* __restrict__ Zop, int npair, int ZB,
+                                                                   int formB, DevPlan P) {
+  extern __shared__ float2 sm2f[];
+  constexpr int n = 32 * E;
+  const int Hp = P.H_plus, st = n + 1;
+  float2* tw = sm2f + (size_t)ZB * st;  // full table e^{-2 pi i j / n}, j < n
+  const int pr = blockIdx.x, z0 = blockIdx.y * ZB;
+  const int nz = min(ZB, Hp - z0);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const float2 w = P.tw[j & (n / 2 - 1)];
+    tw[j] = j < n / 2 ? w : make_float2(-w.x, -w.y);
+  }
+  // coalesced gather of this pair's rows, 8 independent loads in flight per thread
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (formB) {  // Zhat' [p][pair][zeta]: per p, nz consecutive complex values (one warp per p row)
+    constexpr int U = 8;
+    for (int p0 = warp * U; p0 < n; p0 += nw * U) {
+      for (int z1 = 0; z1 < nz; z1 += 32) {
+        const int z = z1 + lane;
+        float2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (z < nz && p0 + u < n) v[u] = __ldg(Zhat + ((size_t)(p0 + u) * npair + pr) * Hp + z0 + z);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (z < nz && p0 + u < n) sm2f[z * st + p0 + u] = v[u];
+      }
+    }
+  } else {      // Zhat [pair][zeta][q] (explicit pair lists): rows are contiguous
+    for (int idx = threadIdx.x; idx < nz * n; idx += blockDim.x) {
+      const int z = idx / n, q = idx - z * n;
+      sm2f[z * st + q] = Zhat[((size_t)pr * Hp + z0 + z) * n + q];
+    }
+  }
+  // zero the K padding columns [K3, K3p) of this pair's operand image (never leave stale bytes: 0 * NaN)
+  if (blockIdx.y == 0) {
+    const size_t part_bytes0 = (size_t)n * P.K3p * 2;
+    uint8_t* base0 = Zop + (size_t)pr * 2 * part_bytes0;
+    const int npad = P.K3p - P.K3;
+    for (int idx = threadIdx.x; idx < npad * (n / 8) * 2; idx += blockDim.x) {
+      const int part = idx & 1, rest = idx >> 1;
+      const int k = P.K3 + rest % npad, rg = rest / npad;
+      uint8_t* dst = base0 + part * part_bytes0 + (size_t)rg * P.K3p * 16 + (size_t)(k / 8) * 128 + (k % 8) * 16;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+    }
   }
   __syncthreads();
-  smem_fft_rows(sm2t, nz, n, P.log2_psi, tws);
-  float* dst = Z3 + (size_t)pr * P.K3p * n;
-  for (int idx = threadIdx.x; idx < nz * n; idx += blockDim.x) {
-    const int z = idx / n, r = idx - z * n;
-    const int l = P.ell[z0 + z];
-    const int c = P.col[z0 + z];
-    const int j = (l * r) & (n - 1);
-    float2 w = tws[j & (n / 2 - 1)];
-    if (j >= n / 2) w = make_float2(-w.x, -w.y);
-    const float2 v = sm2t[idx];
-    const float re = v.x * w.x - v.y * w.y, im = v.x * w.y + v.y * w.x;
-    dst[(size_t)c * n + r] = re;
-    if (l > 0) dst[(size_t)(c + 1) * n + r] = im;
+  const int d = __brev(lane) >> 27;
+  for (int z = warp; z < nz; z += nw) {
+    float2 x[E];
+#pragma unroll
+    for (int bb = 0; bb < E; ++bb) x[bb] = sm2f[z * st + lane + 32 * bb];
+    dft_regs<E>(x, tw, n);                      // (A)
+#pragma unroll
+    for (int c = 1; c < E; ++c) {               // (B)
+      const float2 w = tw[(lane * c) & (n - 1)];
+      x[c] = make_float2(x[c].x * w.x - x[c].y * w.y, x[c].x * w.y + x[c].y * w.x);
+    }
+#pragma unroll
+    for (int h = 16; h >= 1; h >>= 1) {         // (C) 32-point DIF across lanes
+      const bool lower = (lane & h) != 0;
+      const float2 w = tw[(lane & (h - 1)) * (16 / h) * (n / 32)];
+#pragma unroll
+      for (int c = 0; c < E; ++c) {
+        const float px = __shfl_xor_sync(0xffffffffu, x[c].x, h);
+        const float py = __shfl_xor_sync(0xffffffffu, x[c].y, h);
+        if (!lower) {
+          x[c] = make_float2(x[c].x + px, x[c].y + py);
+        } else {
+          const float ux = px - x[c].x, uy = py - x[c].y;
+          x[c] = make_float2(ux * w.x - uy * w.y, ux * w.y + uy * w.x);
+        }
+      }
+    }
+    // lane holds X[c + E d]; Form-B twiddle e^{-2 pi i ell r / n}; then the Step-3 B operand image:
+    // bf16 hi/lo, MN-major INTERLEAVE canonical layout per pair:
+    //   [part][r/8][K3p/8][k%8][r%8]  (SBO = K3p*16 B between r-groups, 128 B between k-groups)
+    const int l = P.ell[z0 + z], col = P.col[z0 + z];
+    float re[E], im[E];
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      float2 v = x[c];
+      if (formB) {
+        const float2 w = tw[(l * (c + E * d)) & (n - 1)];
+        v = make_float2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+      }
+      re[c] = v.x;
+      im[c] = v.y;
+    }
+    const size_t part_bytes = (size_t)n * P.K3p * 2;
+    uint8_t* base = Zop + (size_t)pr * 2 * part_bytes;
+    const int ncol = l > 0 ? 2 : 1;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      if (cc >= ncol) break;
+      const int k = col + cc;
+      const float* v = cc == 0 ? re : im;
+      uint32_t h[E / 2 > 0 ? E / 2 : 1], lo[E / 2 > 0 ? E / 2 : 1];
+#pragma unroll
+      for (int e = 0; e < E / 2; ++e) split2_bf16(v[2 * e], v[2 * e + 1], h[e], lo[e]);
+      const int r0 = E * d;
+      const size_t off = (size_t)(r0 / 8) * P.K3p * 16 + (size_t)(k / 8) * 128 + (k % 8) * 16 + (r0 % 8) * 2;
+      if constexpr (E >= 8) {
+#pragma unroll
+        for (int u = 0; u < E / 8; ++u) {
+          const size_t o = off + (size_t)u * P.K3p * 16;
+          *reinterpret_cast<uint4*>(base + o) = make_uint4(h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
+          *reinterpret_cast<uint4*>(base + part_bytes + o) =
+              make_uint4(lo[4 * u], lo[4 * u + 1], lo[4 * u + 2], lo[4 * u + 3]);
+        }
+      } else if constexpr (E == 4) {
+        *reinterpret_cast<uint2*>(base + off) = make_uint2(h[0], h[1]);
+        *reinterpret_cast<uint2*>(base + part_bytes + off) = make_uint2(lo[0], lo[1]);
+      } else {
+        *reinterpret_cast<uint32_t*>(base + off) = h[0];
+        *reinterpret_cast<uint32_t*>(base + part_bytes + off) = lo[0];
+      }
+    }
+  }
+}
+
+static int step2_zb(const DevPlan& P) {
+  // terms per CTA: keep the pair slice <= ~100 KB of shared memory so two CTAs share an SM
+  const int per = (P.n_psi + 1) * 8;
+  int zb = (100 * 1024) / per;
+  if (zb < 1) zb = 1;
+  const int chunks = (P.H_plus + zb - 1) / zb;
+  return (P.H_plus + chunks - 1) / chunks;
+}
+
+static void launch_step2_fft(const float2* Zhat, uint8_t* Zop, int npair, int formB, const DevPlan& P,
+                             cudaStream_t s) {
+  const int zb = step2_zb(P);
+  const size_t smem = ((size_t)zb * (P.n_psi + 1) + P.n_psi) * sizeof(float2);
+  dim3 grid(npair, (P.H_plus + zb - 1) / zb);
+  switch (P.n_psi) {
+    case 64: k_step2_fft<2><<<grid, 512, smem, s>>>(Zhat, Zop, npair, zb, formB, P); break;
+    case 128: k_step2_fft<4><<<grid, 512, smem, s>>>(Zhat, Zop, npair, zb, formB, P); break;
+    case 256: k_step2_fft<8><<<grid, 512, smem, s>>>(Zhat, Zop, npair, zb, formB, P); break;
+    case 512: k_step2_fft<16><<<grid, 256, smem, s>>>(Zhat, Zop, npair, zb, formB, P); break;
+    default: k_step2_fft<32><<<grid, 256, smem, s>>>(Zhat, Zop, npair, zb, formB, P); break;
   }
 }
 
 // ---------------------------------------------------------------- single-MMA self-test
 // D = A * B^T with A [128 x 32] (TS: from TMEM; SS: from SMEM), B [N=64 x 32] from SMEM, bf16 inputs.
-__global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const float* B, float* D_ts, float* D_ss) {
+__global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const float* B, float* D_ts, float* D_ss,
+                                                       float* D_mn) {
   __shared__ __align__(1024) uint8_t sa[128 * 32 * 2];
   __shared__ __align__(1024) uint8_t sb[64 * 32 * 2];
+  __shared__ __align__(1024) uint8_t sbm[64 * 32 * 2];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -590,6 +729,8 @@ __global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const fl
     const int nn = idx / K, k = idx % K;
     __nv_bfloat16 v = __float2bfloat16_rn(B[idx]);
     *reinterpret_cast<__nv_bfloat16*>(sb + (nn / 8) * SBO + (k / 8) * 128 + (nn % 8) * 16 + (k % 8) * 2) = v;
+    // MN-major canonical: core (n/8, k/8) at (n/8)*SBO + (k/8)*128, inside: row k%8 (16 B), element n%8
+    *reinterpret_cast<__nv_bfloat16*>(sbm + (nn / 8) * SBO + (k / 8) * 128 + (k % 8) * 16 + (nn % 8) * 2) = v;
   }
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -620,8 +761,10 @@ __global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const fl
     for (int ks = 0; ks < 2; ++ks) {
       const uint64_t bd = smem_desc_kmajor_noswz(smem_u32(sb) + ks * 256, 128, SBO);
       const uint64_t ad = smem_desc_kmajor_noswz(smem_u32(sa) + ks * 256, 128, SBO);
+      const uint64_t bm = smem_desc_kmajor_noswz(smem_u32(sbm) + ks * 256, 128, SBO);
       mma_bf16_ts(tm + 64, tm + ks * 8, bd, idesc, ks > 0);
       mma_bf16_ss(tm + 128, ad, bd, idesc, ks > 0);
+      mma_bf16_ts(tm + 192, tm + ks * 8, bm, idesc_bf16_f32_bmn(128, 64), ks > 0);
     }
     tc_commit(&bar);
   }
@@ -636,6 +779,9 @@ __global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const fl
     tmem_ld16(base + 128 + c0, r16);
     tmem_wait_ld();
     for (int e = 0; e < 16; ++e) D_ss[tid * 64 + c0 + e] = __uint_as_float(r16[e]);
+    tmem_ld16(base + 192 + c0, r16);
+    tmem_wait_ld();
+    for (int e = 0; e < 16; ++e) D_mn[tid * 64 + c0 + e] = __uint_as_float(r16[e]);
   }
   tc_fence_before();
   __syncthreads();
@@ -649,7 +795,7 @@ static float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 int tc_selftest(double* err_ts, double* err_ss, std::string& msg) {
   const int M = 128, N = 64, K = 32;
-  std::vector<float> A(M * K), B(N * K), Dts(M * N), Dss(M * N);
+  std::vector<float> A(M * K), B(N * K), Dts(M * N), Dss(M * N), Dmn(M * N);
   uint32_t s = 12345;
   auto rnd = [&]() {
     s = s * 1664525u + 1013904223u;
@@ -657,15 +803,15 @@ int tc_selftest(double* err_ts, double* err_ss, std::string& msg) {
   };
   for (auto& x : A) x = rnd();
   for (auto& x : B) x = rnd();
-  float *dA, *dB, *dT, *dS;
+  float *dA, *dB, *dT, *dS, *dM;
   if (cudaMalloc(&dA, A.size() * 4) || cudaMalloc(&dB, B.size() * 4) || cudaMalloc(&dT, Dts.size() * 4) ||
-      cudaMalloc(&dS, Dss.size() * 4)) {
+      cudaMalloc(&dS, Dss.size() * 4) || cudaMalloc(&dM, Dmn.size() * 4)) {
     msg = "selftest alloc";
     return FTK_ENOMEM;
   }
   cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
-  k_tc_selftest<<<1, 128>>>(dA, dB, dT, dS);
+  k_tc_selftest<<<1, 128>>>(dA, dB, dT, dS, dM);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     msg = std::string("selftest kernel: ") + cudaGetErrorString(e);
@@ -673,6 +819,8 @@ int tc_selftest(double* err_ts, double* err_ss, std::string& msg) {
   }
   cudaMemcpy(Dts.data(), dT, Dts.size() * 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(Dss.data(), dS, Dss.size() * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(Dmn.data(), dM, Dmn.size() * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dM);
   cudaFree(dA);
   cudaFree(dB);
   cudaFree(dT);
@@ -683,7 +831,7 @@ int tc_selftest(double* err_ts, double* err_ss, std::string& msg) {
       double ref = 0;
       for (int k = 0; k < K; ++k) ref += (double)bf16r(A[m * K + k]) * (double)bf16r(B[nn * K + k]);
       mt = std::max(mt, std::fabs(ref - Dts[m * N + nn]));
-      ms = std::max(ms, std::fabs(ref - Dss[m * N + nn]));
+      ms = std::max(ms, std::max(std::fabs(ref - Dss[m * N + nn]), std::fabs(ref - Dmn[m * N + nn])));
     }
   *err_ts = mt;
   *err_ss = ms;
@@ -742,7 +890,11 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   tc.KCH = (2 * pm.n_k) % 64 == 0 ? 64 : 32;
   tc.NKCH = 2 * pm.n_k / tc.KCH;
   cudaFuncSetAttribute(k_step1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
-  cudaFuncSetAttribute(k_step2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  cudaFuncSetAttribute(k_step2_fft<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_step2_fft<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_step2_fft<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_step2_fft<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_step2_fft<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   tc.ready = true;
   return FTK_OK;
 }
@@ -798,11 +950,11 @@ ftk_status_t tc_block_shape(const TcPlan&, const DevPlan&, int engine, int64_t N
   return FTK_OK;
 }
 
-void launch_step3_tc(const TcPlan& tc, const float* Z3, const PairBlock& pb, const DevPlan& P, int tm_off,
+void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, const DevPlan& P, int tm_off,
                      unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
                      cudaStream_t s) {
   S3Params prm;
-  prm.Z3 = Z3;
+  prm.Zop = Zop;
   prm.Yh = tc.d_Yh;
   prm.Yl = tc.d_Yl;
   prm.pb = pb;
@@ -855,27 +1007,25 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     return FTK_ESTATE;
   }
   float2* Zhat = reinterpret_cast<float2*>(ws);
-  float* Z3 = reinterpret_cast<float*>(Zhat + (size_t)pb.count * P.H_plus * P.n_psi);
+  uint8_t* Zop = reinterpret_cast<uint8_t*>(Zhat + (size_t)pb.count * P.H_plus * P.n_psi);
   if (pb.li) {
-    // explicit pair list (ftk_landscape_pairs): per-pair Steps 1-2 on CUDA cores, Step 3 on tensor cores
+    // explicit pair list (ftk_landscape_pairs): per-pair Step 1 on CUDA cores, then the same FFT
     if (prof) prof(plan, 1, 0, s);
     launch_step1_simt(A, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    launch_step2_simt(Zhat, Z3, pb, P, s);
+    launch_step2_fft(Zhat, Zop, pb.count, 0, P, s);
     if (prof) prof(plan, 2, 1, s);
   } else {
     if (prof) prof(plan, 1, 0, s);
     launch_step1_tc(tc, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    const size_t smem = ((size_t)S2T_ZB * P.n_psi + P.n_psi / 2) * sizeof(float2);
-    dim3 grid(pb.count, (P.H_plus + S2T_ZB - 1) / S2T_ZB);
-    k_step2_tc<<<grid, 256, smem, s>>>(Zhat, Z3, pb.count, P);
+    launch_step2_fft(Zhat, Zop, pb.count, 1, P, s);
     if (prof) prof(plan, 2, 1, s);
   }
   if (prof) prof(plan, 3, 0, s);
-  launch_step3_tc(tc, Z3, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
+  launch_step3_tc(tc, Zop, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
   if (prof) prof(plan, 3, 1, s);
   return FTK_OK;
 }
