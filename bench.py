@@ -281,11 +281,19 @@ def main():
         mhz = (peaks or {}).get("sm_max_mhz", 1965.0)
         peak = 148 * 128 * 2 * mhz * 1e6 / 1e12   # fp32 FMA lanes x 2 flop x clock
         peak_src = "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz"
+    issued = None
+    if engine == pkg.ENGINE_TC and dom == "step3":
+        rows = -(-info["n_rep"] // 128) * 128
+        issued_flops = 3.0 * 2.0 * rows * cfg.n_psi * info["K3p"] * pairs_local * args.steps / max(dom_cnt, 1)
+        issued = issued_flops / avg_launch_s / 1e12 if avg_launch_s > 0 else None
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "tensor_issued_tflops": issued,
                 "frac": (achieved / peak) if achieved else None, "traffic": None, "kernel": dom,
                 "launches": dom_cnt, "avg_launch_ms": avg_launch_s * 1e3, "peak_source": peak_src,
                 "flops_per_launch": flops_per_launch,
-                "note": "algorithmic flops (one real GEMM per term); the bf16x3 split issues 3x these on the tensor pipe"
+                "note": "achieved = algorithmic flops 2*N_t*n_psi*K3 per pair (minimal real Step-3 GEMM) / launch time; "
+                        "tensor_issued_tflops counts the MMAs actually issued (bf16x3 = 3 products, +-delta symmetry "
+                        "halves the rows, tile padding)"
                 if engine == pkg.ENGINE_TC else "algorithmic flops on CUDA cores"}
     launches = sum(v[1] for v in kt_acc.values())
 

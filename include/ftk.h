@@ -91,6 +91,8 @@ typedef struct {
   double certificate;        /* max |F - F^SVD| over (sampled shifts) x (k_m) x (psi_p) */
   int64_t n_images, n_templates_total, n_templates_local, template_offset;
   int engine, device, rank, world;
+  int K3p;                   /* device Step-3 width (K3 + block padding; multiple of 16 for engine 0) */
+  int n_rep;                 /* engine 0: representative shifts (+-delta pairs share one row of Step 3) */
 } ftk_plan_info_t;
 
 /* Build the plan (host, double precision, untimed per P:1321): radial rule, per-ell operator SVD of

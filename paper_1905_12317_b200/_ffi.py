@@ -20,7 +20,8 @@ class PlanInfo(C.Structure):
                 ("K_cycles", C.c_double), ("k_max", C.c_double), ("delta_max", C.c_double), ("W", C.c_double),
                 ("eps", C.c_double), ("certificate", C.c_double), ("n_images", C.c_int64),
                 ("n_templates_total", C.c_int64), ("n_templates_local", C.c_int64), ("template_offset", C.c_int64),
-                ("engine", C.c_int), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int)]
+                ("engine", C.c_int), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
+                ("K3p", C.c_int), ("n_rep", C.c_int)]
 
 
 class Best(C.Structure):

@@ -27,7 +27,9 @@ struct ftk_plan_s {
   int* d_col = nullptr;
   float* d_Y3 = nullptr;
   float2* d_tw = nullptr;
-  int K3p = 0, log2_psi = 0;
+  int K3p = 0, K3dev = 0, Ke = 0, log2_psi = 0;
+  int* d_pads = nullptr;
+  int npads = 0;
   TcPlan tc;  // tensor-core engine constants (ftk_tc.cu)
   // data
   float2* d_A = nullptr;
@@ -76,7 +78,10 @@ DevPlan devplan(ftk_plan_t p) {
   d.log2_psi = p->log2_psi;
   d.N_t = p->pm.N_t;
   d.H_plus = p->pm.H_plus;
-  d.K3 = p->pm.K3;
+  d.K3 = p->K3dev;
+  d.Ke = p->Ke;
+  d.npads = p->npads;
+  d.pads = p->d_pads;
   d.K3p = p->K3p;
   int lm = 0;
   for (const auto& t : p->pm.terms)
@@ -185,7 +190,18 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
   }
   plan->log2_psi = 0;
   while ((1 << plan->log2_psi) < np) plan->log2_psi++;
-  plan->K3p = plan->engine == 0 ? (pm.K3 + 15) / 16 * 16 : (pm.K3 + 7) / 8 * 8;
+  // Step-3 column blocks (see the column map below): even-ell block [0, Ke), odd-ell block [Ke, K3p)
+  {
+    int n_even = 0, n_odd = 0;
+    for (const auto& tm : pm.terms) {
+      if (tm.ell > 0 && (tm.ell % 2) == 0) ++n_even;
+      if (tm.ell > 0 && (tm.ell % 2) == 1) ++n_odd;
+    }
+    const int ce = pm.H0 + ((pm.H0 & 1) && n_even > 0 ? 1 : 0) + 2 * n_even;
+    plan->Ke = (ce + 15) / 16 * 16;
+    plan->K3p = plan->Ke + (2 * n_odd + 15) / 16 * 16;
+    plan->K3dev = plan->K3p;
+  }
   if (plan->device < 0) {
     *out = plan;
     return FTK_OK;
@@ -199,14 +215,31 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
   // ---- device constants: ell >= 0 terms in zeta order
   std::vector<float> g, Y3((size_t)N_t * plan->K3p, 0.f);
   std::vector<int> ell, col;
+  // device term order: ell = 0 terms, then even ell > 0, then odd ell (each in zeta order).  Step-3
+  // columns: one per ell = 0 term; (Re, Im) pairs of the even ell > 0 terms on even columns; the odd-ell
+  // pairs from column Ke (a multiple of 16).  Every group of 8 columns holds whole terms (Step 2 writes
+  // column groups) and Y_zeta(-delta) = (-1)^ell Y_zeta(delta) splits X(+-delta) = E(delta) +- O(delta)
+  // between the two blocks (the tensor-core Step 3 evaluates half of a symmetric shift list).
   std::vector<int> zplus;
-  for (int z = 0; z < pm.H; ++z)
-    if (pm.terms[z].ell >= 0) zplus.push_back(z);
+  for (int pass = 0; pass < 3; ++pass)
+    for (int z = 0; z < pm.H; ++z) {
+      const int l = pm.terms[z].ell;
+      if ((pass == 0 && l == 0) || (pass == 1 && l > 0 && l % 2 == 0) || (pass == 2 && l % 2 == 1)) zplus.push_back(z);
+    }
+  std::vector<char> used(plan->K3p, 0);
   int c = 0;
+  bool odd_started = false;
   for (int z : zplus) {
     const int l = pm.terms[z].ell;
+    if (l % 2 == 1 && !odd_started) {
+      c = plan->Ke;
+      odd_started = true;
+    }
+    if (l > 0 && (c & 1)) c += 1;  // pairs on even columns
     ell.push_back(l);
     col.push_back(c);
+    used[c] = 1;
+    if (l > 0) used[c + 1] = 1;
     for (int m = 0; m < pm.n_k; ++m) g.push_back((float)(2.0 * M_PI * pm.w[m] * pm.G[(size_t)z * pm.n_k + m]));
     for (int t = 0; t < N_t; ++t) {
       const std::complex<double> y = pm.Y[(size_t)t * pm.H + z];
@@ -219,6 +252,10 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
     }
     c += (l == 0) ? 1 : 2;
   }
+  std::vector<int> pads;
+  for (int k = 0; k < plan->K3p; ++k)
+    if (!used[k]) pads.push_back(k);
+  plan->npads = (int)pads.size();
   std::vector<float2> tw(np / 2);
   for (int j = 0; j < np / 2; ++j) {
     const double ph = -2.0 * M_PI * j / np;
@@ -228,11 +265,12 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
   if ((s = upload(plan, &plan->d_g, g)) != FTK_OK) return bail(s);
   if ((s = upload(plan, &plan->d_ell, ell)) != FTK_OK) return bail(s);
   if ((s = upload(plan, &plan->d_col, col)) != FTK_OK) return bail(s);
+  if ((s = upload(plan, &plan->d_pads, pads)) != FTK_OK) return bail(s);
   if ((s = upload(plan, &plan->d_Y3, Y3)) != FTK_OK) return bail(s);
   if ((s = upload(plan, &plan->d_tw, tw)) != FTK_OK) return bail(s);
   if (plan->engine == 0) {
     std::string msg;
-    int ts = tc_plan_init(plan->tc, pm, g, ell, Y3, plan->K3p, msg);
+    int ts = tc_plan_init(plan->tc, pm, g, ell, col, Y3, plan->K3p, plan->Ke, msg);
     if (ts != FTK_OK) {
       plan->err = msg;
       fprintf(stderr, "ftk_plan_create: %s\n", msg.c_str());
@@ -250,6 +288,7 @@ void ftk_plan_destroy(ftk_plan_t plan) {
     cudaFree(plan->d_g);
     cudaFree(plan->d_ell);
     cudaFree(plan->d_col);
+    cudaFree(plan->d_pads);
     cudaFree(plan->d_Y3);
     cudaFree(plan->d_tw);
     cudaFree(plan->d_A);
@@ -295,6 +334,8 @@ ftk_status_t ftk_plan_query(ftk_plan_t plan, ftk_plan_info_t* info) {
   info->device = plan->device;
   info->rank = plan->rank;
   info->world = plan->world;
+  info->K3p = plan->K3p;
+  info->n_rep = plan->engine == 0 ? plan->tc.n_rep : plan->pm.N_t;
   return FTK_OK;
 }
 

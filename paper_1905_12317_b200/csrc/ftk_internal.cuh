@@ -67,7 +67,10 @@ __host__ __device__ inline bool best_better(const ftk_best_t& a, const ftk_best_
 // Device plan constants used by every engine.
 struct DevPlan {
   int n_k, n_psi, log2_psi, N_t, H_plus, K3, K3p, ell_max;
-  const float* g;        // [H_plus][n_k]   2 pi w_m G_zeta(k_m), ell >= 0 terms in zeta order
+  int Ke;                // even-ell column block [0, Ke); odd-ell block [Ke, K3p)
+  int npads;             // unused (zero) Step-3 columns
+  const int* pads;       // [npads]
+  const float* g;        // [H_plus][n_k]   2 pi w_m G_zeta(k_m), ell >= 0 terms (ell = 0 block first)
   const int* ell;        // [H_plus]
   const int* col;        // [H_plus] first Step-3 column of the term
   const float* Y3;       // [N_t][K3p]       Step-3 real operand (reading R13), zero-padded

@@ -136,8 +136,10 @@ __global__ void __launch_bounds__(256) k_step2_simt(const float2* __restrict__ Z
   __syncthreads();
   smem_fft_rows(sm2, nz, n, P.log2_psi, tws);
   float* dst = Z3 + (int64_t)p * P.K3p * n;
-  if (blockIdx.y == 0)  // zero the K padding rows (the region's offset moves with the block size)
-    for (int idx = threadIdx.x; idx < (P.K3p - P.K3) * n; idx += blockDim.x) dst[(int64_t)P.K3 * n + idx] = 0.f;
+  if (blockIdx.y == 0) {  // zero the K padding rows (the region's offset moves with the block size)
+    for (int idx = threadIdx.x; idx < P.npads * n; idx += blockDim.x)
+      dst[(int64_t)P.pads[idx / n] * n + idx % n] = 0.f;
+  }
   for (int idx = threadIdx.x; idx < nz * n; idx += blockDim.x) {
     const int z = idx / n, r = idx - z * n;
     const int c = P.col[z0 + z];

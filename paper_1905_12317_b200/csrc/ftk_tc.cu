@@ -5,16 +5,19 @@
 // Every operand x is split x = hi + lo in bf16 and the product is hi*hi + hi*lo + lo*hi with fp32
 // accumulation in TMEM (measured <= 6e-6 ||A|| ||B|| vs the 1e-4 budget).
 //
-// Kernel k_step3_tc (one CTA per SM, persistent over a contiguous range of pairs):
+// Kernel k_step3_tc (one CTA per SM, persistent over a contiguous range of pairs).  Shifts are taken in
+// +-delta pairs: Y_zeta(-delta) = (-1)^ell Y_zeta(delta), so with the columns split by the parity of ell
+// (even block [0, Ke), odd block [Ke, K3p)) X(+delta) = E + O and X(-delta) = E - O, where
+// E = Y_even Z_even and O = Y_odd Z_odd are accumulated separately: half the rows, same K.
 //   * Z producer (warp 0, one lane): per pair, bulk-copies (cp.async.bulk) the pair's operand image
 //     written by Step 2 -- bf16 hi/lo, MN-major SWIZZLE_NONE canonical layout -- into SMEM, chunk by
-//     chunk of 128 r (z_full[rc] / z_empty[rc] mbarriers) -> the B operand (N = r).
-//   * Y loaders (warps 8-11): per 128-row t-tile, Y3 hi/lo rows -> TMEM via tcgen05.st -> the A
-//     operand (M = t), double-buffered (y_full / y_empty).
-//   * MMA issuer (warp 12, one lane): per (t-tile, r-chunk) 3 x K3p/16 tcgen05.mma (M128 N<=128 K16,
-//     A from TMEM, B from SMEM) into one of two TMEM accumulators (acc_full / acc_empty).
-//   * Epilogue (warps 4-7): tcgen05.ld the accumulator, running max/argmax per row, per-pair
-//     reduction, one packed-key atomicMax per pair (image key and optional pair key).
+//     chunk of 64 r (z_full[rc] / z_empty[rc] mbarriers) -> the B operand (N = r).
+//   * MMA issuer (warp 1, one lane): per (t-tile, r-chunk) 3 x K3p/16 tcgen05.mma (M128 N64 K16, A = Y
+//     tile from TMEM, B from SMEM) into the E and O accumulators of one of two TMEM buffers.
+//   * Epilogue (warps 2-9, two per TMEM lane quarter): tcgen05.ld E and O, X = E +- O, running
+//     max/argmax per row, per-pair reduction, one packed-key atomicMax per pair.
+//   * Y loaders (warps 10-13): per 128-row tile of representative shifts, Y hi/lo rows -> TMEM via
+//     tcgen05.st -> the A operand (M = t), double-buffered (y_full / y_empty).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -27,16 +30,18 @@
 namespace ftk {
 using namespace sm100;
 
-constexpr int S3_THREADS = 13 * 32;
-constexpr int S3_MAX_RC = 8;  // n_psi / 128 <= 8
+constexpr int S3_THREADS = 14 * 32;
+constexpr int S3_MAX_RC = 16;  // n_psi / 64 <= 16
 
 struct S3Params {
   const uint8_t* Zop;     // per pair: bf16 hi/lo MN-major operand image (see k_step2_fft)
   const uint32_t* Yh;     // [T*128][K3p/2]
   const uint32_t* Yl;
   PairBlock pb;
-  int n, K3p, N_t, T, NC, RC;
+  int n, K3p, Ke, N_t, T, NC, RC;
   int tm_off, n_tm_local;
+  const int* rep_t;       // [T*128] shift index of representative row (-1: padding row)
+  const int* partner;     // [T*128] shift index of -delta (-1: none)
   unsigned long long* img_keys;
   unsigned long long* pair_keys;
   float* land;
@@ -47,8 +52,8 @@ struct S3Smem {
   uint64_t y_full[2], y_empty[2];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
-  float red_v[4];
-  uint32_t red_f[4];
+  float red_v[8];
+  uint32_t red_f[8];
 };
 
 __device__ __forceinline__ bool better(float v, uint32_t f, float bv, uint32_t bf) {
@@ -72,11 +77,11 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
       mbar_init(&S.y_full[i], 128);
       mbar_init(&S.y_empty[i], 1);
       mbar_init(&S.acc_full[i], 1);
-      mbar_init(&S.acc_empty[i], 128);
+      mbar_init(&S.acc_empty[i], 256);
     }
     fence_barrier_init();
   }
-  if (warp == 12) tmem_alloc<512>(&S.tmem_base);
+  if (warp == 1) tmem_alloc<512>(&S.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -87,9 +92,9 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   const int p_begin = blockIdx.x * per;
   const int p_end = min(count, p_begin + per);
 
-  if (warp < 4) {
+  if (warp == 0) {
     // ---------------- Z producer: the pair's operand image chunk by chunk (hi and lo) via bulk copies
-    if (warp == 0 && lane == 0) {
+    if (lane == 0) {
       const uint32_t chunk_bytes = (uint32_t)(NC / 8) * SBO;
       int it = 0;
       for (int p = p_begin; p < p_end; ++p, ++it) {
@@ -104,51 +109,92 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
       }
     }
     __syncwarp();
-  } else if (warp < 8) {
-    // ---------------- epilogue
+  } else if (warp >= 2 && warp < 10) {
+    // ---------------- epilogue (8 warps: two per TMEM lane quarter, each half of the chunk's columns):
+    // X(+delta) = E + O on the representative row, X(-delta) = E - O on its partner
     const int q = warp & 3;
     const int row = q * 32 + lane;
+    const int half = (warp - 2) >> 2;  // 0 or 1
+    const bool has_odd = P.Ke < K3p;
     int it = 0;
     uint32_t g_acc = 0;
     for (int p = p_begin; p < p_end; ++p, ++it) {
       float bv = -INFINITY;
       uint32_t bf = 0xffffffffu;
       for (int tt = 0; tt < T; ++tt) {
-        const int t = tt * 128 + row;
+        const int tp = __ldg(P.rep_t + tt * 128 + row);
+        const int tm = __ldg(P.partner + tt * 128 + row);
         for (int rc = 0; rc < RC; ++rc, ++g_acc) {
           const int ab = g_acc & 1;
           mbar_wait(&S.acc_full[ab], (g_acc >> 1) & 1);
           tc_fence_after();
-          const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * 128);
-          for (int c0 = 0; c0 < NC; c0 += 64) {
-            uint32_t r[4][16];
+          const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * 2 * NC);
+          for (int c0 = half * (NC / 2); c0 < (half + 1) * (NC / 2); c0 += 32) {
+            uint32_t e[2][16], o[2][16];
 #pragma unroll
-            for (int h = 0; h < 4; ++h)
-              if (c0 + 16 * h < NC) tmem_ld16(base + c0 + 16 * h, r[h]);
+            for (int h = 0; h < 2; ++h) {
+              tmem_ld16(base + c0 + 16 * h, e[h]);
+              if (has_odd) tmem_ld16(base + NC + c0 + 16 * h, o[h]);
+            }
             tmem_wait_ld();
-            if (t < P.N_t) {
+            if (!has_odd) {
 #pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                if (c0 + 16 * h >= NC) break;
-                // max first (1 FMNMX per value); locate the column only when the running best improves
-                float m = __uint_as_float(r[h][0]);
+              for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int e = 1; e < 16; ++e) m = fmaxf(m, __uint_as_float(r[h][e]));
-                if (m > bv) {
-                  int e0 = 0;
+                for (int k = 0; k < 16; ++k) o[h][k] = 0u;
+            }
+            if (tp >= 0) {
 #pragma unroll
-                  for (int e = 15; e >= 0; --e)
-                    if (__uint_as_float(r[h][e]) == m) e0 = e;
-                  bv = m;
-                  bf = (uint32_t)t * (uint32_t)n + (uint32_t)(rc * NC + c0 + 16 * h + e0);
+              for (int h = 0; h < 2; ++h) {
+                const int r0 = rc * NC + c0 + 16 * h;
+                float xp[16], xm[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                  const float ev = __uint_as_float(e[h][k]), ov = __uint_as_float(o[h][k]);
+                  xp[k] = ev + ov;
+                  xm[k] = ev - ov;
+                }
+                // max first; locate the column only when the running best can change (ties -> smaller flat)
+                float mp = xp[0];
+#pragma unroll
+                for (int k = 1; k < 16; ++k) mp = fmaxf(mp, xp[k]);
+                const uint32_t fp0 = (uint32_t)tp * (uint32_t)n + (uint32_t)r0;
+                if (mp > bv || (mp == bv && fp0 < bf)) {
+                  int k0 = 0;
+#pragma unroll
+                  for (int k = 15; k >= 0; --k)
+                    if (xp[k] == mp) k0 = k;
+                  if (better(mp, fp0 + k0, bv, bf)) {
+                    bv = mp;
+                    bf = fp0 + k0;
+                  }
+                }
+                if (tm >= 0) {
+                  float mm = xm[0];
+#pragma unroll
+                  for (int k = 1; k < 16; ++k) mm = fmaxf(mm, xm[k]);
+                  const uint32_t fm0 = (uint32_t)tm * (uint32_t)n + (uint32_t)r0;
+                  if (mm > bv || (mm == bv && fm0 < bf)) {
+                    int k0 = 0;
+#pragma unroll
+                    for (int k = 15; k >= 0; --k)
+                      if (xm[k] == mm) k0 = k;
+                    if (better(mm, fm0 + k0, bv, bf)) {
+                      bv = mm;
+                      bf = fm0 + k0;
+                    }
+                  }
                 }
                 if (P.land) {
-                  float4* dst =
-                      reinterpret_cast<float4*>(P.land + ((size_t)p * P.N_t + t) * n + rc * NC + c0 + 16 * h);
+                  float4* dp = reinterpret_cast<float4*>(P.land + ((size_t)p * P.N_t + tp) * n + r0);
 #pragma unroll
-                  for (int e = 0; e < 4; ++e)
-                    dst[e] = make_float4(__uint_as_float(r[h][4 * e]), __uint_as_float(r[h][4 * e + 1]),
-                                         __uint_as_float(r[h][4 * e + 2]), __uint_as_float(r[h][4 * e + 3]));
+                  for (int k = 0; k < 4; ++k) dp[k] = make_float4(xp[4 * k], xp[4 * k + 1], xp[4 * k + 2], xp[4 * k + 3]);
+                  if (tm >= 0) {
+                    float4* dm = reinterpret_cast<float4*>(P.land + ((size_t)p * P.N_t + tm) * n + r0);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                      dm[k] = make_float4(xm[4 * k], xm[4 * k + 1], xm[4 * k + 2], xm[4 * k + 3]);
+                  }
                 }
               }
             }
@@ -168,14 +214,14 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         }
       }
       if (lane == 0) {
-        S.red_v[q] = bv;
-        S.red_f[q] = bf;
+        S.red_v[warp - 2] = bv;
+        S.red_f[warp - 2] = bf;
       }
-      named_bar(1, 128);
-      if (warp == 4 && lane == 0) {
+      named_bar(1, 256);
+      if (warp == 2 && lane == 0) {
         float v = S.red_v[0];
         uint32_t f = S.red_f[0];
-        for (int k = 1; k < 4; ++k)
+        for (int k = 1; k < 8; ++k)
           if (better(S.red_v[k], S.red_f[k], v, f)) {
             v = S.red_v[k];
             f = S.red_f[k];
@@ -190,9 +236,9 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           if (P.pair_keys) atomicMax(&P.pair_keys[(size_t)i * P.n_tm_local + j], key);
         }
       }
-      named_bar(1, 128);
+      named_bar(1, 256);
     }
-  } else if (warp < 12) {
+  } else if (warp >= 10) {
     // ---------------- Y loaders: Y tile (128 t-rows x K3p) hi/lo -> TMEM columns 256 + ybuf*K3p
     const int q = warp & 3;
     const int row = q * 32 + lane;
@@ -220,12 +266,12 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         mbar_arrive(&S.y_full[yb]);
       }
     }
-  } else {
-    // ---------------- MMA issuer (warp 12, lane 0)
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (warp 1, lane 0)
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32_bmn(128, NC);  // B (Z) is MN-major
+      const uint32_t idesc = idesc_bf16_f32_bmn(128, NC);  // B (Z) is MN-major; N = NC = 64
       const uint32_t zbase = smem_u32(zs);
-      const int ksteps = K3p / 16;
+      const int ksteps = K3p / 16, ke_steps = P.Ke / 16;
       const int halfk = K3p / 2;
       int it = 0;
       uint32_t g_t = 0, g_acc = 0;
@@ -237,18 +283,20 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           const uint32_t a_hi0 = tmem + 256 + (uint32_t)(yb * K3p);
           for (int rc = 0; rc < RC; ++rc, ++g_acc) {
             const int ab = g_acc & 1;
-            if (tt == 0) {
-              mbar_wait(&S.z_full[rc], it & 1);
-            }
+            if (tt == 0) mbar_wait(&S.z_full[rc], it & 1);
             mbar_wait(&S.acc_empty[ab], ((g_acc >> 1) & 1) ^ 1);
             tc_fence_after();
-            const uint32_t d = tmem + (uint32_t)(ab * 128);
+            const uint32_t dE = tmem + (uint32_t)(ab * 2 * NC), dO = dE + (uint32_t)NC;
             const uint32_t bchunk = zbase + (uint32_t)(rc * (NC / 8)) * SBO;
+            const uint64_t bh0 = smem_desc_kmajor_noswz(bchunk, 128, SBO);
+            const uint64_t bl0 = smem_desc_kmajor_noswz(bchunk + part_bytes, 128, SBO);
             for (int ks = 0; ks < ksteps; ++ks) {
+              const bool odd = ks >= ke_steps;
+              const uint32_t d = odd ? dO : dE;
+              const uint32_t acc0 = (odd ? ks > ke_steps : ks > 0) ? 1u : 0u;
               const uint32_t a_hi = a_hi0 + ks * 8, a_lo = a_hi + halfk;
-              const uint64_t b_hi = smem_desc_kmajor_noswz(bchunk + ks * 256, 128, SBO);
-              const uint64_t b_lo = smem_desc_kmajor_noswz(bchunk + part_bytes + ks * 256, 128, SBO);
-              mma_bf16_ts(d, a_hi, b_hi, idesc, ks > 0 ? 1u : 0u);
+              const uint64_t b_hi = bh0 + (uint64_t)(ks * 16), b_lo = bl0 + (uint64_t)(ks * 16);  // +256 B
+              mma_bf16_ts(d, a_hi, b_hi, idesc, acc0);
               mma_bf16_ts(d, a_hi, b_lo, idesc, 1u);
               mma_bf16_ts(d, a_lo, b_hi, idesc, 1u);
             }
@@ -263,7 +311,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 12) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -527,183 +575,237 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 
 // Step 2 for the tensor-core engine (Eq. fbk3 Step 2, Form B):
 //   Z_zeta(r) = e^{-2 pi i ell r / n} sum_p Zhat'_zeta(p) e^{-2 pi i p r / n},   (q = p + ell)
-// read from Zhat' [p][pair][zeta]; written as the Step-3 B-operand image (real rows of reading R13).
+// read from Zhat' [p][pair][zeta]; written as the Step-3 B-operand image (real rows of reading R13):
+// bf16 hi/lo, MN-major INTERLEAVE canonical layout per pair, [part][r/8][K3p/8][k%8][r%8].
+// One CTA = (pair, chunk of whole 8-column groups); one warp per term row.
 // FFT: four-step decomposition n = 32 E, p = a + 32 b (a = lane), r = c + E d:
 //   (A) per lane an E-point DFT over b in registers, (B) twiddle w_n^{a c}, (C) a 32-point radix-2
 //   DIF across the warp with shfl_xor (output index d lands on lane bitrev5(d)).
+// Output core rows are staged in shared memory (16-byte slot XOR-swizzled by the r-group) and written
+// out as contiguous 128-byte core matrices.
+struct S2Chunks {
+  int n;
+  int zs[32], ze[32], g0[32];
+};
+
+__device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 tw_full(const float2* tw, int j, int n) {  // e^{-2 pi i j / n}, 0 <= j < n
+  const float2 w = __ldg(tw + (j & (n / 2 - 1)));
+  return j < n / 2 ? w : make_float2(-w.x, -w.y);
+}
+
 template <int E>
 __device__ __forceinline__ void dft_regs(float2 (&x)[E], const float2* tw, int n) {
-  // radix-2 DIT on bit-reversed register order -> natural-order output; w_E^j = tw[j n / E]
-  float2 y[E];
-  constexpr int LOG = (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
-#pragma unroll
-  for (int i = 0; i < E; ++i) {
+  // radix-2 DIT; x is addressed in bit-reversed order through rv() (a compile-time renaming), so the
+  // natural-order result ends up in x[rv(c)].  w_E^j = tw[j n / E] (warp-uniform loads).
+  constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
+  auto rv = [](int i) {
     int r = 0;
 #pragma unroll
     for (int bb = 0; bb < LOG; ++bb) r |= ((i >> bb) & 1) << (LOG - 1 - bb);
-    y[i] = x[r];
-  }
+    return r;
+  };
 #pragma unroll
   for (int s = 1; s < E; s *= 2) {
 #pragma unroll
     for (int blk = 0; blk < E; blk += 2 * s) {
 #pragma unroll
       for (int j = 0; j < s; ++j) {
-        const float2 w = tw[j * (n / (2 * s))];
-        const float2 u = y[blk + j], v0 = y[blk + j + s];
-        const float2 v = make_float2(v0.x * w.x - v0.y * w.y, v0.x * w.y + v0.y * w.x);
-        y[blk + j] = make_float2(u.x + v.x, u.y + v.y);
-        y[blk + j + s] = make_float2(u.x - v.x, u.y - v.y);
+        const float2 w = __ldg(tw + j * (n / (2 * s)));
+        const float2 u = x[rv(blk + j)], v = cmulf(x[rv(blk + j + s)], w);
+        x[rv(blk + j)] = make_float2(u.x + v.x, u.y + v.y);
+        x[rv(blk + j + s)] = make_float2(u.x - v.x, u.y - v.y);
       }
     }
   }
-#pragma unroll
-  for (int i = 0; i < E; ++i) x[i] = y[i];
 }
 
+__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Persistent CTAs over work items (pair, column group) with the group fastest; the rows of the next
+// item are gathered with cp.async into the second buffer while the current item is transformed.
 template <int E>
-__global__ void __launch_bounds__(E >= 16 ? 256 : 512) k_step2_fft(const float2* __restrict__ Zhat,
-                                                                   uint8_t* __restrict__ Zop, int npair, int ZB,
-                                                                   int formB, DevPlan P) {
-  extern __shared__ float2 sm2f[];
-  constexpr int n = 32 * E;
-  const int Hp = P.H_plus, st = n + 1;
-  float2* tw = sm2f + (size_t)ZB * st;  // full table e^{-2 pi i j / n}, j < n
-  const int pr = blockIdx.x, z0 = blockIdx.y * ZB;
-  const int nz = min(ZB, Hp - z0);
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    const float2 w = P.tw[j & (n / 2 - 1)];
-    tw[j] = j < n / 2 ? w : make_float2(-w.x, -w.y);
-  }
-  // coalesced gather of this pair's rows, 8 independent loads in flight per thread
+__global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
+                                                      int npair, int formB, DevPlan P, S2Chunks C, int maxz) {
+  extern __shared__ __align__(16) uint8_t s2raw[];
+  constexpr int n = 32 * E, st = n + 1;
+  constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
+  const int Hp = P.H_plus;
+  const size_t rows_bytes = ((size_t)maxz * st * sizeof(float2) + 127) & ~(size_t)127;
+  auto rowbuf = [&](int b) { return reinterpret_cast<float2*>(s2raw + (size_t)b * rows_bytes); };
+  uint8_t* stg = s2raw + 2 * rows_bytes;  // [2][n/8][128 B] (one 8-column group)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (formB) {  // Zhat' [p][pair][zeta]: per p, nz consecutive complex values (one warp per p row)
-    constexpr int U = 8;
-    for (int p0 = warp * U; p0 < n; p0 += nw * U) {
-      for (int z1 = 0; z1 < nz; z1 += 32) {
-        const int z = z1 + lane;
-        float2 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (z < nz && p0 + u < n) v[u] = __ldg(Zhat + ((size_t)(p0 + u) * npair + pr) * Hp + z0 + z);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (z < nz && p0 + u < n) sm2f[z * st + p0 + u] = v[u];
+  const int total = npair * C.n;
+
+  auto issue = [&](int item, float2* rows) {
+    const int ch = item % C.n, pr = item / C.n;
+    const int zs = C.zs[ch], nz = C.ze[ch] - zs;
+    if (formB) {  // Zhat' [p][pair][zeta]: lanes = 4 p-rows x 8 consecutive zeta
+      const int zl = lane & 7, pl = lane >> 3;
+      if (zl < nz)
+        for (int p = warp * 4 + pl; p < n; p += nw * 4)
+          cp_async8(rows + zl * st + p, Zhat + ((size_t)p * npair + pr) * Hp + zs + zl);
+    } else {      // Zhat [pair][zeta][q]
+      for (int idx = threadIdx.x; idx < nz * n; idx += blockDim.x) {
+        const int z = idx / n, q = idx - z * n;
+        cp_async8(rows + z * st + q, Zhat + ((size_t)pr * Hp + zs + z) * n + q);
       }
     }
-  } else {      // Zhat [pair][zeta][q] (explicit pair lists): rows are contiguous
-    for (int idx = threadIdx.x; idx < nz * n; idx += blockDim.x) {
-      const int z = idx / n, q = idx - z * n;
-      sm2f[z * st + q] = Zhat[((size_t)pr * Hp + z0 + z) * n + q];
-    }
+    cp_async_commit();
+  };
+
+  // per-lane constant twiddles
+  float2 wc[5];
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int h = 16 >> s;
+    wc[s] = tw_full(P.tw, (lane & (h - 1)) * (16 / h) * (n / 32), n);
   }
-  // zero the K padding columns [K3, K3p) of this pair's operand image (never leave stale bytes: 0 * NaN)
-  if (blockIdx.y == 0) {
-    const size_t part_bytes0 = (size_t)n * P.K3p * 2;
-    uint8_t* base0 = Zop + (size_t)pr * 2 * part_bytes0;
-    const int npad = P.K3p - P.K3;
-    for (int idx = threadIdx.x; idx < npad * (n / 8) * 2; idx += blockDim.x) {
-      const int part = idx & 1, rest = idx >> 1;
-      const int k = P.K3 + rest % npad, rg = rest / npad;
-      uint8_t* dst = base0 + part * part_bytes0 + (size_t)rg * P.K3p * 16 + (size_t)(k / 8) * 128 + (k % 8) * 16;
-      *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
-    }
-  }
-  __syncthreads();
+  const float2 wlane = tw_full(P.tw, lane & (n - 1), n);
   const int d = __brev(lane) >> 27;
-  for (int z = warp; z < nz; z += nw) {
-    float2 x[E];
+  auto rv = [](int i) {
+    int r = 0;
 #pragma unroll
-    for (int bb = 0; bb < E; ++bb) x[bb] = sm2f[z * st + lane + 32 * bb];
-    dft_regs<E>(x, tw, n);                      // (A)
-#pragma unroll
-    for (int c = 1; c < E; ++c) {               // (B)
-      const float2 w = tw[(lane * c) & (n - 1)];
-      x[c] = make_float2(x[c].x * w.x - x[c].y * w.y, x[c].x * w.y + x[c].y * w.x);
+    for (int bb = 0; bb < LOG; ++bb) r |= ((i >> bb) & 1) << (LOG - 1 - bb);
+    return r;
+  };
+
+  int item = blockIdx.x;
+  if (item < total) issue(item, rowbuf(0));
+  for (int k = 0; item < total; item += gridDim.x, ++k) {
+    const int next = item + gridDim.x;
+    if (next < total) {
+      issue(next, rowbuf((k + 1) & 1));
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
+    // clear the staged group (padding columns must stay zero)
+    for (int idx = threadIdx.x; idx < 2 * (n / 8) * 8; idx += blockDim.x)
+      reinterpret_cast<uint4*>(stg)[idx] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    const float2* rows = rowbuf(k & 1);
+    const int ch = item % C.n, pr = item / C.n;
+    const int zs = C.zs[ch], nz = C.ze[ch] - zs, g0 = C.g0[ch];
+    for (int z = warp; z < nz; z += nw) {
+      float2 x[E];
 #pragma unroll
-    for (int h = 16; h >= 1; h >>= 1) {         // (C) 32-point DIF across lanes
-      const bool lower = (lane & h) != 0;
-      const float2 w = tw[(lane & (h - 1)) * (16 / h) * (n / 32)];
+      for (int bb = 0; bb < E; ++bb) x[bb] = rows[z * st + lane + 32 * bb];
+      dft_regs<E>(x, P.tw, n);  // (A): natural-order result in x[rv(c)]
+      {                         // (B) x_c *= w_n^{lane c} by recurrence
+        float2 acc = wlane;
 #pragma unroll
-      for (int c = 0; c < E; ++c) {
-        const float px = __shfl_xor_sync(0xffffffffu, x[c].x, h);
-        const float py = __shfl_xor_sync(0xffffffffu, x[c].y, h);
-        if (!lower) {
-          x[c] = make_float2(x[c].x + px, x[c].y + py);
-        } else {
-          const float ux = px - x[c].x, uy = py - x[c].y;
-          x[c] = make_float2(ux * w.x - uy * w.y, ux * w.y + uy * w.x);
+        for (int c = 1; c < E; ++c) {
+          x[rv(c)] = cmulf(x[rv(c)], acc);
+          acc = cmulf(acc, wlane);
         }
       }
-    }
-    // lane holds X[c + E d]; Form-B twiddle e^{-2 pi i ell r / n}; then the Step-3 B operand image:
-    // bf16 hi/lo, MN-major INTERLEAVE canonical layout per pair:
-    //   [part][r/8][K3p/8][k%8][r%8]  (SBO = K3p*16 B between r-groups, 128 B between k-groups)
-    const int l = P.ell[z0 + z], col = P.col[z0 + z];
-    float re[E], im[E];
 #pragma unroll
-    for (int c = 0; c < E; ++c) {
-      float2 v = x[c];
+      for (int s = 0; s < 5; ++s) {  // (C) 32-point DIF across lanes
+        const int h = 16 >> s;
+        const bool lower = (lane & h) != 0;
+#pragma unroll
+        for (int c = 0; c < E; ++c) {
+          const float px = __shfl_xor_sync(0xffffffffu, x[c].x, h);
+          const float py = __shfl_xor_sync(0xffffffffu, x[c].y, h);
+          if (!lower) {
+            x[c] = make_float2(x[c].x + px, x[c].y + py);
+          } else {
+            x[c] = cmulf(make_float2(px - x[c].x, py - x[c].y), wc[s]);
+          }
+        }
+      }
+      // lane holds X[c + E d] in x[rv(c)]; Form-B twiddle e^{-2 pi i ell (c + E d) / n}
+      const int l = P.ell[zs + z], col = P.col[zs + z];
       if (formB) {
-        const float2 w = tw[(l * (c + E * d)) & (n - 1)];
-        v = make_float2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
-      }
-      re[c] = v.x;
-      im[c] = v.y;
-    }
-    const size_t part_bytes = (size_t)n * P.K3p * 2;
-    uint8_t* base = Zop + (size_t)pr * 2 * part_bytes;
-    const int ncol = l > 0 ? 2 : 1;
+        float2 acc = tw_full(P.tw, (l * E * d) & (n - 1), n);
+        const float2 step = tw_full(P.tw, l & (n - 1), n);
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      if (cc >= ncol) break;
-      const int k = col + cc;
-      const float* v = cc == 0 ? re : im;
-      uint32_t h[E / 2 > 0 ? E / 2 : 1], lo[E / 2 > 0 ? E / 2 : 1];
-#pragma unroll
-      for (int e = 0; e < E / 2; ++e) split2_bf16(v[2 * e], v[2 * e + 1], h[e], lo[e]);
-      const int r0 = E * d;
-      const size_t off = (size_t)(r0 / 8) * P.K3p * 16 + (size_t)(k / 8) * 128 + (k % 8) * 16 + (r0 % 8) * 2;
-      if constexpr (E >= 8) {
-#pragma unroll
-        for (int u = 0; u < E / 8; ++u) {
-          const size_t o = off + (size_t)u * P.K3p * 16;
-          *reinterpret_cast<uint4*>(base + o) = make_uint4(h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
-          *reinterpret_cast<uint4*>(base + part_bytes + o) =
-              make_uint4(lo[4 * u], lo[4 * u + 1], lo[4 * u + 2], lo[4 * u + 3]);
+        for (int c = 0; c < E; ++c) {
+          x[rv(c)] = cmulf(x[rv(c)], acc);
+          acc = cmulf(acc, step);
         }
-      } else if constexpr (E == 4) {
-        *reinterpret_cast<uint2*>(base + off) = make_uint2(h[0], h[1]);
-        *reinterpret_cast<uint2*>(base + part_bytes + off) = make_uint2(lo[0], lo[1]);
-      } else {
-        *reinterpret_cast<uint32_t*>(base + off) = h[0];
-        *reinterpret_cast<uint32_t*>(base + part_bytes + off) = lo[0];
+      }
+      const int ncol = l > 0 ? 2 : 1;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        if (cc >= ncol) break;
+        const int kl = col + cc - 8 * g0;  // 0..7 within the group
+        const int r0 = E * d;
+        if constexpr (E >= 8) {
+#pragma unroll
+          for (int u = 0; u < E / 8; ++u) {
+            uint32_t h[4], lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 a0 = x[rv(8 * u + 2 * e)], a1 = x[rv(8 * u + 2 * e + 1)];
+              split2_bf16(cc == 0 ? a0.x : a0.y, cc == 0 ? a1.x : a1.y, h[e], lo[e]);
+            }
+            const int rg = r0 / 8 + u;
+            const uint32_t o = (uint32_t)rg * 128 + (uint32_t)(((kl ^ rg) & 7) * 16);
+            *reinterpret_cast<uint4*>(stg + o) = make_uint4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<uint4*>(stg + (n / 8) * 128 + o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          }
+        } else {
+          uint32_t h[E / 2], lo[E / 2];
+#pragma unroll
+          for (int e = 0; e < E / 2; ++e) {
+            const float2 a0 = x[rv(2 * e)], a1 = x[rv(2 * e + 1)];
+            split2_bf16(cc == 0 ? a0.x : a0.y, cc == 0 ? a1.x : a1.y, h[e], lo[e]);
+          }
+          const int rg = r0 / 8;
+          const uint32_t o = (uint32_t)rg * 128 + (uint32_t)(((kl ^ rg) & 7) * 16) + (r0 % 8) * 2;
+          if constexpr (E == 4) {
+            *reinterpret_cast<uint2*>(stg + o) = make_uint2(h[0], h[1]);
+            *reinterpret_cast<uint2*>(stg + (n / 8) * 128 + o) = make_uint2(lo[0], lo[1]);
+          } else {
+            *reinterpret_cast<uint32_t*>(stg + o) = h[0];
+            *reinterpret_cast<uint32_t*>(stg + (n / 8) * 128 + o) = lo[0];
+          }
+        }
       }
     }
+    __syncthreads();
+    // write out the column group: per (part, r-group) one 128-byte core matrix
+    const size_t part_bytes = (size_t)n * P.K3p * 2;
+    uint8_t* base = Zop + (size_t)pr * 2 * part_bytes + (size_t)g0 * 128;
+    const uint32_t SBO = (uint32_t)P.K3p * 16;
+    for (int idx = threadIdx.x; idx < 2 * (n / 8) * 8; idx += blockDim.x) {
+      const int row = idx & 7, rest = idx >> 3;
+      const int rg = rest % (n / 8), part = rest / (n / 8);
+      const uint4 v = *reinterpret_cast<const uint4*>(stg + part * (n / 8) * 128 + rg * 128 + ((row ^ rg) & 7) * 16);
+      *reinterpret_cast<uint4*>(base + part * part_bytes + (size_t)rg * SBO + row * 16) = v;
+    }
+    __syncthreads();
   }
+  cp_async_wait<0>();
 }
 
-static int step2_zb(const DevPlan& P) {
-  // terms per CTA: keep the pair slice <= ~100 KB of shared memory so two CTAs share an SM
-  const int per = (P.n_psi + 1) * 8;
-  int zb = (100 * 1024) / per;
-  if (zb < 1) zb = 1;
-  const int chunks = (P.H_plus + zb - 1) / zb;
-  return (P.H_plus + chunks - 1) / chunks;
+static size_t step2_smem(const TcPlan& tc, int n) {
+  return 2 * (((size_t)tc.s2_maxz * (n + 1) * sizeof(float2) + 127) & ~(size_t)127) + (size_t)2 * (n / 8) * 128;
 }
 
-static void launch_step2_fft(const float2* Zhat, uint8_t* Zop, int npair, int formB, const DevPlan& P,
-                             cudaStream_t s) {
-  const int zb = step2_zb(P);
-  const size_t smem = ((size_t)zb * (P.n_psi + 1) + P.n_psi) * sizeof(float2);
-  dim3 grid(npair, (P.H_plus + zb - 1) / zb);
+static void launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, int formB,
+                             const DevPlan& P, cudaStream_t s) {
+  S2Chunks C;
+  std::memcpy(&C, &tc.s2_chunks, sizeof C);
+  const size_t smem = step2_smem(tc, P.n_psi);
+  // persistent: two CTAs per SM (shared memory and registers allow two)
+  const int items = C.n * npair;
+  dim3 grid(items < 2 * tc.num_sms ? items : 2 * tc.num_sms);
   switch (P.n_psi) {
-    case 64: k_step2_fft<2><<<grid, 512, smem, s>>>(Zhat, Zop, npair, zb, formB, P); break;
-    case 128: k_step2_fft<4><<<grid, 512, smem, s>>>(Zhat, Zop, npair, zb, formB, P); break;
-    case 256: k_step2_fft<8><<<grid, 512, smem, s>>>(Zhat, Zop, npair, zb, formB, P); break;
-    case 512: k_step2_fft<16><<<grid, 256, smem, s>>>(Zhat, Zop, npair, zb, formB, P); break;
-    default: k_step2_fft<32><<<grid, 256, smem, s>>>(Zhat, Zop, npair, zb, formB, P); break;
+    case 64: k_step2_fft<2><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, C, tc.s2_maxz); break;
+    case 128: k_step2_fft<4><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, C, tc.s2_maxz); break;
+    case 256: k_step2_fft<8><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, C, tc.s2_maxz); break;
+    case 512: k_step2_fft<16><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, C, tc.s2_maxz); break;
+    default: k_step2_fft<32><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, C, tc.s2_maxz); break;
   }
 }
 
@@ -839,11 +941,12 @@ int tc_selftest(double* err_ts, double* err_ss, std::string& msg) {
 }
 
 // ---------------------------------------------------------------- engine plumbing
-int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, const std::vector<int>&,
-                 const std::vector<float>& Y3, int K3p, std::string& msg) {
+int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, const std::vector<int>& ell,
+                 const std::vector<int>& col, const std::vector<float>& Y3, int K3p, int Ke, std::string& msg) {
   tc_plan_free(tc);
   if (K3p % 16 != 0 || K3p > 128) {
-    msg = "tensor-core engine: K3 = 2 H_plus - H0 = " + std::to_string(pm.K3) + " exceeds 128 (use engine=1)";
+    msg = "tensor-core engine: Step-3 width " + std::to_string(K3p) + " (K3 = 2 H_plus - H0 = " +
+          std::to_string(pm.K3) + " plus block padding) exceeds 128 (use engine=1)";
     return FTK_EINVAL;
   }
   if (pm.n_psi % 64 != 0 || pm.n_psi > 1024) {
@@ -854,10 +957,37 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&tc.num_sms, cudaDevAttrMultiProcessorCount, dev);
   tc.K3p = K3p;
-  tc.n_ttiles = (pm.N_t + 127) / 128;
+  tc.Ke = Ke;
+  // representative shifts: delta_t paired with delta_t' = -delta_t (X(-delta) = E - O); the rest alone
+  std::vector<int> rep, partner;
+  {
+    std::vector<char> taken(pm.N_t, 0);
+    for (int t = 0; t < pm.N_t; ++t) {
+      if (taken[t]) continue;
+      taken[t] = 1;
+      int mate = -1;
+      const double x = pm.shifts[2 * t], y = pm.shifts[2 * t + 1];
+      if (x != 0.0 || y != 0.0) {
+        for (int u = t + 1; u < pm.N_t; ++u)
+          if (!taken[u] && std::fabs(pm.shifts[2 * u] + x) <= 1e-12 * (1.0 + std::fabs(x)) &&
+              std::fabs(pm.shifts[2 * u + 1] + y) <= 1e-12 * (1.0 + std::fabs(y))) {
+            mate = u;
+            taken[u] = 1;
+            break;
+          }
+      }
+      rep.push_back(t);
+      partner.push_back(mate);
+    }
+  }
+  tc.n_rep = (int)rep.size();
+  tc.n_ttiles = (tc.n_rep + 127) / 128;
   const int rows = tc.n_ttiles * 128, hk = K3p / 2;
+  rep.resize(rows, -1);
+  partner.resize(rows, -1);
   std::vector<uint32_t> yh((size_t)rows * hk, 0u), yl((size_t)rows * hk, 0u);
-  for (int t = 0; t < pm.N_t; ++t)
+  for (int rr = 0; rr < tc.n_rep; ++rr) {
+    const int t = rep[rr];
     for (int j = 0; j < hk; ++j) {
       const float x0 = Y3[(size_t)t * K3p + 2 * j], x1 = Y3[(size_t)t * K3p + 2 * j + 1];
       const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
@@ -868,9 +998,17 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       std::memcpy(&b, &h1, 2);
       std::memcpy(&c, &l0, 2);
       std::memcpy(&d, &l1, 2);
-      yh[(size_t)t * hk + j] = (uint32_t)a | ((uint32_t)b << 16);
-      yl[(size_t)t * hk + j] = (uint32_t)c | ((uint32_t)d << 16);
+      yh[(size_t)rr * hk + j] = (uint32_t)a | ((uint32_t)b << 16);
+      yl[(size_t)rr * hk + j] = (uint32_t)c | ((uint32_t)d << 16);
     }
+  }
+  if (cudaMalloc(&tc.d_rep, rows * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&tc.d_partner, rows * sizeof(int)) != cudaSuccess) {
+    msg = "tensor-core engine: allocation failed";
+    return FTK_ENOMEM;
+  }
+  cudaMemcpy(tc.d_rep, rep.data(), rows * sizeof(int), cudaMemcpyHostToDevice);
+  cudaMemcpy(tc.d_partner, partner.data(), rows * sizeof(int), cudaMemcpyHostToDevice);
   if (cudaMalloc(&tc.d_Yh, yh.size() * 4) != cudaSuccess || cudaMalloc(&tc.d_Yl, yl.size() * 4) != cudaSuccess) {
     msg = "tensor-core engine: allocation failed";
     return FTK_ENOMEM;
@@ -890,11 +1028,41 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   tc.KCH = (2 * pm.n_k) % 64 == 0 ? 64 : 32;
   tc.NKCH = 2 * pm.n_k / tc.KCH;
   cudaFuncSetAttribute(k_step1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
-  cudaFuncSetAttribute(k_step2_fft<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_step2_fft<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_step2_fft<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_step2_fft<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_step2_fft<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  // Step-2 chunks: one group of 8 Step-3 columns each (whole terms, see the column map in ftk_capi.cu)
+  {
+    std::memset(&tc.s2_chunks, 0, sizeof tc.s2_chunks);
+    const int ngroups = K3p / 8;
+    if (ngroups > 32) {
+      msg = "tensor-core engine: too many Step-3 column groups";
+      return FTK_EINVAL;
+    }
+    int maxz = 1;
+    for (int gi = 0; gi < ngroups; ++gi) {
+      int zs = -1, ze = -1;
+      for (int z = 0; z < (int)col.size(); ++z)
+        if (col[z] / 8 == gi) {
+          if (zs < 0) zs = z;
+          ze = z + 1;
+          if (ell[z] > 0 && (col[z] + 1) / 8 != gi) {
+            msg = "tensor-core engine: a term straddles a column group";
+            return FTK_EINVAL;
+          }
+        }
+      if (zs < 0) zs = ze = 0;  // padding-only group
+      tc.s2_chunks.zs[gi] = zs;
+      tc.s2_chunks.ze[gi] = ze;
+      tc.s2_chunks.g0[gi] = gi;
+      maxz = std::max(maxz, ze - zs);
+    }
+    tc.s2_chunks.n = ngroups;
+    tc.s2_maxz = maxz;
+    const int sm2 = (int)step2_smem(tc, pm.n_psi);
+    cudaFuncSetAttribute(k_step2_fft<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+  }
   tc.ready = true;
   return FTK_OK;
 }
@@ -904,6 +1072,9 @@ void tc_plan_free(TcPlan& tc) {
   cudaFree(tc.d_Yl);
   cudaFree(tc.d_Bop);
   cudaFree(tc.d_Aop);
+  cudaFree(tc.d_rep);
+  cudaFree(tc.d_partner);
+  tc.d_rep = tc.d_partner = nullptr;
   tc.d_Yh = tc.d_Yl = tc.d_Bop = nullptr;
   tc.d_Aop = nullptr;
   tc.aop_bytes = 0;
@@ -960,10 +1131,13 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
   prm.pb = pb;
   prm.n = P.n_psi;
   prm.K3p = P.K3p;
+  prm.Ke = P.Ke;
   prm.N_t = P.N_t;
   prm.T = tc.n_ttiles;
-  prm.NC = P.n_psi < 128 ? P.n_psi : 128;
+  prm.NC = 64;
   prm.RC = P.n_psi / prm.NC;
+  prm.rep_t = tc.d_rep;
+  prm.partner = tc.d_partner;
   prm.tm_off = tm_off;
   prm.n_tm_local = n_tm_local;
   prm.img_keys = img_keys;
@@ -1014,14 +1188,14 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     launch_step1_simt(A, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    launch_step2_fft(Zhat, Zop, pb.count, 0, P, s);
+    launch_step2_fft(tc, Zhat, Zop, pb.count, 0, P, s);
     if (prof) prof(plan, 2, 1, s);
   } else {
     if (prof) prof(plan, 1, 0, s);
     launch_step1_tc(tc, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    launch_step2_fft(Zhat, Zop, pb.count, 1, P, s);
+    launch_step2_fft(tc, Zhat, Zop, pb.count, 1, P, s);
     if (prof) prof(plan, 2, 1, s);
   }
   if (prof) prof(plan, 3, 0, s);

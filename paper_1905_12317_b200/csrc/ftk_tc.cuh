@@ -13,7 +13,11 @@ namespace ftk {
 struct TcPlan {
   bool ready = false;
   int K3p = 0;          // Step-3 contraction length padded to a multiple of 16
-  int n_ttiles = 0;     // ceil(N_t / 128)
+  int n_ttiles = 0;     // ceil(n_rep / 128)
+  int n_rep = 0;        // representative shifts (+-delta pairs share a row)
+  int Ke = 0;           // even-ell column block length
+  int* d_rep = nullptr;
+  int* d_partner = nullptr;
   uint32_t* d_Yh = nullptr;  // [n_ttiles*128][K3p/2] packed bf16x2, hi part
   uint32_t* d_Yl = nullptr;  // lo part
   // Step 1 operands
@@ -21,6 +25,12 @@ struct TcPlan {
   uint8_t* d_Aop = nullptr;    // images, bf16 hi/lo split, Step-1 K-major tiles [p][tile][kchunk][part]...
   size_t aop_bytes = 0;
   int NIT = 0, KCH = 64, NKCH = 0;
+  // Step 2 chunk table (one 8-column group per chunk)
+  struct {
+    int n;
+    int zs[32], ze[32], g0[32];
+  } s2_chunks;
+  int s2_maxz = 1;
   int64_t n_tm = 0;
   int num_sms = 148;
 };
@@ -28,7 +38,7 @@ struct TcPlan {
 typedef void (*prof_cb_t)(void* plan, int cls, int end, cudaStream_t s);
 
 int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, const std::vector<int>& ell,
-                 const std::vector<float>& Y3, int K3p_simt, std::string& msg);
+                 const std::vector<int>& col, const std::vector<float>& Y3, int K3p, int Ke, std::string& msg);
 void tc_plan_free(TcPlan& tc);
 int tc_prepare_images(TcPlan& tc, const float2* fb, int64_t n, const DevPlan& P, cudaStream_t s, std::string& msg);
 int tc_prepare_templates(TcPlan& tc, const float2* fb, int64_t n, const DevPlan& P, cudaStream_t s, std::string& msg);
