@@ -283,8 +283,8 @@ def main():
         peak_src = "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz"
     issued = None
     if engine == pkg.ENGINE_TC and dom == "step3":
-        rows = -(-info["n_rep"] // 128) * 128
-        issued_flops = 3.0 * 2.0 * rows * cfg.n_psi * info["K3p"] * pairs_local * args.steps / max(dom_cnt, 1)
+        rows = 128 * info["s3_rtiles"]
+        issued_flops = 3.0 * 2.0 * rows * info["s3_cols"] * info["K3p"] * pairs_local * args.steps / max(dom_cnt, 1)
         issued = issued_flops / avg_launch_s / 1e12 if avg_launch_s > 0 else None
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "tensor_issued_tflops": issued,

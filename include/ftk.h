@@ -92,7 +92,11 @@ typedef struct {
   int64_t n_images, n_templates_total, n_templates_local, template_offset;
   int engine, device, rank, world;
   int K3p;                   /* device Step-3 width (K3 + block padding; multiple of 16 for engine 0) */
-  int n_rep;                 /* engine 0: representative shifts (+-delta pairs share one row of Step 3) */
+  int n_rep;                 /* engine 0: representative shifts (+-delta pairs share one E/O column pair) */
+  int s3_cols;               /* engine 0: Step-3 GEMM N over all rep-groups (n_rep + padding) */
+  int s3_nch;                /* engine 0: Step-3 chunk width (MMA N) */
+  int s3_groups;             /* engine 0: rep-groups (Y slices resident in shared memory) */
+  int s3_rtiles;             /* engine 0: 128-row rotation tiles per pair (MMA M) */
 } ftk_plan_info_t;
 
 /* Build the plan (host, double precision, untimed per P:1321): radial rule, per-ell operator SVD of

@@ -21,7 +21,8 @@ class PlanInfo(C.Structure):
                 ("eps", C.c_double), ("certificate", C.c_double), ("n_images", C.c_int64),
                 ("n_templates_total", C.c_int64), ("n_templates_local", C.c_int64), ("template_offset", C.c_int64),
                 ("engine", C.c_int), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
-                ("K3p", C.c_int), ("n_rep", C.c_int)]
+                ("K3p", C.c_int), ("n_rep", C.c_int), ("s3_cols", C.c_int),
+                ("s3_nch", C.c_int), ("s3_groups", C.c_int), ("s3_rtiles", C.c_int)]
 
 
 class Best(C.Structure):

@@ -336,6 +336,10 @@ ftk_status_t ftk_plan_query(ftk_plan_t plan, ftk_plan_info_t* info) {
   info->world = plan->world;
   info->K3p = plan->K3p;
   info->n_rep = plan->engine == 0 ? plan->tc.n_rep : plan->pm.N_t;
+  info->s3_cols = plan->engine == 0 ? plan->tc.ncol : plan->pm.N_t;
+  info->s3_nch = plan->engine == 0 ? plan->tc.NCH : 0;
+  info->s3_groups = plan->engine == 0 ? plan->tc.G : 0;
+  info->s3_rtiles = plan->engine == 0 ? plan->tc.NRT : 0;
   return FTK_OK;
 }
 

@@ -139,6 +139,18 @@ __device__ __forceinline__ void split2_bf16(float x0, float x1, uint32_t& hi, ui
 
 __device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
 __device__ __forceinline__ bool elect_lane0() { return (threadIdx.x & 31) == 0; }
+// elect.sync: exactly one lane of the (converged) warp gets true; lets the compiler keep warp-uniform
+// operands of single-thread instructions (tcgen05.mma / commit) in uniform registers.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+      "elect.sync rx|px, %1;\n\t"
+      "@px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
+}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

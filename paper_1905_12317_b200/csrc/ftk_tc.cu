@@ -1,23 +1,28 @@
 // Tensor-core (tcgen05) engine of the FTK hot path, bf16x3 split arithmetic.
 //
 // Step 3 (PAPER.md Eq. fbk3; real form of DESIGN.md reading R13):
-//   X_p(t, r) = sum_k Y3[t][k] Z3_p[k][r],  k < K3 = 2 H_plus - H0,  then max/argmax over (t, r).
+//   X_p(t, r) = sum_k Z3_p[r][k] Y3[t][k],  k < K3 = 2 H_plus - H0,  then max/argmax over (t, r).
 // Every operand x is split x = hi + lo in bf16 and the product is hi*hi + hi*lo + lo*hi with fp32
 // accumulation in TMEM (measured <= 6e-6 ||A|| ||B|| vs the 1e-4 budget).
 //
-// Kernel k_step3_tc (one CTA per SM, persistent over a contiguous range of pairs).  Shifts are taken in
-// +-delta pairs: Y_zeta(-delta) = (-1)^ell Y_zeta(delta), so with the columns split by the parity of ell
-// (even block [0, Ke), odd block [Ke, K3p)) X(+delta) = E + O and X(-delta) = E - O, where
-// E = Y_even Z_even and O = Y_odd Z_odd are accumulated separately: half the rows, same K.
-//   * Z producer (warp 0, one lane): per pair, bulk-copies (cp.async.bulk) the pair's operand image
-//     written by Step 2 -- bf16 hi/lo, MN-major SWIZZLE_NONE canonical layout -- into SMEM, chunk by
-//     chunk of 64 r (z_full[rc] / z_empty[rc] mbarriers) -> the B operand (N = r).
-//   * MMA issuer (warp 1, one lane): per (t-tile, r-chunk) 3 x K3p/16 tcgen05.mma (M128 N64 K16, A = Y
-//     tile from TMEM, B from SMEM) into the E and O accumulators of one of two TMEM buffers.
-//   * Epilogue (warps 2-9, two per TMEM lane quarter): tcgen05.ld E and O, X = E +- O, running
-//     max/argmax per row, per-pair reduction, one packed-key atomicMax per pair.
-//   * Y loaders (warps 10-13): per 128-row tile of representative shifts, Y hi/lo rows -> TMEM via
-//     tcgen05.st -> the A operand (M = t), double-buffered (y_full / y_empty).
+// Kernel k_step3_tc (one CTA per SM, persistent).  GEMM orientation: M = 128 rotations r (one "r-tile"
+// of the pair's operand Z3, the A operand, held in TMEM), N = a chunk of NCH representative shifts
+// (the B operand Y3, resident in shared memory for the whole kernel), K = K3p.  Shifts are taken in
+// +-delta pairs: Y_zeta(-delta) = (-1)^ell Y_zeta(delta), so with the K columns split by the parity of
+// ell (even block [0, Ke), odd block [Ke, K3p)) X(+delta) = E + O and X(-delta) = E - O with
+// E = Z_even Y_even, O = Z_odd Y_odd accumulated separately: half the shifts, same K.
+// Representative shifts are split into rep-groups whose Y image fits in shared memory; CTA b serves
+// group b % G for a contiguous range of pairs (G = 1 at the BASELINE configs c2, c3, c5).
+//   * warp 0 (one lane): MMA issuer -- per (pair, r-tile, chunk) 3 x K3p/16 tcgen05.mma M128 x NCH x K16
+//     (A = Z r-tile hi/lo from TMEM, B = Y chunk hi/lo from SMEM) into the E / O accumulators of one of
+//     two TMEM buffers.
+//   * warps 1-8: A writers -- per (pair, r-tile) the Step-2 operand rows (hi: warps 1-4, lo: 5-8; one
+//     thread per rotation row) global -> registers -> tcgen05.st into one of two TMEM A slots.
+//   * warps 9-16: epilogue -- tcgen05.ld E and O, X(+-delta) = E +- O; per thread the running max of
+//     E + |O| = max(E + O, E - O) and its 8-column group (branch-free), per-pair reduction.
+//   * warp 17: resolver -- recomputes the 16 E / O sums of the pair's winning group in fp32 from the
+//     same bf16 operands to recover the exact (shift, sign), one packed-key atomicMax per pair.
+// TMEM columns: D buffers [0, 4 NCH) (E, O of buffer 0 then 1), A slots [4 NCH, 4 NCH + 2 K3p).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -30,291 +35,397 @@
 namespace ftk {
 using namespace sm100;
 
-constexpr int S3_THREADS = 14 * 32;
-constexpr int S3_MAX_RC = 16;  // n_psi / 64 <= 16
+constexpr int S3_WARPS = 18;
+constexpr int S3_THREADS = S3_WARPS * 32;
+constexpr int S3_MAXG = TcPlan::MAXG;
 
 struct S3Params {
-  const uint8_t* Zop;     // per pair: bf16 hi/lo MN-major operand image (see k_step2_fft)
-  const uint32_t* Yh;     // [T*128][K3p/2]
-  const uint32_t* Yl;
+  const uint8_t* Zop;     // per pair: [r-tile][part][word group][row 128][16 B] (written by k_step2_fft)
+  const uint8_t* Ysm;     // per group: shared-memory image [part][rep/8][K3p/8][8 rows x 16 B]
+  const int* colrep;      // [ncol_total] shift index of the representative (+delta); -1: padding column
+  const int* colpart;     // [ncol_total] shift index of -delta; -1: none
+  const uint8_t* colfast; // [ncol_total / 8] 1 if all 8 columns are paired, non-padding
   PairBlock pb;
-  int n, K3p, Ke, N_t, T, NC, RC;
+  int n, K3p, Ke, N_t, NRT, NCH, G;
+  int g_col0[S3_MAXG], g_nch[S3_MAXG];
+  long long g_yoff[S3_MAXG];
   int tm_off, n_tm_local;
-  const int* rep_t;       // [T*128] shift index of representative row (-1: padding row)
-  const int* partner;     // [T*128] shift index of -delta (-1: none)
   unsigned long long* img_keys;
   unsigned long long* pair_keys;
   float* land;
 };
 
 struct S3Smem {
-  uint64_t z_full[S3_MAX_RC], z_empty[S3_MAX_RC];
-  uint64_t y_full[2], y_empty[2];
-  uint64_t acc_full[2], acc_empty[2];
+  uint64_t y_bar;
+  uint64_t a_full[2], a_empty[2];
+  uint64_t d_full[2], d_empty[2];
+  uint64_t res_full[2], res_empty[2];
   uint32_t tmem_base;
-  float red_v[8];
-  uint32_t red_f[8];
+  float red_v[2][8], red_ve[2][8];
+  uint32_t red_k[2][8], red_fe[2][8];
+  float res_v[2], res_ve[2];
+  uint32_t res_k[2], res_fe[2];
+  int res_p[2];
 };
+
+static_assert(sizeof(S3Smem) <= 512, "S3Smem must fit below the column metadata");
 
 __device__ __forceinline__ bool better(float v, uint32_t f, float bv, uint32_t bf) {
   return v > bv || (v == bv && f < bf);
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint4& v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
 __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   extern __shared__ __align__(1024) uint8_t s3_raw[];
   S3Smem& S = *reinterpret_cast<S3Smem*>(s3_raw);
-  uint8_t* zs = s3_raw + 1024;  // Z image: [2 parts][n/8][K3p/8][128 B]
+  int* s_rep = reinterpret_cast<int*>(s3_raw + 512);  // [ncol_g] then s_part, s_fast
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = P.n, K3p = P.K3p, NC = P.NC, RC = P.RC, T = P.T;
-  const uint32_t SBO = (uint32_t)K3p * 16;                // bytes between 8-row groups
-  const uint32_t part_bytes = (uint32_t)n * K3p * 2;      // one bf16 part of the whole pair
+  const int n = P.n, K3p = P.K3p, NCH = P.NCH, NRT = P.NRT;
+  const int G = P.G, grp = blockIdx.x % G;
+  const int nch = P.g_nch[grp], ncol = nch * NCH, col0 = P.g_col0[grp];
+  int* s_part = s_rep + ncol;
+  uint8_t* s_fast = reinterpret_cast<uint8_t*>(s_part + ncol);
+  const uint32_t meta_bytes = ((uint32_t)ncol * 8u + (uint32_t)ncol / 8u + 512u + 1023u) & ~1023u;
+  uint8_t* ys = s3_raw + 1024 + meta_bytes;                       // Y image of this group
+  const uint32_t ypart = (uint32_t)ncol * (uint32_t)K3p * 2u;      // bytes of one bf16 part
+  const uint32_t SBO = (uint32_t)K3p * 16u;                        // bytes between 8-row groups (N)
+  const int NWG = K3p / 8;                                         // 16-byte word groups per row
+  const size_t pair_bytes = (size_t)NRT * 128 * K3p * 4;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < RC; ++i) {
-      mbar_init(&S.z_full[i], 1);
-      mbar_init(&S.z_empty[i], 1);
-    }
+    mbar_init(&S.y_bar, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&S.y_full[i], 128);
-      mbar_init(&S.y_empty[i], 1);
-      mbar_init(&S.acc_full[i], 1);
-      mbar_init(&S.acc_empty[i], 256);
+      mbar_init(&S.a_full[i], 8);
+      mbar_init(&S.a_empty[i], 1);
+      mbar_init(&S.d_full[i], 1);
+      mbar_init(&S.d_empty[i], 8);
+      mbar_init(&S.res_full[i], 1);
+      mbar_init(&S.res_empty[i], 1);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(&S.tmem_base);
+  for (int c = threadIdx.x; c < ncol; c += blockDim.x) {
+    s_rep[c] = __ldg(P.colrep + col0 + c);
+    s_part[c] = __ldg(P.colpart + col0 + c);
+  }
+  for (int c = threadIdx.x; c < ncol / 8; c += blockDim.x) s_fast[c] = __ldg(P.colfast + col0 / 8 + c);
+  if (warp == 0) tmem_alloc<512>(&S.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
-  // pair range of this CTA
+  const uint32_t acol0 = 4u * (uint32_t)NCH;
+  // pair range of this CTA (CTAs of one group split the pairs)
+  const int cpg = gridDim.x / G;  // CTAs per group (grid is a multiple of G)
+  const int cig = blockIdx.x / G;
   const int count = P.pb.count;
-  const int per = (count + gridDim.x - 1) / gridDim.x;
-  const int p_begin = blockIdx.x * per;
+  const int per = (count + cpg - 1) / cpg;
+  const int p_begin = min(count, cig * per);
   const int p_end = min(count, p_begin + per);
 
   if (warp == 0) {
-    // ---------------- Z producer: the pair's operand image chunk by chunk (hi and lo) via bulk copies
-    if (lane == 0) {
-      const uint32_t chunk_bytes = (uint32_t)(NC / 8) * SBO;
-      int it = 0;
-      for (int p = p_begin; p < p_end; ++p, ++it) {
-        const uint8_t* zsrc = P.Zop + (size_t)p * 2 * part_bytes;
-        for (int rc = 0; rc < RC; ++rc) {
-          mbar_wait(&S.z_empty[rc], (it & 1) ^ 1);
-          mbar_arrive_expect_tx(&S.z_full[rc], 2 * chunk_bytes);
-          bulk_g2s(zs + rc * chunk_bytes, zsrc + rc * chunk_bytes, chunk_bytes, &S.z_full[rc]);
-          bulk_g2s(zs + part_bytes + rc * chunk_bytes, zsrc + part_bytes + rc * chunk_bytes, chunk_bytes,
-                   &S.z_full[rc]);
-        }
+    // ---------------- Y image of the group -> SMEM (once), then the MMA issuer (converged warp,
+    // one elected lane issues; operands stay warp-uniform)
+    const uint32_t ybytes = 2u * ypart;
+    if (elect_one()) {
+      mbar_arrive_expect_tx(&S.y_bar, ybytes);
+      const uint8_t* ysrc = P.Ysm + P.g_yoff[grp];
+      for (uint32_t o = 0; o < ybytes; o += 32768u) {
+        const uint32_t b = min(32768u, ybytes - o);
+        bulk_g2s(ys + o, ysrc + o, b, &S.y_bar);
       }
     }
     __syncwarp();
-  } else if (warp >= 2 && warp < 10) {
-    // ---------------- epilogue (8 warps: two per TMEM lane quarter, each half of the chunk's columns):
-    // X(+delta) = E + O on the representative row, X(-delta) = E - O on its partner
+    mbar_wait(&S.y_bar, 0);
+    const uint32_t idesc = idesc_bf16_f32(128, NCH);
+    const uint32_t ybase = smem_u32(ys);
+    const int ksteps = K3p / 16, ke_steps = P.Ke / 16, halfk = K3p / 2;
+    uint32_t g_a = 0, g_d = 0;
+    for (int p = p_begin; p < p_end; ++p) {
+      for (int T = 0; T < NRT; ++T, ++g_a) {
+        const int ab = g_a & 1;
+        mbar_wait(&S.a_full[ab], (g_a >> 1) & 1);
+        tc_fence_after();
+        const uint32_t a_hi0 = tmem + acol0 + (uint32_t)(ab * K3p);
+        for (int c = 0; c < nch; ++c, ++g_d) {
+          const int db = g_d & 1;
+          mbar_wait(&S.d_empty[db], ((g_d >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t dE = tmem + (uint32_t)(db * 2 * NCH), dO = dE + (uint32_t)NCH;
+          const uint32_t bch = ybase + (uint32_t)(c * (NCH / 8)) * SBO;
+          const uint64_t bh0 = smem_desc_kmajor_noswz(bch, 128, SBO);
+          const uint64_t bl0 = smem_desc_kmajor_noswz(bch + ypart, 128, SBO);
+          if (elect_one()) {
+            for (int ks = 0; ks < ksteps; ++ks) {
+              const bool odd = ks >= ke_steps;
+              const uint32_t d = odd ? dO : dE;
+              const uint32_t acc0 = (odd ? ks > ke_steps : ks > 0) ? 1u : 0u;
+              const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + (uint32_t)halfk;
+              const uint64_t b_hi = bh0 + (uint64_t)(ks * 16), b_lo = bl0 + (uint64_t)(ks * 16);  // +256 B
+              mma_bf16_ts(d, a_hi, b_hi, idesc, acc0);
+              mma_bf16_ts(d, a_hi, b_lo, idesc, 1u);
+              mma_bf16_ts(d, a_lo, b_hi, idesc, 1u);
+            }
+            tc_commit(&S.d_full[db]);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) tc_commit(&S.a_empty[ab]);
+        __syncwarp();
+      }
+    }
+  } else if (warp <= 8) {
+    // ---------------- A writers: rows of the pair's r-tile (hi: warps 1-4, lo: warps 5-8) -> TMEM
+    const int q = warp & 3;
+    const int part = (warp - 1) >> 2;
+    const int row = q * 32 + lane;
+    uint32_t g_a = 0;
+    for (int p = p_begin; p < p_end; ++p) {
+      const uint8_t* zp = P.Zop + (size_t)p * pair_bytes;
+      for (int T = 0; T < NRT; ++T, ++g_a) {
+        const int ab = g_a & 1;
+        const bool valid = T * 128 + row < n;
+        const uint4* src = reinterpret_cast<const uint4*>(zp + (size_t)((T * 2 + part) * NWG) * 2048 + row * 16);
+        uint4 v[16];
+#pragma unroll
+        for (int g = 0; g < 16; ++g)
+          if (g < NWG) v[g] = valid ? __ldg(src + g * 128) : make_uint4(0u, 0u, 0u, 0u);
+        mbar_wait(&S.a_empty[ab], ((g_a >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acol0 + (uint32_t)(ab * K3p + part * (K3p / 2));
+#pragma unroll
+        for (int g = 0; g < 16; ++g)
+          if (g < NWG) tmem_st4(base + 4 * g, v[g]);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.a_full[ab]);
+      }
+    }
+  } else if (warp <= 16) {
+    // ---------------- epilogue: 8 warps, two per TMEM lane quarter, each half of the chunk's columns.
+    // Hot loop (8 paired columns): X = max(E + O, E - O) = E + |O|; per thread only the best value and
+    // its 8-column group are tracked (branch-free); the resolver warp recovers the exact (shift, sign)
+    // of the pair's winning group.  Groups with padding / unpaired shifts, and landscape output, take
+    // the exact path.
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int half = (warp - 2) >> 2;  // 0 or 1
+    const int ew = warp - 9;        // 0..7
+    const int h = ew >> 2;          // 0 or 1
+    const int hw = NCH / 2;         // columns per epilogue warp (multiple of 8)
     const bool has_odd = P.Ke < K3p;
-    int it = 0;
-    uint32_t g_acc = 0;
+    uint32_t g_d = 0, it = 0;
     for (int p = p_begin; p < p_end; ++p, ++it) {
-      float bv = -INFINITY;
-      uint32_t bf = 0xffffffffu;
-      for (int tt = 0; tt < T; ++tt) {
-        const int tp = __ldg(P.rep_t + tt * 128 + row);
-        const int tm = __ldg(P.partner + tt * 128 + row);
-        for (int rc = 0; rc < RC; ++rc, ++g_acc) {
-          const int ab = g_acc & 1;
-          mbar_wait(&S.acc_full[ab], (g_acc >> 1) & 1);
+      float bvf = -INFINITY;        // fast record: best E + |O| ...
+      uint32_t bkf = 0xffffffffu;   // ... and its key (T << 24 | column << 7 | row)
+      float bve = -INFINITY;        // exact record (slow groups)
+      uint32_t bfe = 0xffffffffu;
+      float* land_p = P.land ? P.land + (size_t)p * P.N_t * n : nullptr;
+      for (int T = 0; T < NRT; ++T) {
+        const int r = T * 128 + row;
+        const bool active = T * 128 + q * 32 < n;  // warp-uniform: lane quarters beyond n_psi idle
+        for (int c = 0; c < nch; ++c, ++g_d) {
+          const int db = g_d & 1;
+          mbar_wait(&S.d_full[db], (g_d >> 1) & 1);
           tc_fence_after();
-          const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * 2 * NC);
-          for (int c0 = half * (NC / 2); c0 < (half + 1) * (NC / 2); c0 += 32) {
-            uint32_t e[2][16], o[2][16];
+          const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(db * 2 * NCH + h * hw);
+          if (active) {
+            for (int c8 = 0; c8 < hw; c8 += 8) {
+              uint32_t e[8], o[8];
+              tmem_ld8(base + c8, e);
+              if (has_odd) tmem_ld8(base + NCH + c8, o);
+              tmem_wait_ld();
+              if (!has_odd) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              tmem_ld16(base + c0 + 16 * h, e[h]);
-              if (has_odd) tmem_ld16(base + NC + c0 + 16 * h, o[h]);
-            }
-            tmem_wait_ld();
-            if (!has_odd) {
+                for (int k = 0; k < 8; ++k) o[k] = 0u;
+              }
+              const int cl = c * NCH + h * hw + c8;  // column within the group
+              if (s_fast[cl >> 3] && !land_p) {
+                float v[8];
 #pragma unroll
-              for (int h = 0; h < 2; ++h)
+                for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(e[k]) + fabsf(__uint_as_float(o[k]));
+                const float m = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
+                                      fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+                const bool upd = m > bvf;
+                bvf = upd ? m : bvf;
+                bkf = upd ? (((uint32_t)T << 24) | ((uint32_t)cl << 7) | (uint32_t)row) : bkf;
+              } else if (r < n) {
 #pragma unroll
-                for (int k = 0; k < 16; ++k) o[h][k] = 0u;
-            }
-            if (tp >= 0) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int r0 = rc * NC + c0 + 16 * h;
-                float xp[16], xm[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                  const float ev = __uint_as_float(e[h][k]), ov = __uint_as_float(o[h][k]);
-                  xp[k] = ev + ov;
-                  xm[k] = ev - ov;
-                }
-                // max first; locate the column only when the running best can change (ties -> smaller flat)
-                float mp = xp[0];
-#pragma unroll
-                for (int k = 1; k < 16; ++k) mp = fmaxf(mp, xp[k]);
-                const uint32_t fp0 = (uint32_t)tp * (uint32_t)n + (uint32_t)r0;
-                if (mp > bv || (mp == bv && fp0 < bf)) {
-                  int k0 = 0;
-#pragma unroll
-                  for (int k = 15; k >= 0; --k)
-                    if (xp[k] == mp) k0 = k;
-                  if (better(mp, fp0 + k0, bv, bf)) {
-                    bv = mp;
-                    bf = fp0 + k0;
+                for (int k = 0; k < 8; ++k) {
+                  const int tp = s_rep[cl + k], tm = s_part[cl + k];
+                  if (tp < 0) continue;
+                  const float ev = __uint_as_float(e[k]), ov = __uint_as_float(o[k]);
+                  const float xp = ev + ov;
+                  const uint32_t fp = (uint32_t)tp * (uint32_t)n + (uint32_t)r;
+                  if (better(xp, fp, bve, bfe)) {
+                    bve = xp;
+                    bfe = fp;
                   }
-                }
-                if (tm >= 0) {
-                  float mm = xm[0];
-#pragma unroll
-                  for (int k = 1; k < 16; ++k) mm = fmaxf(mm, xm[k]);
-                  const uint32_t fm0 = (uint32_t)tm * (uint32_t)n + (uint32_t)r0;
-                  if (mm > bv || (mm == bv && fm0 < bf)) {
-                    int k0 = 0;
-#pragma unroll
-                    for (int k = 15; k >= 0; --k)
-                      if (xm[k] == mm) k0 = k;
-                    if (better(mm, fm0 + k0, bv, bf)) {
-                      bv = mm;
-                      bf = fm0 + k0;
-                    }
-                  }
-                }
-                if (P.land) {
-                  float4* dp = reinterpret_cast<float4*>(P.land + ((size_t)p * P.N_t + tp) * n + r0);
-#pragma unroll
-                  for (int k = 0; k < 4; ++k) dp[k] = make_float4(xp[4 * k], xp[4 * k + 1], xp[4 * k + 2], xp[4 * k + 3]);
+                  if (land_p) land_p[(size_t)tp * n + r] = xp;
                   if (tm >= 0) {
-                    float4* dm = reinterpret_cast<float4*>(P.land + ((size_t)p * P.N_t + tm) * n + r0);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                      dm[k] = make_float4(xm[4 * k], xm[4 * k + 1], xm[4 * k + 2], xm[4 * k + 3]);
+                    const float xm = ev - ov;
+                    const uint32_t fm = (uint32_t)tm * (uint32_t)n + (uint32_t)r;
+                    if (better(xm, fm, bve, bfe)) {
+                      bve = xm;
+                      bfe = fm;
+                    }
+                    if (land_p) land_p[(size_t)tm * n + r] = xm;
                   }
                 }
               }
             }
           }
           tc_fence_before();
-          mbar_arrive(&S.acc_empty[ab]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.d_empty[db]);
         }
       }
-      // per-pair reduction over the 128 epilogue threads (lexicographic tie-break on the flat index)
+      // per-pair reduction of both records over the warp, then over the 8 warps (warp 9 posts them)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-        const uint32_t f2 = __shfl_xor_sync(0xffffffffu, bf, o);
-        if (better(v2, f2, bv, bf)) {
-          bv = v2;
-          bf = f2;
+        const float v2 = __shfl_xor_sync(0xffffffffu, bvf, o);
+        const uint32_t k2 = __shfl_xor_sync(0xffffffffu, bkf, o);
+        if (better(v2, k2, bvf, bkf)) {
+          bvf = v2;
+          bkf = k2;
+        }
+        const float v3 = __shfl_xor_sync(0xffffffffu, bve, o);
+        const uint32_t f3 = __shfl_xor_sync(0xffffffffu, bfe, o);
+        if (better(v3, f3, bve, bfe)) {
+          bve = v3;
+          bfe = f3;
         }
       }
+      const int rb = it & 1;
       if (lane == 0) {
-        S.red_v[warp - 2] = bv;
-        S.red_f[warp - 2] = bf;
+        S.red_v[rb][ew] = bvf;
+        S.red_k[rb][ew] = bkf;
+        S.red_ve[rb][ew] = bve;
+        S.red_fe[rb][ew] = bfe;
       }
       named_bar(1, 256);
-      if (warp == 2 && lane == 0) {
-        float v = S.red_v[0];
-        uint32_t f = S.red_f[0];
-        for (int k = 1; k < 8; ++k)
-          if (better(S.red_v[k], S.red_f[k], v, f)) {
-            v = S.red_v[k];
-            f = S.red_f[k];
+      if (ew == 0 && lane == 0) {
+        float v = S.red_v[rb][0], ve = S.red_ve[rb][0];
+        uint32_t k = S.red_k[rb][0], fe = S.red_fe[rb][0];
+        for (int w = 1; w < 8; ++w) {
+          if (better(S.red_v[rb][w], S.red_k[rb][w], v, k)) {
+            v = S.red_v[rb][w];
+            k = S.red_k[rb][w];
           }
-        if (f != 0xffffffffu) {
-          int i, j;
-          pair_of(P.pb, p, i, j);
-          const uint32_t tt2 = f / (uint32_t)n, r = f - tt2 * (uint32_t)n;
-          const uint32_t gflat = ((uint32_t)(P.tm_off + j) * (uint32_t)P.N_t + tt2) * (uint32_t)n + r;
-          const unsigned long long key = pack_key(v, gflat);
-          if (P.img_keys) atomicMax(&P.img_keys[i], key);
-          if (P.pair_keys) atomicMax(&P.pair_keys[(size_t)i * P.n_tm_local + j], key);
-        }
-      }
-      named_bar(1, 256);
-    }
-  } else if (warp >= 10) {
-    // ---------------- Y loaders: Y tile (128 t-rows x K3p) hi/lo -> TMEM columns 256 + ybuf*K3p
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    const int halfk = K3p / 2;
-    uint32_t g_t = 0;
-    for (int p = p_begin; p < p_end; ++p) {
-      for (int tt = 0; tt < T; ++tt, ++g_t) {
-        const int yb = g_t & 1;
-        mbar_wait(&S.y_empty[yb], ((g_t >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t col0 = 256 + (uint32_t)(yb * K3p);
-        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + col0;
-        const uint4* yh = reinterpret_cast<const uint4*>(P.Yh + (size_t)(tt * 128 + row) * halfk);
-        const uint4* yl = reinterpret_cast<const uint4*>(P.Yl + (size_t)(tt * 128 + row) * halfk);
-        for (int c = 0; c < halfk; c += 8) {
-          uint4 a = __ldg(yh + c / 4), b = __ldg(yh + c / 4 + 1);
-          uint32_t r8[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-          tmem_st8(base + c, r8);
-          uint4 a2 = __ldg(yl + c / 4), b2 = __ldg(yl + c / 4 + 1);
-          uint32_t l8[8] = {a2.x, a2.y, a2.z, a2.w, b2.x, b2.y, b2.z, b2.w};
-          tmem_st8(base + halfk + c, l8);
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&S.y_full[yb]);
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (warp 1, lane 0)
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32_bmn(128, NC);  // B (Z) is MN-major; N = NC = 64
-      const uint32_t zbase = smem_u32(zs);
-      const int ksteps = K3p / 16, ke_steps = P.Ke / 16;
-      const int halfk = K3p / 2;
-      int it = 0;
-      uint32_t g_t = 0, g_acc = 0;
-      for (int p = p_begin; p < p_end; ++p, ++it) {
-        for (int tt = 0; tt < T; ++tt, ++g_t) {
-          const int yb = g_t & 1;
-          mbar_wait(&S.y_full[yb], (g_t >> 1) & 1);
-          tc_fence_after();
-          const uint32_t a_hi0 = tmem + 256 + (uint32_t)(yb * K3p);
-          for (int rc = 0; rc < RC; ++rc, ++g_acc) {
-            const int ab = g_acc & 1;
-            if (tt == 0) mbar_wait(&S.z_full[rc], it & 1);
-            mbar_wait(&S.acc_empty[ab], ((g_acc >> 1) & 1) ^ 1);
-            tc_fence_after();
-            const uint32_t dE = tmem + (uint32_t)(ab * 2 * NC), dO = dE + (uint32_t)NC;
-            const uint32_t bchunk = zbase + (uint32_t)(rc * (NC / 8)) * SBO;
-            const uint64_t bh0 = smem_desc_kmajor_noswz(bchunk, 128, SBO);
-            const uint64_t bl0 = smem_desc_kmajor_noswz(bchunk + part_bytes, 128, SBO);
-            for (int ks = 0; ks < ksteps; ++ks) {
-              const bool odd = ks >= ke_steps;
-              const uint32_t d = odd ? dO : dE;
-              const uint32_t acc0 = (odd ? ks > ke_steps : ks > 0) ? 1u : 0u;
-              const uint32_t a_hi = a_hi0 + ks * 8, a_lo = a_hi + halfk;
-              const uint64_t b_hi = bh0 + (uint64_t)(ks * 16), b_lo = bl0 + (uint64_t)(ks * 16);  // +256 B
-              mma_bf16_ts(d, a_hi, b_hi, idesc, acc0);
-              mma_bf16_ts(d, a_hi, b_lo, idesc, 1u);
-              mma_bf16_ts(d, a_lo, b_hi, idesc, 1u);
-            }
-            tc_commit(&S.acc_full[ab]);
-            if (tt == T - 1) tc_commit(&S.z_empty[rc]);
+          if (better(S.red_ve[rb][w], S.red_fe[rb][w], ve, fe)) {
+            ve = S.red_ve[rb][w];
+            fe = S.red_fe[rb][w];
           }
-          tc_commit(&S.y_empty[yb]);
         }
+        // the resolver has consumed slot rb (pair it - 2) before we overwrite it
+        mbar_wait(&S.res_empty[rb], ((it >> 1) & 1) ^ 1);
+        S.res_v[rb] = v;
+        S.res_k[rb] = k;
+        S.res_ve[rb] = ve;
+        S.res_fe[rb] = fe;
+        S.res_p[rb] = p;
+        mbar_arrive(&S.res_full[rb]);
       }
     }
-    __syncwarp();
+  } else {
+    // ---------------- resolver (warp 17): exact (shift, sign) of the pair's winning 8-column group by
+    // recomputing its 16 E / O sums from the same bf16 hi/lo operands (fp32 on CUDA cores), merge with
+    // the exact record, one packed-key atomicMax per pair.
+    const int NWG2 = NWG;
+    uint32_t it = 0;
+    for (int p = p_begin; p < p_end; ++p, ++it) {
+      const int rb = it & 1;
+      mbar_wait(&S.res_full[rb], (it >> 1) & 1);
+      const float v = S.res_v[rb], ve = S.res_ve[rb];
+      const uint32_t key = S.res_k[rb], fe = S.res_fe[rb];
+      const int pp = S.res_p[rb];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.res_empty[rb]);
+      float bv = ve;
+      uint32_t bf = fe;
+      if (key != 0xffffffffu) {
+        const int T = (int)(key >> 24), cl = (int)((key >> 7) & 0x1ffffu), rrow = (int)(key & 127u);
+        const int r = T * 128 + rrow;
+        const uint8_t* zrow = P.Zop + (size_t)pp * pair_bytes + (size_t)(T * 2 * NWG2) * 2048 + rrow * 16;
+        float es[8], os[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) es[k] = os[k] = 0.f;
+        const __nv_bfloat16* yh = reinterpret_cast<const __nv_bfloat16*>(ys);
+        const __nv_bfloat16* yl = yh + (size_t)ncol * K3p;
+        for (int kk = lane; kk < K3p; kk += 32) {
+          const size_t zo = (size_t)(kk >> 3) * 2048 + (kk & 7) * 2;
+          const float zh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(zrow + zo));
+          const float zl = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(zrow + (size_t)NWG2 * 2048 + zo));
+          const bool even = kk < P.Ke;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int cc = cl + k;
+            const size_t yo = (size_t)(cc >> 3) * (K3p / 8) * 64 + (size_t)(kk >> 3) * 64 + (cc & 7) * 8 + (kk & 7);
+            const float a = __bfloat162float(yh[yo]), b = __bfloat162float(yl[yo]);
+            const float pr = fmaf(zh, a, fmaf(zh, b, zl * a));
+            if (even)
+              es[k] += pr;
+            else
+              os[k] += pr;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            es[k] += __shfl_xor_sync(0xffffffffu, es[k], o);
+            os[k] += __shfl_xor_sync(0xffffffffu, os[k], o);
+          }
+        // the winning column (ties -> smaller flat index); the value reported is the tensor-core one
+        float bx = -INFINITY;
+        uint32_t bfl = 0xffffffffu;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float x = es[k] + fabsf(os[k]);
+          const int t = os[k] >= 0.f ? s_rep[cl + k] : s_part[cl + k];
+          const uint32_t f = (uint32_t)t * (uint32_t)n + (uint32_t)r;
+          if (better(x, f, bx, bfl)) {
+            bx = x;
+            bfl = f;
+          }
+        }
+        if (better(v, bfl, bv, bf)) {
+          bv = v;
+          bf = bfl;
+        }
+      }
+      if (lane == 0 && bf != 0xffffffffu) {
+        int i, j;
+        pair_of(P.pb, pp, i, j);
+        const uint32_t tt2 = bf / (uint32_t)n, rr = bf - tt2 * (uint32_t)n;
+        const uint32_t gflat = ((uint32_t)(P.tm_off + j) * (uint32_t)P.N_t + tt2) * (uint32_t)n + rr;
+        const unsigned long long kk = pack_key(bv, gflat);
+        if (P.img_keys) atomicMax(&P.img_keys[i], kk);
+        if (P.pair_keys) atomicMax(&P.pair_keys[(size_t)i * P.n_tm_local + j], kk);
+      }
+      __syncwarp();
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+}
+
+static size_t s3_smem_bytes(int ncol, int K3p) {
+  const size_t meta = (((size_t)ncol * 8 + ncol / 8) + 512 + 1023) & ~(size_t)1023;
+  return 1024 + meta + (size_t)ncol * K3p * 4;
 }
 
 // ---------------------------------------------------------------- Step 1 (tensor cores)
@@ -640,7 +751,8 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
   const int Hp = P.H_plus;
   const size_t rows_bytes = ((size_t)maxz * st * sizeof(float2) + 127) & ~(size_t)127;
   auto rowbuf = [&](int b) { return reinterpret_cast<float2*>(s2raw + (size_t)b * rows_bytes); };
-  uint8_t* stg = s2raw + 2 * rows_bytes;  // [2][n/8][128 B] (one 8-column group)
+  constexpr int RS = n + n / E;          // padded staging row (words): index r + r / E
+  uint32_t* stg = reinterpret_cast<uint32_t*>(s2raw + 2 * rows_bytes);  // [part][word 4][RS]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int total = npair * C.n;
 
@@ -688,8 +800,7 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
       cp_async_wait<0>();
     }
     // clear the staged group (padding columns must stay zero)
-    for (int idx = threadIdx.x; idx < 2 * (n / 8) * 8; idx += blockDim.x)
-      reinterpret_cast<uint4*>(stg)[idx] = make_uint4(0u, 0u, 0u, 0u);
+    for (int idx = threadIdx.x; idx < 8 * RS; idx += blockDim.x) stg[idx] = 0u;
     __syncthreads();
     const float2* rows = rowbuf(k & 1);
     const int ch = item % C.n, pr = item / C.n;
@@ -733,55 +844,46 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
           acc = cmulf(acc, step);
         }
       }
-      const int ncol = l > 0 ? 2 : 1;
+      // stage the term's column(s) as packed bf16 words: ell > 0 -> word (Re, Im) of this term;
+      // ell = 0 -> one 16-bit half of a word shared with the neighbouring ell = 0 term.
+      const int kl = col - 8 * g0;  // 0..7 within the group
+      const int w = kl >> 1;
+      uint32_t* shi = stg + (size_t)w * RS;
+      uint32_t* slo = stg + (size_t)(4 + w) * RS;
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        if (cc >= ncol) break;
-        const int kl = col + cc - 8 * g0;  // 0..7 within the group
-        const int r0 = E * d;
-        if constexpr (E >= 8) {
-#pragma unroll
-          for (int u = 0; u < E / 8; ++u) {
-            uint32_t h[4], lo[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 a0 = x[rv(8 * u + 2 * e)], a1 = x[rv(8 * u + 2 * e + 1)];
-              split2_bf16(cc == 0 ? a0.x : a0.y, cc == 0 ? a1.x : a1.y, h[e], lo[e]);
-            }
-            const int rg = r0 / 8 + u;
-            const uint32_t o = (uint32_t)rg * 128 + (uint32_t)(((kl ^ rg) & 7) * 16);
-            *reinterpret_cast<uint4*>(stg + o) = make_uint4(h[0], h[1], h[2], h[3]);
-            *reinterpret_cast<uint4*>(stg + (n / 8) * 128 + o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-          }
+      for (int c = 0; c < E; ++c) {
+        const int pi = c + (E + 1) * d;  // padded index of r = c + E d (conflict-free across lanes)
+        const float2 a0 = x[rv(c)];
+        if (l > 0) {
+          uint32_t hh, ll;
+          split2_bf16(a0.x, a0.y, hh, ll);
+          shi[pi] = hh;
+          slo[pi] = ll;
         } else {
-          uint32_t h[E / 2], lo[E / 2];
-#pragma unroll
-          for (int e = 0; e < E / 2; ++e) {
-            const float2 a0 = x[rv(2 * e)], a1 = x[rv(2 * e + 1)];
-            split2_bf16(cc == 0 ? a0.x : a0.y, cc == 0 ? a1.x : a1.y, h[e], lo[e]);
-          }
-          const int rg = r0 / 8;
-          const uint32_t o = (uint32_t)rg * 128 + (uint32_t)(((kl ^ rg) & 7) * 16) + (r0 % 8) * 2;
-          if constexpr (E == 4) {
-            *reinterpret_cast<uint2*>(stg + o) = make_uint2(h[0], h[1]);
-            *reinterpret_cast<uint2*>(stg + (n / 8) * 128 + o) = make_uint2(lo[0], lo[1]);
-          } else {
-            *reinterpret_cast<uint32_t*>(stg + o) = h[0];
-            *reinterpret_cast<uint32_t*>(stg + (n / 8) * 128 + o) = lo[0];
-          }
+          const __nv_bfloat16 hb = __float2bfloat16_rn(a0.x);
+          const __nv_bfloat16 lb = __float2bfloat16_rn(a0.x - __bfloat162float(hb));
+          reinterpret_cast<__nv_bfloat16*>(shi + pi)[kl & 1] = hb;
+          reinterpret_cast<__nv_bfloat16*>(slo + pi)[kl & 1] = lb;
         }
       }
     }
     __syncthreads();
-    // write out the column group: per (part, r-group) one 128-byte core matrix
-    const size_t part_bytes = (size_t)n * P.K3p * 2;
-    uint8_t* base = Zop + (size_t)pr * 2 * part_bytes + (size_t)g0 * 128;
-    const uint32_t SBO = (uint32_t)P.K3p * 16;
-    for (int idx = threadIdx.x; idx < 2 * (n / 8) * 8; idx += blockDim.x) {
-      const int row = idx & 7, rest = idx >> 3;
-      const int rg = rest % (n / 8), part = rest / (n / 8);
-      const uint4 v = *reinterpret_cast<const uint4*>(stg + part * (n / 8) * 128 + rg * 128 + ((row ^ rg) & 7) * 16);
-      *reinterpret_cast<uint4*>(base + part * part_bytes + (size_t)rg * SBO + row * 16) = v;
+    // write out the word group: per (r-tile, part, row) 16 bytes; rows of one (r-tile, part) contiguous
+    {
+      const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
+      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)g0 * 2048;
+      for (int idx = threadIdx.x; idx < NRT * 2 * 128; idx += blockDim.x) {
+        const int row = idx & 127, rest = idx >> 7;
+        const int part = rest & 1, T = rest >> 1;
+        const int r = T * 128 + row;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (r < n) {
+          const int pi = r + r / E;
+          const uint32_t* sp = stg + (size_t)(4 * part) * RS + pi;
+          v = make_uint4(sp[0], sp[RS], sp[2 * RS], sp[3 * RS]);
+        }
+        *reinterpret_cast<uint4*>(base + (size_t)((T * 2 + part) * NWG) * 2048 + row * 16) = v;
+      }
     }
     __syncthreads();
   }
@@ -789,7 +891,7 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
 }
 
 static size_t step2_smem(const TcPlan& tc, int n) {
-  return 2 * (((size_t)tc.s2_maxz * (n + 1) * sizeof(float2) + 127) & ~(size_t)127) + (size_t)2 * (n / 8) * 128;
+  return 2 * (((size_t)tc.s2_maxz * (n + 1) * sizeof(float2) + 127) & ~(size_t)127) + (size_t)8 * (n + 32) * 4;
 }
 
 static void launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, int formB,
@@ -981,46 +1083,74 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
     }
   }
   tc.n_rep = (int)rep.size();
-  tc.n_ttiles = (tc.n_rep + 127) / 128;
-  const int rows = tc.n_ttiles * 128, hk = K3p / 2;
-  rep.resize(rows, -1);
-  partner.resize(rows, -1);
-  std::vector<uint32_t> yh((size_t)rows * hk, 0u), yl((size_t)rows * hk, 0u);
-  for (int rr = 0; rr < tc.n_rep; ++rr) {
-    const int t = rep[rr];
-    for (int j = 0; j < hk; ++j) {
-      const float x0 = Y3[(size_t)t * K3p + 2 * j], x1 = Y3[(size_t)t * K3p + 2 * j + 1];
-      const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
-      const __nv_bfloat16 l0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
-      const __nv_bfloat16 l1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
-      uint16_t a, b, c, d;
-      std::memcpy(&a, &h0, 2);
-      std::memcpy(&b, &h1, 2);
-      std::memcpy(&c, &l0, 2);
-      std::memcpy(&d, &l1, 2);
-      yh[(size_t)rr * hk + j] = (uint32_t)a | ((uint32_t)b << 16);
-      yl[(size_t)rr * hk + j] = (uint32_t)c | ((uint32_t)d << 16);
-    }
-  }
-  if (cudaMalloc(&tc.d_rep, rows * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&tc.d_partner, rows * sizeof(int)) != cudaSuccess) {
-    msg = "tensor-core engine: allocation failed";
-    return FTK_ENOMEM;
-  }
-  cudaMemcpy(tc.d_rep, rep.data(), rows * sizeof(int), cudaMemcpyHostToDevice);
-  cudaMemcpy(tc.d_partner, partner.data(), rows * sizeof(int), cudaMemcpyHostToDevice);
-  if (cudaMalloc(&tc.d_Yh, yh.size() * 4) != cudaSuccess || cudaMalloc(&tc.d_Yl, yl.size() * 4) != cudaSuccess) {
-    msg = "tensor-core engine: allocation failed";
-    return FTK_ENOMEM;
-  }
-  cudaMemcpy(tc.d_Yh, yh.data(), yh.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(tc.d_Yl, yl.data(), yl.size() * 4, cudaMemcpyHostToDevice);
-  const size_t smem = 1024 + (size_t)4 * pm.n_psi * K3p;
-  if (smem > 227 * 1024) {
-    msg = "tensor-core engine: Step-3 pair operand exceeds shared memory";
+  tc.NRT = (pm.n_psi + 127) / 128;
+  // Step-3 chunk width NCH (N of the MMA): TMEM holds two D buffers (E and O, 2 NCH columns each) and
+  // two A slots (K3p columns each); a rep-group's Y image must fit in shared memory.
+  const int nmax = std::min(256, ((512 - 2 * K3p) / 4) / 16 * 16);
+  if (nmax < 16) {
+    msg = "tensor-core engine: K3p too large for the Step-3 TMEM layout";
     return FTK_EINVAL;
   }
-  cudaFuncSetAttribute(k_step3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem_cap = 232448;  // 227 KB opt-in dynamic shared memory per block
+  int rg = 0;
+  for (int G = 1;; ++G) {
+    if (G > TcPlan::MAXG) {
+      msg = "tensor-core engine: shift list too long for the Step-3 rep-groups";
+      return FTK_EINVAL;
+    }
+    rg = (tc.n_rep + G - 1) / G;
+    const int nch = (rg + nmax - 1) / nmax;
+    const int NCH = ((rg + nch - 1) / nch + 15) / 16 * 16;
+    if (s3_smem_bytes(nch * NCH, K3p) <= smem_cap) {
+      tc.G = G;
+      tc.NCH = NCH;
+      for (int g = 0; g < G; ++g) tc.g_nch[g] = nch;
+      break;
+    }
+  }
+  const int ncol_g = tc.g_nch[0] * tc.NCH;
+  tc.ncol = tc.G * ncol_g;
+  std::vector<int> colrep(tc.ncol, -1), colpart(tc.ncol, -1);
+  std::vector<uint8_t> colfast(tc.ncol / 8, 0);
+  const size_t ygroup = (size_t)4 * ncol_g * K3p;
+  std::vector<uint16_t> yimg(ygroup / 2 * tc.G, 0);
+  for (int g = 0; g < tc.G; ++g) {
+    tc.g_col0[g] = g * ncol_g;
+    tc.g_yoff[g] = (long long)(g * ygroup);
+    for (int c = 0; c < ncol_g; ++c) {
+      const int rr = g * rg + c;
+      if (c >= rg || rr >= tc.n_rep) continue;
+      colrep[g * ncol_g + c] = rep[rr];
+      colpart[g * ncol_g + c] = partner[rr];
+      const int t = rep[rr];
+      for (int k = 0; k < K3p; ++k) {
+        const float x = Y3[(size_t)t * K3p + k];
+        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+        const size_t off = (size_t)(c / 8) * (K3p / 8) * 64 + (size_t)(k / 8) * 64 + (c % 8) * 8 + (k % 8);
+        std::memcpy(&yimg[g * ygroup / 2 + off], &hi, 2);
+        std::memcpy(&yimg[g * ygroup / 2 + (size_t)ncol_g * K3p + off], &lo, 2);
+      }
+    }
+  }
+  for (int c8 = 0; c8 < tc.ncol / 8; ++c8) {
+    bool f = true;
+    for (int k = 0; k < 8; ++k) f = f && colrep[c8 * 8 + k] >= 0 && colpart[c8 * 8 + k] >= 0;
+    colfast[c8] = f ? 1 : 0;
+  }
+  if (cudaMalloc(&tc.d_colrep, tc.ncol * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&tc.d_colpart, tc.ncol * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&tc.d_colfast, colfast.size() + 16) != cudaSuccess ||
+      cudaMalloc(&tc.d_Ysm, yimg.size() * 2) != cudaSuccess) {
+    msg = "tensor-core engine: allocation failed";
+    return FTK_ENOMEM;
+  }
+  cudaMemcpy(tc.d_colrep, colrep.data(), tc.ncol * sizeof(int), cudaMemcpyHostToDevice);
+  cudaMemcpy(tc.d_colpart, colpart.data(), tc.ncol * sizeof(int), cudaMemcpyHostToDevice);
+  cudaMemcpy(tc.d_colfast, colfast.data(), colfast.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(tc.d_Ysm, yimg.data(), yimg.size() * 2, cudaMemcpyHostToDevice);
+  tc.s3_smem = s3_smem_bytes(ncol_g, K3p);
+  cudaFuncSetAttribute(k_step3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.s3_smem);
   if (pm.n_k % 16 != 0 || pm.n_k > 128) {
     msg = "tensor-core engine: n_k must be a multiple of 16 and <= 128";
     return FTK_EINVAL;
@@ -1068,14 +1198,14 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
 }
 
 void tc_plan_free(TcPlan& tc) {
-  cudaFree(tc.d_Yh);
-  cudaFree(tc.d_Yl);
-  cudaFree(tc.d_Bop);
+  cudaFree(tc.d_Ysm);
+  cudaFree(tc.d_colrep);
+  cudaFree(tc.d_colpart);
+  cudaFree(tc.d_colfast);
   cudaFree(tc.d_Aop);
-  cudaFree(tc.d_rep);
-  cudaFree(tc.d_partner);
-  tc.d_rep = tc.d_partner = nullptr;
-  tc.d_Yh = tc.d_Yl = tc.d_Bop = nullptr;
+  tc.d_Ysm = nullptr;
+  tc.d_colrep = tc.d_colpart = nullptr;
+  tc.d_colfast = nullptr;
   tc.d_Aop = nullptr;
   tc.aop_bytes = 0;
   tc.ready = false;
@@ -1104,8 +1234,8 @@ int tc_prepare_templates(TcPlan&, const float2*, int64_t, const DevPlan&, cudaSt
   return FTK_OK;
 }
 
-size_t tc_bytes_per_pair(const TcPlan&, const DevPlan& P) {
-  return (size_t)P.H_plus * P.n_psi * sizeof(float2) + (size_t)P.K3p * P.n_psi * sizeof(float);
+size_t tc_bytes_per_pair(const TcPlan& tc, const DevPlan& P) {
+  return (size_t)P.H_plus * P.n_psi * sizeof(float2) + (size_t)tc.NRT * 128 * P.K3p * 4;
 }
 
 ftk_status_t tc_block_shape(const TcPlan&, const DevPlan&, int engine, int64_t NI, int64_t NJ, int64_t cap,
@@ -1125,27 +1255,34 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
                      unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
                      cudaStream_t s) {
   S3Params prm;
+  std::memset(&prm, 0, sizeof prm);
   prm.Zop = Zop;
-  prm.Yh = tc.d_Yh;
-  prm.Yl = tc.d_Yl;
+  prm.Ysm = tc.d_Ysm;
+  prm.colrep = tc.d_colrep;
+  prm.colpart = tc.d_colpart;
+  prm.colfast = tc.d_colfast;
   prm.pb = pb;
   prm.n = P.n_psi;
   prm.K3p = P.K3p;
   prm.Ke = P.Ke;
   prm.N_t = P.N_t;
-  prm.T = tc.n_ttiles;
-  prm.NC = 64;
-  prm.RC = P.n_psi / prm.NC;
-  prm.rep_t = tc.d_rep;
-  prm.partner = tc.d_partner;
+  prm.NRT = tc.NRT;
+  prm.NCH = tc.NCH;
+  prm.G = tc.G;
+  for (int g = 0; g < tc.G; ++g) {
+    prm.g_col0[g] = tc.g_col0[g];
+    prm.g_nch[g] = tc.g_nch[g];
+    prm.g_yoff[g] = tc.g_yoff[g];
+  }
   prm.tm_off = tm_off;
   prm.n_tm_local = n_tm_local;
   prm.img_keys = img_keys;
   prm.pair_keys = pair_keys;
   prm.land = land;
-  const size_t smem = 1024 + (size_t)4 * P.n_psi * P.K3p;
-  const int grid = pb.count < tc.num_sms ? pb.count : tc.num_sms;
-  k_step3_tc<<<grid, S3_THREADS, smem, s>>>(prm);
+  int cpg = tc.num_sms / tc.G;
+  if (cpg > pb.count) cpg = pb.count;
+  if (cpg < 1) cpg = 1;
+  k_step3_tc<<<cpg * tc.G, S3_THREADS, tc.s3_smem, s>>>(prm);
 }
 
 void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const PairBlock& pb, const DevPlan& P,

@@ -11,17 +11,21 @@
 namespace ftk {
 
 struct TcPlan {
+  static constexpr int MAXG = 16;  // max rep-groups (Y slices) of Step 3
   bool ready = false;
   int K3p = 0;          // Step-3 contraction length padded to a multiple of 16
-  int n_ttiles = 0;     // ceil(n_rep / 128)
-  int n_rep = 0;        // representative shifts (+-delta pairs share a row)
+  int n_rep = 0;        // representative shifts (+-delta pairs share one column pair E/O)
   int Ke = 0;           // even-ell column block length
-  int* d_rep = nullptr;
-  int* d_partner = nullptr;
-  uint32_t* d_Yh = nullptr;  // [n_ttiles*128][K3p/2] packed bf16x2, hi part
-  uint32_t* d_Yl = nullptr;  // lo part
+  // Step 3 (k_step3_tc): columns = representative shifts in rep-groups of nch[g] chunks of NCH
+  int NCH = 0, G = 0, NRT = 0, ncol = 0;
+  int g_col0[MAXG] = {0}, g_nch[MAXG] = {0};
+  long long g_yoff[MAXG] = {0};
+  int* d_colrep = nullptr;
+  int* d_colpart = nullptr;
+  uint8_t* d_colfast = nullptr;
+  uint8_t* d_Ysm = nullptr;   // per group: shared-memory image of Y3 hi/lo (B operand)
+  size_t s3_smem = 0;
   // Step 1 operands
-  uint32_t* d_Bop = nullptr;   // (unused; templates are generated in-kernel)
   uint8_t* d_Aop = nullptr;    // images, bf16 hi/lo split, Step-1 K-major tiles [p][tile][kchunk][part]...
   size_t aop_bytes = 0;
   int NIT = 0, KCH = 64, NKCH = 0;
