@@ -83,6 +83,7 @@ DevPlan devplan(ftk_plan_t p) {
   d.npads = p->npads;
   d.pads = p->d_pads;
   d.K3p = p->K3p;
+  d.Hs = (p->pm.H_plus + 1) / 2 * 2;
   int lm = 0;
   for (const auto& t : p->pm.terms)
     if (t.ell >= 0) lm = std::max(lm, t.ell);

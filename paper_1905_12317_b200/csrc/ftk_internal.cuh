@@ -67,6 +67,7 @@ __host__ __device__ inline bool best_better(const ftk_best_t& a, const ftk_best_
 // Device plan constants used by every engine.
 struct DevPlan {
   int n_k, n_psi, log2_psi, N_t, H_plus, K3, K3p, ell_max;
+  int Hs;                // row stride (complex) of the engine-0 Step-1 output Zhat' [pair][p][Hs] (H_plus, even)
   int Ke;                // even-ell column block [0, Ke); odd-ell block [Ke, K3p)
   int npads;             // unused (zero) Step-3 columns
   const int* pads;       // [npads]

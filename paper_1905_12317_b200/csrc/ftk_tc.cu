@@ -434,7 +434,7 @@ static size_t s3_smem_bytes(int ncol, int K3p) {
 // so that Zhat_zeta(q) = Zhat'_zeta(q - ell) and Step 2 applies e^{-i ell gamma_r} after the FFT.
 // Real GEMM per p with K' = 2 n_k:  rows (j, zeta, part) of the GENERATED operand c (A, in TMEM):
 //   Re-row = [c_r | -c_i],  Im-row = [c_i | c_r];  columns = images, B = [a_r | a_i] (pre-split, SMEM).
-// Output Zhat' [p][pair][zeta] complex (pair = il * nj + jl within the block).
+// Output Zhat' [pair][p][Hs] complex (pair = il * nj + jl within the block; Hs = H_plus rounded up to even).
 constexpr int S1_THREADS = 10 * 32;
 constexpr int S1_STAGES = 4;
 
@@ -443,11 +443,20 @@ struct S1Params {
   const float2* B;      // template FB coefficients [j][q][m] (local templates)
   const float* g;       // [H_plus][n_k]
   const int* ell;       // [H_plus]
-  float2* Zhat;         // [p][pairs][H_plus]
+  float2* Zhat;         // [pair][p][Hs]
   int i0, ni, j0, nj;   // block (i0 multiple of 128)
-  int n, n_k, Hp, KCH, NKCH, NIT;  // NIT = image tiles per mode in Aop
+  int n, n_k, Hp, Hs, KCH, NKCH, NIT;  // NIT = image tiles per mode in Aop
   int F, NCT;           // F = nj * Hp flattened (j, zeta) columns, NCT = ceil(F / 64)
 };
+
+// Unit order: u -> (mode p, column tile ct) with p = 8 p_hi + p_lo, p_lo fastest, then ct, then p_hi.
+// The ~148 units in flight then share 8 image-operand modes (L2-resident) and write 8 consecutive
+// p-rows of each of their pairs' Zhat' rows together (contiguous runs merged in L2).
+__device__ __forceinline__ void s1_unit(int u, int NCT, int& p, int& ct) {
+  const int p_lo = u & 7, rest = u >> 3;
+  ct = rest % NCT;
+  p = (rest / NCT) * 8 + p_lo;
+}
 
 struct S1Smem {
   uint64_t st_full[S1_STAGES], st_empty[S1_STAGES];
@@ -491,7 +500,8 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
     if (lane == 0) {
       uint32_t g_st = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int p = u / P.NCT;
+        int p, ct_unused;
+        s1_unit(u, P.NCT, p, ct_unused);
         for (int t = 0; t < nit; ++t) {
           for (int kc = 0; kc < P.NKCH; ++kc, ++g_st) {
             const int s = g_st % S1_STAGES;
@@ -552,7 +562,8 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
     const int half = nk / 2;  // u32 columns per K' half
     uint32_t g_u = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++g_u) {
-      const int p = u / P.NCT, ct = u - p * P.NCT;
+      int p, ct;
+      s1_unit(u, P.NCT, p, ct);
       const int f = ct * 64 + c;
       mbar_wait(&S.a_empty, (g_u & 1) ^ 1);
       tc_fence_after();
@@ -602,10 +613,21 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
     const int row = q * 32 + lane;
     const int ew = warp - 6;  // 0..3
     uint32_t g_acc = 0;
-    const size_t npair = (size_t)P.ni * P.nj;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int p = u / P.NCT, ct = u - p * P.NCT;
+      int p, ct;
+      s1_unit(u, P.NCT, p, ct);
       const int nvalid = min(128, 2 * (P.F - ct * 64));
+      // this lane's two complex columns cc = lane, lane + 32 -> offsets (template jl, term z) in Zhat'
+      long long coff[2];
+      bool cval[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = lane + 32 * h;
+        const int f = ct * 64 + cc;
+        const int jl = f / P.Hp, z = f - jl * P.Hp;
+        cval[h] = 2 * cc < nvalid;
+        coff[h] = (long long)jl * n * P.Hs + z;
+      }
       for (int t = 0; t < nit; ++t, ++g_acc) {
         const int ab = g_acc & 1;
         mbar_wait(&S.acc_full[ab], (g_acc >> 1) & 1);
@@ -621,16 +643,15 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
         tc_fence_before();
         mbar_arrive(&S.acc_empty[ab]);
         named_bar(2, 128);
-        // coalesced write-out: image ii -> 128 consecutive floats (rows) at pair (il, ct*64 ...)
+        // write-out: image ii, complex column cc = (template jl, term z) -> Zhat'[pair (il, jl)][p][z]
+        // (runs of consecutive terms of one pair row)
         for (int ii = ew; ii < 128; ii += 4) {
           const int il = t * 128 + ii;  // local image index within the block
           if (il >= P.ni) continue;
-          float2* dst = P.Zhat + ((size_t)p * npair + (size_t)il * P.nj) * P.Hp + (size_t)ct * 64;
+          float2* dst = P.Zhat + ((size_t)il * P.nj * n + p) * P.Hs;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int cc = lane + 32 * h;  // complex column within the tile
-            if (2 * cc < nvalid) dst[cc] = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * cc);
-          }
+          for (int h = 0; h < 2; ++h)
+            if (cval[h]) dst[coff[h]] = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
         }
         named_bar(2, 128);
       }
@@ -686,18 +707,26 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 
 // Step 2 for the tensor-core engine (Eq. fbk3 Step 2, Form B):
 //   Z_zeta(r) = e^{-2 pi i ell r / n} sum_p Zhat'_zeta(p) e^{-2 pi i p r / n},   (q = p + ell)
-// read from Zhat' [p][pair][zeta]; written as the Step-3 B-operand image (real rows of reading R13):
-// bf16 hi/lo, MN-major INTERLEAVE canonical layout per pair, [part][r/8][K3p/8][k%8][r%8].
-// One CTA = (pair, chunk of whole 8-column groups); one warp per term row.
+// read from Zhat' [pair][p][Hs] (Form B, written by k_step1_tc) or Zhat [pair][zeta][q] (Form A, the
+// explicit-pair path); written as the Step-3 A operand rows (real columns of reading R13), bf16 hi/lo
+// packed in 32-bit words (two K columns per word): Zop [pair][r-tile][part][word group][row 128][16 B].
+// Work item = (pair, block of two word groups = 16 Step-3 columns, <= 16 terms); persistent CTAs, two
+// per SM.  The item's input rows are gathered with cp.async into a [p][17] shared-memory buffer (odd
+// stride: conflict-free column reads), one warp per term row.
 // FFT: four-step decomposition n = 32 E, p = a + 32 b (a = lane), r = c + E d:
 //   (A) per lane an E-point DFT over b in registers, (B) twiddle w_n^{a c}, (C) a 32-point radix-2
 //   DIF across the warp with shfl_xor (output index d lands on lane bitrev5(d)).
-// Output core rows are staged in shared memory (16-byte slot XOR-swizzled by the r-group) and written
-// out as contiguous 128-byte core matrices.
+// Output words are staged per (group, part, word) in padded rows (index r + r / E: conflict-free) and
+// written out as contiguous 2 KB row blocks.
 struct S2Chunks {
   int n;
   int zs[32], ze[32], g0[32];
 };
+struct S2Blocks {
+  int nb;
+  int zs[16], ze[16];  // term range of block b (word groups 2b, 2b + 1)
+};
+constexpr int S2_ROWSTRIDE = 17;
 
 __device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -740,45 +769,28 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Persistent CTAs over work items (pair, column group) with the group fastest; the rows of the next
-// item are gathered with cp.async into the second buffer while the current item is transformed.
 template <int E>
 __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
-                                                      int npair, int formB, DevPlan P, S2Chunks C, int maxz) {
+                                                      int npair, int formB, DevPlan P, S2Blocks B) {
   extern __shared__ __align__(16) uint8_t s2raw[];
-  constexpr int n = 32 * E, st = n + 1;
+  constexpr int n = 32 * E, S = S2_ROWSTRIDE;
   constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
-  const int Hp = P.H_plus;
-  const size_t rows_bytes = ((size_t)maxz * st * sizeof(float2) + 127) & ~(size_t)127;
-  auto rowbuf = [&](int b) { return reinterpret_cast<float2*>(s2raw + (size_t)b * rows_bytes); };
-  constexpr int RS = n + n / E;          // padded staging row (words): index r + r / E
-  uint32_t* stg = reinterpret_cast<uint32_t*>(s2raw + 2 * rows_bytes);  // [part][word 4][RS]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int total = npair * C.n;
-
-  auto issue = [&](int item, float2* rows) {
-    const int ch = item % C.n, pr = item / C.n;
-    const int zs = C.zs[ch], nz = C.ze[ch] - zs;
-    if (formB) {  // Zhat' [p][pair][zeta]: lanes = 4 p-rows x 8 consecutive zeta
-      const int zl = lane & 7, pl = lane >> 3;
-      if (zl < nz)
-        for (int p = warp * 4 + pl; p < n; p += nw * 4)
-          cp_async8(rows + zl * st + p, Zhat + ((size_t)p * npair + pr) * Hp + zs + zl);
-    } else {      // Zhat [pair][zeta][q]
-      for (int idx = threadIdx.x; idx < nz * n; idx += blockDim.x) {
-        const int z = idx / n, q = idx - z * n;
-        cp_async8(rows + z * st + q, Zhat + ((size_t)pr * Hp + zs + z) * n + q);
-      }
-    }
-    cp_async_commit();
-  };
+  constexpr int RS = n + n / E;  // padded staging row (words): index r + r / E
+  float2* rows = reinterpret_cast<float2*>(s2raw);                            // [n][S]
+  uint32_t* stg = reinterpret_cast<uint32_t*>(s2raw + (size_t)n * S * 8);     // [group 2][part 2][word 4][RS]
+  // warp index made provably warp-uniform (shfl from lane 0) so the shuffles below sit in convergent code
+  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int nw = blockDim.x >> 5;
+  const int total = npair * B.nb;
+  const int Hp = P.H_plus, Hs = P.Hs;
+  const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
 
   // per-lane constant twiddles
-  float2 wc[5];
+  float2 wc[5];  // stage twiddle of this lane (1 on the upper lanes of each butterfly)
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
     const int h = 16 >> s;
-    wc[s] = tw_full(P.tw, (lane & (h - 1)) * (16 / h) * (n / 32), n);
+    wc[s] = (lane & h) ? tw_full(P.tw, (lane & (h - 1)) * (16 / h) * (n / 32), n) : make_float2(1.f, 0.f);
   }
   const float2 wlane = tw_full(P.tw, lane & (n - 1), n);
   const int d = __brev(lane) >> 27;
@@ -789,26 +801,28 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
     return r;
   };
 
-  int item = blockIdx.x;
-  if (item < total) issue(item, rowbuf(0));
-  for (int k = 0; item < total; item += gridDim.x, ++k) {
-    const int next = item + gridDim.x;
-    if (next < total) {
-      issue(next, rowbuf((k + 1) & 1));
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int b = item % B.nb, pr = item / B.nb;
+    const int zs = B.zs[b], nz = B.ze[b] - zs;
+    // ---- gather the item's input rows
+    if (formB) {  // [pair][p][Hs]: 16 threads per p-row, consecutive terms
+      const float2* src = Zhat + (size_t)pr * n * Hs + zs;
+      const int zl = threadIdx.x & 15;
+      if (zl < nz)
+        for (int p = threadIdx.x >> 4; p < n; p += blockDim.x >> 4) cp_async8(rows + p * S + zl, src + (size_t)p * Hs + zl);
+    } else {      // [pair][zeta][q]
+      const float2* src = Zhat + ((size_t)pr * Hp + zs) * n;
+      for (int z = 0; z < nz; ++z)
+        for (int q = threadIdx.x; q < n; q += blockDim.x) cp_async8(rows + q * S + z, src + (size_t)z * n + q);
     }
-    // clear the staged group (padding columns must stay zero)
-    for (int idx = threadIdx.x; idx < 8 * RS; idx += blockDim.x) stg[idx] = 0u;
+    cp_async_commit();
+    for (int idx = threadIdx.x; idx < 16 * RS; idx += blockDim.x) stg[idx] = 0u;  // padding columns stay zero
+    cp_async_wait<0>();
     __syncthreads();
-    const float2* rows = rowbuf(k & 1);
-    const int ch = item % C.n, pr = item / C.n;
-    const int zs = C.zs[ch], nz = C.ze[ch] - zs, g0 = C.g0[ch];
-    for (int z = warp; z < nz; z += nw) {
+    for (int zz = warp; zz < nz; zz += nw) {
       float2 x[E];
 #pragma unroll
-      for (int bb = 0; bb < E; ++bb) x[bb] = rows[z * st + lane + 32 * bb];
+      for (int bb = 0; bb < E; ++bb) x[bb] = rows[(lane + 32 * bb) * S + zz];
       dft_regs<E>(x, P.tw, n);  // (A): natural-order result in x[rv(c)]
       {                         // (B) x_c *= w_n^{lane c} by recurrence
         float2 acc = wlane;
@@ -819,22 +833,19 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
         }
       }
 #pragma unroll
-      for (int s = 0; s < 5; ++s) {  // (C) 32-point DIF across lanes
+      for (int s = 0; s < 5; ++s) {  // (C) 32-point DIF across lanes (branch-free butterfly)
         const int h = 16 >> s;
-        const bool lower = (lane & h) != 0;
+        const float sg = (lane & h) ? -1.f : 1.f;  // upper lane: x + x', lower lane: (x' - x) w
 #pragma unroll
         for (int c = 0; c < E; ++c) {
           const float px = __shfl_xor_sync(0xffffffffu, x[c].x, h);
           const float py = __shfl_xor_sync(0xffffffffu, x[c].y, h);
-          if (!lower) {
-            x[c] = make_float2(x[c].x + px, x[c].y + py);
-          } else {
-            x[c] = cmulf(make_float2(px - x[c].x, py - x[c].y), wc[s]);
-          }
+          x[c] = cmulf(make_float2(fmaf(sg, x[c].x, px), fmaf(sg, x[c].y, py)), wc[s]);
         }
       }
       // lane holds X[c + E d] in x[rv(c)]; Form-B twiddle e^{-2 pi i ell (c + E d) / n}
-      const int l = P.ell[zs + z], col = P.col[zs + z];
+      const int z = zs + zz;
+      const int l = P.ell[z], col = P.col[z];
       if (formB) {
         float2 acc = tw_full(P.tw, (l * E * d) & (n - 1), n);
         const float2 step = tw_full(P.tw, l & (n - 1), n);
@@ -844,12 +855,12 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
           acc = cmulf(acc, step);
         }
       }
-      // stage the term's column(s) as packed bf16 words: ell > 0 -> word (Re, Im) of this term;
-      // ell = 0 -> one 16-bit half of a word shared with the neighbouring ell = 0 term.
-      const int kl = col - 8 * g0;  // 0..7 within the group
-      const int w = kl >> 1;
-      uint32_t* shi = stg + (size_t)w * RS;
-      uint32_t* slo = stg + (size_t)(4 + w) * RS;
+      // stage: ell > 0 -> word (Re, Im) of this term; ell = 0 -> one 16-bit half of a word shared with
+      // the neighbouring ell = 0 term
+      const int kl = col - 16 * b;  // 0..15 within the block
+      const int grp = kl >> 3, w = (kl & 7) >> 1;
+      uint32_t* shi = stg + (size_t)((grp * 2 + 0) * 4 + w) * RS;
+      uint32_t* slo = stg + (size_t)((grp * 2 + 1) * 4 + w) * RS;
 #pragma unroll
       for (int c = 0; c < E; ++c) {
         const int pi = c + (E + 1) * d;  // padded index of r = c + E d (conflict-free across lanes)
@@ -868,46 +879,44 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
       }
     }
     __syncthreads();
-    // write out the word group: per (r-tile, part, row) 16 bytes; rows of one (r-tile, part) contiguous
+    // ---- write out the two word groups: per (group, r-tile, part) 128 rows x 16 B contiguous
     {
-      const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
-      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)g0 * 2048;
-      for (int idx = threadIdx.x; idx < NRT * 2 * 128; idx += blockDim.x) {
+      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)(2 * b) * 2048;
+      for (int idx = threadIdx.x; idx < 2 * NRT * 2 * 128; idx += blockDim.x) {
         const int row = idx & 127, rest = idx >> 7;
-        const int part = rest & 1, T = rest >> 1;
+        const int part = rest & 1, T = (rest >> 1) % NRT, grp = (rest >> 1) / NRT;
         const int r = T * 128 + row;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (r < n) {
           const int pi = r + r / E;
-          const uint32_t* sp = stg + (size_t)(4 * part) * RS + pi;
+          const uint32_t* sp = stg + (size_t)((grp * 2 + part) * 4) * RS + pi;
           v = make_uint4(sp[0], sp[RS], sp[2 * RS], sp[3 * RS]);
         }
-        *reinterpret_cast<uint4*>(base + (size_t)((T * 2 + part) * NWG) * 2048 + row * 16) = v;
+        *reinterpret_cast<uint4*>(base + (size_t)((T * 2 + part) * NWG + grp) * 2048 + row * 16) = v;
       }
     }
     __syncthreads();
   }
-  cp_async_wait<0>();
 }
 
-static size_t step2_smem(const TcPlan& tc, int n) {
-  return 2 * (((size_t)tc.s2_maxz * (n + 1) * sizeof(float2) + 127) & ~(size_t)127) + (size_t)8 * (n + 32) * 4;
+static size_t step2_smem(int n) {
+  const int E = n / 32;
+  return (size_t)n * S2_ROWSTRIDE * 8 + (size_t)16 * (n + n / E) * 4;
 }
 
 static void launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, int formB,
                              const DevPlan& P, cudaStream_t s) {
-  S2Chunks C;
-  std::memcpy(&C, &tc.s2_chunks, sizeof C);
-  const size_t smem = step2_smem(tc, P.n_psi);
-  // persistent: two CTAs per SM (shared memory and registers allow two)
-  const int items = C.n * npair;
+  S2Blocks B;
+  std::memcpy(&B, &tc.s2_blocks, sizeof B);
+  const size_t smem = step2_smem(P.n_psi);
+  const int items = B.nb * npair;
   dim3 grid(items < 2 * tc.num_sms ? items : 2 * tc.num_sms);
   switch (P.n_psi) {
-    case 64: k_step2_fft<2><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, C, tc.s2_maxz); break;
-    case 128: k_step2_fft<4><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, C, tc.s2_maxz); break;
-    case 256: k_step2_fft<8><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, C, tc.s2_maxz); break;
-    case 512: k_step2_fft<16><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, C, tc.s2_maxz); break;
-    default: k_step2_fft<32><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, C, tc.s2_maxz); break;
+    case 64: k_step2_fft<2><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B); break;
+    case 128: k_step2_fft<4><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B); break;
+    case 256: k_step2_fft<8><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B); break;
+    case 512: k_step2_fft<16><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B); break;
+    default: k_step2_fft<32><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B); break;
   }
 }
 
@@ -1158,35 +1167,40 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   tc.KCH = (2 * pm.n_k) % 64 == 0 ? 64 : 32;
   tc.NKCH = 2 * pm.n_k / tc.KCH;
   cudaFuncSetAttribute(k_step1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
-  // Step-2 chunks: one group of 8 Step-3 columns each (whole terms, see the column map in ftk_capi.cu)
+  // Step-2 blocks: two word groups (16 Step-3 columns, whole terms) each; the device term order makes
+  // the terms of consecutive columns consecutive (see the column map in ftk_capi.cu)
   {
-    std::memset(&tc.s2_chunks, 0, sizeof tc.s2_chunks);
+    std::memset(&tc.s2_blocks, 0, sizeof tc.s2_blocks);
     const int ngroups = K3p / 8;
-    if (ngroups > 32) {
-      msg = "tensor-core engine: too many Step-3 column groups";
+    if (ngroups % 2 != 0 || ngroups / 2 > 16) {
+      msg = "tensor-core engine: unsupported Step-3 column count for Step 2";
       return FTK_EINVAL;
     }
-    int maxz = 1;
-    for (int gi = 0; gi < ngroups; ++gi) {
+    for (int bi = 0; bi < ngroups / 2; ++bi) {
       int zs = -1, ze = -1;
       for (int z = 0; z < (int)col.size(); ++z)
-        if (col[z] / 8 == gi) {
+        if (col[z] / 16 == bi) {
           if (zs < 0) zs = z;
+          if (ze >= 0 && z != ze) {
+            msg = "tensor-core engine: Step-2 block terms not contiguous";
+            return FTK_EINVAL;
+          }
           ze = z + 1;
-          if (ell[z] > 0 && (col[z] + 1) / 8 != gi) {
-            msg = "tensor-core engine: a term straddles a column group";
+          if (ell[z] > 0 && (col[z] + 1) / 16 != bi) {
+            msg = "tensor-core engine: a term straddles a Step-2 block";
             return FTK_EINVAL;
           }
         }
-      if (zs < 0) zs = ze = 0;  // padding-only group
-      tc.s2_chunks.zs[gi] = zs;
-      tc.s2_chunks.ze[gi] = ze;
-      tc.s2_chunks.g0[gi] = gi;
-      maxz = std::max(maxz, ze - zs);
+      if (zs < 0) zs = ze = 0;  // padding-only block
+      if (ze - zs > 16) {
+        msg = "tensor-core engine: Step-2 block with more than 16 terms";
+        return FTK_EINVAL;
+      }
+      tc.s2_blocks.zs[bi] = zs;
+      tc.s2_blocks.ze[bi] = ze;
     }
-    tc.s2_chunks.n = ngroups;
-    tc.s2_maxz = maxz;
-    const int sm2 = (int)step2_smem(tc, pm.n_psi);
+    tc.s2_blocks.nb = ngroups / 2;
+    const int sm2 = (int)step2_smem(pm.n_psi);
     cudaFuncSetAttribute(k_step2_fft<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(k_step2_fft<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(k_step2_fft<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
@@ -1235,7 +1249,7 @@ int tc_prepare_templates(TcPlan&, const float2*, int64_t, const DevPlan&, cudaSt
 }
 
 size_t tc_bytes_per_pair(const TcPlan& tc, const DevPlan& P) {
-  return (size_t)P.H_plus * P.n_psi * sizeof(float2) + (size_t)tc.NRT * 128 * P.K3p * 4;
+  return (size_t)P.Hs * P.n_psi * sizeof(float2) + (size_t)tc.NRT * 128 * P.K3p * 4;
 }
 
 ftk_status_t tc_block_shape(const TcPlan&, const DevPlan&, int engine, int64_t NI, int64_t NJ, int64_t cap,
@@ -1300,6 +1314,7 @@ void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const Pair
   prm.n = P.n_psi;
   prm.n_k = P.n_k;
   prm.Hp = P.H_plus;
+  prm.Hs = P.Hs;
   prm.KCH = tc.KCH;
   prm.NKCH = tc.NKCH;
   prm.NIT = tc.NIT;
@@ -1318,7 +1333,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     return FTK_ESTATE;
   }
   float2* Zhat = reinterpret_cast<float2*>(ws);
-  uint8_t* Zop = reinterpret_cast<uint8_t*>(Zhat + (size_t)pb.count * P.H_plus * P.n_psi);
+  uint8_t* Zop = reinterpret_cast<uint8_t*>(Zhat + (size_t)pb.count * P.Hs * P.n_psi);
   if (pb.li) {
     // explicit pair list (ftk_landscape_pairs): per-pair Step 1 on CUDA cores, then the same FFT
     if (prof) prof(plan, 1, 0, s);

@@ -29,12 +29,11 @@ struct TcPlan {
   uint8_t* d_Aop = nullptr;    // images, bf16 hi/lo split, Step-1 K-major tiles [p][tile][kchunk][part]...
   size_t aop_bytes = 0;
   int NIT = 0, KCH = 64, NKCH = 0;
-  // Step 2 chunk table (one 8-column group per chunk)
+  // Step 2 block table (two 8-column word groups per block)
   struct {
-    int n;
-    int zs[32], ze[32], g0[32];
-  } s2_chunks;
-  int s2_maxz = 1;
+    int nb;
+    int zs[16], ze[16];
+  } s2_blocks;
   int64_t n_tm = 0;
   int num_sms = 148;
 };
