@@ -95,7 +95,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   const int nch = P.g_nch[grp], ncol = nch * NCH, col0 = P.g_col0[grp];
   int* s_part = s_rep + ncol;
   uint8_t* s_fast = reinterpret_cast<uint8_t*>(s_part + ncol);
-  const uint32_t meta_bytes = ((uint32_t)ncol * 8u + (uint32_t)ncol / 8u + 512u + 1023u) & ~1023u;
+  uint8_t* s_fastc = s_fast + ncol / 8;  // [nch * 2]: leading columns of a half chunk in fast groups
+  const uint32_t meta_bytes = ((uint32_t)ncol * 8u + (uint32_t)ncol / 8u + 2u * (uint32_t)nch + 512u + 1023u) & ~1023u;
   uint8_t* ys = s3_raw + 1024 + meta_bytes;                       // Y image of this group
   const uint32_t ypart = (uint32_t)ncol * (uint32_t)K3p * 2u;      // bytes of one bf16 part
   const uint32_t SBO = (uint32_t)K3p * 16u;                        // bytes between 8-row groups (N)
@@ -118,6 +119,12 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
     s_part[c] = __ldg(P.colpart + col0 + c);
   }
   for (int c = threadIdx.x; c < ncol / 8; c += blockDim.x) s_fast[c] = __ldg(P.colfast + col0 / 8 + c);
+  for (int hc = threadIdx.x; hc < 2 * nch; hc += blockDim.x) {  // leading fast columns of each half chunk
+    int nf = 0;
+    if (P.Ke < K3p)
+      for (int c8 = hc * (NCH / 2); c8 < (hc + 1) * (NCH / 2) && __ldg(P.colfast + (col0 + c8) / 8) != 0; c8 += 8) nf += 8;
+    s_fastc[hc] = (uint8_t)nf;
+  }
   if (warp == 0) tmem_alloc<512>(&S.tmem_base);
   tc_fence_before();
   __syncthreads();
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
 #pragma unroll
         for (int g = 0; g < 16; ++g)
           if (g < NWG) v[g] = valid ? __ldg(src + g * 128) : make_uint4(0u, 0u, 0u, 0u);
-        mbar_wait(&S.a_empty[ab], ((g_a >> 1) & 1) ^ 1);
+        mbar_wait_lazy(&S.a_empty[ab], ((g_a >> 1) & 1) ^ 1, 64);
         tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acol0 + (uint32_t)(ab * K3p + part * (K3p / 2));
 #pragma unroll
@@ -238,8 +245,48 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           mbar_wait(&S.d_full[db], (g_d >> 1) & 1);
           tc_fence_after();
           const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(db * 2 * NCH + h * hw);
-          if (active) {
-            for (int c8 = 0; c8 < hw; c8 += 8) {
+          const int clb = c * NCH + h * hw;  // first column of this warp's half chunk
+          const int nfast = land_p ? 0 : (int)s_fastc[c * 2 + h];
+          if (active && nfast > 0) {
+            // all columns paired: per 8-column group max of E + |O| -> (value, group key), branch-free
+            const uint32_t kb = ((uint32_t)T << 24) | ((uint32_t)clb << 7) | (uint32_t)row;
+            int c8 = 0;
+            for (; c8 + 16 <= nfast; c8 += 16) {
+              uint32_t e[16], o[16];
+              tmem_ld16(base + c8, e);
+              tmem_ld16(base + NCH + c8, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int g2 = 0; g2 < 2; ++g2) {
+                float v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                  v[k] = __uint_as_float(e[8 * g2 + k]) + fabsf(__uint_as_float(o[8 * g2 + k]));
+                const float m = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
+                                      fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+                const bool upd = m > bvf;
+                bvf = upd ? m : bvf;
+                bkf = upd ? kb + ((uint32_t)(c8 + 8 * g2) << 7) : bkf;
+              }
+            }
+            if (c8 < nfast) {
+              uint32_t e[8], o[8];
+              tmem_ld8(base + c8, e);
+              tmem_ld8(base + NCH + c8, o);
+              tmem_wait_ld();
+              float v[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(e[k]) + fabsf(__uint_as_float(o[k]));
+              const float m = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
+                                    fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+              const bool upd = m > bvf;
+              bvf = upd ? m : bvf;
+              bkf = upd ? kb + ((uint32_t)c8 << 7) : bkf;
+            }
+          }
+          if (active && nfast < hw) {
+            // exact path: padding / unpaired columns, no odd block, or landscape output
+            for (int c8 = nfast; c8 < hw; c8 += 8) {
               uint32_t e[8], o[8];
               tmem_ld8(base + c8, e);
               if (has_odd) tmem_ld8(base + NCH + c8, o);
@@ -248,17 +295,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) o[k] = 0u;
               }
-              const int cl = c * NCH + h * hw + c8;  // column within the group
-              if (s_fast[cl >> 3] && !land_p) {
-                float v[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(e[k]) + fabsf(__uint_as_float(o[k]));
-                const float m = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
-                                      fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
-                const bool upd = m > bvf;
-                bvf = upd ? m : bvf;
-                bkf = upd ? (((uint32_t)T << 24) | ((uint32_t)cl << 7) | (uint32_t)row) : bkf;
-              } else if (r < n) {
+              const int cl = clb + c8;
+              if (r < n) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                   const int tp = s_rep[cl + k], tm = s_part[cl + k];
@@ -424,7 +462,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
 }
 
 static size_t s3_smem_bytes(int ncol, int K3p) {
-  const size_t meta = (((size_t)ncol * 8 + ncol / 8) + 512 + 1023) & ~(size_t)1023;
+  const size_t meta = (((size_t)ncol * 8 + ncol / 8) + 2 * (size_t)(ncol / 16) + 512 + 1023) & ~(size_t)1023;
   return 1024 + meta + (size_t)ncol * K3p * 4;
 }
 
@@ -711,8 +749,8 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 // explicit-pair path); written as the Step-3 A operand rows (real columns of reading R13), bf16 hi/lo
 // packed in 32-bit words (two K columns per word): Zop [pair][r-tile][part][word group][row 128][16 B].
 // Work item = (pair, block of two word groups = 16 Step-3 columns, <= 16 terms); persistent CTAs, two
-// per SM.  The item's input rows are gathered with cp.async into a [p][17] shared-memory buffer (odd
-// stride: conflict-free column reads), one warp per term row.
+// per SM.  The item's input rows are gathered with 16-byte cp.async into a [p][18] shared-memory buffer,
+// one warp per term row.
 // FFT: four-step decomposition n = 32 E, p = a + 32 b (a = lane), r = c + E d:
 //   (A) per lane an E-point DFT over b in registers, (B) twiddle w_n^{a c}, (C) a 32-point radix-2
 //   DIF across the warp with shfl_xor (output index d lands on lane bitrev5(d)).
@@ -726,7 +764,7 @@ struct S2Blocks {
   int nb;
   int zs[16], ze[16];  // term range of block b (word groups 2b, 2b + 1)
 };
-constexpr int S2_ROWSTRIDE = 17;
+constexpr int S2_ROWSTRIDE = 18;  // complex; even -> 16-byte rows for cp.async 16 (2-way bank conflict)
 
 __device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -764,6 +802,9 @@ __device__ __forceinline__ void dft_regs(float2 (&x)[E], const float2* tw, int n
 
 __device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -805,11 +846,32 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
     const int b = item % B.nb, pr = item / B.nb;
     const int zs = B.zs[b], nz = B.ze[b] - zs;
     // ---- gather the item's input rows
-    if (formB) {  // [pair][p][Hs]: 16 threads per p-row, consecutive terms
-      const float2* src = Zhat + (size_t)pr * n * Hs + zs;
-      const int zl = threadIdx.x & 15;
-      if (zl < nz)
-        for (int p = threadIdx.x >> 4; p < n; p += blockDim.x >> 4) cp_async8(rows + p * S + zl, src + (size_t)p * Hs + zl);
+    int zoff = 0;  // buffer column of term zs
+    if (formB) {  // [pair][p][Hs]: 16-byte chunks of the even-aligned term range [zs2, zs2 + 2 cpr)
+      const int zs2 = zs & ~1;
+      const int cpr = (zs + nz - zs2 + 1) >> 1;  // chunks per row (<= S / 2)
+      zoff = zs - zs2;
+      if (cpr > 0) {
+        int p = threadIdx.x / cpr, c = threadIdx.x - p * cpr;
+        const int dq = blockDim.x / cpr, dr = blockDim.x - dq * cpr;
+        const uint8_t* sp = reinterpret_cast<const uint8_t*>(Zhat + ((size_t)pr * n + p) * Hs + zs2) + 16 * c;
+        float2* dp = rows + p * S + 2 * c;
+        const size_t sstep = (size_t)dq * Hs * 8 + 16 * dr, swrap = (size_t)Hs * 8 - 16 * cpr;
+        const int dstep = dq * S + 2 * dr, dwrap = S - 2 * cpr;
+        while (p < n) {
+          cp_async16(dp, sp);
+          sp += sstep;
+          dp += dstep;
+          p += dq;
+          c += dr;
+          if (c >= cpr) {
+            c -= cpr;
+            ++p;
+            sp += swrap;
+            dp += dwrap;
+          }
+        }
+      }
     } else {      // [pair][zeta][q]
       const float2* src = Zhat + ((size_t)pr * Hp + zs) * n;
       for (int z = 0; z < nz; ++z)
@@ -822,7 +884,7 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
     for (int zz = warp; zz < nz; zz += nw) {
       float2 x[E];
 #pragma unroll
-      for (int bb = 0; bb < E; ++bb) x[bb] = rows[(lane + 32 * bb) * S + zz];
+      for (int bb = 0; bb < E; ++bb) x[bb] = rows[(lane + 32 * bb) * S + zoff + zz];
       dft_regs<E>(x, P.tw, n);  // (A): natural-order result in x[rv(c)]
       {                         // (B) x_c *= w_n^{lane c} by recurrence
         float2 acc = wlane;
@@ -1090,6 +1152,17 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       rep.push_back(t);
       partner.push_back(mate);
     }
+  }
+  {  // columns: paired representatives first (fast epilogue groups), unpaired ones last
+    std::vector<int> r2, p2;
+    for (int pass = 0; pass < 2; ++pass)
+      for (size_t i = 0; i < rep.size(); ++i)
+        if ((partner[i] >= 0) == (pass == 0)) {
+          r2.push_back(rep[i]);
+          p2.push_back(partner[i]);
+        }
+    rep.swap(r2);
+    partner.swap(p2);
   }
   tc.n_rep = (int)rep.size();
   tc.NRT = (pm.n_psi + 127) / 128;
