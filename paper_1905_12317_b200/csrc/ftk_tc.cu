@@ -774,10 +774,33 @@ __device__ __forceinline__ float2 tw_full(const float2* tw, int j, int n) {  // 
   return j < n / 2 ? w : make_float2(-w.x, -w.y);
 }
 
+// w_32^m = e^{-2 pi i m / 32}, m = 0..31 (cos, -sin): compile-time constants for the in-register DFTs
+__device__ constexpr float kW32c[32] = {
+    1.f, 0.98078528f, 0.92387953f, 0.83146961f, 0.70710678f, 0.55557023f, 0.38268343f, 0.19509032f,
+    0.f, -0.19509032f, -0.38268343f, -0.55557023f, -0.70710678f, -0.83146961f, -0.92387953f, -0.98078528f,
+    -1.f, -0.98078528f, -0.92387953f, -0.83146961f, -0.70710678f, -0.55557023f, -0.38268343f, -0.19509032f,
+    0.f, 0.19509032f, 0.38268343f, 0.55557023f, 0.70710678f, 0.83146961f, 0.92387953f, 0.98078528f};
+__device__ constexpr float kW32s[32] = {
+    0.f, -0.19509032f, -0.38268343f, -0.55557023f, -0.70710678f, -0.83146961f, -0.92387953f, -0.98078528f,
+    -1.f, -0.98078528f, -0.92387953f, -0.83146961f, -0.70710678f, -0.55557023f, -0.38268343f, -0.19509032f,
+    0.f, 0.19509032f, 0.38268343f, 0.55557023f, 0.70710678f, 0.83146961f, 0.92387953f, 0.98078528f,
+    1.f, 0.98078528f, 0.92387953f, 0.83146961f, 0.70710678f, 0.55557023f, 0.38268343f, 0.19509032f};
+
+// x * w_32^m for a compile-time m (after unrolling): the trivial rotations cost no multiplies
+__device__ __forceinline__ float2 cmul_w32(float2 x, int m) {
+  m &= 31;
+  if (m == 0) return x;
+  if (m == 8) return make_float2(x.y, -x.x);
+  if (m == 16) return make_float2(-x.x, -x.y);
+  if (m == 24) return make_float2(-x.y, x.x);
+  const float c = kW32c[m], sn = kW32s[m];
+  return make_float2(fmaf(x.x, c, -x.y * sn), fmaf(x.x, sn, x.y * c));
+}
+
 template <int E>
-__device__ __forceinline__ void dft_regs(float2 (&x)[E], const float2* tw, int n) {
-  // radix-2 DIT; x is addressed in bit-reversed order through rv() (a compile-time renaming), so the
-  // natural-order result ends up in x[rv(c)].  w_E^j = tw[j n / E] (warp-uniform loads).
+__device__ __forceinline__ void dft_regs(float2 (&x)[E]) {
+  // radix-2 DIT over E <= 32 points with compile-time twiddles; x is addressed in bit-reversed order
+  // through rv() (a compile-time renaming), so the natural-order result ends up in x[rv(c)].
   constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
   auto rv = [](int i) {
     int r = 0;
@@ -791,8 +814,7 @@ __device__ __forceinline__ void dft_regs(float2 (&x)[E], const float2* tw, int n
     for (int blk = 0; blk < E; blk += 2 * s) {
 #pragma unroll
       for (int j = 0; j < s; ++j) {
-        const float2 w = __ldg(tw + j * (n / (2 * s)));
-        const float2 u = x[rv(blk + j)], v = cmulf(x[rv(blk + j + s)], w);
+        const float2 u = x[rv(blk + j)], v = cmul_w32(x[rv(blk + j + s)], j * (32 / (2 * s)));
         x[rv(blk + j)] = make_float2(u.x + v.x, u.y + v.y);
         x[rv(blk + j + s)] = make_float2(u.x - v.x, u.y - v.y);
       }
@@ -833,8 +855,11 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
     const int h = 16 >> s;
     wc[s] = (lane & h) ? tw_full(P.tw, (lane & (h - 1)) * (16 / h) * (n / 32), n) : make_float2(1.f, 0.f);
   }
-  const float2 wlane = tw_full(P.tw, lane & (n - 1), n);
   const int d = __brev(lane) >> 27;
+  // (B) twiddles w_n^{a c} (a = lane, c < E), [c][a]: conflict-free
+  float2* twB = reinterpret_cast<float2*>(stg + 16 * RS);
+  for (int i = threadIdx.x; i < E * 32; i += blockDim.x) twB[i] = tw_full(P.tw, ((i & 31) * (i >> 5)) & (n - 1), n);
+  __syncthreads();
   auto rv = [](int i) {
     int r = 0;
 #pragma unroll
@@ -884,16 +909,15 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
     for (int zz = warp; zz < nz; zz += nw) {
       float2 x[E];
 #pragma unroll
-      for (int bb = 0; bb < E; ++bb) x[bb] = rows[(lane + 32 * bb) * S + zoff + zz];
-      dft_regs<E>(x, P.tw, n);  // (A): natural-order result in x[rv(c)]
-      {                         // (B) x_c *= w_n^{lane c} by recurrence
-        float2 acc = wlane;
+      const int z = zs + zz;
+      const int l = P.ell[z], col = P.col[z];
+      // Form B: Z(r) w^{ell r} = DFT of the cyclically shifted row Zhat'(q - ell) (reading R5)
+      const int q0 = formB ? ((lane - l) & (n - 1)) : lane;
 #pragma unroll
-        for (int c = 1; c < E; ++c) {
-          x[rv(c)] = cmulf(x[rv(c)], acc);
-          acc = cmulf(acc, wlane);
-        }
-      }
+      for (int bb = 0; bb < E; ++bb) x[bb] = rows[((q0 + 32 * bb) & (n - 1)) * S + zoff + zz];
+      dft_regs<E>(x);  // (A): natural-order result in x[rv(c)]
+#pragma unroll
+      for (int c = 1; c < E; ++c) x[rv(c)] = cmulf(x[rv(c)], twB[c * 32 + lane]);  // (B) x_c *= w_n^{lane c}
 #pragma unroll
       for (int s = 0; s < 5; ++s) {  // (C) 32-point DIF across lanes (branch-free butterfly)
         const int h = 16 >> s;
@@ -905,18 +929,7 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
           x[c] = cmulf(make_float2(fmaf(sg, x[c].x, px), fmaf(sg, x[c].y, py)), wc[s]);
         }
       }
-      // lane holds X[c + E d] in x[rv(c)]; Form-B twiddle e^{-2 pi i ell (c + E d) / n}
-      const int z = zs + zz;
-      const int l = P.ell[z], col = P.col[z];
-      if (formB) {
-        float2 acc = tw_full(P.tw, (l * E * d) & (n - 1), n);
-        const float2 step = tw_full(P.tw, l & (n - 1), n);
-#pragma unroll
-        for (int c = 0; c < E; ++c) {
-          x[rv(c)] = cmulf(x[rv(c)], acc);
-          acc = cmulf(acc, step);
-        }
-      }
+      // lane holds X[c + E d] in x[rv(c)]
       // stage: ell > 0 -> word (Re, Im) of this term; ell = 0 -> one 16-bit half of a word shared with
       // the neighbouring ell = 0 term
       const int kl = col - 16 * b;  // 0..15 within the block
@@ -963,7 +976,7 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
 
 static size_t step2_smem(int n) {
   const int E = n / 32;
-  return (size_t)n * S2_ROWSTRIDE * 8 + (size_t)16 * (n + n / E) * 4;
+  return (size_t)n * S2_ROWSTRIDE * 8 + (size_t)16 * (n + n / E) * 4 + (size_t)n * 8;
 }
 
 static void launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, int formB,
