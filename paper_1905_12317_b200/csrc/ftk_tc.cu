@@ -834,7 +834,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <int E>
 __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
-                                                      int npair, int formB, DevPlan P, S2Blocks B) {
+                                                      int npair, int formB, DevPlan P, S2Blocks B,
+                                                      const float2* __restrict__ twtab) {
   extern __shared__ __align__(16) uint8_t s2raw[];
   constexpr int n = 32 * E, S = S2_ROWSTRIDE;
   constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
@@ -849,17 +850,24 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
   const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
 
   // per-lane constant twiddles
-  float2 wc[5];  // stage twiddle of this lane (1 on the upper lanes of each butterfly)
+  // 32 = L x E: the 32-point DFT over the lane index runs as an E-point register DFT and an L-point
+  // DIF across L lanes (log2 L shuffle stages)
+  constexpr int L = 32 / E;
+  constexpr int LL = (L == 16) ? 4 : (L == 8) ? 3 : (L == 4) ? 2 : (L == 2) ? 1 : 0;
+  float2 wc[LL > 0 ? LL : 1];  // stage twiddle of this lane (1 on the upper lanes of each butterfly)
 #pragma unroll
-  for (int s = 0; s < 5; ++s) {
-    const int h = 16 >> s;
-    wc[s] = (lane & h) ? tw_full(P.tw, (lane & (h - 1)) * (16 / h) * (n / 32), n) : make_float2(1.f, 0.f);
+  for (int s = 0; s < LL; ++s) {
+    const int h = (L / 2) >> s;
+    wc[s] = (lane & h) ? tw_full(P.tw, (lane & (h - 1)) * ((L / 2) / h) * (n / L), n) : make_float2(1.f, 0.f);
   }
-  const int d = __brev(lane) >> 27;
+  int gq = 0;  // L-point DIF output index of this lane: bit-reversed lane % L
+#pragma unroll
+  for (int bb = 0; bb < LL; ++bb) gq |= (((lane % L) >> bb) & 1) << (LL - 1 - bb);
   // (B) twiddles w_n^{a c} (a = lane, c < E), [c][a]: conflict-free
-  float2* twB = reinterpret_cast<float2*>(stg + 16 * RS);
-  for (int i = threadIdx.x; i < E * 32; i += blockDim.x) twB[i] = tw_full(P.tw, ((i & 31) * (i >> 5)) & (n - 1), n);
-  __syncthreads();
+  // (B) twiddles w_n^{a c} (a = lane, c < E) and (B2) twiddles w_32^{h d'} (h = lane % L, d' < E), both
+  // [c][lane] (plan-time tables, L1-resident)
+  const float2* __restrict__ twB = twtab;
+  const float2* __restrict__ twC = twtab + E * 32;
   auto rv = [](int i) {
     int r = 0;
 #pragma unroll
@@ -867,7 +875,11 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
     return r;
   };
 
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+  // contiguous item range per CTA: the blocks of one pair run back to back on the same SM, so the row
+  // sectors shared by neighbouring blocks are L2 hits
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int i_end = min(total, (int)(blockIdx.x + 1) * per);
+  for (int item = blockIdx.x * per; item < i_end; ++item) {
     const int b = item % B.nb, pr = item / B.nb;
     const int zs = B.zs[b], nz = B.ze[b] - zs;
     // ---- gather the item's input rows
@@ -908,38 +920,56 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
     __syncthreads();
     for (int zz = warp; zz < nz; zz += nw) {
       float2 x[E];
-#pragma unroll
       const int z = zs + zz;
       const int l = P.ell[z], col = P.col[z];
+      float2* colp = rows + zoff + zz;  // this term's column of the row buffer (stride S)
       // Form B: Z(r) w^{ell r} = DFT of the cyclically shifted row Zhat'(q - ell) (reading R5)
       const int q0 = formB ? ((lane - l) & (n - 1)) : lane;
 #pragma unroll
-      for (int bb = 0; bb < E; ++bb) x[bb] = rows[((q0 + 32 * bb) & (n - 1)) * S + zoff + zz];
-      dft_regs<E>(x);  // (A): natural-order result in x[rv(c)]
+      for (int bb = 0; bb < E; ++bb) x[bb] = colp[((q0 + 32 * bb) & (n - 1)) * S];
+      dft_regs<E>(x);  // (A) E-point DFT over b (p = a + 32 b, a = lane): natural order in x[rv(c)]
 #pragma unroll
-      for (int c = 1; c < E; ++c) x[rv(c)] = cmulf(x[rv(c)], twB[c * 32 + lane]);  // (B) x_c *= w_n^{lane c}
+      for (int c = 1; c < E; ++c) x[rv(c)] = cmulf(x[rv(c)], __ldg(twB + c * 32 + lane));  // (B) x_c *= w_n^{a c}
+      // (T) the 32-point DFT over a: transpose through the column (slot c*32 + (a + c) % 32) so that lane
+      //     (c = lane / L, h = lane % L) holds a = L i + h, i < E; then (A2) an E-point DFT over i in
+      //     registers, (B2) twiddle w_32^{h d'}, (C2) an L-point DIF across the L lanes of each c.
+      __syncwarp();
 #pragma unroll
-      for (int s = 0; s < 5; ++s) {  // (C) 32-point DIF across lanes (branch-free butterfly)
-        const int h = 16 >> s;
-        const float sg = (lane & h) ? -1.f : 1.f;  // upper lane: x + x', lower lane: (x' - x) w
+      for (int c = 0; c < E; ++c) colp[(c * 32 + ((lane + c) & 31)) * S] = x[rv(c)];
+      __syncwarp();
+      {
+        const int cq = lane / L, hq = lane % L;
 #pragma unroll
-        for (int c = 0; c < E; ++c) {
-          const float px = __shfl_xor_sync(0xffffffffu, x[c].x, h);
-          const float py = __shfl_xor_sync(0xffffffffu, x[c].y, h);
-          x[c] = cmulf(make_float2(fmaf(sg, x[c].x, px), fmaf(sg, x[c].y, py)), wc[s]);
+        for (int i = 0; i < E; ++i) x[i] = colp[(cq * 32 + ((L * i + hq + cq) & 31)) * S];
+      }
+      dft_regs<E>(x);  // (A2): natural order in x[rv(d')]
+      if constexpr (L > 1) {
+#pragma unroll
+        for (int dd = 1; dd < E; ++dd) x[rv(dd)] = cmulf(x[rv(dd)], __ldg(twC + dd * 32 + lane));  // (B2)
+#pragma unroll
+        for (int s = 0; s < LL; ++s) {  // (C2) L-point DIF across lanes (branch-free butterfly)
+          const int h = (L / 2) >> s;
+          const float sg = (lane & h) ? -1.f : 1.f;  // upper lane: x + x', lower lane: (x' - x) w
+#pragma unroll
+          for (int c = 0; c < E; ++c) {
+            const float px = __shfl_xor_sync(0xffffffffu, x[c].x, h);
+            const float py = __shfl_xor_sync(0xffffffffu, x[c].y, h);
+            x[c] = cmulf(make_float2(fmaf(sg, x[c].x, px), fmaf(sg, x[c].y, py)), wc[s]);
+          }
         }
       }
-      // lane holds X[c + E d] in x[rv(c)]
+      // lane holds Z(r), r = cq + E (d' + E g) in x[rv(d')], cq = lane / L, g = bitrev_L(lane % L)
       // stage: ell > 0 -> word (Re, Im) of this term; ell = 0 -> one 16-bit half of a word shared with
       // the neighbouring ell = 0 term
       const int kl = col - 16 * b;  // 0..15 within the block
       const int grp = kl >> 3, w = (kl & 7) >> 1;
       uint32_t* shi = stg + (size_t)((grp * 2 + 0) * 4 + w) * RS;
       uint32_t* slo = stg + (size_t)((grp * 2 + 1) * 4 + w) * RS;
+      const int pbase = lane / L + (E * E + E) * gq;  // padded index pi(r) = r + r / E
 #pragma unroll
-      for (int c = 0; c < E; ++c) {
-        const int pi = c + (E + 1) * d;  // padded index of r = c + E d (conflict-free across lanes)
-        const float2 a0 = x[rv(c)];
+      for (int dd = 0; dd < E; ++dd) {
+        const int pi = pbase + (E + 1) * dd;
+        const float2 a0 = x[rv(dd)];
         if (l > 0) {
           uint32_t hh, ll;
           split2_bf16(a0.x, a0.y, hh, ll);
@@ -976,7 +1006,7 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
 
 static size_t step2_smem(int n) {
   const int E = n / 32;
-  return (size_t)n * S2_ROWSTRIDE * 8 + (size_t)16 * (n + n / E) * 4 + (size_t)n * 8;
+  return (size_t)n * S2_ROWSTRIDE * 8 + (size_t)16 * (n + n / E) * 4;
 }
 
 static void launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, int formB,
@@ -987,11 +1017,11 @@ static void launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop,
   const int items = B.nb * npair;
   dim3 grid(items < 2 * tc.num_sms ? items : 2 * tc.num_sms);
   switch (P.n_psi) {
-    case 64: k_step2_fft<2><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B); break;
-    case 128: k_step2_fft<4><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B); break;
-    case 256: k_step2_fft<8><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B); break;
-    case 512: k_step2_fft<16><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B); break;
-    default: k_step2_fft<32><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B); break;
+    case 64: k_step2_fft<2><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
+    case 128: k_step2_fft<4><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
+    case 256: k_step2_fft<8><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
+    case 512: k_step2_fft<16><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
+    default: k_step2_fft<32><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
   }
 }
 
@@ -1286,6 +1316,22 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       tc.s2_blocks.ze[bi] = ze;
     }
     tc.s2_blocks.nb = ngroups / 2;
+    {  // Step-2 twiddle tables: [c][a] w_n^{a c} and [d'][a] w_32^{(a % L) d'}, E = n / 32, L = 32 / E
+      const int n = pm.n_psi, E = n / 32, L = 32 / E;
+      std::vector<float2> tw((size_t)2 * E * 32);
+      for (int c = 0; c < E; ++c)
+        for (int a = 0; a < 32; ++a) {
+          const double ph1 = -2.0 * M_PI * (double)((a * c) % n) / n;
+          const double ph2 = -2.0 * M_PI * (double)(((a % L) * c) % 32) / 32.0;
+          tw[(size_t)c * 32 + a] = make_float2((float)std::cos(ph1), (float)std::sin(ph1));
+          tw[(size_t)E * 32 + c * 32 + a] = make_float2((float)std::cos(ph2), (float)std::sin(ph2));
+        }
+      if (cudaMalloc(&tc.d_s2tw, tw.size() * sizeof(float2)) != cudaSuccess) {
+        msg = "tensor-core engine: allocation failed";
+        return FTK_ENOMEM;
+      }
+      cudaMemcpy(tc.d_s2tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice);
+    }
     const int sm2 = (int)step2_smem(pm.n_psi);
     cudaFuncSetAttribute(k_step2_fft<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(k_step2_fft<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
@@ -1298,6 +1344,8 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
 }
 
 void tc_plan_free(TcPlan& tc) {
+  cudaFree(tc.d_s2tw);
+  tc.d_s2tw = nullptr;
   cudaFree(tc.d_Ysm);
   cudaFree(tc.d_colrep);
   cudaFree(tc.d_colpart);

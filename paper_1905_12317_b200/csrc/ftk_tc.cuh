@@ -34,6 +34,7 @@ struct TcPlan {
     int nb;
     int zs[16], ze[16];
   } s2_blocks;
+  float2* d_s2tw = nullptr;  // Step-2 four-step twiddle tables
   int64_t n_tm = 0;
   int num_sms = 148;
 };
