@@ -36,7 +36,7 @@ import synth  # noqa: E402
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ftk", choices=["ftk", "reference"])
@@ -286,9 +286,19 @@ def main():
         rows = 128 * info["s3_rtiles"]
         issued_flops = 3.0 * 2.0 * rows * info["s3_cols"] * info["K3p"] * pairs_local * args.steps / max(dom_cnt, 1)
         issued = issued_flops / avg_launch_s / 1e12 if avg_launch_s > 0 else None
+    traffic = None
+    try:  # DRAM bytes per pair of this kernel from the committed ncu capture (same config only)
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        if tj.get("config") == cfg.name and dom in tj.get("bytes_per_pair", {}):
+            traffic = tj["bytes_per_pair"][dom] * pairs_local * args.steps / max(dom_cnt, 1)
+    except (OSError, ValueError):
+        traffic = None
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "tensor_issued_tflops": issued,
-                "frac": (achieved / peak) if achieved else None, "traffic": None, "kernel": dom,
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_unit": "bytes/launch",
+                "traffic_algorithmic": (4.0 * 128 * info["s3_rtiles"] * info["K3p"] * pairs_local * args.steps
+                                        / max(dom_cnt, 1)) if dom == "step3" else None,
+                "kernel": dom,
                 "launches": dom_cnt, "avg_launch_ms": avg_launch_s * 1e3, "peak_source": peak_src,
                 "flops_per_launch": flops_per_launch,
                 "note": "achieved = algorithmic flops 2*N_t*n_psi*K3 per pair (minimal real Step-3 GEMM) / launch time; "
