@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "ftk_fft.cuh"
@@ -1609,6 +1610,12 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       }
       cudaMemcpy(tc.d_s2dft, img.data(), img.size() * 2, cudaMemcpyHostToDevice);
     }
+    // FTK_STEP2_TC=1 selects k_step2_tc (32-point DFT stage on the tensor cores) for n_psi = 256, 512;
+    // measured slower than k_step2_fft at c3 / c5 (the extra bf16 split of the GEMM operand and the
+    // per-item overheads cost as much as the FFT arithmetic it removes), so the CUDA-core kernel is the
+    // default
+    const char* e2 = std::getenv("FTK_STEP2_TC");
+    tc.step2_tensor = e2 && e2[0] == '1';
     if (pm.n_psi == 256 || pm.n_psi == 512) {
       const int sm3 = (int)step2tc_smem(pm.n_psi);
       cudaFuncSetAttribute(k_step2_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
@@ -1774,7 +1781,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     launch_step1_simt(A, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    if (P.n_psi == 256 || P.n_psi == 512)
+    if (tc.step2_tensor && (P.n_psi == 256 || P.n_psi == 512))
       launch_step2_tc(tc, Zhat, Zop, pb.count, 0, P, s);
     else
       launch_step2_fft(tc, Zhat, Zop, pb.count, 0, P, s);
@@ -1784,7 +1791,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     launch_step1_tc(tc, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    if (P.n_psi == 256 || P.n_psi == 512)
+    if (tc.step2_tensor && (P.n_psi == 256 || P.n_psi == 512))
       launch_step2_tc(tc, Zhat, Zop, pb.count, 1, P, s);
     else
       launch_step2_fft(tc, Zhat, Zop, pb.count, 1, P, s);
