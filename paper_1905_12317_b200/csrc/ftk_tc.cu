@@ -207,7 +207,9 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
 #pragma unroll
         for (int g = 0; g < 16; ++g)
           if (g < NWG) v[g] = valid ? __ldg(src + g * 128) : make_uint4(0u, 0u, 0u, 0u);
-        mbar_wait_lazy(&S.a_empty[ab], ((g_a >> 1) & 1) ^ 1, 64);
+        // one warp polls the slot barrier, the other writers sleep in a hardware named barrier
+        if (warp == 1) mbar_wait(&S.a_empty[ab], ((g_a >> 1) & 1) ^ 1);
+        named_bar(2, 256);
         tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acol0 + (uint32_t)(ab * K3p + part * (K3p / 2));
 #pragma unroll
@@ -243,7 +245,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         const bool active = T * 128 + q * 32 < n;  // warp-uniform: lane quarters beyond n_psi idle
         for (int c = 0; c < nch; ++c, ++g_d) {
           const int db = g_d & 1;
-          mbar_wait(&S.d_full[db], (g_d >> 1) & 1);
+          if (warp == 9) mbar_wait(&S.d_full[db], (g_d >> 1) & 1);
+          named_bar(3, 256);
           tc_fence_after();
           const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(db * 2 * NCH + h * hw);
           const int clb = c * NCH + h * hw;  // first column of this warp's half chunk
