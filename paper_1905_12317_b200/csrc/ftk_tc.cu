@@ -13,19 +13,24 @@
 // E = Z_even Y_even, O = Z_odd Y_odd accumulated separately: half the shifts, same K.
 // Representative shifts are split into rep-groups whose Y image fits in shared memory; CTA b serves
 // group b % G for a contiguous range of pairs (G = 1 at the BASELINE configs c2, c3, c5).
-//   * warp 0 (one lane): MMA issuer -- per (pair, r-tile, chunk) 3 x K3p/16 tcgen05.mma M128 x NCH x K16
-//     (A = Z r-tile hi/lo from TMEM, B = Y chunk hi/lo from SMEM) into the E / O accumulators of one of
-//     two TMEM buffers.
-//   * warps 1-8: A writers -- per (pair, r-tile) the Step-2 operand rows (hi: warps 1-4, lo: 5-8; one
-//     thread per rotation row) global -> registers -> tcgen05.st into one of two TMEM A slots.
-//   * warps 9-16: epilogue -- tcgen05.ld E and O, X(+-delta) = E +- O; per thread the running max of
-//     E + |O| = max(E + O, E - O) and its 8-column group (branch-free), per-pair reduction.
-//   * warp 17: resolver -- recomputes the 16 E / O sums of the pair's winning group in fp32 from the
-//     same bf16 operands to recover the exact (shift, sign), one packed-key atomicMax per pair.
+//   * warp 1 (one lane): producer -- per (pair, r-tile) one bulk copy of the Step-2 operand image (bf16
+//     hi/lo, canonical K-major core matrices) into a shared-memory staging ring.
+//   * warp 0 (one elected lane): per r-tile 2 x K3p/16 tcgen05.cp.128x256b staging -> TMEM A slot, then
+//     per chunk 3 x K3p/16 tcgen05.mma M128 x NCH x K16 (A = Z r-tile from TMEM, B = Y chunk from SMEM)
+//     into the E / O accumulators of one of two TMEM buffers.  cp and mma execute in issue order, so
+//     the A slots need no barriers.
+//   * warps 2-9: epilogue -- per chunk, tcgen05.ld of this warp's E and O columns into registers and
+//     immediate release of the TMEM buffer; then per thread the running max of E + |O| =
+//     max(E + O, E - O) and its 8-column group (branch-free); per pair the partial records go to the
+//     resolver through shared memory (no CTA-wide barrier).
+//   * warp 10: resolver -- merges the 8 partial records, recomputes the 16 E / O sums of the pair's
+//     winning group in fp32 from the same bf16 operands to recover the exact (shift, sign), one
+//     packed-key atomicMax per pair.
 // TMEM columns: D buffers [0, 4 NCH) (E, O of buffer 0 then 1), A slots [4 NCH, 4 NCH + 2 K3p).
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -36,39 +41,37 @@
 namespace ftk {
 using namespace sm100;
 
-constexpr int S3_WARPS = 18;
+constexpr int S3_WARPS = 11;
 constexpr int S3_THREADS = S3_WARPS * 32;
 constexpr int S3_MAXG = TcPlan::MAXG;
+constexpr int S3_MAXNS = 4;
 
 struct S3Params {
-  const uint8_t* Zop;     // per pair: [r-tile][part][word group][row 128][16 B] (written by k_step2_fft)
+  const uint8_t* Zop;     // per pair: [r-tile][part][row/8][K3p/8][8 rows x 16 B] bf16x2 words (Step 2 output)
   const uint8_t* Ysm;     // per group: shared-memory image [part][rep/8][K3p/8][8 rows x 16 B]
   const int* colrep;      // [ncol_total] shift index of the representative (+delta); -1: padding column
   const int* colpart;     // [ncol_total] shift index of -delta; -1: none
   const uint8_t* colfast; // [ncol_total / 8] 1 if all 8 columns are paired, non-padding
   PairBlock pb;
-  int n, K3p, Ke, N_t, NRT, NCH, G;
+  int n, K3p, Ke, N_t, NRT, NCH, G, NS;
   int g_col0[S3_MAXG], g_nch[S3_MAXG];
   long long g_yoff[S3_MAXG];
   int tm_off, n_tm_local;
   unsigned long long* img_keys;
   unsigned long long* pair_keys;
   float* land;
+  unsigned long long* trace;  // nullable (FTK_S3_TRACE=1): wait / busy cycle counters of CTA 0
 };
 
 struct S3Smem {
   uint64_t y_bar;
-  uint64_t a_full[2], a_empty[2];
+  uint64_t st_full[S3_MAXNS], st_empty[S3_MAXNS];
   uint64_t d_full[2], d_empty[2];
-  uint64_t res_full[2], res_empty[2];
+  uint64_t red_full[2], red_empty[2];
   uint32_t tmem_base;
   float red_v[2][8], red_ve[2][8];
   uint32_t red_k[2][8], red_fe[2][8];
-  float res_v[2], res_ve[2];
-  uint32_t res_k[2], res_fe[2];
-  int res_p[2];
 };
-
 static_assert(sizeof(S3Smem) <= 512, "S3Smem must fit below the column metadata");
 
 __device__ __forceinline__ bool better(float v, uint32_t f, float bv, uint32_t bf) {
@@ -85,33 +88,40 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint4& v) {
                "r"(v.z), "r"(v.w)
                : "memory");
 }
+// SMEM -> TMEM: 128 rows x 32 bytes (two K-adjacent canonical core matrices per 8-row group)
+__device__ __forceinline__ void tc_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 
 __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   extern __shared__ __align__(1024) uint8_t s3_raw[];
   S3Smem& S = *reinterpret_cast<S3Smem*>(s3_raw);
-  int* s_rep = reinterpret_cast<int*>(s3_raw + 512);  // [ncol_g] then s_part, s_fast
+  int* s_rep = reinterpret_cast<int*>(s3_raw + 512);  // [ncol_g] then s_part, s_fast, s_fastc
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = P.n, K3p = P.K3p, NCH = P.NCH, NRT = P.NRT;
+  const int n = P.n, K3p = P.K3p, NCH = P.NCH, NRT = P.NRT, NS = P.NS;
   const int G = P.G, grp = blockIdx.x % G;
   const int nch = P.g_nch[grp], ncol = nch * NCH, col0 = P.g_col0[grp];
   int* s_part = s_rep + ncol;
   uint8_t* s_fast = reinterpret_cast<uint8_t*>(s_part + ncol);
   uint8_t* s_fastc = s_fast + ncol / 8;  // [nch * 2]: leading columns of a half chunk in fast groups
   const uint32_t meta_bytes = ((uint32_t)ncol * 8u + (uint32_t)ncol / 8u + 2u * (uint32_t)nch + 512u + 1023u) & ~1023u;
-  uint8_t* ys = s3_raw + 1024 + meta_bytes;                       // Y image of this group
-  const uint32_t ypart = (uint32_t)ncol * (uint32_t)K3p * 2u;      // bytes of one bf16 part
-  const uint32_t SBO = (uint32_t)K3p * 16u;                        // bytes between 8-row groups (N)
-  const int NWG = K3p / 8;                                         // 16-byte word groups per row
-  const size_t pair_bytes = (size_t)NRT * 128 * K3p * 4;
+  uint8_t* ys = s3_raw + 1024 + meta_bytes;                        // Y image of this group
+  const uint32_t ypart = (uint32_t)ncol * (uint32_t)K3p * 2u;       // bytes of one bf16 part
+  const uint32_t rt_part = 128u * (uint32_t)K3p * 2u;              // one part of an r-tile image
+  uint8_t* stg = ys + ((2u * ypart + 1023u) & ~1023u);              // staging ring: NS r-tile images
+  const uint32_t SBO = (uint32_t)K3p * 16u;                         // bytes between 8-row groups
+  const size_t pair_bytes = (size_t)NRT * 2 * rt_part;
   if (threadIdx.x == 0) {
     mbar_init(&S.y_bar, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&S.st_full[i], 1);
+      mbar_init(&S.st_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&S.a_full[i], 8);
-      mbar_init(&S.a_empty[i], 1);
       mbar_init(&S.d_full[i], 1);
       mbar_init(&S.d_empty[i], 8);
-      mbar_init(&S.res_full[i], 1);
-      mbar_init(&S.res_empty[i], 1);
+      mbar_init(&S.red_full[i], 8);
+      mbar_init(&S.red_empty[i], 1);
     }
     fence_barrier_init();
   }
@@ -141,8 +151,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   const int p_end = min(count, p_begin + per);
 
   if (warp == 0) {
-    // ---------------- Y image of the group -> SMEM (once), then the MMA issuer (converged warp,
-    // one elected lane issues; operands stay warp-uniform)
+    // ---------------- Y image of the group -> SMEM (once); then A copies + MMAs
     const uint32_t ybytes = 2u * ypart;
     if (elect_one()) {
       mbar_arrive_expect_tx(&S.y_bar, ybytes);
@@ -155,18 +164,33 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
     __syncwarp();
     mbar_wait(&S.y_bar, 0);
     const uint32_t idesc = idesc_bf16_f32(128, NCH);
-    const uint32_t ybase = smem_u32(ys);
+    const uint32_t ybase = smem_u32(ys), sbase = smem_u32(stg);
     const int ksteps = K3p / 16, ke_steps = P.Ke / 16, halfk = K3p / 2;
     uint32_t g_a = 0, g_d = 0;
+    long long tr0 = clock64(), tr_a = 0, tr_d = 0;
     for (int p = p_begin; p < p_end; ++p) {
       for (int T = 0; T < NRT; ++T, ++g_a) {
-        const int ab = g_a & 1;
-        mbar_wait(&S.a_full[ab], (g_a >> 1) & 1);
+        const int ab = g_a & 1, s = g_a % NS;
+        long long t1 = clock64();
+        mbar_wait(&S.st_full[s], (g_a / NS) & 1);
+        tr_a += clock64() - t1;
         tc_fence_after();
         const uint32_t a_hi0 = tmem + acol0 + (uint32_t)(ab * K3p);
+        if (elect_one()) {
+          // staging -> TMEM A slot (after the MMAs that last read this slot: in-order tensor pipe)
+          const uint32_t src = sbase + (uint32_t)s * 2u * rt_part;
+          for (int part = 0; part < 2; ++part)
+            for (int j = 0; j < ksteps; ++j)
+              tc_cp_128x256b(a_hi0 + (uint32_t)(part * halfk + 8 * j),
+                             smem_desc_kmajor_noswz(src + part * rt_part + j * 256, 128, SBO));
+          tc_commit(&S.st_empty[s]);
+        }
+        __syncwarp();
         for (int c = 0; c < nch; ++c, ++g_d) {
           const int db = g_d & 1;
+          long long t2 = clock64();
           mbar_wait(&S.d_empty[db], ((g_d >> 1) & 1) ^ 1);
+          tr_d += clock64() - t2;
           tc_fence_after();
           const uint32_t dE = tmem + (uint32_t)(db * 2 * NCH), dO = dE + (uint32_t)NCH;
           const uint32_t bch = ybase + (uint32_t)(c * (NCH / 8)) * SBO;
@@ -187,53 +211,46 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           }
           __syncwarp();
         }
-        if (elect_one()) tc_commit(&S.a_empty[ab]);
-        __syncwarp();
       }
     }
-  } else if (warp <= 8) {
-    // ---------------- A writers: rows of the pair's r-tile (hi: warps 1-4, lo: warps 5-8) -> TMEM
-    const int q = warp & 3;
-    const int part = (warp - 1) >> 2;
-    const int row = q * 32 + lane;
-    uint32_t g_a = 0;
-    for (int p = p_begin; p < p_end; ++p) {
-      const uint8_t* zp = P.Zop + (size_t)p * pair_bytes;
-      for (int T = 0; T < NRT; ++T, ++g_a) {
-        const int ab = g_a & 1;
-        const bool valid = T * 128 + row < n;
-        const uint4* src = reinterpret_cast<const uint4*>(zp + (size_t)((T * 2 + part) * NWG) * 2048 + row * 16);
-        uint4 v[16];
-#pragma unroll
-        for (int g = 0; g < 16; ++g)
-          if (g < NWG) v[g] = valid ? __ldg(src + g * 128) : make_uint4(0u, 0u, 0u, 0u);
-        // one warp polls the slot barrier, the other writers sleep in a hardware named barrier
-        if (warp == 1) mbar_wait(&S.a_empty[ab], ((g_a >> 1) & 1) ^ 1);
-        named_bar(2, 256);
-        tc_fence_after();
-        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acol0 + (uint32_t)(ab * K3p + part * (K3p / 2));
-#pragma unroll
-        for (int g = 0; g < 16; ++g)
-          if (g < NWG) tmem_st4(base + 4 * g, v[g]);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.a_full[ab]);
+    if (P.trace && blockIdx.x == 0 && lane == 0) {
+      P.trace[0] = clock64() - tr0;
+      P.trace[1] = tr_a;
+      P.trace[2] = tr_d;
+      P.trace[3] = p_end - p_begin;
+    }
+  } else if (warp == 1) {
+    // ---------------- producer: one bulk copy per (pair, r-tile) into the staging ring
+    if (lane == 0) {
+      uint32_t g_a = 0;
+      for (int p = p_begin; p < p_end; ++p) {
+        const uint8_t* zp = P.Zop + (size_t)p * pair_bytes;
+        for (int T = 0; T < NRT; ++T, ++g_a) {
+          const int s = g_a % NS;
+          mbar_wait(&S.st_empty[s], ((g_a / NS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&S.st_full[s], 2u * rt_part);
+          const uint8_t* src = zp + (size_t)T * 2 * rt_part;
+          uint8_t* dst = stg + (size_t)s * 2 * rt_part;
+          for (uint32_t o = 0; o < 2u * rt_part; o += 32768u) bulk_g2s(dst + o, src + o, min(32768u, 2u * rt_part - o), &S.st_full[s]);
+        }
       }
     }
-  } else if (warp <= 16) {
+    __syncwarp();
+  } else if (warp <= 9) {
     // ---------------- epilogue: 8 warps, two per TMEM lane quarter, each half of the chunk's columns.
-    // Hot loop (8 paired columns): X = max(E + O, E - O) = E + |O|; per thread only the best value and
-    // its 8-column group are tracked (branch-free); the resolver warp recovers the exact (shift, sign)
-    // of the pair's winning group.  Groups with padding / unpaired shifts, and landscape output, take
-    // the exact path.
+    // Per chunk the warp's E / O columns (hw <= 40 each) are drained to registers and the TMEM buffer is
+    // released at once.  Paired columns: X = max(E + O, E - O) = E + |O| per 8-column group, and per
+    // thread only the best value and its group are tracked (branch-free); the resolver recovers the
+    // exact (shift, sign).  Groups with padding / unpaired shifts, and landscape output, take the exact
+    // path.
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int ew = warp - 9;        // 0..7
+    const int ew = warp - 2;        // 0..7
     const int h = ew >> 2;          // 0 or 1
-    const int hw = NCH / 2;         // columns per epilogue warp (multiple of 8)
+    const int hw = NCH / 2;         // columns per epilogue warp (multiple of 8, <= 40)
     const bool has_odd = P.Ke < K3p;
     uint32_t g_d = 0, it = 0;
+    long long tr_e = 0, tr_x = 0;
     for (int p = p_begin; p < p_end; ++p, ++it) {
       float bvf = -INFINITY;        // fast record: best E + |O| ...
       uint32_t bkf = 0xffffffffu;   // ... and its key (T << 24 | column << 7 | row)
@@ -245,62 +262,69 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         const bool active = T * 128 + q * 32 < n;  // warp-uniform: lane quarters beyond n_psi idle
         for (int c = 0; c < nch; ++c, ++g_d) {
           const int db = g_d & 1;
-          if (warp == 9) mbar_wait(&S.d_full[db], (g_d >> 1) & 1);
+          long long te = clock64();
+          if (warp == 2) mbar_wait(&S.d_full[db], (g_d >> 1) & 1);
           named_bar(3, 256);
+          tr_e += clock64() - te;
+          te = clock64();
           tc_fence_after();
           const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(db * 2 * NCH + h * hw);
           const int clb = c * NCH + h * hw;  // first column of this warp's half chunk
           const int nfast = land_p ? 0 : (int)s_fastc[c * 2 + h];
-          if (active && nfast > 0) {
-            // all columns paired: per 8-column group max of E + |O| -> (value, group key), branch-free
-            const uint32_t kb = ((uint32_t)T << 24) | ((uint32_t)clb << 7) | (uint32_t)row;
-            int c8 = 0;
-            for (; c8 + 16 <= nfast; c8 += 16) {
-              uint32_t e[16], o[16];
-              tmem_ld16(base + c8, e);
-              tmem_ld16(base + NCH + c8, o);
-              tmem_wait_ld();
+          uint32_t e01[32], e2[8], o01[32], o2[8];
+          uint32_t* e0 = e01;
+          uint32_t* e1 = e01 + 16;
+          uint32_t* o0 = o01;
+          uint32_t* o1 = o01 + 16;
+          if (active) {
+            if (hw > 16) {
+              tmem_ld32(base, e01);
+            } else {
+              tmem_ld16(base, *reinterpret_cast<uint32_t(*)[16]>(e01));
+            }
+            if (hw > 32) tmem_ld8(base + 32, e2);
+            if (has_odd) {
+              if (hw > 16) {
+                tmem_ld32(base + NCH, o01);
+              } else {
+                tmem_ld16(base + NCH, *reinterpret_cast<uint32_t(*)[16]>(o01));
+              }
+              if (hw > 32) tmem_ld8(base + NCH + 32, o2);
+            }
+            tmem_wait_ld();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.d_empty[db]);
+          tr_x += clock64() - te;
+          if (!has_odd) {
 #pragma unroll
-              for (int g2 = 0; g2 < 2; ++g2) {
+            for (int k = 0; k < 16; ++k) o0[k] = o1[k] = 0u;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o2[k] = 0u;
+          }
+          if (active) {
+            const uint32_t kb = ((uint32_t)T << 24) | ((uint32_t)clb << 7) | (uint32_t)row;
+#pragma unroll
+            for (int g8 = 0; g8 < 5; ++g8) {
+              if (8 * g8 >= hw) break;
+              uint32_t e[8], o[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                e[k] = g8 < 2 ? e0[8 * g8 + k] : (g8 < 4 ? e1[8 * (g8 - 2) + k] : e2[k]);
+                o[k] = g8 < 2 ? o0[8 * g8 + k] : (g8 < 4 ? o1[8 * (g8 - 2) + k] : o2[k]);
+              }
+              if (8 * g8 < nfast) {
                 float v[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                  v[k] = __uint_as_float(e[8 * g2 + k]) + fabsf(__uint_as_float(o[8 * g2 + k]));
+                for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(e[k]) + fabsf(__uint_as_float(o[k]));
                 const float m = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
                                       fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
                 const bool upd = m > bvf;
                 bvf = upd ? m : bvf;
-                bkf = upd ? kb + ((uint32_t)(c8 + 8 * g2) << 7) : bkf;
-              }
-            }
-            if (c8 < nfast) {
-              uint32_t e[8], o[8];
-              tmem_ld8(base + c8, e);
-              tmem_ld8(base + NCH + c8, o);
-              tmem_wait_ld();
-              float v[8];
-#pragma unroll
-              for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(e[k]) + fabsf(__uint_as_float(o[k]));
-              const float m = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
-                                    fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
-              const bool upd = m > bvf;
-              bvf = upd ? m : bvf;
-              bkf = upd ? kb + ((uint32_t)c8 << 7) : bkf;
-            }
-          }
-          if (active && nfast < hw) {
-            // exact path: padding / unpaired columns, no odd block, or landscape output
-            for (int c8 = nfast; c8 < hw; c8 += 8) {
-              uint32_t e[8], o[8];
-              tmem_ld8(base + c8, e);
-              if (has_odd) tmem_ld8(base + NCH + c8, o);
-              tmem_wait_ld();
-              if (!has_odd) {
-#pragma unroll
-                for (int k = 0; k < 8; ++k) o[k] = 0u;
-              }
-              const int cl = clb + c8;
-              if (r < n) {
+                bkf = upd ? kb + ((uint32_t)(8 * g8) << 7) : bkf;
+              } else if (r < n) {
+                const int cl = clb + 8 * g8;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                   const int tp = s_rep[cl + k], tm = s_part[cl + k];
@@ -326,12 +350,9 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
               }
             }
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&S.d_empty[db]);
         }
       }
-      // per-pair reduction of both records over the warp, then over the 8 warps (warp 9 posts them)
+      // per-pair reduction over the warp; the resolver merges the 8 warps' records
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const float v2 = __shfl_xor_sync(0xffffffffu, bvf, o);
@@ -349,64 +370,58 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
       }
       const int rb = it & 1;
       if (lane == 0) {
+        mbar_wait(&S.red_empty[rb], ((it >> 1) & 1) ^ 1);  // slot consumed by the resolver (pair it - 2)
         S.red_v[rb][ew] = bvf;
         S.red_k[rb][ew] = bkf;
         S.red_ve[rb][ew] = bve;
         S.red_fe[rb][ew] = bfe;
+        mbar_arrive(&S.red_full[rb]);
       }
-      named_bar(1, 256);
-      if (ew == 0 && lane == 0) {
-        float v = S.red_v[rb][0], ve = S.red_ve[rb][0];
-        uint32_t k = S.red_k[rb][0], fe = S.red_fe[rb][0];
-        for (int w = 1; w < 8; ++w) {
-          if (better(S.red_v[rb][w], S.red_k[rb][w], v, k)) {
-            v = S.red_v[rb][w];
-            k = S.red_k[rb][w];
-          }
-          if (better(S.red_ve[rb][w], S.red_fe[rb][w], ve, fe)) {
-            ve = S.red_ve[rb][w];
-            fe = S.red_fe[rb][w];
-          }
-        }
-        // the resolver has consumed slot rb (pair it - 2) before we overwrite it
-        mbar_wait(&S.res_empty[rb], ((it >> 1) & 1) ^ 1);
-        S.res_v[rb] = v;
-        S.res_k[rb] = k;
-        S.res_ve[rb] = ve;
-        S.res_fe[rb] = fe;
-        S.res_p[rb] = p;
-        mbar_arrive(&S.res_full[rb]);
-      }
+      __syncwarp();
+    }
+    if (P.trace && blockIdx.x == 0 && lane == 0 && warp == 2) {
+      P.trace[4] = tr_e;
+      P.trace[5] = tr_x;
     }
   } else {
-    // ---------------- resolver (warp 17): exact (shift, sign) of the pair's winning 8-column group by
-    // recomputing its 16 E / O sums from the same bf16 hi/lo operands (fp32 on CUDA cores), merge with
-    // the exact record, one packed-key atomicMax per pair.
-    const int NWG2 = NWG;
+    // ---------------- resolver (warp 10): merge the 8 partial records; exact (shift, sign) of the pair's
+    // winning group by recomputing its 16 E / O sums from the same bf16 hi/lo operands (fp32 on CUDA
+    // cores); merge with the exact record; one packed-key atomicMax per pair.
     uint32_t it = 0;
     for (int p = p_begin; p < p_end; ++p, ++it) {
       const int rb = it & 1;
-      mbar_wait(&S.res_full[rb], (it >> 1) & 1);
-      const float v = S.res_v[rb], ve = S.res_ve[rb];
-      const uint32_t key = S.res_k[rb], fe = S.res_fe[rb];
-      const int pp = S.res_p[rb];
+      mbar_wait_lazy(&S.red_full[rb], (it >> 1) & 1, 200);
+      float v = S.red_v[rb][0], ve = S.red_ve[rb][0];
+      uint32_t key = S.red_k[rb][0], fe = S.red_fe[rb][0];
+      for (int w = 1; w < 8; ++w) {
+        if (better(S.red_v[rb][w], S.red_k[rb][w], v, key)) {
+          v = S.red_v[rb][w];
+          key = S.red_k[rb][w];
+        }
+        if (better(S.red_ve[rb][w], S.red_fe[rb][w], ve, fe)) {
+          ve = S.red_ve[rb][w];
+          fe = S.red_fe[rb][w];
+        }
+      }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.res_empty[rb]);
+      if (lane == 0) mbar_arrive(&S.red_empty[rb]);
       float bv = ve;
       uint32_t bf = fe;
       if (key != 0xffffffffu) {
         const int T = (int)(key >> 24), cl = (int)((key >> 7) & 0x1ffffu), rrow = (int)(key & 127u);
         const int r = T * 128 + rrow;
-        const uint8_t* zrow = P.Zop + (size_t)pp * pair_bytes + (size_t)(T * 2 * NWG2) * 2048 + rrow * 16;
+        // row rrow of the pair's r-tile image: word w at (rrow / 8) SBO + (w / 4) 128 + (rrow % 8) 16 + (w % 4) 4
+        const uint8_t* zrow = P.Zop + (size_t)p * pair_bytes + (size_t)T * 2 * rt_part + (size_t)(rrow >> 3) * SBO +
+                              (rrow & 7) * 16;
         float es[8], os[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) es[k] = os[k] = 0.f;
         const __nv_bfloat16* yh = reinterpret_cast<const __nv_bfloat16*>(ys);
         const __nv_bfloat16* yl = yh + (size_t)ncol * K3p;
         for (int kk = lane; kk < K3p; kk += 32) {
-          const size_t zo = (size_t)(kk >> 3) * 2048 + (kk & 7) * 2;
+          const size_t zo = (size_t)(kk >> 3) * 128 + (kk & 7) * 2;
           const float zh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(zrow + zo));
-          const float zl = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(zrow + (size_t)NWG2 * 2048 + zo));
+          const float zl = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(zrow + rt_part + zo));
           const bool even = kk < P.Ke;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -447,7 +462,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
       }
       if (lane == 0 && bf != 0xffffffffu) {
         int i, j;
-        pair_of(P.pb, pp, i, j);
+        pair_of(P.pb, p, i, j);
         const uint32_t tt2 = bf / (uint32_t)n, rr = bf - tt2 * (uint32_t)n;
         const uint32_t gflat = ((uint32_t)(P.tm_off + j) * (uint32_t)P.N_t + tt2) * (uint32_t)n + rr;
         const unsigned long long kk = pack_key(bv, gflat);
@@ -465,10 +480,12 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   }
 }
 
-static size_t s3_smem_bytes(int ncol, int K3p) {
+static size_t s3_smem_bytes(int ncol, int K3p, int NS) {
   const size_t meta = (((size_t)ncol * 8 + ncol / 8) + 2 * (size_t)(ncol / 16) + 512 + 1023) & ~(size_t)1023;
-  return 1024 + meta + (size_t)ncol * K3p * 4;
+  const size_t y = ((size_t)ncol * K3p * 4 + 1023) & ~(size_t)1023;
+  return 1024 + meta + y + (size_t)NS * 128 * K3p * 4;
 }
+
 
 // ---------------------------------------------------------------- Step 1 (tensor cores)
 // Form B of Eq. (fbk3) Step 1 (P:836 with p = q - ell): for each image mode p
@@ -751,7 +768,7 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 //   Z_zeta(r) = e^{-2 pi i ell r / n} sum_p Zhat'_zeta(p) e^{-2 pi i p r / n},   (q = p + ell)
 // read from Zhat' [pair][p][Hs] (Form B, written by k_step1_tc) or Zhat [pair][zeta][q] (Form A, the
 // explicit-pair path); written as the Step-3 A operand rows (real columns of reading R13), bf16 hi/lo
-// packed in 32-bit words (two K columns per word): Zop [pair][r-tile][part][word group][row 128][16 B].
+// packed in 32-bit words (two K columns per word), per (pair, r-tile, part) the canonical K-major core-matrix image [row/8][word group][8 rows x 16 B] that k_step3_tc bulk-copies and tcgen05.cp-s into TMEM.
 // Work item = (pair, block of two word groups = 16 Step-3 columns, <= 16 terms); persistent CTAs, two
 // per SM.  The item's input rows are gathered with 16-byte cp.async into a [p][18] shared-memory buffer,
 // one warp per term row.
@@ -990,7 +1007,7 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
     __syncthreads();
     // ---- write out the two word groups: per (group, r-tile, part) 128 rows x 16 B contiguous
     {
-      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)(2 * b) * 2048;
+      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)(2 * b) * 128;
       for (int idx = threadIdx.x; idx < 2 * NRT * 2 * 128; idx += blockDim.x) {
         const int row = idx & 127, rest = idx >> 7;
         const int part = rest & 1, T = (rest >> 1) % NRT, grp = (rest >> 1) / NRT;
@@ -1001,7 +1018,8 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
           const uint32_t* sp = stg + (size_t)((grp * 2 + part) * 4) * RS + pi;
           v = make_uint4(sp[0], sp[RS], sp[2 * RS], sp[3 * RS]);
         }
-        *reinterpret_cast<uint4*>(base + (size_t)((T * 2 + part) * NWG + grp) * 2048 + row * 16) = v;
+        *reinterpret_cast<uint4*>(base + (size_t)((T * 2 + part) * NWG) * 2048 + (size_t)(row >> 3) * NWG * 128 +
+                                  (size_t)grp * 128 + (row & 7) * 16) = v;
       }
     }
     __syncthreads();
@@ -1241,7 +1259,7 @@ __global__ void __launch_bounds__(S2T_THREADS, 3) k_step2_tc(const float2* __res
     __syncthreads();
     // ---- write out the word group: per (r-tile, part) 128 rows x 16 B contiguous
     {
-      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)g * 2048;
+      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)g * 128;
       for (int idx = threadIdx.x; idx < NRT * 2 * 128; idx += blockDim.x) {
         const int row = idx & 127, rest = idx >> 7;
         const int part = rest & 1, T = rest >> 1;
@@ -1252,7 +1270,8 @@ __global__ void __launch_bounds__(S2T_THREADS, 3) k_step2_tc(const float2* __res
           const uint32_t* sp = stg + (size_t)(4 * part) * RS + pi;
           v = make_uint4(sp[0], sp[RS], sp[2 * RS], sp[3 * RS]);
         }
-        *reinterpret_cast<uint4*>(base + (size_t)((T * 2 + part) * NWG) * 2048 + row * 16) = v;
+        *reinterpret_cast<uint4*>(base + (size_t)((T * 2 + part) * NWG) * 2048 + (size_t)(row >> 3) * NWG * 128 +
+                                  (row & 7) * 16) = v;
       }
     }
     __syncthreads();
@@ -1485,10 +1504,13 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
     rg = (tc.n_rep + G - 1) / G;
     const int nch = (rg + nmax - 1) / nmax;
     const int NCH = ((rg + nch - 1) / nch + 15) / 16 * 16;
-    if (s3_smem_bytes(nch * NCH, K3p) <= smem_cap) {
+    if (s3_smem_bytes(nch * NCH, K3p, 1) <= smem_cap) {
       tc.G = G;
       tc.NCH = NCH;
       for (int g = 0; g < G; ++g) tc.g_nch[g] = nch;
+      // staging ring depth: as many r-tile images as fit (1..4)
+      tc.NS = 1;
+      while (tc.NS < 4 && s3_smem_bytes(nch * NCH, K3p, tc.NS + 1) <= smem_cap) ++tc.NS;
       break;
     }
   }
@@ -1533,7 +1555,7 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   cudaMemcpy(tc.d_colpart, colpart.data(), tc.ncol * sizeof(int), cudaMemcpyHostToDevice);
   cudaMemcpy(tc.d_colfast, colfast.data(), colfast.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(tc.d_Ysm, yimg.data(), yimg.size() * 2, cudaMemcpyHostToDevice);
-  tc.s3_smem = s3_smem_bytes(ncol_g, K3p);
+  tc.s3_smem = s3_smem_bytes(ncol_g, K3p, tc.NS);
   cudaFuncSetAttribute(k_step3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.s3_smem);
   if (pm.n_k % 16 != 0 || pm.n_k > 128) {
     msg = "tensor-core engine: n_k must be a multiple of 16 and <= 128";
@@ -1727,6 +1749,7 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
   prm.NRT = tc.NRT;
   prm.NCH = tc.NCH;
   prm.G = tc.G;
+  prm.NS = tc.NS;
   for (int g = 0; g < tc.G; ++g) {
     prm.g_col0[g] = tc.g_col0[g];
     prm.g_nch[g] = tc.g_nch[g];
@@ -1740,7 +1763,21 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
   int cpg = tc.num_sms / tc.G;
   if (cpg > pb.count) cpg = pb.count;
   if (cpg < 1) cpg = 1;
+  static unsigned long long* d_trace = nullptr;  // diagnostics: FTK_S3_TRACE=1 prints CTA 0's counters
+  const char* tenv = std::getenv("FTK_S3_TRACE");
+  if (tenv && tenv[0] == '1') {
+    if (!d_trace) cudaMalloc(&d_trace, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(d_trace, 0, 16 * sizeof(unsigned long long), s);
+    prm.trace = d_trace;
+  }
   k_step3_tc<<<cpg * tc.G, S3_THREADS, tc.s3_smem, s>>>(prm);
+  if (prm.trace) {
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, d_trace, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "s3trace pairs=%llu total=%llu mma_wait_stage=%llu mma_wait_dempty=%llu epi_wait_dfull=%llu "
+            "epi_drain=%llu\n", h[3], h[0], h[1], h[2], h[4], h[5]);
+  }
 }
 
 void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const PairBlock& pb, const DevPlan& P,

@@ -17,7 +17,7 @@ struct TcPlan {
   int n_rep = 0;        // representative shifts (+-delta pairs share one column pair E/O)
   int Ke = 0;           // even-ell column block length
   // Step 3 (k_step3_tc): columns = representative shifts in rep-groups of nch[g] chunks of NCH
-  int NCH = 0, G = 0, NRT = 0, ncol = 0;
+  int NCH = 0, G = 0, NRT = 0, ncol = 0, NS = 1;  // NS: Step-3 staging ring depth
   int g_col0[MAXG] = {0}, g_nch[MAXG] = {0};
   long long g_yoff[MAXG] = {0};
   int* d_colrep = nullptr;
