@@ -494,7 +494,7 @@ static size_t s3_smem_bytes(int ncol, int K3p, int NS) {
 // Real GEMM per p with K' = 2 n_k:  rows (j, zeta, part) of the GENERATED operand c (A, in TMEM):
 //   Re-row = [c_r | -c_i],  Im-row = [c_i | c_r];  columns = images, B = [a_r | a_i] (pre-split, SMEM).
 // Output Zhat' [pair][p][Hs] complex (pair = il * nj + jl within the block; Hs = H_plus rounded up to even).
-constexpr int S1_THREADS = 10 * 32;
+constexpr int S1_THREADS = 14 * 32;
 constexpr int S1_STAGES = 4;
 
 struct S1Params {
@@ -506,6 +506,7 @@ struct S1Params {
   int i0, ni, j0, nj;   // block (i0 multiple of 128)
   int n, n_k, Hp, Hs, KCH, NKCH, NIT;  // NIT = image tiles per mode in Aop
   int F, NCT;           // F = nj * Hp flattened (j, zeta) columns, NCT = ceil(F / 64)
+  unsigned long long* trace;  // nullable (FTK_S1_TRACE=1): wait cycle counters of CTA 0
 };
 
 // Unit order: u -> (mode p, column tile ct) with p = 8 p_hi + p_lo, p_lo fastest, then ct, then p_hi.
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
       mbar_init(&S.st_full[i], 1);
       mbar_init(&S.st_empty[i], 1);
     }
-    mbar_init(&S.a_full, 128);
+    mbar_init(&S.a_full, 8);
     mbar_init(&S.a_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.acc_full[i], 1);
@@ -581,17 +582,24 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
       const uint32_t part_bytes = 128u * P.KCH * 2u;
       const uint32_t SBO = (uint32_t)(P.KCH / 8) * 128u;
       uint32_t g_st = 0, g_acc = 0, g_u = 0;
+      long long tr0 = clock64(), tra = 0, trc = 0, trs = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++g_u) {
+        long long t1 = clock64();
         mbar_wait(&S.a_full, g_u & 1);
+        tra += clock64() - t1;
         tc_fence_after();
         for (int t = 0; t < nit; ++t, ++g_acc) {
           const int ab = g_acc & 1;
+          t1 = clock64();
           mbar_wait(&S.acc_empty[ab], ((g_acc >> 1) & 1) ^ 1);
+          trc += clock64() - t1;
           tc_fence_after();
           const uint32_t d = tmem + 256 + (uint32_t)(ab * 128);
           for (int kc = 0; kc < P.NKCH; ++kc, ++g_st) {
             const int s = g_st % S1_STAGES;
+            t1 = clock64();
             mbar_wait(&S.st_full[s], (g_st / S1_STAGES) & 1);
+            trs += clock64() - t1;
             tc_fence_after();
             const uint32_t st = sbase + s * stage_bytes;
             for (int ks = 0; ks < P.KCH / 16; ++ks) {
@@ -610,22 +618,32 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
         }
         tc_commit(&S.a_empty);
       }
+      if (P.trace && blockIdx.x == 0) {
+        P.trace[0] = clock64() - tr0;
+        P.trace[1] = tra;
+        P.trace[2] = trc;
+        P.trace[3] = trs;
+        P.trace[4] = g_u;
+      }
     }
     __syncwarp();
-  } else if (warp < 6) {
-    // ---------------- generators of the template x G operand (A, TMEM columns [0, 2 n_k))
+  } else if (warp < 10) {
+    // ---------------- generators of the template x G operand (A, TMEM columns [0, 2 n_k)); 8 warps: two
+    // per TMEM lane quarter, each half of the radial nodes m; loads issued two 16-node steps at a time
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int c = row >> 1, part = row & 1;
+    const int mh = (warp - 2) >> 2;  // radial half
     const uint32_t base = tmem + ((uint32_t)(q * 32) << 16);
     const int half = nk / 2;  // u32 columns per K' half
+    // (n_k < 32: a half would be narrower than one 16-node STTM step; the first-half warps do all nodes)
+    const int m_beg = nk >= 32 ? mh * half : 0;
+    const int m_end = nk >= 32 ? m_beg + half : (mh == 0 ? nk : 0);
     uint32_t g_u = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++g_u) {
       int p, ct;
       s1_unit(u, P.NCT, p, ct);
       const int f = ct * 64 + c;
-      mbar_wait(&S.a_empty, (g_u & 1) ^ 1);
-      tc_fence_after();
       const bool valid = f < P.F;
       int jl = 0, z = 0;
       if (valid) {
@@ -635,42 +653,49 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
       const int qt = valid ? ((p + __ldg(P.ell + z)) & (n - 1)) : 0;
       const float2* brow = P.B + ((size_t)(P.j0 + jl) * n + qt) * nk;
       const float* grow = P.g + (size_t)z * nk;
-      for (int m0 = 0; m0 < nk; m0 += 16) {
-        uint32_t h1[8], l1[8], h2[8], l2[8];
+      mbar_wait(&S.a_empty, (g_u & 1) ^ 1);
+      tc_fence_after();
+      for (int m0 = m_beg; m0 < m_end; m0 += 32) {
+        float4 bb[2][8];
+        float2 gg[2][8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          float cr0 = 0.f, ci0 = 0.f, cr1 = 0.f, ci1 = 0.f;
-          if (valid) {
-            const float4 bb = __ldg(reinterpret_cast<const float4*>(brow + m0 + 2 * e));
-            const float2 gg = __ldg(reinterpret_cast<const float2*>(grow + m0 + 2 * e));
-            cr0 = gg.x * bb.x;
-            ci0 = -gg.x * bb.y;
-            cr1 = gg.y * bb.z;
-            ci1 = -gg.y * bb.w;
+        for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int m = m0 + 16 * s2 + 2 * e;
+            const bool ok = valid && m < m_end;
+            bb[s2][e] = ok ? __ldg(reinterpret_cast<const float4*>(brow + m)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            gg[s2][e] = ok ? __ldg(reinterpret_cast<const float2*>(grow + m)) : make_float2(0.f, 0.f);
           }
-          if (part == 0) {  // Re-row: [c_r | -c_i]
-            split2_bf16(cr0, cr1, h1[e], l1[e]);
-            split2_bf16(-ci0, -ci1, h2[e], l2[e]);
-          } else {          // Im-row: [c_i | c_r]
-            split2_bf16(ci0, ci1, h1[e], l1[e]);
-            split2_bf16(cr0, cr1, h2[e], l2[e]);
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+          if (m0 + 16 * s2 >= m_end) break;
+          uint32_t h1[8], l1[8], h2[8], l2[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float cr0 = gg[s2][e].x * bb[s2][e].x, ci0 = -gg[s2][e].x * bb[s2][e].y;
+            const float cr1 = gg[s2][e].y * bb[s2][e].z, ci1 = -gg[s2][e].y * bb[s2][e].w;
+            // Re-row: [c_r | -c_i],  Im-row: [c_i | c_r]  (branch-free)
+            split2_bf16(part ? ci0 : cr0, part ? ci1 : cr1, h1[e], l1[e]);
+            split2_bf16(part ? cr0 : -ci0, part ? cr1 : -ci1, h2[e], l2[e]);
           }
+          const uint32_t col = (uint32_t)((m0 + 16 * s2) / 2);
+          tmem_st8(base + col, h1);
+          tmem_st8(base + half + col, h2);
+          tmem_st8(base + nk + col, l1);
+          tmem_st8(base + nk + half + col, l2);
         }
-        const uint32_t col = (uint32_t)(m0 / 2);
-        tmem_st8(base + col, h1);
-        tmem_st8(base + half + col, h2);
-        tmem_st8(base + nk + col, l1);
-        tmem_st8(base + nk + half + col, l2);
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&S.a_full);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.a_full);
     }
   } else {
     // ---------------- epilogue: accumulator [128 rows (j,zeta,part)] x [128 images] -> Zhat'
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int ew = warp - 6;  // 0..3
+    const int ew = warp - 10;  // 0..3
     uint32_t g_acc = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int p, ct;
@@ -1803,7 +1828,22 @@ void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const Pair
   prm.NCT = (prm.F + 63) / 64;
   const int units = P.n_psi * prm.NCT;
   const int grid = units < tc.num_sms ? units : tc.num_sms;
+  static unsigned long long* d_trace = nullptr;  // diagnostics: FTK_S1_TRACE=1 prints CTA 0's counters
+  const char* tenv = std::getenv("FTK_S1_TRACE");
+  prm.trace = nullptr;
+  if (tenv && tenv[0] == '1') {
+    if (!d_trace) cudaMalloc(&d_trace, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(d_trace, 0, 16 * sizeof(unsigned long long), s);
+    prm.trace = d_trace;
+  }
   k_step1_tc<<<grid, S1_THREADS, s1_smem_bytes(tc), s>>>(prm);
+  if (prm.trace) {
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, d_trace, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "s1trace units=%llu total=%llu mma_wait_a=%llu mma_wait_acc=%llu mma_wait_stage=%llu\n", h[4],
+            h[0], h[1], h[2], h[3]);
+  }
 }
 
 int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2* A, const float2* B, void* ws,
