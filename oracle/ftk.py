@@ -7,6 +7,13 @@ Eq. (fbk3), for every retained term zeta = (ell, eta) (both signs of 
 with q cyclic mod n_psi (reading R5), gamma_r = 2 pi r / n_psi (reading R3/R4), so
 Step 2 is numpy's forward DFT over q (exp(-2 pi i q r / n_psi)).  X is complex; its
 imaginary part is kept as a diagnostic (it vanishes for real images).
+
+More rotations than angular samples (n_gamma > n_psi; "by zero-padding and using a larger
+FFT in the second step"): Step 2 is evaluated at gamma_r = 2 pi r / n_gamma as the trigonometric
+sum over the signed frequencies q in [-n_psi/2, n_psi/2] with the Nyquist coefficient split equally
+between -n_psi/2 and +n_psi/2 (reading R21: the paper's sum over q = -Q..Q counts the aliased
+Nyquist index twice; the symmetric split keeps X real for real images and reproduces the n_psi-grid
+values exactly).
 """
 from __future__ import annotations
 
@@ -17,9 +24,25 @@ import numpy as np
 from .kernel_svd import OraclePlan
 
 
-def ftk_landscapes(a, b, plan: OraclePlan):
+def step2_rotations(Zhat, n_gamma=None):
+    """Step 2 (Eq. 1dfft): Z(gamma_r) = sum_q exp(-i q gamma_r) Zhat(q),
+    gamma_r = 2 pi r / n_gamma.  Zhat [..., n_psi] over cyclic q; n_gamma = n_psi is numpy's FFT,
+    n_gamma > n_psi the direct sum over signed q with the Nyquist term split (reading R21)."""
+    n_psi = Zhat.shape[-1]
+    if n_gamma is None or n_gamma == n_psi:
+        return np.fft.fft(Zhat, axis=-1)
+    Q = n_psi // 2
+    q = np.arange(n_psi)
+    qs = np.where(q < Q, q, q - n_psi).astype(np.float64)        # signed frequency of cyclic index q
+    gam = 2.0 * math.pi * np.arange(n_gamma) / n_gamma
+    E = np.exp(-1j * qs[:, None] * gam[None, :])                  # [q, r]
+    E[Q, :] = np.cos(Q * gam)                                     # Nyquist: (e^{-iQg} + e^{iQg}) / 2
+    return np.einsum("...q,qr->...r", Zhat, E)
+
+
+def ftk_landscapes(a, b, plan: OraclePlan, n_gamma=None):
     """a: FB coeffs of images [I, n_k, n_psi]; b: templates [J, n_k, n_psi] (complex).
-    Returns X [I, J, N_t, n_psi] complex128."""
+    Returns X [I, J, N_t, n_gamma] complex128 (n_gamma defaults to n_psi)."""
     a = np.asarray(a, dtype=np.complex128)
     b = np.asarray(b, dtype=np.complex128)
     I, J = a.shape[0], b.shape[0]
@@ -34,7 +57,7 @@ def ftk_landscapes(a, b, plan: OraclePlan):
         P = a_shift[:, None, :, :] * bc[None, :, :, :]          # [I, J, m, q]
         Gw = 2.0 * math.pi * plan.w[None, :] * plan.G[zs]       # [h, m]
         Zhat[:, :, zs, :] = np.einsum("hm,ijmq->ijhq", Gw, P)   # Step 1
-    Z = np.fft.fft(Zhat, axis=-1)                               # Step 2
+    Z = step2_rotations(Zhat, n_gamma)                          # Step 2
     return np.einsum("th,ijhr->ijtr", plan.Y, Z)                # Step 3
 
 
@@ -52,14 +75,14 @@ def best_per_image(X):
     return val, j, t, r, gap
 
 
-def ftk_best(a, b, plan: OraclePlan, chunk_i: int = 4, chunk_j: int = 16):
+def ftk_best(a, b, plan: OraclePlan, chunk_i: int = 4, chunk_j: int = 16, n_gamma=None):
     """Per-image bests over all templates, blocked over pairs (same arithmetic as ftk_landscapes)."""
     I, J = a.shape[0], b.shape[0]
     best_v = np.full(I, -np.inf)
     best_idx = np.zeros((I, 3), dtype=np.int64)
     for i0 in range(0, I, chunk_i):
         for j0 in range(0, J, chunk_j):
-            X = np.real(ftk_landscapes(a[i0:i0 + chunk_i], b[j0:j0 + chunk_j], plan))
+            X = np.real(ftk_landscapes(a[i0:i0 + chunk_i], b[j0:j0 + chunk_j], plan, n_gamma))
             v, j, t, r, _ = best_per_image(X)
             for ii in range(v.size):
                 if v[ii] > best_v[i0 + ii]:     # strict: earlier j wins ties

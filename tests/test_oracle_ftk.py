@@ -179,3 +179,69 @@ def test_c2_ftk_vs_brute_sampled():
         for j in range(2):
             v = brute.brute_points(x[i], y[j], plan.k, plan.w, plan.shifts, T, R)
             assert np.max(np.abs(X[i, j][T, R] - v)) <= 4 * cfg.eps * na[i] * nb[j]
+
+
+# ---------------- more rotations than angular samples (n_gamma > n_psi, reading R21)
+
+def _small_exact_plan():
+    """n = 32 px, n_k = 32 (radial rule exact to ~1e-11 for these blobs), n_psi = 64, eps = 1e-5."""
+    cfg = synth.config("tiny", n_k=32, eps=1e-5)
+    sh = synth.shift_list(cfg)[[0, 24, 30]]
+    plan = ks.build_plan(cfg.n, cfg.K, synth.delta_max(cfg), sh, cfg.eps, cfg.n_k, cfg.n_psi, n_nodes=96)
+    return cfg, plan
+
+
+def test_n_gamma_grid_subsampling_and_reality():
+    """Every (n_gamma / n_psi)-th rotation reproduces the n_gamma = n_psi landscape (the zero padding
+    changes no grid value), and for real images X stays real at the new angles too (only the symmetric
+    Nyquist split has this property)."""
+    cfg, plan = _small_exact_plan()
+    cfg = synth.config("tiny", n_k=32, eps=1e-5, snr=0.5)  # white noise: energy up to the Nyquist index
+    x, _ = synth.draw_items(cfg, "images", [0, 1], plan.k)
+    y, _ = synth.draw_items(cfg, "templates", [0, 1, 2], plan.k)
+    a, b = fb.fb_coeffs(x), fb.fb_coeffs(y)
+    assert np.min(np.abs(a[..., cfg.n_psi // 2])) > 0.0
+    X1 = ftk.ftk_landscapes(a, b, plan)
+    X4 = ftk.ftk_landscapes(a, b, plan, n_gamma=4 * cfg.n_psi)
+    scale = np.max(np.abs(X1))
+    assert np.max(np.abs(X4[..., ::4] - X1)) < 1e-12 * scale
+    assert np.max(np.abs(np.imag(X4))) < 1e-12 * scale
+
+
+def test_n_gamma_off_grid_matches_closed_form():
+    """Off-grid rotations gamma = 2 pi r / n_gamma (r odd) of noiseless Gaussian-blob images against
+    the exact (2 pi)^2 <R_gamma T_delta A, B> (closed form, any gamma): the trigonometric interpolation
+    of Step 2 is exact for angularly band-limited data, so the error is the FTK one (<= 4 eps) plus the
+    quadrature error."""
+    cfg, plan = _small_exact_plan()
+    x, px = synth.draw_items(cfg, "images", [0], plan.k, noise=False)
+    y, py = synth.draw_items(cfg, "templates", [0], plan.k, noise=False)
+    ng = 4 * cfg.n_psi
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(x), fb.fb_coeffs(y), plan, n_gamma=ng))[0, 0]
+    na = fb.discrete_norm(x, plan.w)[0]
+    nb = fb.discrete_norm(y, plan.w)[0]
+    worst = 0.0
+    for t in range(plan.shifts.shape[0]):
+        for r in range(1, ng, 7):
+            cf = closed_form.gaussian_ip(px, py, 0, 0, plan.shifts[t], 2 * math.pi * r / ng)
+            worst = max(worst, abs(X[t, r] - cf) / (na * nb))
+    assert worst < 4 * plan.eps + 1e-8, worst
+
+
+def test_n_gamma_planted_off_grid_rotation_recovered():
+    """A template rotated by an off-grid angle gamma0 (analytic blobs) peaks at gamma = -gamma0 on the
+    finer rotation grid (reading R12), which the n_psi grid cannot represent."""
+    cfg, plan = _small_exact_plan()
+    k = plan.k
+    py = synth.blob_params(cfg, "templates", [0])
+    ng = 8 * cfg.n_psi
+    r0 = 37                                   # gamma0 = 2 pi r0 / ng: not a multiple of ng / n_psi
+    g0 = 2 * math.pi * r0 / ng
+    c, s = math.cos(g0), math.sin(g0)
+    px = {key: np.array(v, copy=True) for key, v in py.items()}
+    px["cx"], px["cy"] = c * py["cx"] - s * py["cy"], s * py["cx"] + c * py["cy"]
+    x = synth.polar_samples(px, k, cfg.n_psi)
+    y = synth.polar_samples(py, k, cfg.n_psi)
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(x), fb.fb_coeffs(y), plan, n_gamma=ng))[0, 0]
+    t0 = int(np.argmin(np.sum(plan.shifts ** 2, axis=1)))     # delta = 0
+    assert int(np.argmax(X[t0])) == (ng - r0) % ng
