@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--images", type=int, default=0, help="override N_im (debug only; the metric uses the config)")
     ap.add_argument("--templates", type=int, default=0)
+    ap.add_argument("--n-gamma", type=int, default=0,
+                    help="rotations per (pair, shift); 0 = n_psi (the configs). > n_psi: zero-padded Step 2 (NEXT-3)")
     return ap.parse_args()
 
 
@@ -207,7 +209,8 @@ def main():
     n_t = shifts.shape[0]
     engine = pkg.ENGINE_TC if args.engine == "tc" else pkg.ENGINE_SIMT
     plan = pkg.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), shifts, cfg.eps, n_k=cfg.n_k, n_psi=cfg.n_psi,
-                       device=local, rank=rank, world=world, engine=engine)
+                       device=local, rank=rank, world=world, engine=engine, n_gamma=args.n_gamma)
+    n_gamma = plan.info["n_gamma"]
     k, w = plan.radial()
     # synthetic inputs generated on the device (seeded), resident in HBM
     imgs, _ = synth.draw_items(cfg, "images", range(ni), k, backend="torch", device=dev)
@@ -255,7 +258,7 @@ def main():
         t = torch.tensor([dt_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt_ms = float(t.item())
-    total_ips = float(ni) * nj * n_t * cfg.n_psi
+    total_ips = float(ni) * nj * n_t * n_gamma
     value = total_ips * args.steps / (dt_ms / 1e3)
 
     # ---- roofline of the dominant kernel (largest device time in the timed region)
@@ -264,7 +267,7 @@ def main():
     info = plan.info
     pairs_local = ni * info["n_templates_local"]
     if dom == "step3":
-        flops = 2.0 * n_t * cfg.n_psi * info["K3"] * pairs_local          # real GEMM, K = 2 H_plus - H0
+        flops = 2.0 * n_t * n_gamma * info["K3"] * pairs_local            # real GEMM, K = 2 H_plus - H0
     else:
         flops = 8.0 * cfg.n_psi * info["H_plus"] * cfg.n_k * pairs_local  # complex GEMM over k_m
     flops_per_launch = flops * args.steps / max(dom_cnt, 1)
@@ -360,6 +363,7 @@ def main():
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "bf16x3" if engine == pkg.ENGINE_TC else "f32", "data": "synthetic",
                 "config": {"workload": cfg.name, "n": cfg.n, "K": cfg.K, "n_k": cfg.n_k, "n_psi": cfg.n_psi,
+                           "n_gamma": n_gamma,
                            "N_im": ni, "N_tm": nj, "N_t": n_t, "eps": cfg.eps, "H": info["H"],
                            "H_plus": info["H_plus"], "K3": info["K3"], "engine": args.engine,
                            "parallelism": f"template-shard x{world}", "l2": "inputs (6+ GB FB arrays) exceed L2",

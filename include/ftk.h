@@ -70,6 +70,9 @@ typedef struct {
   int engine;           /* 0 = tcgen05 bf16x3 tensor-core path (default), 1 = SIMT fp32 reference kernels */
   int svd_nodes;        /* Nystrom nodes per axis for the operator SVD; 0 -> 96 */
   size_t workspace_bytes;  /* pair-block workspace; 0 -> 1 GiB */
+  int n_gamma;          /* rotations gamma_r = 2 pi r / n_gamma; 0 -> n_psi.  n_gamma > n_psi evaluates Step 2
+                           as the zero-padded trigonometric sum (DESIGN reading R21); power of two,
+                           n_psi <= n_gamma <= 1024, engine 0 only (engine 1 -> FTK_EINVAL) */
 } ftk_plan_opts_t;
 
 /* One per-image (or per-pair) result, 16 bytes. */
@@ -97,6 +100,7 @@ typedef struct {
   int s3_nch;                /* engine 0: Step-3 chunk width (MMA N) */
   int s3_groups;             /* engine 0: rep-groups (Y slices resident in shared memory) */
   int s3_rtiles;             /* engine 0: 128-row rotation tiles per pair (MMA M) */
+  int n_gamma;               /* rotations per (pair, shift): gamma_r = 2 pi r / n_gamma */
 } ftk_plan_info_t;
 
 /* Build the plan (host, double precision, untimed per P:1321): radial rule, per-ell operator SVD of

@@ -11,7 +11,7 @@ LIB_PATH = os.path.join(_HERE, "libftk.so")
 class PlanOpts(C.Structure):
     _fields_ = [("n_k", C.c_int), ("n_psi", C.c_int), ("radial_rule", C.c_int), ("device", C.c_int),
                 ("rank", C.c_int), ("world", C.c_int), ("engine", C.c_int), ("svd_nodes", C.c_int),
-                ("workspace_bytes", C.c_size_t)]
+                ("workspace_bytes", C.c_size_t), ("n_gamma", C.c_int)]
 
 
 class PlanInfo(C.Structure):
@@ -22,7 +22,8 @@ class PlanInfo(C.Structure):
                 ("n_templates_total", C.c_int64), ("n_templates_local", C.c_int64), ("template_offset", C.c_int64),
                 ("engine", C.c_int), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
                 ("K3p", C.c_int), ("n_rep", C.c_int), ("s3_cols", C.c_int),
-                ("s3_nch", C.c_int), ("s3_groups", C.c_int), ("s3_rtiles", C.c_int)]
+                ("s3_nch", C.c_int), ("s3_groups", C.c_int), ("s3_rtiles", C.c_int),
+                ("n_gamma", C.c_int)]
 
 
 class Best(C.Structure):

@@ -55,10 +55,11 @@ class FTKPlan:
 
     def __init__(self, n: int, K: float, delta_max: float, shifts, eps: float, *, n_k: int = 0, n_psi: int = 0,
                  radial_rule: int = 0, device: int = 0, rank: int = 0, world: int = 1, engine: int = ENGINE_TC,
-                 svd_nodes: int = 0, workspace_bytes: int = 0):
+                 svd_nodes: int = 0, workspace_bytes: int = 0, n_gamma: int = 0):
         self._L = _ffi.lib()
         sh = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(-1, 2))
-        opts = _ffi.PlanOpts(n_k, n_psi, radial_rule, device, rank, world, engine, svd_nodes, workspace_bytes)
+        opts = _ffi.PlanOpts(n_k, n_psi, radial_rule, device, rank, world, engine, svd_nodes, workspace_bytes,
+                             n_gamma)
         out = C.c_void_p()
         st = self._L.ftk_plan_create(n, float(K), float(delta_max), sh.ctypes.data_as(C.c_void_p), sh.shape[0],
                                      float(eps), C.byref(opts), C.byref(out))
@@ -128,13 +129,13 @@ class FTKPlan:
     # ---------------- hot path
     def align(self, pair_best: bool = False, landscape: bool = False, stream=None, out=None):
         """Returns dict with 'best' (int32 [N_im,4] device tensor of ftk_best_t), optionally 'pair_best'
-        [N_im, N_tm_local, 4] and 'landscape' float [N_im, N_tm_local, N_t, n_psi]."""
+        [N_im, N_tm_local, 4] and 'landscape' float [N_im, N_tm_local, N_t, n_gamma]."""
         import torch
         dev = f"cuda:{self.device}"
         NI, NJ = self.info["n_images"], self.info["n_templates_local"]
         best = out if out is not None else torch.empty((NI, 4), dtype=torch.int32, device=dev)
         pb = torch.empty((NI, NJ, 4), dtype=torch.int32, device=dev) if pair_best else None
-        land = torch.empty((NI, NJ, self.info["N_t"], self.info["n_psi"]), dtype=torch.float32, device=dev) \
+        land = torch.empty((NI, NJ, self.info["N_t"], self.info["n_gamma"]), dtype=torch.float32, device=dev) \
             if landscape else None
         _check(self._L.ftk_align(self._p, C.c_void_p(best.data_ptr()),
                                  C.c_void_p(pb.data_ptr() if pb is not None else 0),
@@ -159,7 +160,7 @@ class FTKPlan:
         dev = f"cuda:{self.device}"
         ii = torch.as_tensor(np.asarray(img_idx, dtype=np.int32), device=dev)
         jj = torch.as_tensor(np.asarray(tpl_idx, dtype=np.int32), device=dev)
-        out = torch.empty((ii.numel(), self.info["N_t"], self.info["n_psi"]), dtype=torch.float32, device=dev)
+        out = torch.empty((ii.numel(), self.info["N_t"], self.info["n_gamma"]), dtype=torch.float32, device=dev)
         _check(self._L.ftk_landscape_pairs(self._p, C.c_void_p(ii.data_ptr()), C.c_void_p(jj.data_ptr()), ii.numel(),
                                            C.c_void_p(out.data_ptr()), _stream_ptr(stream)), self._p)
         return out

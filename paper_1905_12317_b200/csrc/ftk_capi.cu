@@ -27,7 +27,8 @@ struct ftk_plan_s {
   int* d_col = nullptr;
   float* d_Y3 = nullptr;
   float2* d_tw = nullptr;
-  int K3p = 0, K3dev = 0, Ke = 0, log2_psi = 0;
+  int K3p = 0, K3dev = 0, Ke = 0, log2_psi = 0, n_gamma = 0;
+  float2* d_twg = nullptr;  // e^{-2 pi i j / n_gamma}, j < n_gamma / 2 (Step-2 FFT)
   int* d_pads = nullptr;
   int npads = 0;
   TcPlan tc;  // tensor-core engine constants (ftk_tc.cu)
@@ -75,6 +76,8 @@ DevPlan devplan(ftk_plan_t p) {
   DevPlan d;
   d.n_k = p->pm.n_k;
   d.n_psi = p->pm.n_psi;
+  d.n_gamma = p->n_gamma;
+  d.twg = p->d_twg;
   d.log2_psi = p->log2_psi;
   d.N_t = p->pm.N_t;
   d.H_plus = p->pm.H_plus;
@@ -183,6 +186,9 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
     return bail(FTK_EINVAL);
   const int np = pm.n_psi;
   if (np < 64 || np > 1024 || (np & (np - 1)) != 0) return bail(FTK_EINVAL);
+  plan->n_gamma = o.n_gamma > 0 ? o.n_gamma : np;
+  if (plan->n_gamma < np || plan->n_gamma > 1024 || (plan->n_gamma & (plan->n_gamma - 1)) != 0) return bail(FTK_EINVAL);
+  if (plan->n_gamma != np && plan->engine != 0) return bail(FTK_EINVAL);
   if (pm.n_k > 1024) return bail(FTK_EINVAL);
   int st = pm.build();
   if (st != FTK_OK) {
@@ -257,10 +263,14 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
   for (int k = 0; k < plan->K3p; ++k)
     if (!used[k]) pads.push_back(k);
   plan->npads = (int)pads.size();
-  std::vector<float2> tw(np / 2);
+  std::vector<float2> tw(np / 2), twg(plan->n_gamma / 2);
   for (int j = 0; j < np / 2; ++j) {
     const double ph = -2.0 * M_PI * j / np;
     tw[j] = make_float2((float)std::cos(ph), (float)std::sin(ph));
+  }
+  for (int j = 0; j < plan->n_gamma / 2; ++j) {
+    const double ph = -2.0 * M_PI * j / plan->n_gamma;
+    twg[j] = make_float2((float)std::cos(ph), (float)std::sin(ph));
   }
   ftk_status_t s;
   if ((s = upload(plan, &plan->d_g, g)) != FTK_OK) return bail(s);
@@ -269,9 +279,10 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
   if ((s = upload(plan, &plan->d_pads, pads)) != FTK_OK) return bail(s);
   if ((s = upload(plan, &plan->d_Y3, Y3)) != FTK_OK) return bail(s);
   if ((s = upload(plan, &plan->d_tw, tw)) != FTK_OK) return bail(s);
+  if ((s = upload(plan, &plan->d_twg, twg)) != FTK_OK) return bail(s);
   if (plan->engine == 0) {
     std::string msg;
-    int ts = tc_plan_init(plan->tc, pm, g, ell, col, Y3, plan->K3p, plan->Ke, msg);
+    int ts = tc_plan_init(plan->tc, pm, g, ell, col, Y3, plan->K3p, plan->Ke, plan->n_gamma, msg);
     if (ts != FTK_OK) {
       plan->err = msg;
       fprintf(stderr, "ftk_plan_create: %s\n", msg.c_str());
@@ -292,6 +303,7 @@ void ftk_plan_destroy(ftk_plan_t plan) {
     cudaFree(plan->d_pads);
     cudaFree(plan->d_Y3);
     cudaFree(plan->d_tw);
+    cudaFree(plan->d_twg);
     cudaFree(plan->d_A);
     cudaFree(plan->d_B);
     cudaFree(plan->d_ws);
@@ -337,6 +349,7 @@ ftk_status_t ftk_plan_query(ftk_plan_t plan, ftk_plan_info_t* info) {
   info->world = plan->world;
   info->K3p = plan->K3p;
   info->n_rep = plan->engine == 0 ? plan->tc.n_rep : plan->pm.N_t;
+  info->n_gamma = plan->n_gamma;
   info->s3_cols = plan->engine == 0 ? plan->tc.ncol : plan->pm.N_t;
   info->s3_nch = plan->engine == 0 ? plan->tc.NCH : 0;
   info->s3_groups = plan->engine == 0 ? plan->tc.G : 0;
@@ -432,9 +445,9 @@ ftk_status_t ftk_load_templates(ftk_plan_t plan, const void* polar_c64, int64_t 
   const int64_t lo = (int64_t)plan->rank * N_total / plan->world;
   const int64_t hi = (int64_t)(plan->rank + 1) * N_total / plan->world;
   const int64_t nl = hi - lo;
-  const double flat_max = (double)N_total * plan->pm.N_t * plan->pm.n_psi;
+  const double flat_max = (double)N_total * plan->pm.N_t * plan->n_gamma;
   if (flat_max > 4294967295.0)
-    return fail(plan, FTK_ECAPACITY, "N_templates * N_t * n_psi exceeds the 32-bit argmax index");
+    return fail(plan, FTK_ECAPACITY, "N_templates * N_t * n_gamma exceeds the 32-bit argmax index");
   if (nl != plan->n_tm_local) {
     cudaFree(plan->d_B);
     plan->d_B = nullptr;
@@ -521,7 +534,7 @@ ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best,
   cudaStream_t s = (cudaStream_t)stream;
   const DevPlan P = devplan(plan);
   const int64_t NI = plan->n_im, NJ = plan->n_tm_local;
-  if (landscape && landscape_capacity < NI * NJ * P.N_t * (int64_t)P.n_psi)
+  if (landscape && landscape_capacity < NI * NJ * P.N_t * (int64_t)P.n_gamma)
     return fail(plan, FTK_ECAPACITY, "landscape buffer too small");
   if (plan->keys_cap < NI * (pair_best ? NJ + 1 : 1)) {
     cudaFree(plan->d_keys);
@@ -562,7 +575,7 @@ ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best,
         pb.nj = (int)std::min(nj, NJ - j0);
         pb.li = pb.lj = nullptr;
         pb.count = pb.ni * pb.nj;
-        float* land = landscape ? landscape + (size_t)i0 * NJ * P.N_t * P.n_psi : nullptr;
+        float* land = landscape ? landscape + (size_t)i0 * NJ * P.N_t * P.n_gamma : nullptr;
         st = run_block(plan, pb, img_keys, pair_keys, land, s);
         if (st != FTK_OK) return st;
       }
@@ -576,8 +589,8 @@ ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best,
     plan->best_tmp_cap = NI;
   }
   prof_begin(plan, 4, s);
-  launch_finalize(img_keys, NI, P.N_t, P.n_psi, host_out ? plan->d_best_tmp : best, s);
-  if (pair_best) launch_finalize(pair_keys, NI * NJ, P.N_t, P.n_psi, pair_best, s);
+  launch_finalize(img_keys, NI, P.N_t, P.n_gamma, host_out ? plan->d_best_tmp : best, s);
+  if (pair_best) launch_finalize(pair_keys, NI * NJ, P.N_t, P.n_gamma, pair_best, s);
   prof_end(plan, 4, s);
   CK(cudaGetLastError());
   if (host_out) {
@@ -607,7 +620,7 @@ ftk_status_t ftk_landscape_pairs(ftk_plan_t plan, const int32_t* img_idx, const 
     pb.li = img_idx + p0;
     pb.lj = tpl_idx + p0;
     pb.count = (int)std::min<int64_t>(chunk, n_pairs - p0);
-    st = run_block(plan, pb, nullptr, nullptr, out + p0 * (int64_t)P.N_t * P.n_psi, s);
+    st = run_block(plan, pb, nullptr, nullptr, out + p0 * (int64_t)P.N_t * P.n_gamma, s);
     if (st != FTK_OK) return st;
   }
   return FTK_OK;

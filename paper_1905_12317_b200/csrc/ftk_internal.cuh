@@ -67,6 +67,7 @@ __host__ __device__ inline bool best_better(const ftk_best_t& a, const ftk_best_
 // Device plan constants used by every engine.
 struct DevPlan {
   int n_k, n_psi, log2_psi, N_t, H_plus, K3, K3p, ell_max;
+  int n_gamma;           // rotations (Step-2 FFT length); >= n_psi, zero-padded sum (reading R21)
   int Hs;                // row stride (complex) of the engine-0 Step-1 output Zhat' [pair][p][Hs] (H_plus, even)
   int Ke;                // even-ell column block [0, Ke); odd-ell block [Ke, K3p)
   int npads;             // unused (zero) Step-3 columns
@@ -76,6 +77,7 @@ struct DevPlan {
   const int* col;        // [H_plus] first Step-3 column of the term
   const float* Y3;       // [N_t][K3p]       Step-3 real operand (reading R13), zero-padded
   const float2* tw;      // [n_psi/2] e^{-2 pi i j / n_psi}
+  const float2* twg;     // [n_gamma/2] e^{-2 pi i j / n_gamma}
 };
 
 // ---------------- SIMT reference engine (ftk_simt.cu) ----------------

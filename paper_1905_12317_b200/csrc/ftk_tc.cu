@@ -886,14 +886,15 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
   constexpr int n = 32 * E, S = S2_ROWSTRIDE;
   constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
   constexpr int RS = n + n / E;  // padded staging row (words): index r + r / E
-  float2* rows = reinterpret_cast<float2*>(s2raw);                            // [n][S]
+  const int n_in = P.n_psi;  // input rows (cyclic q); the FFT length n = n_gamma >= n_in (reading R21)
+  // [n][S]: rows [0, n_in) hold the input; each warp's column doubles as its n-slot transpose scratch
+  float2* rows = reinterpret_cast<float2*>(s2raw);
   uint32_t* stg = reinterpret_cast<uint32_t*>(s2raw + (size_t)n * S * 8);     // [group 2][part 2][word 4][RS]
   // warp index made provably warp-uniform (shfl from lane 0) so the shuffles below sit in convergent code
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int nw = blockDim.x >> 5;
   const int total = npair * B.nb;
   const int Hp = P.H_plus, Hs = P.Hs;
-  const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
 
   // per-lane constant twiddles
   // 32 = L x E: the 32-point DFT over the lane index runs as an E-point register DFT and an L-point
@@ -904,7 +905,7 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
 #pragma unroll
   for (int s = 0; s < LL; ++s) {
     const int h = (L / 2) >> s;
-    wc[s] = (lane & h) ? tw_full(P.tw, (lane & (h - 1)) * ((L / 2) / h) * (n / L), n) : make_float2(1.f, 0.f);
+    wc[s] = (lane & h) ? tw_full(P.twg, (lane & (h - 1)) * ((L / 2) / h) * (n / L), n) : make_float2(1.f, 0.f);
   }
   int gq = 0;  // L-point DIF output index of this lane: bit-reversed lane % L
 #pragma unroll
@@ -937,11 +938,11 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
       if (cpr > 0) {
         int p = threadIdx.x / cpr, c = threadIdx.x - p * cpr;
         const int dq = blockDim.x / cpr, dr = blockDim.x - dq * cpr;
-        const uint8_t* sp = reinterpret_cast<const uint8_t*>(Zhat + ((size_t)pr * n + p) * Hs + zs2) + 16 * c;
+        const uint8_t* sp = reinterpret_cast<const uint8_t*>(Zhat + ((size_t)pr * n_in + p) * Hs + zs2) + 16 * c;
         float2* dp = rows + p * S + 2 * c;
         const size_t sstep = (size_t)dq * Hs * 8 + 16 * dr, swrap = (size_t)Hs * 8 - 16 * cpr;
         const int dstep = dq * S + 2 * dr, dwrap = S - 2 * cpr;
-        while (p < n) {
+        while (p < n_in) {
           cp_async16(dp, sp);
           sp += sstep;
           dp += dstep;
@@ -956,9 +957,9 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
         }
       }
     } else {      // [pair][zeta][q]
-      const float2* src = Zhat + ((size_t)pr * Hp + zs) * n;
+      const float2* src = Zhat + ((size_t)pr * Hp + zs) * n_in;
       for (int z = 0; z < nz; ++z)
-        for (int q = threadIdx.x; q < n; q += blockDim.x) cp_async8(rows + q * S + z, src + (size_t)z * n + q);
+        for (int q = threadIdx.x; q < n_in; q += blockDim.x) cp_async8(rows + q * S + z, src + (size_t)z * n_in + q);
     }
     cp_async_commit();
     for (int idx = threadIdx.x; idx < 16 * RS; idx += blockDim.x) stg[idx] = 0u;  // padding columns stay zero
@@ -970,9 +971,23 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
       const int l = P.ell[z], col = P.col[z];
       float2* colp = rows + zoff + zz;  // this term's column of the row buffer (stride S)
       // Form B: Z(r) w^{ell r} = DFT of the cyclically shifted row Zhat'(q - ell) (reading R5)
-      const int q0 = formB ? ((lane - l) & (n - 1)) : lane;
+      if (n_in == n) {
+        const int q0 = formB ? ((lane - l) & (n - 1)) : lane;
 #pragma unroll
-      for (int bb = 0; bb < E; ++bb) x[bb] = colp[((q0 + 32 * bb) & (n - 1)) * S];
+        for (int bb = 0; bb < E; ++bb) x[bb] = colp[((q0 + 32 * bb) & (n - 1)) * S];
+      } else {
+        // n_gamma > n_psi: zero-padded signed frequencies, Nyquist split (reading R21)
+        const int Qh = n_in >> 1;
+#pragma unroll
+        for (int bb = 0; bb < E; ++bb) {
+          const int qp = lane + 32 * bb;
+          const int qc = qp < Qh ? qp : (qp > n - Qh ? qp - n + n_in : Qh);
+          const float wgt = (qp < Qh || qp > n - Qh) ? 1.f : ((qp == Qh || qp == n - Qh) ? 0.5f : 0.f);
+          const int src = formB ? ((qc - l) & (n_in - 1)) : qc;
+          const float2 v = colp[src * S];
+          x[bb] = make_float2(wgt * v.x, wgt * v.y);
+        }
+      }
       dft_regs<E>(x);  // (A) E-point DFT over b (p = a + 32 b, a = lane): natural order in x[rv(c)]
 #pragma unroll
       for (int c = 1; c < E; ++c) x[rv(c)] = cmulf(x[rv(c)], __ldg(twB + c * 32 + lane));  // (B) x_c *= w_n^{a c}
@@ -1030,8 +1045,9 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
       }
     }
     __syncthreads();
-    // ---- write out the two word groups: per (group, r-tile, part) 128 rows x 16 B contiguous
+    // ---- write out the two word groups: per (group, r-tile, part) 128 rows as core-matrix rows
     {
+      const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
       uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)(2 * b) * 128;
       for (int idx = threadIdx.x; idx < 2 * NRT * 2 * 128; idx += blockDim.x) {
         const int row = idx & 127, rest = idx >> 7;
@@ -1051,8 +1067,9 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
   }
 }
 
-static size_t step2_smem(int n) {
+static size_t step2_smem(int n_in, int n) {  // n_in = n_psi input rows, n = n_gamma >= n_in FFT length
   const int E = n / 32;
+  (void)n_in;  // the row buffer holds n rows: the transpose scratch needs the FFT length
   return (size_t)n * S2_ROWSTRIDE * 8 + (size_t)16 * (n + n / E) * 4;
 }
 
@@ -1060,10 +1077,10 @@ static void launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop,
                              const DevPlan& P, cudaStream_t s) {
   S2Blocks B;
   std::memcpy(&B, &tc.s2_blocks, sizeof B);
-  const size_t smem = step2_smem(P.n_psi);
+  const size_t smem = step2_smem(P.n_psi, P.n_gamma);
   const int items = B.nb * npair;
   dim3 grid(items < 2 * tc.num_sms ? items : 2 * tc.num_sms);
-  switch (P.n_psi) {
+  switch (P.n_gamma) {
     case 64: k_step2_fft<2><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
     case 128: k_step2_fft<4><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
     case 256: k_step2_fft<8><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
@@ -1461,7 +1478,8 @@ int tc_selftest(double* err_ts, double* err_ss, std::string& msg) {
 
 // ---------------------------------------------------------------- engine plumbing
 int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, const std::vector<int>& ell,
-                 const std::vector<int>& col, const std::vector<float>& Y3, int K3p, int Ke, std::string& msg) {
+                 const std::vector<int>& col, const std::vector<float>& Y3, int K3p, int Ke, int n_gamma,
+                 std::string& msg) {
   tc_plan_free(tc);
   if (K3p % 16 != 0 || K3p > 128) {
     msg = "tensor-core engine: Step-3 width " + std::to_string(K3p) + " (K3 = 2 H_plus - H0 = " +
@@ -1511,7 +1529,7 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
     partner.swap(p2);
   }
   tc.n_rep = (int)rep.size();
-  tc.NRT = (pm.n_psi + 127) / 128;
+  tc.NRT = (n_gamma + 127) / 128;
   // Step-3 chunk width NCH (N of the MMA): TMEM holds two D buffers (E and O, 2 NCH columns each) and
   // two A slots (K3p columns each); a rep-group's Y image must fit in shared memory.
   const int nmax = std::min(256, ((512 - 2 * K3p) / 4) / 16 * 16);
@@ -1672,7 +1690,7 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       cudaFuncSetAttribute(k_step2_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
     }
     {  // Step-2 twiddle tables: [c][a] w_n^{a c} and [d'][a] w_32^{(a % L) d'}, E = n / 32, L = 32 / E
-      const int n = pm.n_psi, E = n / 32, L = 32 / E;
+      const int n = n_gamma, E = n / 32, L = 32 / E;
       std::vector<float2> tw((size_t)2 * E * 32);
       for (int c = 0; c < E; ++c)
         for (int a = 0; a < 32; ++a) {
@@ -1687,7 +1705,7 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       }
       cudaMemcpy(tc.d_s2tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice);
     }
-    const int sm2 = (int)step2_smem(pm.n_psi);
+    const int sm2 = (int)step2_smem(pm.n_psi, n_gamma);
     cudaFuncSetAttribute(k_step2_fft<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(k_step2_fft<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(k_step2_fft<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
@@ -1767,7 +1785,7 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
   prm.colpart = tc.d_colpart;
   prm.colfast = tc.d_colfast;
   prm.pb = pb;
-  prm.n = P.n_psi;
+  prm.n = P.n_gamma;
   prm.K3p = P.K3p;
   prm.Ke = P.Ke;
   prm.N_t = P.N_t;
@@ -1861,7 +1879,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     launch_step1_simt(A, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    if (tc.step2_tensor && (P.n_psi == 256 || P.n_psi == 512))
+    if (tc.step2_tensor && P.n_gamma == P.n_psi && (P.n_psi == 256 || P.n_psi == 512))
       launch_step2_tc(tc, Zhat, Zop, pb.count, 0, P, s);
     else
       launch_step2_fft(tc, Zhat, Zop, pb.count, 0, P, s);
@@ -1871,7 +1889,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     launch_step1_tc(tc, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    if (tc.step2_tensor && (P.n_psi == 256 || P.n_psi == 512))
+    if (tc.step2_tensor && P.n_gamma == P.n_psi && (P.n_psi == 256 || P.n_psi == 512))
       launch_step2_tc(tc, Zhat, Zop, pb.count, 1, P, s);
     else
       launch_step2_fft(tc, Zhat, Zop, pb.count, 1, P, s);

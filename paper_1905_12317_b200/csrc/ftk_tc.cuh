@@ -48,7 +48,8 @@ struct TcPlan {
 typedef void (*prof_cb_t)(void* plan, int cls, int end, cudaStream_t s);
 
 int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, const std::vector<int>& ell,
-                 const std::vector<int>& col, const std::vector<float>& Y3, int K3p, int Ke, std::string& msg);
+                 const std::vector<int>& col, const std::vector<float>& Y3, int K3p, int Ke, int n_gamma,
+                 std::string& msg);
 void tc_plan_free(TcPlan& tc);
 int tc_prepare_images(TcPlan& tc, const float2* fb, int64_t n, const DevPlan& P, cudaStream_t s, std::string& msg);
 int tc_prepare_templates(TcPlan& tc, const float2* fb, int64_t n, const DevPlan& P, cudaStream_t s, std::string& msg);

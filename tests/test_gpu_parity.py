@@ -214,3 +214,59 @@ def test_tc_selftest(pkg):
     st = pkg.lib().ftk_tc_selftest(0, C.byref(ets), C.byref(ess))
     assert st == 0
     assert ets.value < 1e-4 and ess.value < 1e-4, (ets.value, ess.value)
+
+
+@pytest.mark.parametrize("name,mult", [("tiny", 2), ("c2", 4)])
+def test_n_gamma_more_rotations(pkg, name, mult):
+    """n_gamma = mult * n_psi rotations (zero-padded Step 2, reading R21): full landscapes, per-image
+    bests and the explicit-pair path against the oracle evaluated at the same angles."""
+    cfg = synth.config(name)
+    ng = mult * cfg.n_psi
+    p = make(pkg, cfg, 0, n_gamma=ng)
+    assert p.info["n_gamma"] == ng
+    k, w = p.radial()
+    imgs, _ = synth.draw_items(cfg, "images", range(3), k)
+    tpls, _ = synth.draw_items(cfg, "templates", range(5), k)
+    p.load_images(torch.from_numpy(imgs).cuda())
+    p.load_templates(torch.from_numpy(tpls).cuda())
+    res = p.align(landscape=True)
+    torch.cuda.synchronize()
+    L = res["landscape"].cpu().numpy()
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), oracle_plan(cfg), n_gamma=ng))
+    assert L.shape == X.shape
+    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+    err = np.max(np.abs(L - X) / (na[:, None, None, None] * nb[None, :, None, None]))
+    assert err <= TOL, err
+    check_best(pkg.best_to_numpy(res["best"]), X, na, nb)
+    ii, jj = np.array([0, 2]), np.array([4, 1])
+    Lp = p.landscape_pairs(ii, jj).cpu().numpy()
+    for n in range(2):
+        assert np.max(np.abs(Lp[n] - X[ii[n], jj[n]])) <= TOL * na[ii[n]] * nb[jj[n]]
+
+
+def test_n_gamma_option_errors(pkg):
+    cfg = synth.config("tiny")
+    for ng, engine in [(96, 0), (32, 0), (2 * cfg.n_psi, 1)]:  # not a power of two; < n_psi; SIMT engine
+        with pytest.raises(pkg.FTKError):
+            make(pkg, cfg, engine, n_gamma=ng)
+
+
+def test_step2_tensor_variant(pkg, monkeypatch):
+    """k_step2_tc (FTK_STEP2_TC=1: the 32-point DFT stage on tcgen05) on a ragged c3 subset."""
+    monkeypatch.setenv("FTK_STEP2_TC", "1")
+    cfg = synth.config("c3")
+    p = make(pkg, cfg, 0)
+    k, w = p.radial()
+    imgs, _ = synth.draw_items(cfg, "images", range(5), k)
+    tpls, _ = synth.draw_items(cfg, "templates", range(7), k)
+    p.load_images(torch.from_numpy(imgs).cuda())
+    p.load_templates(torch.from_numpy(tpls).cuda())
+    res = p.align(pair_best=True)
+    torch.cuda.synchronize()
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), oracle_plan(cfg)))
+    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+    check_best(pkg.best_to_numpy(res["best"]), X, na, nb)
+    pb = pkg.best_to_numpy(res["pair_best"].reshape(-1, 4)).reshape(5, 7)
+    for i in range(5):
+        for j in range(7):
+            assert abs(pb["value"][i, j] - X[i, j].max()) <= TOL * na[i] * nb[j]
