@@ -1089,262 +1089,6 @@ static void launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop,
   }
 }
 
-// ---------------------------------------------------------------- Step 2 on the tensor cores (n <= 512)
-// Same operation and output as k_step2_fft.  Four-step n = 32 E with p = a + 32 b (a = lane):
-//   (A) E-point DFT over b in registers, (B) twiddle w_n^{a c}, then the 32-point DFT over a for every
-//   (term, c) as one real GEMM on the tensor cores (bf16x3):
-//     rows m = (term, c) [M = 128: 128 / E terms], K' = 64 = [Re X(a) | Im X(a)], N' = 64 = [Re Z(d) | Im Z(d)]
-//     against the constant matrix [[cos, -sin], [sin, cos]](2 pi a d / 32); Z(r = c + E d).
-// Work item = (pair, one 8-column word group, <= 8 terms); CTA = 4 warps (one TMEM lane quarter each),
-// 3 CTAs per SM.  The A operand (MN-major: m contiguous) is written by the warps straight from registers
-// into the row buffer once its inputs have been consumed; one thread issues the 12 MMAs; the warps read
-// the accumulator rows back and stage bf16 hi/lo words exactly as k_step2_fft does.
-constexpr int S2T_THREADS = 128;
-constexpr int S2T_S = 10;  // row-buffer stride (complex): <= 8 terms + alignment slack, even (16-byte rows)
-
-struct S2Groups {
-  int ng;
-  int zs[32], ze[32];  // term range of word group g
-};
-
-__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-
-template <int E>  // E = 8 or 16 (n = 256, 512)
-__global__ void __launch_bounds__(S2T_THREADS, 3) k_step2_tc(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
-                                                            int npair, int formB, DevPlan P, S2Groups G,
-                                                            const float2* __restrict__ twtab,
-                                                            const uint8_t* __restrict__ dftop) {
-  extern __shared__ __align__(1024) uint8_t s2t_raw[];
-  constexpr int n = 32 * E, S = S2T_S;
-  constexpr int LOG = (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
-  constexpr int RS = n + n / E + 16;  // padded staging row (words)
-  constexpr size_t ROWS_BYTES = ((size_t)n * S * 8 > 32768 ? (size_t)n * S * 8 : 32768);
-  float2* rows = reinterpret_cast<float2*>(s2t_raw);                                  // [n][S] fp32 complex
-  uint8_t* aop = s2t_raw;                                                             // A tile: hi 16 KB, lo 16 KB
-  uint8_t* bop = s2t_raw + ROWS_BYTES;                                                // DFT matrix hi/lo 16 KB
-  uint32_t* stg = reinterpret_cast<uint32_t*>(bop + 16384);                           // [part][word 4][RS]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 8 * RS);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
-  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-  const int Hp = P.H_plus, Hs = P.Hs;
-  const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
-  const int total = npair * G.ng;
-  auto rv = [](int i) {
-    int r = 0;
-#pragma unroll
-    for (int bb = 0; bb < LOG; ++bb) r |= ((i >> bb) & 1) << (LOG - 1 - bb);
-    return r;
-  };
-  // constant DFT operand -> SMEM (16 KB), barriers, TMEM (64 columns: D = 128 lanes x 64 fp32)
-  for (int i = threadIdx.x; i < 16384 / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(bop)[i] = __ldg(reinterpret_cast<const uint4*>(dftop) + i);
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc<64>(tslot);
-  fence_proxy_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  const uint32_t idesc = idesc_bf16_f32(128, 64) | (1u << 15);  // A MN-major, B K-major
-  const int per = (total + gridDim.x - 1) / gridDim.x;
-  const int i_end = min(total, (int)(blockIdx.x + 1) * per);
-  uint32_t phase = 0;
-  for (int item = blockIdx.x * per; item < i_end; ++item, phase ^= 1u) {
-    const int g = item % G.ng, pr = item / G.ng;
-    const int zs = G.zs[g], nz = G.ze[g] - zs;
-    // ---- gather the item's input rows (16-byte chunks of the even-aligned term range)
-    int zoff = 0;
-    if (formB) {
-      const int zs2 = zs & ~1;
-      const int cpr = (zs + nz - zs2 + 1) >> 1;
-      zoff = zs - zs2;
-      if (cpr > 0) {
-        int p = threadIdx.x / cpr, c = threadIdx.x - p * cpr;
-        const int dq = blockDim.x / cpr, dr = blockDim.x - dq * cpr;
-        const uint8_t* sp = reinterpret_cast<const uint8_t*>(Zhat + ((size_t)pr * n + p) * Hs + zs2) + 16 * c;
-        float2* dp = rows + p * S + 2 * c;
-        const size_t sstep = (size_t)dq * Hs * 8 + 16 * dr, swrap = (size_t)Hs * 8 - 16 * cpr;
-        const int dstep = dq * S + 2 * dr, dwrap = S - 2 * cpr;
-        while (p < n) {
-          cp_async16(dp, sp);
-          sp += sstep;
-          dp += dstep;
-          p += dq;
-          c += dr;
-          if (c >= cpr) {
-            c -= cpr;
-            ++p;
-            sp += swrap;
-            dp += dwrap;
-          }
-        }
-      }
-    } else {
-      const float2* src = Zhat + ((size_t)pr * Hp + zs) * n;
-      for (int z = 0; z < nz; ++z)
-        for (int q = threadIdx.x; q < n; q += blockDim.x) cp_async8(rows + q * S + z, src + (size_t)z * n + q);
-    }
-    cp_async_commit();
-    for (int idx = threadIdx.x; idx < 8 * RS; idx += blockDim.x) stg[idx] = 0u;  // padding columns stay zero
-    cp_async_wait<0>();
-    __syncthreads();
-    // ---- (A), (B) per term in registers; warp w takes terms w, w + 4
-    float2 x[2][E];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int zz = warp + 4 * k;
-      if (zz < nz) {
-        const int l = P.ell[zs + zz];
-        const int q0 = formB ? ((lane - l) & (n - 1)) : lane;  // Form B: cyclic shift by ell (reading R5)
-        const float2* colp = rows + zoff + zz;
-#pragma unroll
-        for (int bb = 0; bb < E; ++bb) x[k][bb] = colp[((q0 + 32 * bb) & (n - 1)) * S];
-      }
-    }
-    __syncthreads();  // the row buffer is free: it becomes the A tile
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int zz = warp + 4 * k;
-      if (zz < nz) {
-        dft_regs<E>(x[k]);
-#pragma unroll
-        for (int c = 1; c < E; ++c) x[k][rv(c)] = cmulf(x[k][rv(c)], __ldg(twtab + c * 32 + lane));
-        // A rows m = zz E + c, k' = lane (Re) and 32 + lane (Im); MN-major: 8 consecutive m per 16 bytes
-#pragma unroll
-        for (int h8 = 0; h8 < E; h8 += 8) {
-          const int m8 = (zz * E + h8) >> 3;
-          uint32_t rh[4], rl[4], ih[4], il[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 v0 = x[k][rv(h8 + 2 * e)], v1 = x[k][rv(h8 + 2 * e + 1)];
-            split2_bf16(v0.x, v1.x, rh[e], rl[e]);
-            split2_bf16(v0.y, v1.y, ih[e], il[e]);
-          }
-          const uint32_t o_re = (uint32_t)m8 * 1024u + (uint32_t)(lane >> 3) * 128u + (uint32_t)(lane & 7) * 16u;
-          const uint32_t o_im = o_re + 4u * 128u;  // k' = 32 + lane
-          *reinterpret_cast<uint4*>(aop + o_re) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
-          *reinterpret_cast<uint4*>(aop + 16384 + o_re) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
-          *reinterpret_cast<uint4*>(aop + o_im) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
-          *reinterpret_cast<uint4*>(aop + 16384 + o_im) = make_uint4(il[0], il[1], il[2], il[3]);
-        }
-      }
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-    // ---- 32-point DFT over a: 4 k-steps x 3 bf16 products, D [128 rows] x [64 cols] in TMEM
-    if (warp == 0) {
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t abase = smem_u32(aop), bbase = smem_u32(bop);
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t ah = smem_desc_kmajor_noswz(abase + ks * 256, 128, 1024);
-          const uint64_t al = smem_desc_kmajor_noswz(abase + 16384 + ks * 256, 128, 1024);
-          const uint64_t bh = smem_desc_kmajor_noswz(bbase + ks * 256, 128, 1024);
-          const uint64_t bl = smem_desc_kmajor_noswz(bbase + 8192 + ks * 256, 128, 1024);
-          mma_bf16_ss(tmem, ah, bh, idesc, ks > 0 ? 1u : 0u);
-          mma_bf16_ss(tmem, ah, bl, idesc, 1u);
-          mma_bf16_ss(tmem, al, bh, idesc, 1u);
-        }
-        tc_commit(&bar[0]);
-      }
-      __syncwarp();
-    }
-    mbar_wait(&bar[0], phase);
-    tc_fence_after();
-    // ---- accumulator row m = 32 warp + lane -> (term zz, c); Z(c + E d) = col d + i col (32 + d)
-    {
-      const int m = warp * 32 + lane;
-      const int zz = m / E, c = m % E;
-      const bool valid = zz < nz;
-      int kl = 0, l = 0;
-      if (valid) {
-        l = P.ell[zs + zz];
-        kl = P.col[zs + zz] - 8 * g;  // 0..7 within the word group
-      }
-      uint32_t* shi = stg + (size_t)(kl >> 1) * RS;
-      uint32_t* slo = stg + (size_t)(4 + (kl >> 1)) * RS;
-      const uint32_t tb = tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll
-      for (int d0 = 0; d0 < 32; d0 += 16) {
-        uint32_t re[16], im[16];
-        tmem_ld16(tb + d0, re);
-        tmem_ld16(tb + 32 + d0, im);
-        tmem_wait_ld();
-        if (valid) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int pi = c + (E + 1) * (d0 + e);  // padded index of r = c + E d
-            const float zr = __uint_as_float(re[e]), zi = __uint_as_float(im[e]);
-            if (l > 0) {
-              uint32_t hh, ll;
-              split2_bf16(zr, zi, hh, ll);
-              shi[pi] = hh;
-              slo[pi] = ll;
-            } else {
-              const __nv_bfloat16 hb = __float2bfloat16_rn(zr);
-              const __nv_bfloat16 lb = __float2bfloat16_rn(zr - __bfloat162float(hb));
-              reinterpret_cast<__nv_bfloat16*>(shi + pi)[kl & 1] = hb;
-              reinterpret_cast<__nv_bfloat16*>(slo + pi)[kl & 1] = lb;
-            }
-          }
-        }
-      }
-    }
-    tc_fence_before();
-    __syncthreads();
-    // ---- write out the word group: per (r-tile, part) 128 rows x 16 B contiguous
-    {
-      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)g * 128;
-      for (int idx = threadIdx.x; idx < NRT * 2 * 128; idx += blockDim.x) {
-        const int row = idx & 127, rest = idx >> 7;
-        const int part = rest & 1, T = rest >> 1;
-        const int r = T * 128 + row;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (r < n) {
-          const int pi = r + r / E;
-          const uint32_t* sp = stg + (size_t)(4 * part) * RS + pi;
-          v = make_uint4(sp[0], sp[RS], sp[2 * RS], sp[3 * RS]);
-        }
-        *reinterpret_cast<uint4*>(base + (size_t)((T * 2 + part) * NWG) * 2048 + (size_t)(row >> 3) * NWG * 128 +
-                                  (row & 7) * 16) = v;
-      }
-    }
-    __syncthreads();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc<64>(tmem);
-  }
-}
-
-static size_t step2tc_smem(int n) {
-  const int E = n / 32;
-  const size_t rows = std::max<size_t>((size_t)n * S2T_S * 8, 32768);
-  return rows + 16384 + (size_t)8 * (n + n / E + 16) * 4 + 64;
-}
-
-static void launch_step2_tc(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, int formB,
-                            const DevPlan& P, cudaStream_t s) {
-  S2Groups G;
-  std::memcpy(&G, &tc.s2_groups, sizeof G);
-  const size_t smem = step2tc_smem(P.n_psi);
-  const int items = G.ng * npair;
-  dim3 grid(items < 3 * tc.num_sms ? items : 3 * tc.num_sms);
-  switch (P.n_psi) {
-    case 256: k_step2_tc<8><<<grid, S2T_THREADS, smem, s>>>(Zhat, Zop, npair, formB, P, G, tc.d_s2tw, tc.d_s2dft); break;
-    default: k_step2_tc<16><<<grid, S2T_THREADS, smem, s>>>(Zhat, Zop, npair, formB, P, G, tc.d_s2tw, tc.d_s2dft); break;
-  }
-}
-
 // ---------------------------------------------------------------- single-MMA self-test
 // D = A * B^T with A [128 x 32] (TS: from TMEM; SS: from SMEM), B [N=64 x 32] from SMEM, bf16 inputs.
 __global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const float* B, float* D_ts, float* D_ss,
@@ -1640,71 +1384,6 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       tc.s2_blocks.ze[bi] = ze;
     }
     tc.s2_blocks.nb = ngroups / 2;
-    // word groups for k_step2_tc (terms of each 8-column group, contiguous)
-    std::memset(&tc.s2_groups, 0, sizeof tc.s2_groups);
-    tc.s2_groups.ng = ngroups;
-    for (int gi = 0; gi < ngroups; ++gi) {
-      int zs = -1, ze = -1;
-      for (int z = 0; z < (int)col.size(); ++z)
-        if (col[z] / 8 == gi) {
-          if (zs < 0) zs = z;
-          ze = z + 1;
-        }
-      if (zs < 0) zs = ze = 0;
-      tc.s2_groups.zs[gi] = zs;
-      tc.s2_groups.ze[gi] = ze;
-    }
-    {  // constant B operand of the 32-point DFT: K-major [n' 64][k' 64], hi then lo (8 KB each)
-      //   n' < 32: Re Z(d = n'), n' >= 32: Im Z(d = n' - 32); k' < 32: Re X(a = k'), k' >= 32: Im X(a)
-      std::vector<uint16_t> img(8192, 0);
-      for (int np = 0; np < 64; ++np)
-        for (int kp = 0; kp < 64; ++kp) {
-          const int d = np & 31, a = kp & 31;
-          const double th = 2.0 * M_PI * (double)((a * d) & 31) / 32.0;
-          double v;
-          if (np < 32)
-            v = kp < 32 ? std::cos(th) : std::sin(th);
-          else
-            v = kp < 32 ? -std::sin(th) : std::cos(th);
-          const __nv_bfloat16 hi = __float2bfloat16_rn((float)v);
-          const __nv_bfloat16 lo = __float2bfloat16_rn((float)(v - (double)__bfloat162float(hi)));
-          const size_t off = (size_t)(np / 8) * 512 + (size_t)(kp / 8) * 64 + (np % 8) * 8 + (kp % 8);
-          std::memcpy(&img[off], &hi, 2);
-          std::memcpy(&img[4096 + off], &lo, 2);
-        }
-      if (cudaMalloc(&tc.d_s2dft, img.size() * 2) != cudaSuccess) {
-        msg = "tensor-core engine: allocation failed";
-        return FTK_ENOMEM;
-      }
-      cudaMemcpy(tc.d_s2dft, img.data(), img.size() * 2, cudaMemcpyHostToDevice);
-    }
-    // FTK_STEP2_TC=1 selects k_step2_tc (32-point DFT stage on the tensor cores) for n_psi = 256, 512;
-    // measured slower than k_step2_fft at c3 / c5 (the extra bf16 split of the GEMM operand and the
-    // per-item overheads cost as much as the FFT arithmetic it removes), so the CUDA-core kernel is the
-    // default
-    const char* e2 = std::getenv("FTK_STEP2_TC");
-    tc.step2_tensor = e2 && e2[0] == '1';
-    if (pm.n_psi == 256 || pm.n_psi == 512) {
-      const int sm3 = (int)step2tc_smem(pm.n_psi);
-      cudaFuncSetAttribute(k_step2_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
-      cudaFuncSetAttribute(k_step2_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
-    }
-    {  // Step-2 twiddle tables: [c][a] w_n^{a c} and [d'][a] w_32^{(a % L) d'}, E = n / 32, L = 32 / E
-      const int n = n_gamma, E = n / 32, L = 32 / E;
-      std::vector<float2> tw((size_t)2 * E * 32);
-      for (int c = 0; c < E; ++c)
-        for (int a = 0; a < 32; ++a) {
-          const double ph1 = -2.0 * M_PI * (double)((a * c) % n) / n;
-          const double ph2 = -2.0 * M_PI * (double)(((a % L) * c) % 32) / 32.0;
-          tw[(size_t)c * 32 + a] = make_float2((float)std::cos(ph1), (float)std::sin(ph1));
-          tw[(size_t)E * 32 + c * 32 + a] = make_float2((float)std::cos(ph2), (float)std::sin(ph2));
-        }
-      if (cudaMalloc(&tc.d_s2tw, tw.size() * sizeof(float2)) != cudaSuccess) {
-        msg = "tensor-core engine: allocation failed";
-        return FTK_ENOMEM;
-      }
-      cudaMemcpy(tc.d_s2tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice);
-    }
     const int sm2 = (int)step2_smem(pm.n_psi, n_gamma);
     cudaFuncSetAttribute(k_step2_fft<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(k_step2_fft<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
@@ -1719,8 +1398,6 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
 void tc_plan_free(TcPlan& tc) {
   cudaFree(tc.d_s2tw);
   tc.d_s2tw = nullptr;
-  cudaFree(tc.d_s2dft);
-  tc.d_s2dft = nullptr;
   cudaFree(tc.d_Ysm);
   cudaFree(tc.d_colrep);
   cudaFree(tc.d_colpart);
@@ -1879,20 +1556,14 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     launch_step1_simt(A, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    if (tc.step2_tensor && P.n_gamma == P.n_psi && (P.n_psi == 256 || P.n_psi == 512))
-      launch_step2_tc(tc, Zhat, Zop, pb.count, 0, P, s);
-    else
-      launch_step2_fft(tc, Zhat, Zop, pb.count, 0, P, s);
+    launch_step2_fft(tc, Zhat, Zop, pb.count, 0, P, s);
     if (prof) prof(plan, 2, 1, s);
   } else {
     if (prof) prof(plan, 1, 0, s);
     launch_step1_tc(tc, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    if (tc.step2_tensor && P.n_gamma == P.n_psi && (P.n_psi == 256 || P.n_psi == 512))
-      launch_step2_tc(tc, Zhat, Zop, pb.count, 1, P, s);
-    else
-      launch_step2_fft(tc, Zhat, Zop, pb.count, 1, P, s);
+    launch_step2_fft(tc, Zhat, Zop, pb.count, 1, P, s);
     if (prof) prof(plan, 2, 1, s);
   }
   if (prof) prof(plan, 3, 0, s);

@@ -35,12 +35,6 @@ struct TcPlan {
     int zs[16], ze[16];
   } s2_blocks;
   float2* d_s2tw = nullptr;  // Step-2 four-step twiddle tables
-  struct {
-    int ng;
-    int zs[32], ze[32];
-  } s2_groups;                  // word groups (k_step2_tc work items)
-  uint8_t* d_s2dft = nullptr;   // k_step2_tc: 32-point DFT B operand (bf16 hi/lo, 16 KB)
-  bool step2_tensor = false;    // FTK_STEP2_TC=1: use k_step2_tc
   int64_t n_tm = 0;
   int num_sms = 148;
 };

@@ -250,23 +250,3 @@ def test_n_gamma_option_errors(pkg):
         with pytest.raises(pkg.FTKError):
             make(pkg, cfg, engine, n_gamma=ng)
 
-
-def test_step2_tensor_variant(pkg, monkeypatch):
-    """k_step2_tc (FTK_STEP2_TC=1: the 32-point DFT stage on tcgen05) on a ragged c3 subset."""
-    monkeypatch.setenv("FTK_STEP2_TC", "1")
-    cfg = synth.config("c3")
-    p = make(pkg, cfg, 0)
-    k, w = p.radial()
-    imgs, _ = synth.draw_items(cfg, "images", range(5), k)
-    tpls, _ = synth.draw_items(cfg, "templates", range(7), k)
-    p.load_images(torch.from_numpy(imgs).cuda())
-    p.load_templates(torch.from_numpy(tpls).cuda())
-    res = p.align(pair_best=True)
-    torch.cuda.synchronize()
-    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), oracle_plan(cfg)))
-    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
-    check_best(pkg.best_to_numpy(res["best"]), X, na, nb)
-    pb = pkg.best_to_numpy(res["pair_best"].reshape(-1, 4)).reshape(5, 7)
-    for i in range(5):
-        for j in range(7):
-            assert abs(pb["value"][i, j] - X[i, j].max()) <= TOL * na[i] * nb[j]
