@@ -493,7 +493,7 @@ static size_t s3_smem_bytes(int ncol, int K3p, int NS) {
 // so that Zhat_zeta(q) = Zhat'_zeta(q - ell) and Step 2 applies e^{-i ell gamma_r} after the FFT.
 // Real GEMM per p with K' = 2 n_k:  rows (j, zeta, part) of the GENERATED operand c (A, in TMEM):
 //   Re-row = [c_r | -c_i],  Im-row = [c_i | c_r];  columns = images, B = [a_r | a_i] (pre-split, SMEM).
-// Output Zhat' [pair][p][Hs] complex (pair = il * nj + jl within the block; Hs = H_plus rounded up to even).
+// Output Zhat' per pair (pair = il * nj + jl within the block): the Step-2 block regions (S2Blocks).
 constexpr int S1_THREADS = 14 * 32;
 constexpr int S1_STAGES = 4;
 
@@ -502,7 +502,10 @@ struct S1Params {
   const float2* B;      // template FB coefficients [j][q][m] (local templates)
   const float* g;       // [H_plus][n_k]
   const int* ell;       // [H_plus]
-  float2* Zhat;         // [pair][p][Hs]
+  float2* Zhat;         // per pair the Step-2 block regions [p][W] (rotated slots, see S2Blocks)
+  const int* termoff;   // [H_plus] region offset (complex) of term z's block
+  const int* termpk;    // [H_plus] W | u << 4 | nz << 8 (u = index of z in its block)
+  long long zpair;      // complex elements per pair
   int i0, ni, j0, nj;   // block (i0 multiple of 128)
   int n, n_k, Hp, Hs, KCH, NKCH, NIT;  // NIT = image tiles per mode in Aop
   int F, NCT;           // F = nj * Hp flattened (j, zeta) columns, NCT = ceil(F / 64)
@@ -702,15 +705,25 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
       s1_unit(u, P.NCT, p, ct);
       const int nvalid = min(128, 2 * (P.F - ct * 64));
       // this lane's two complex columns cc = lane, lane + 32 -> offsets (template jl, term z) in Zhat'
-      long long coff[2];
+      // Zhat' placement (S2Blocks): region off + p W + ((u + (p >> sh)) & (W - 1)); the lane holding a
+      // block's last term also zeroes the block's empty slots of this row (whole sectors written)
+      long long coff[2], rowb[2];
       bool cval[2];
+      int pw[2], pu[2], pnz[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int cc = lane + 32 * h;
         const int f = ct * 64 + cc;
         const int jl = f / P.Hp, z = f - jl * P.Hp;
         cval[h] = 2 * cc < nvalid;
-        coff[h] = (long long)jl * n * P.Hs + z;
+        const int pk = cval[h] ? __ldg(P.termpk + z) : 8;
+        pw[h] = pk & 15;
+        pu[h] = (pk >> 4) & 15;
+        pnz[h] = pk >> 8;
+        const int sh = pw[h] == 8 ? 1 : 2;
+        rowb[h] = cval[h] ? (long long)jl * P.zpair + __ldg(P.termoff + z) + (long long)p * pw[h] : 0;
+        coff[h] = rowb[h] + ((pu[h] + (p >> sh)) & (pw[h] - 1));
+        pu[h] |= (p >> sh) << 8;  // keep the rotation for the pad slots
       }
       for (int t = 0; t < nit; ++t, ++g_acc) {
         const int ab = g_acc & 1;
@@ -732,10 +745,15 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
         for (int ii = ew; ii < 128; ii += 4) {
           const int il = t * 128 + ii;  // local image index within the block
           if (il >= P.ni) continue;
-          float2* dst = P.Zhat + ((size_t)il * P.nj * n + p) * P.Hs;
+          float2* dst = P.Zhat + (size_t)il * P.nj * P.zpair;
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            if (cval[h]) dst[coff[h]] = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
+            if (cval[h]) {
+              dst[coff[h]] = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
+              const int u = pu[h] & 255, rot = pu[h] >> 8;
+              if (u == pnz[h] - 1)
+                for (int v = pnz[h]; v < pw[h]; ++v) dst[rowb[h] + ((v + rot) & (pw[h] - 1))] = make_float2(0.f, 0.f);
+            }
         }
         named_bar(2, 128);
       }
@@ -802,15 +820,22 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 //   DIF across the warp with shfl_xor (output index d lands on lane bitrev5(d)).
 // Output words are staged per (group, part, word) in padded rows (index r + r / E: conflict-free) and
 // written out as contiguous 2 KB row blocks.
-struct S2Chunks {
-  int n;
-  int zs[32], ze[32], g0[32];
-};
-struct S2Blocks {
+// Zhat' layout (written by k_step1_tc, read by k_step2_fft): per pair, per Step-2 block b one region
+// [p][W_b] of complex values, W_b = 4 or 8 (rows of 32 / 64 bytes: whole sectors), term u of the block in
+// slot (u + (p >> sh_b)) & (W_b - 1), sh_b = log2(16 / W_b): the rotation makes the column reads of
+// k_step2_fft bank-conflict free.  Slots without a term hold zeros.
+struct S2Blocks {      // Step-2 work blocks: 1 or 2 consecutive word groups holding <= 8 terms
   int nb;
-  int zs[16], ze[16];  // term range of block b (word groups 2b, 2b + 1)
+  long long zpair;     // complex elements of one pair's Zhat'
+  int zs[16], ze[16];  // term range of block b
+  int g0[16], ng[16];  // first word group, number of groups
+  int W[16];           // row width (4 or 8)
+  long long off[16];   // region offset (complex) within the pair
+  int used[16];        // words (bit grp * 4 + w) written by some term
+  int lone[16];        // terms (bit z - zs) with ell = 0 and no neighbour in their word
 };
-constexpr int S2_ROWSTRIDE = 18;  // complex; even -> 16-byte rows for cp.async 16 (2-way bank conflict)
+constexpr int S2_SMAX = 8;  // max row width (complex)
+__host__ __device__ inline int s2_shift(int W) { return W == 8 ? 1 : 2; }
 
 __device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -883,20 +908,22 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
                                                       int npair, int formB, DevPlan P, S2Blocks B,
                                                       const float2* __restrict__ twtab) {
   extern __shared__ __align__(16) uint8_t s2raw[];
-  constexpr int n = 32 * E, S = S2_ROWSTRIDE;
+  constexpr int n = 32 * E;  // FFT length = n_gamma (>= n_psi; zero-padded input, reading R21)
   constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
   constexpr int RS = n + n / E;  // padded staging row (words): index r + r / E
-  const int n_in = P.n_psi;  // input rows (cyclic q); the FFT length n = n_gamma >= n_in (reading R21)
-  // [n][S]: rows [0, n_in) hold the input; each warp's column doubles as its n-slot transpose scratch
+  const int n_in = P.n_psi;     // input rows (cyclic q)
+  // [rows: n_in x S2_SMAX complex][stg: 16 x RS words; also the warps' n-slot transpose scratch][mbarrier]
   float2* rows = reinterpret_cast<float2*>(s2raw);
-  uint32_t* stg = reinterpret_cast<uint32_t*>(s2raw + (size_t)n * S * 8);     // [group 2][part 2][word 4][RS]
+  const size_t rows_bytes = ((size_t)n_in * S2_SMAX * 8 + 15) & ~(size_t)15;
+  uint32_t* stg = reinterpret_cast<uint32_t*>(s2raw + rows_bytes);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 16 * RS);
   // warp index made provably warp-uniform (shfl from lane 0) so the shuffles below sit in convergent code
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-  const int nw = blockDim.x >> 5;
+  float2* scr = reinterpret_cast<float2*>(stg) + warp * n;  // 8 warps x n complex <= 16 x RS words
   const int total = npair * B.nb;
-  const int Hp = P.H_plus, Hs = P.Hs;
+  const int Hp = P.H_plus;
+  const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
 
-  // per-lane constant twiddles
   // 32 = L x E: the 32-point DFT over the lane index runs as an E-point register DFT and an L-point
   // DIF across L lanes (log2 L shuffle stages)
   constexpr int L = 32 / E;
@@ -910,7 +937,6 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
   int gq = 0;  // L-point DIF output index of this lane: bit-reversed lane % L
 #pragma unroll
   for (int bb = 0; bb < LL; ++bb) gq |= (((lane % L) >> bb) & 1) << (LL - 1 - bb);
-  // (B) twiddles w_n^{a c} (a = lane, c < E), [c][a]: conflict-free
   // (B) twiddles w_n^{a c} (a = lane, c < E) and (B2) twiddles w_32^{h d'} (h = lane % L, d' < E), both
   // [c][lane] (plan-time tables, L1-resident)
   const float2* __restrict__ twB = twtab;
@@ -922,59 +948,64 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
     return r;
   };
 
-  // contiguous item range per CTA: the blocks of one pair run back to back on the same SM, so the row
-  // sectors shared by neighbouring blocks are L2 hits
+  // contiguous item range per CTA (the blocks of one pair back to back)
   const int per = (total + gridDim.x - 1) / gridDim.x;
-  const int i_end = min(total, (int)(blockIdx.x + 1) * per);
-  for (int item = blockIdx.x * per; item < i_end; ++item) {
-    const int b = item % B.nb, pr = item / B.nb;
-    const int zs = B.zs[b], nz = B.ze[b] - zs;
-    // ---- gather the item's input rows
-    int zoff = 0;  // buffer column of term zs
-    if (formB) {  // [pair][p][Hs]: 16-byte chunks of the even-aligned term range [zs2, zs2 + 2 cpr)
-      const int zs2 = zs & ~1;
-      const int cpr = (zs + nz - zs2 + 1) >> 1;  // chunks per row (<= S / 2)
-      zoff = zs - zs2;
-      if (cpr > 0) {
-        int p = threadIdx.x / cpr, c = threadIdx.x - p * cpr;
-        const int dq = blockDim.x / cpr, dr = blockDim.x - dq * cpr;
-        const uint8_t* sp = reinterpret_cast<const uint8_t*>(Zhat + ((size_t)pr * n_in + p) * Hs + zs2) + 16 * c;
-        float2* dp = rows + p * S + 2 * c;
-        const size_t sstep = (size_t)dq * Hs * 8 + 16 * dr, swrap = (size_t)Hs * 8 - 16 * cpr;
-        const int dstep = dq * S + 2 * dr, dwrap = S - 2 * cpr;
-        while (p < n_in) {
-          cp_async16(dp, sp);
-          sp += sstep;
-          dp += dstep;
-          p += dq;
-          c += dr;
-          if (c >= cpr) {
-            c -= cpr;
-            ++p;
-            sp += swrap;
-            dp += dwrap;
-          }
-        }
+  const int i_beg = blockIdx.x * per;
+  const int i_end = min(total, i_beg + per);
+  // Form B input: one bulk copy of the block's region [p][W] (k_step1_tc's layout); Form A (explicit
+  // pairs, Zhat [pair][zeta][q]): cp.async gather into the same swizzled [p][8] layout
+  auto issue = [&](int it) {
+    const int bi = it % B.nb, pi2 = it / B.nb;
+    if (formB) {
+      if (threadIdx.x == 0) {
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(Zhat + (size_t)pi2 * B.zpair + B.off[bi]);
+        const uint32_t bytes = (uint32_t)n_in * (uint32_t)B.W[bi] * 8u;
+        mbar_arrive_expect_tx(bar, bytes);
+        for (uint32_t o = 0; o < bytes; o += 32768u) bulk_g2s(s2raw + o, src + o, min(32768u, bytes - o), bar);
       }
-    } else {      // [pair][zeta][q]
-      const float2* src = Zhat + ((size_t)pr * Hp + zs) * n_in;
+    } else {
+      const int zs = B.zs[bi], nz = B.ze[bi] - zs;
+      const float2* src = Zhat + ((size_t)pi2 * Hp + zs) * n_in;
       for (int z = 0; z < nz; ++z)
-        for (int q = threadIdx.x; q < n_in; q += blockDim.x) cp_async8(rows + q * S + z, src + (size_t)z * n_in + q);
+        for (int q = threadIdx.x; q < n_in; q += blockDim.x)
+          cp_async8(rows + q * 8 + ((z + (q >> 1)) & 7), src + (size_t)z * n_in + q);
+      cp_async_commit();
     }
-    cp_async_commit();
-    for (int idx = threadIdx.x; idx < 16 * RS; idx += blockDim.x) stg[idx] = 0u;  // padding columns stay zero
-    cp_async_wait<0>();
-    __syncthreads();
-    for (int zz = warp; zz < nz; zz += nw) {
-      float2 x[E];
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (i_beg < i_end) issue(i_beg);
+  uint32_t phase = 0;
+  for (int item = i_beg; item < i_end; ++item) {
+    const int b = item % B.nb, pr = item / B.nb;
+    const int zs = B.zs[b], nz = B.ze[b] - zs, g0 = B.g0[b];
+    const int W = formB ? B.W[b] : 8, sh = s2_shift(W);
+    if (formB) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    } else {
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+    // ---- each warp takes one term: load its row (cyclic shift by ell, zero padding to n)
+    const int zz = warp;
+    const bool act = zz < nz;
+    float2 x[E];
+    int l = 0, col = 0;
+    if (act) {
       const int z = zs + zz;
-      const int l = P.ell[z], col = P.col[z];
-      float2* colp = rows + zoff + zz;  // this term's column of the row buffer (stride S)
+      l = P.ell[z];
+      col = P.col[z];
+      // element (row p, term zz) at rows[p * W + ((zz + (p >> sh)) & (W - 1))] (rotated slots)
+      auto at = [&](int p) { return rows[p * W + ((zz + (p >> sh)) & (W - 1))]; };
       // Form B: Z(r) w^{ell r} = DFT of the cyclically shifted row Zhat'(q - ell) (reading R5)
       if (n_in == n) {
         const int q0 = formB ? ((lane - l) & (n - 1)) : lane;
 #pragma unroll
-        for (int bb = 0; bb < E; ++bb) x[bb] = colp[((q0 + 32 * bb) & (n - 1)) * S];
+        for (int bb = 0; bb < E; ++bb) x[bb] = at((q0 + 32 * bb) & (n - 1));
       } else {
         // n_gamma > n_psi: zero-padded signed frequencies, Nyquist split (reading R21)
         const int Qh = n_in >> 1;
@@ -984,24 +1015,27 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
           const int qc = qp < Qh ? qp : (qp > n - Qh ? qp - n + n_in : Qh);
           const float wgt = (qp < Qh || qp > n - Qh) ? 1.f : ((qp == Qh || qp == n - Qh) ? 0.5f : 0.f);
           const int src = formB ? ((qc - l) & (n_in - 1)) : qc;
-          const float2 v = colp[src * S];
+          const float2 v = at(src);
           x[bb] = make_float2(wgt * v.x, wgt * v.y);
         }
       }
+    }
+    __syncthreads();  // the row buffer is free: prefetch the next item while this one is transformed
+    if (item + 1 < i_end) issue(item + 1);
+    if (act) {
       dft_regs<E>(x);  // (A) E-point DFT over b (p = a + 32 b, a = lane): natural order in x[rv(c)]
 #pragma unroll
       for (int c = 1; c < E; ++c) x[rv(c)] = cmulf(x[rv(c)], __ldg(twB + c * 32 + lane));  // (B) x_c *= w_n^{a c}
-      // (T) the 32-point DFT over a: transpose through the column (slot c*32 + (a + c) % 32) so that lane
-      //     (c = lane / L, h = lane % L) holds a = L i + h, i < E; then (A2) an E-point DFT over i in
-      //     registers, (B2) twiddle w_32^{h d'}, (C2) an L-point DIF across the L lanes of each c.
-      __syncwarp();
+      // (T) the 32-point DFT over a: transpose through this warp's scratch (slot c*32 + (a + c) % 32) so
+      //     that lane (c = lane / L, h = lane % L) holds a = L i + h, i < E; then (A2) an E-point DFT over i
+      //     in registers, (B2) twiddle w_32^{h d'}, (C2) an L-point DIF across the L lanes of each c.
 #pragma unroll
-      for (int c = 0; c < E; ++c) colp[(c * 32 + ((lane + c) & 31)) * S] = x[rv(c)];
+      for (int c = 0; c < E; ++c) scr[c * 32 + ((lane + c) & 31)] = x[rv(c)];
       __syncwarp();
       {
         const int cq = lane / L, hq = lane % L;
 #pragma unroll
-        for (int i = 0; i < E; ++i) x[i] = colp[(cq * 32 + ((L * i + hq + cq) & 31)) * S];
+        for (int i = 0; i < E; ++i) x[i] = scr[cq * 32 + ((L * i + hq + cq) & 31)];
       }
       dft_regs<E>(x);  // (A2): natural order in x[rv(d')]
       if constexpr (L > 1) {
@@ -1019,11 +1053,15 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
           }
         }
       }
+    }
+    __syncthreads();  // all transposes done: the staging area is free
+    if (act) {
       // lane holds Z(r), r = cq + E (d' + E g) in x[rv(d')], cq = lane / L, g = bitrev_L(lane % L)
       // stage: ell > 0 -> word (Re, Im) of this term; ell = 0 -> one 16-bit half of a word shared with
-      // the neighbouring ell = 0 term
-      const int kl = col - 16 * b;  // 0..15 within the block
+      // the neighbouring ell = 0 term (a term without a neighbour writes the whole word, upper half 0)
+      const int kl = col - 8 * g0;  // 0..15 within the block
       const int grp = kl >> 3, w = (kl & 7) >> 1;
+      const bool lone = (B.lone[b] >> zz) & 1;
       uint32_t* shi = stg + (size_t)((grp * 2 + 0) * 4 + w) * RS;
       uint32_t* slo = stg + (size_t)((grp * 2 + 1) * 4 + w) * RS;
       const int pbase = lane / L + (E * E + E) * gq;  // padded index pi(r) = r + r / E
@@ -1036,6 +1074,11 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
           split2_bf16(a0.x, a0.y, hh, ll);
           shi[pi] = hh;
           slo[pi] = ll;
+        } else if (lone) {
+          uint32_t hh, ll;
+          split2_bf16(a0.x, 0.f, hh, ll);
+          shi[pi] = hh;
+          slo[pi] = ll;
         } else {
           const __nv_bfloat16 hb = __float2bfloat16_rn(a0.x);
           const __nv_bfloat16 lb = __float2bfloat16_rn(a0.x - __bfloat162float(hb));
@@ -1045,33 +1088,36 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
       }
     }
     __syncthreads();
-    // ---- write out the two word groups: per (group, r-tile, part) 128 rows as core-matrix rows
+    // ---- write out the block's word groups as core-matrix rows; words no term writes are zero
     {
-      const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
-      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)(2 * b) * 128;
-      for (int idx = threadIdx.x; idx < 2 * NRT * 2 * 128; idx += blockDim.x) {
+      const int ng = B.ng[b];
+      const uint32_t used = (uint32_t)B.used[b];  // bit grp * 4 + w
+      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)g0 * 128;
+      for (int idx = threadIdx.x; idx < ng * NRT * 2 * 128; idx += blockDim.x) {
         const int row = idx & 127, rest = idx >> 7;
         const int part = rest & 1, T = (rest >> 1) % NRT, grp = (rest >> 1) / NRT;
         const int r = T * 128 + row;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        uint32_t v4[4] = {0u, 0u, 0u, 0u};
         if (r < n) {
           const int pi = r + r / E;
           const uint32_t* sp = stg + (size_t)((grp * 2 + part) * 4) * RS + pi;
-          v = make_uint4(sp[0], sp[RS], sp[2 * RS], sp[3 * RS]);
+#pragma unroll
+          for (int w = 0; w < 4; ++w) v4[w] = ((used >> (grp * 4 + w)) & 1) ? sp[w * RS] : 0u;
         }
         *reinterpret_cast<uint4*>(base + (size_t)((T * 2 + part) * NWG) * 2048 + (size_t)(row >> 3) * NWG * 128 +
-                                  (size_t)grp * 128 + (row & 7) * 16) = v;
+                                  (size_t)grp * 128 + (row & 7) * 16) = make_uint4(v4[0], v4[1], v4[2], v4[3]);
       }
     }
-    __syncthreads();
+    __syncthreads();  // the staging area becomes transpose scratch again
   }
 }
 
 static size_t step2_smem(int n_in, int n) {  // n_in = n_psi input rows, n = n_gamma >= n_in FFT length
   const int E = n / 32;
-  (void)n_in;  // the row buffer holds n rows: the transpose scratch needs the FFT length
-  return (size_t)n * S2_ROWSTRIDE * 8 + (size_t)16 * (n + n / E) * 4;
+  return (((size_t)n_in * S2_SMAX * 8 + 15) & ~(size_t)15) + (size_t)16 * (n + n / E) * 4 + 16;
 }
+
+static_assert(sizeof(S2Blocks) == sizeof(TcPlan::s2_blocks), "S2Blocks must mirror TcPlan::s2_blocks");
 
 static void launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, int formB,
                              const DevPlan& P, cudaStream_t s) {
@@ -1351,39 +1397,94 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   tc.KCH = (2 * pm.n_k) % 64 == 0 ? 64 : 32;
   tc.NKCH = 2 * pm.n_k / tc.KCH;
   cudaFuncSetAttribute(k_step1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
-  // Step-2 blocks: two word groups (16 Step-3 columns, whole terms) each; the device term order makes
-  // the terms of consecutive columns consecutive (see the column map in ftk_capi.cu)
+  // Step-2 blocks: 1 or 2 consecutive word groups (8 Step-3 columns each) holding <= 8 whole terms; the
+  // device term order makes the terms of consecutive columns consecutive (column map in ftk_capi.cu).
   {
     std::memset(&tc.s2_blocks, 0, sizeof tc.s2_blocks);
     const int ngroups = K3p / 8;
-    if (ngroups % 2 != 0 || ngroups / 2 > 16) {
-      msg = "tensor-core engine: unsupported Step-3 column count for Step 2";
-      return FTK_EINVAL;
+    std::vector<int> tg(ngroups, 0);
+    for (int z = 0; z < (int)col.size(); ++z) {
+      tg[col[z] / 8]++;
+      if (ell[z] > 0 && (col[z] & 1)) {
+        msg = "tensor-core engine: an ell > 0 term on an odd column";
+        return FTK_EINVAL;
+      }
     }
-    for (int bi = 0; bi < ngroups / 2; ++bi) {
+    int nb = 0;
+    long long off = 0;
+    for (int g = 0; g < ngroups;) {
+      const int ng = (g + 1 < ngroups && tg[g] + tg[g + 1] <= 8) ? 2 : 1;
+      if (nb >= 16 || tg[g] > 8) {
+        msg = "tensor-core engine: unsupported Step-2 block structure";
+        return FTK_EINVAL;
+      }
       int zs = -1, ze = -1;
       for (int z = 0; z < (int)col.size(); ++z)
-        if (col[z] / 16 == bi) {
+        if (col[z] / 8 >= g && col[z] / 8 < g + ng) {
           if (zs < 0) zs = z;
           if (ze >= 0 && z != ze) {
             msg = "tensor-core engine: Step-2 block terms not contiguous";
             return FTK_EINVAL;
           }
           ze = z + 1;
-          if (ell[z] > 0 && (col[z] + 1) / 16 != bi) {
-            msg = "tensor-core engine: a term straddles a Step-2 block";
-            return FTK_EINVAL;
-          }
         }
-      if (zs < 0) zs = ze = 0;  // padding-only block
-      if (ze - zs > 16) {
-        msg = "tensor-core engine: Step-2 block with more than 16 terms";
-        return FTK_EINVAL;
+      if (zs < 0) zs = ze = 0;
+      const int nz = ze - zs;
+      int used = 0, lone = 0;
+      for (int z = zs; z < ze; ++z) {
+        const int kl = col[z] - 8 * g;
+        used |= 1 << (kl >> 1);
+        if (ell[z] == 0) {
+          bool nbr = false;
+          for (int z2 = zs; z2 < ze; ++z2) nbr = nbr || (z2 != z && ell[z2] == 0 && col[z2] == (col[z] ^ 1));
+          if (!nbr) lone |= 1 << (z - zs);
+        }
       }
-      tc.s2_blocks.zs[bi] = zs;
-      tc.s2_blocks.ze[bi] = ze;
+      tc.s2_blocks.zs[nb] = zs;
+      tc.s2_blocks.ze[nb] = ze;
+      tc.s2_blocks.g0[nb] = g;
+      tc.s2_blocks.ng[nb] = ng;
+      tc.s2_blocks.used[nb] = used;
+      tc.s2_blocks.lone[nb] = lone;
+      tc.s2_blocks.W[nb] = nz <= 4 ? 4 : 8;
+      tc.s2_blocks.off[nb] = off;
+      off += (long long)pm.n_psi * tc.s2_blocks.W[nb];
+      ++nb;
+      g += ng;
     }
-    tc.s2_blocks.nb = ngroups / 2;
+    tc.s2_blocks.nb = nb;
+    tc.s2_blocks.zpair = off;
+    // per-term placement for k_step1_tc: region offset, and W | u << 4 | nz << 8 (u = index in the block)
+    std::vector<int> toff(col.size()), tpk(col.size());
+    for (int bi = 0; bi < nb; ++bi)
+      for (int z = tc.s2_blocks.zs[bi]; z < tc.s2_blocks.ze[bi]; ++z) {
+        toff[z] = (int)tc.s2_blocks.off[bi];
+        tpk[z] = tc.s2_blocks.W[bi] | ((z - tc.s2_blocks.zs[bi]) << 4) |
+                 ((tc.s2_blocks.ze[bi] - tc.s2_blocks.zs[bi]) << 8);
+      }
+    if (cudaMalloc(&tc.d_termoff, toff.size() * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&tc.d_termpk, tpk.size() * sizeof(int)) != cudaSuccess) {
+      msg = "tensor-core engine: allocation failed";
+      return FTK_ENOMEM;
+    }
+    cudaMemcpy(tc.d_termoff, toff.data(), toff.size() * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(tc.d_termpk, tpk.data(), tpk.size() * sizeof(int), cudaMemcpyHostToDevice);
+    {  // Step-2 twiddle tables: [c][a] w_n^{a c} and [d'][a] w_32^{(a % L) d'}, E = n / 32, L = 32 / E
+      const int n = n_gamma, E = n / 32, L = 32 / E;
+      std::vector<float2> tw((size_t)2 * E * 32);
+      for (int c = 0; c < E; ++c)
+        for (int a = 0; a < 32; ++a) {
+          const double ph1 = -2.0 * M_PI * (double)((a * c) % n) / n;
+          const double ph2 = -2.0 * M_PI * (double)(((a % L) * c) % 32) / 32.0;
+          tw[(size_t)c * 32 + a] = make_float2((float)std::cos(ph1), (float)std::sin(ph1));
+          tw[(size_t)E * 32 + c * 32 + a] = make_float2((float)std::cos(ph2), (float)std::sin(ph2));
+        }
+      if (cudaMalloc(&tc.d_s2tw, tw.size() * sizeof(float2)) != cudaSuccess) {
+        msg = "tensor-core engine: allocation failed";
+        return FTK_ENOMEM;
+      }
+      cudaMemcpy(tc.d_s2tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice);
+    }
     const int sm2 = (int)step2_smem(pm.n_psi, n_gamma);
     cudaFuncSetAttribute(k_step2_fft<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(k_step2_fft<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
@@ -1398,6 +1499,9 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
 void tc_plan_free(TcPlan& tc) {
   cudaFree(tc.d_s2tw);
   tc.d_s2tw = nullptr;
+  cudaFree(tc.d_termoff);
+  cudaFree(tc.d_termpk);
+  tc.d_termoff = tc.d_termpk = nullptr;
   cudaFree(tc.d_Ysm);
   cudaFree(tc.d_colrep);
   cudaFree(tc.d_colpart);
@@ -1435,7 +1539,7 @@ int tc_prepare_templates(TcPlan&, const float2*, int64_t, const DevPlan&, cudaSt
 }
 
 size_t tc_bytes_per_pair(const TcPlan& tc, const DevPlan& P) {
-  return (size_t)P.Hs * P.n_psi * sizeof(float2) + (size_t)tc.NRT * 128 * P.K3p * 4;
+  return (size_t)tc.s2_blocks.zpair * sizeof(float2) + (size_t)tc.NRT * 128 * P.K3p * 4;
 }
 
 ftk_status_t tc_block_shape(const TcPlan&, const DevPlan&, int engine, int64_t NI, int64_t NJ, int64_t cap,
@@ -1516,6 +1620,9 @@ void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const Pair
   prm.n_k = P.n_k;
   prm.Hp = P.H_plus;
   prm.Hs = P.Hs;
+  prm.termoff = tc.d_termoff;
+  prm.termpk = tc.d_termpk;
+  prm.zpair = tc.s2_blocks.zpair;
   prm.KCH = tc.KCH;
   prm.NKCH = tc.NKCH;
   prm.NIT = tc.NIT;
@@ -1549,7 +1656,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     return FTK_ESTATE;
   }
   float2* Zhat = reinterpret_cast<float2*>(ws);
-  uint8_t* Zop = reinterpret_cast<uint8_t*>(Zhat + (size_t)pb.count * P.Hs * P.n_psi);
+  uint8_t* Zop = reinterpret_cast<uint8_t*>(Zhat + (size_t)pb.count * tc.s2_blocks.zpair);
   if (pb.li) {
     // explicit pair list (ftk_landscape_pairs): per-pair Step 1 on CUDA cores, then the same FFT
     if (prof) prof(plan, 1, 0, s);

@@ -29,11 +29,16 @@ struct TcPlan {
   uint8_t* d_Aop = nullptr;    // images, bf16 hi/lo split, Step-1 K-major tiles [p][tile][kchunk][part]...
   size_t aop_bytes = 0;
   int NIT = 0, KCH = 64, NKCH = 0;
-  // Step 2 block table (two 8-column word groups per block)
+  // Step-2 work blocks (and the layout of Zhat'), mirrors S2Blocks in ftk_tc.cu
   struct {
     int nb;
-    int zs[16], ze[16];
-  } s2_blocks;
+    long long zpair;
+    int zs[16], ze[16], g0[16], ng[16], W[16];
+    long long off[16];
+    int used[16], lone[16];
+  } s2_blocks;                  // Step-2 work blocks and the layout of Zhat' (S2Blocks in ftk_tc.cu)
+  int* d_termoff = nullptr;     // Step 1: per term block-region offset
+  int* d_termpk = nullptr;      // Step 1: per term W | u << 4 | nz << 8
   float2* d_s2tw = nullptr;  // Step-2 four-step twiddle tables
   int64_t n_tm = 0;
   int num_sms = 148;
