@@ -27,6 +27,7 @@
 //     winning group in fp32 from the same bf16 operands to recover the exact (shift, sign), one
 //     packed-key atomicMax per pair.
 // TMEM columns: D buffers [0, 4 NCH) (E, O of buffer 0 then 1), A slots [4 NCH, 4 NCH + 2 K3p).
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -493,7 +494,7 @@ static size_t s3_smem_bytes(int ncol, int K3p, int NS) {
 // so that Zhat_zeta(q) = Zhat'_zeta(q - ell) and Step 2 applies e^{-i ell gamma_r} after the FFT.
 // Real GEMM per p with K' = 2 n_k:  rows (j, zeta, part) of the GENERATED operand c (A, in TMEM):
 //   Re-row = [c_r | -c_i],  Im-row = [c_i | c_r];  columns = images, B = [a_r | a_i] (pre-split, SMEM).
-// Output Zhat' per pair (pair = il * nj + jl within the block): the Step-2 block regions (S2Blocks).
+// Output Zhat' [pair][p][Hs] complex (pair = il * nj + jl within the block; Hs = H_plus rounded up to even).
 constexpr int S1_THREADS = 14 * 32;
 constexpr int S1_STAGES = 4;
 
@@ -502,10 +503,7 @@ struct S1Params {
   const float2* B;      // template FB coefficients [j][q][m] (local templates)
   const float* g;       // [H_plus][n_k]
   const int* ell;       // [H_plus]
-  float2* Zhat;         // per pair the Step-2 block regions [p][W] (rotated slots, see S2Blocks)
-  const int* termoff;   // [H_plus] region offset (complex) of term z's block
-  const int* termpk;    // [H_plus] W | u << 4 | nz << 8 (u = index of z in its block)
-  long long zpair;      // complex elements per pair
+  float2* Zhat;         // [pair][p][Hs]
   int i0, ni, j0, nj;   // block (i0 multiple of 128)
   int n, n_k, Hp, Hs, KCH, NKCH, NIT;  // NIT = image tiles per mode in Aop
   int F, NCT;           // F = nj * Hp flattened (j, zeta) columns, NCT = ceil(F / 64)
@@ -705,25 +703,16 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
       s1_unit(u, P.NCT, p, ct);
       const int nvalid = min(128, 2 * (P.F - ct * 64));
       // this lane's two complex columns cc = lane, lane + 32 -> offsets (template jl, term z) in Zhat'
-      // Zhat' placement (S2Blocks): region off + p W + ((u + (p >> sh)) & (W - 1)); the lane holding a
-      // block's last term also zeroes the block's empty slots of this row (whole sectors written)
-      long long coff[2], rowb[2];
+      // this lane's two complex columns cc = lane, lane + 32 -> offsets (template jl, term z) in Zhat'
+      long long coff[2];
       bool cval[2];
-      int pw[2], pu[2], pnz[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int cc = lane + 32 * h;
         const int f = ct * 64 + cc;
         const int jl = f / P.Hp, z = f - jl * P.Hp;
         cval[h] = 2 * cc < nvalid;
-        const int pk = cval[h] ? __ldg(P.termpk + z) : 8;
-        pw[h] = pk & 15;
-        pu[h] = (pk >> 4) & 15;
-        pnz[h] = pk >> 8;
-        const int sh = pw[h] == 8 ? 1 : 2;
-        rowb[h] = cval[h] ? (long long)jl * P.zpair + __ldg(P.termoff + z) + (long long)p * pw[h] : 0;
-        coff[h] = rowb[h] + ((pu[h] + (p >> sh)) & (pw[h] - 1));
-        pu[h] |= (p >> sh) << 8;  // keep the rotation for the pad slots
+        coff[h] = (long long)jl * n * P.Hs + z;
       }
       for (int t = 0; t < nit; ++t, ++g_acc) {
         const int ab = g_acc & 1;
@@ -745,15 +734,10 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
         for (int ii = ew; ii < 128; ii += 4) {
           const int il = t * 128 + ii;  // local image index within the block
           if (il >= P.ni) continue;
-          float2* dst = P.Zhat + (size_t)il * P.nj * P.zpair;
+          float2* dst = P.Zhat + ((size_t)il * P.nj * n + p) * P.Hs;
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            if (cval[h]) {
-              dst[coff[h]] = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
-              const int u = pu[h] & 255, rot = pu[h] >> 8;
-              if (u == pnz[h] - 1)
-                for (int v = pnz[h]; v < pw[h]; ++v) dst[rowb[h] + ((v + rot) & (pw[h] - 1))] = make_float2(0.f, 0.f);
-            }
+            if (cval[h]) dst[coff[h]] = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
         }
         named_bar(2, 128);
       }
@@ -820,22 +804,19 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 //   DIF across the warp with shfl_xor (output index d lands on lane bitrev5(d)).
 // Output words are staged per (group, part, word) in padded rows (index r + r / E: conflict-free) and
 // written out as contiguous 2 KB row blocks.
-// Zhat' layout (written by k_step1_tc, read by k_step2_fft): per pair, per Step-2 block b one region
-// [p][W_b] of complex values, W_b = 4 or 8 (rows of 32 / 64 bytes: whole sectors), term u of the block in
-// slot (u + (p >> sh_b)) & (W_b - 1), sh_b = log2(16 / W_b): the rotation makes the column reads of
-// k_step2_fft bank-conflict free.  Slots without a term hold zeros.
 struct S2Blocks {      // Step-2 work blocks: 1 or 2 consecutive word groups holding <= 8 terms
   int nb;
-  long long zpair;     // complex elements of one pair's Zhat'
   int zs[16], ze[16];  // term range of block b
   int g0[16], ng[16];  // first word group, number of groups
-  int W[16];           // row width (4 or 8)
-  long long off[16];   // region offset (complex) within the pair
   int used[16];        // words (bit grp * 4 + w) written by some term
   int lone[16];        // terms (bit z - zs) with ell = 0 and no neighbour in their word
 };
-constexpr int S2_SMAX = 8;  // max row width (complex)
-__host__ __device__ inline int s2_shift(int W) { return W == 8 ? 1 : 2; }
+// Step-2 row buffer: [p][8 terms] complex (64-byte rows) in the TMA SWIZZLE_64B layout: the 16-byte
+// chunk c of row p sits at chunk c ^ ((p >> 1) & 3), which makes the warps' column reads conflict-free.
+constexpr int S2_SMAX = 8;
+__device__ __forceinline__ int s2_slot(int p, int zz) {  // complex index of (row p, term zz < 8)
+  return p * 8 + ((((zz >> 1) ^ (p >> 1)) & 3) << 1) + (zz & 1);
+}
 
 __device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -906,15 +887,16 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <int E>
 __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
                                                       int npair, int formB, DevPlan P, S2Blocks B,
-                                                      const float2* __restrict__ twtab) {
-  extern __shared__ __align__(16) uint8_t s2raw[];
+                                                      const float2* __restrict__ twtab,
+                                                      const __grid_constant__ CUtensorMap zmap) {
+  extern __shared__ __align__(1024) uint8_t s2raw[];
   constexpr int n = 32 * E;  // FFT length = n_gamma (>= n_psi; zero-padded input, reading R21)
   constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
   constexpr int RS = n + n / E;  // padded staging row (words): index r + r / E
   const int n_in = P.n_psi;     // input rows (cyclic q)
-  // [rows: n_in x S2_SMAX complex][stg: 16 x RS words; also the warps' n-slot transpose scratch][mbarrier]
+  // [rows: 2 x n_in x S2_SMAX complex][stg: 16 x RS words; also the warps' n-slot transpose scratch][mbarrier]
   float2* rows = reinterpret_cast<float2*>(s2raw);
-  const size_t rows_bytes = ((size_t)n_in * S2_SMAX * 8 + 15) & ~(size_t)15;
+  const size_t rows_bytes = (size_t)2 * n_in * S2_SMAX * 8;
   uint32_t* stg = reinterpret_cast<uint32_t*>(s2raw + rows_bytes);
   uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 16 * RS);
   // warp index made provably warp-uniform (shfl from lane 0) so the shuffles below sit in convergent code
@@ -952,23 +934,27 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
   const int per = (total + gridDim.x - 1) / gridDim.x;
   const int i_beg = blockIdx.x * per;
   const int i_end = min(total, i_beg + per);
-  // Form B input: one bulk copy of the block's region [p][W] (k_step1_tc's layout); Form A (explicit
-  // pairs, Zhat [pair][zeta][q]): cp.async gather into the same swizzled [p][8] layout
+  // Form B input: the block's term columns of the pair's n_psi rows of Zhat' [pair][p][Hs] as 2-D TMA
+  // boxes (8 x 256, zero fill beyond Hs) into the swizzled [p][8] row buffers.  A box must start on a
+  // 16-byte boundary (an odd 8-byte column start faults), so the window starts at the even column
+  // zs & ~1 and takes a second 8-column box when the block's terms reach past it.  Form A (explicit
+  // pairs, Zhat [pair][zeta][q]): cp.async gather into the same layout
   auto issue = [&](int it) {
     const int bi = it % B.nb, pi2 = it / B.nb;
     if (formB) {
       if (threadIdx.x == 0) {
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(Zhat + (size_t)pi2 * B.zpair + B.off[bi]);
-        const uint32_t bytes = (uint32_t)n_in * (uint32_t)B.W[bi] * 8u;
-        mbar_arrive_expect_tx(bar, bytes);
-        for (uint32_t o = 0; o < bytes; o += 32768u) bulk_g2s(s2raw + o, src + o, min(32768u, bytes - o), bar);
+        const int box = n_in < 256 ? n_in : 256;
+        const int x0 = B.zs[bi] & ~1, nbox = (B.ze[bi] - x0 > 8) ? 2 : 1;
+        mbar_arrive_expect_tx(bar, (uint32_t)(n_in * 64 * nbox));
+        for (int h = 0; h < nbox; ++h)
+          for (int k = 0; k < n_in; k += box)
+            tma_load_2d(s2raw + (size_t)(h * n_in + k) * 64, &zmap, x0 + 8 * h, pi2 * n_in + k, bar);
       }
     } else {
       const int zs = B.zs[bi], nz = B.ze[bi] - zs;
       const float2* src = Zhat + ((size_t)pi2 * Hp + zs) * n_in;
       for (int z = 0; z < nz; ++z)
-        for (int q = threadIdx.x; q < n_in; q += blockDim.x)
-          cp_async8(rows + q * 8 + ((z + (q >> 1)) & 7), src + (size_t)z * n_in + q);
+        for (int q = threadIdx.x; q < n_in; q += blockDim.x) cp_async8(rows + s2_slot(q, z), src + (size_t)z * n_in + q);
       cp_async_commit();
     }
   };
@@ -982,7 +968,6 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
   for (int item = i_beg; item < i_end; ++item) {
     const int b = item % B.nb, pr = item / B.nb;
     const int zs = B.zs[b], nz = B.ze[b] - zs, g0 = B.g0[b];
-    const int W = formB ? B.W[b] : 8, sh = s2_shift(W);
     if (formB) {
       mbar_wait(bar, phase);
       phase ^= 1u;
@@ -999,8 +984,9 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
       const int z = zs + zz;
       l = P.ell[z];
       col = P.col[z];
-      // element (row p, term zz) at rows[p * W + ((zz + (p >> sh)) & (W - 1))] (rotated slots)
-      auto at = [&](int p) { return rows[p * W + ((zz + (p >> sh)) & (W - 1))]; };
+      const int e = formB ? (zs & 1) + zz : zz;  // window column of this term
+      const float2* rb = rows + (size_t)(e >> 3) * n_in * S2_SMAX;
+      auto at = [&](int p) { return rb[s2_slot(p, e & 7)]; };
       // Form B: Z(r) w^{ell r} = DFT of the cyclically shifted row Zhat'(q - ell) (reading R5)
       if (n_in == n) {
         const int q0 = formB ? ((lane - l) & (n - 1)) : lane;
@@ -1114,25 +1100,64 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
 
 static size_t step2_smem(int n_in, int n) {  // n_in = n_psi input rows, n = n_gamma >= n_in FFT length
   const int E = n / 32;
-  return (((size_t)n_in * S2_SMAX * 8 + 15) & ~(size_t)15) + (size_t)16 * (n + n / E) * 4 + 16;
+  return (size_t)2 * n_in * S2_SMAX * 8 + (size_t)16 * (n + n / E) * 4 + 16;
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode_tiled() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
 }
 
 static_assert(sizeof(S2Blocks) == sizeof(TcPlan::s2_blocks), "S2Blocks must mirror TcPlan::s2_blocks");
 
-static void launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, int formB,
-                             const DevPlan& P, cudaStream_t s) {
+// Zhat' [pair][p][Hs] as a 2-D tensor of 8-byte elements (rows = pair * n_psi + p), 8 x 256 boxes,
+// 64-byte swizzle (the layout s2_slot() reads)
+static int make_zmap(CUtensorMap* m, const float2* Zhat, int npair, const DevPlan& P) {
+  PFN_encodeTiled enc = get_encode_tiled();
+  if (!enc) return FTK_ECUDA;
+  const cuuint64_t dims[2] = {(cuuint64_t)P.Hs, (cuuint64_t)npair * P.n_psi};
+  const cuuint64_t strides[1] = {(cuuint64_t)P.Hs * 8};
+  const cuuint32_t box[2] = {8u, (cuuint32_t)(P.n_psi < 256 ? P.n_psi : 256)};
+  const cuuint32_t es[2] = {1u, 1u};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<float2*>(Zhat), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? FTK_OK : FTK_ECUDA;
+}
+
+static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, int formB,
+                            const DevPlan& P, cudaStream_t s) {
   S2Blocks B;
   std::memcpy(&B, &tc.s2_blocks, sizeof B);
+  alignas(64) CUtensorMap zmap;
+  std::memset(&zmap, 0, sizeof zmap);
+  if (formB && make_zmap(&zmap, Zhat, npair, P) != FTK_OK) return FTK_ECUDA;
+  if (tc.sync_debug)
+    fprintf(stderr, "step2: Zhat %p (mod 256 = %d) Hs %d npair %d n_psi %d n_gamma %d smem %zu grid %d\n", (const void*)Zhat,
+            (int)((uintptr_t)Zhat & 255), P.Hs, npair, P.n_psi, P.n_gamma, step2_smem(P.n_psi, P.n_gamma),
+            B.nb * npair < 2 * tc.num_sms ? B.nb * npair : 2 * tc.num_sms);
   const size_t smem = step2_smem(P.n_psi, P.n_gamma);
   const int items = B.nb * npair;
   dim3 grid(items < 2 * tc.num_sms ? items : 2 * tc.num_sms);
   switch (P.n_gamma) {
-    case 64: k_step2_fft<2><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
-    case 128: k_step2_fft<4><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
-    case 256: k_step2_fft<8><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
-    case 512: k_step2_fft<16><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
-    default: k_step2_fft<32><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw); break;
+    case 64: k_step2_fft<2><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
+    case 128: k_step2_fft<4><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
+    case 256: k_step2_fft<8><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
+    case 512: k_step2_fft<16><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
+    default: k_step2_fft<32><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
   }
+  return FTK_OK;
 }
 
 // ---------------------------------------------------------------- single-MMA self-test
@@ -1411,7 +1436,6 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       }
     }
     int nb = 0;
-    long long off = 0;
     for (int g = 0; g < ngroups;) {
       const int ng = (g + 1 < ngroups && tg[g] + tg[g + 1] <= 8) ? 2 : 1;
       if (nb >= 16 || tg[g] > 8) {
@@ -1446,29 +1470,10 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       tc.s2_blocks.ng[nb] = ng;
       tc.s2_blocks.used[nb] = used;
       tc.s2_blocks.lone[nb] = lone;
-      tc.s2_blocks.W[nb] = nz <= 4 ? 4 : 8;
-      tc.s2_blocks.off[nb] = off;
-      off += (long long)pm.n_psi * tc.s2_blocks.W[nb];
       ++nb;
       g += ng;
     }
     tc.s2_blocks.nb = nb;
-    tc.s2_blocks.zpair = off;
-    // per-term placement for k_step1_tc: region offset, and W | u << 4 | nz << 8 (u = index in the block)
-    std::vector<int> toff(col.size()), tpk(col.size());
-    for (int bi = 0; bi < nb; ++bi)
-      for (int z = tc.s2_blocks.zs[bi]; z < tc.s2_blocks.ze[bi]; ++z) {
-        toff[z] = (int)tc.s2_blocks.off[bi];
-        tpk[z] = tc.s2_blocks.W[bi] | ((z - tc.s2_blocks.zs[bi]) << 4) |
-                 ((tc.s2_blocks.ze[bi] - tc.s2_blocks.zs[bi]) << 8);
-      }
-    if (cudaMalloc(&tc.d_termoff, toff.size() * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&tc.d_termpk, tpk.size() * sizeof(int)) != cudaSuccess) {
-      msg = "tensor-core engine: allocation failed";
-      return FTK_ENOMEM;
-    }
-    cudaMemcpy(tc.d_termoff, toff.data(), toff.size() * sizeof(int), cudaMemcpyHostToDevice);
-    cudaMemcpy(tc.d_termpk, tpk.data(), tpk.size() * sizeof(int), cudaMemcpyHostToDevice);
     {  // Step-2 twiddle tables: [c][a] w_n^{a c} and [d'][a] w_32^{(a % L) d'}, E = n / 32, L = 32 / E
       const int n = n_gamma, E = n / 32, L = 32 / E;
       std::vector<float2> tw((size_t)2 * E * 32);
@@ -1492,6 +1497,12 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
     cudaFuncSetAttribute(k_step2_fft<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     cudaFuncSetAttribute(k_step2_fft<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
   }
+  const char* sdbg = std::getenv("FTK_SYNC_DEBUG");
+  tc.sync_debug = sdbg && sdbg[0] == '1';
+  if (tc.sync_debug)
+    for (int bi = 0; bi < tc.s2_blocks.nb; ++bi)
+      fprintf(stderr, "s2 block %d: terms [%d,%d) groups %d+%d used %x lone %x\n", bi, tc.s2_blocks.zs[bi],
+              tc.s2_blocks.ze[bi], tc.s2_blocks.g0[bi], tc.s2_blocks.ng[bi], tc.s2_blocks.used[bi], tc.s2_blocks.lone[bi]);
   tc.ready = true;
   return FTK_OK;
 }
@@ -1499,9 +1510,6 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
 void tc_plan_free(TcPlan& tc) {
   cudaFree(tc.d_s2tw);
   tc.d_s2tw = nullptr;
-  cudaFree(tc.d_termoff);
-  cudaFree(tc.d_termpk);
-  tc.d_termoff = tc.d_termpk = nullptr;
   cudaFree(tc.d_Ysm);
   cudaFree(tc.d_colrep);
   cudaFree(tc.d_colpart);
@@ -1539,7 +1547,7 @@ int tc_prepare_templates(TcPlan&, const float2*, int64_t, const DevPlan&, cudaSt
 }
 
 size_t tc_bytes_per_pair(const TcPlan& tc, const DevPlan& P) {
-  return (size_t)tc.s2_blocks.zpair * sizeof(float2) + (size_t)tc.NRT * 128 * P.K3p * 4;
+  return (size_t)P.Hs * P.n_psi * sizeof(float2) + (size_t)tc.NRT * 128 * P.K3p * 4;
 }
 
 ftk_status_t tc_block_shape(const TcPlan&, const DevPlan&, int engine, int64_t NI, int64_t NJ, int64_t cap,
@@ -1620,9 +1628,6 @@ void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const Pair
   prm.n_k = P.n_k;
   prm.Hp = P.H_plus;
   prm.Hs = P.Hs;
-  prm.termoff = tc.d_termoff;
-  prm.termpk = tc.d_termpk;
-  prm.zpair = tc.s2_blocks.zpair;
   prm.KCH = tc.KCH;
   prm.NKCH = tc.NKCH;
   prm.NIT = tc.NIT;
@@ -1656,26 +1661,53 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     return FTK_ESTATE;
   }
   float2* Zhat = reinterpret_cast<float2*>(ws);
-  uint8_t* Zop = reinterpret_cast<uint8_t*>(Zhat + (size_t)pb.count * tc.s2_blocks.zpair);
+  uint8_t* Zop = reinterpret_cast<uint8_t*>(Zhat + (size_t)pb.count * P.Hs * P.n_psi);
   if (pb.li) {
     // explicit pair list (ftk_landscape_pairs): per-pair Step 1 on CUDA cores, then the same FFT
     if (prof) prof(plan, 1, 0, s);
     launch_step1_simt(A, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
     if (prof) prof(plan, 2, 0, s);
-    launch_step2_fft(tc, Zhat, Zop, pb.count, 0, P, s);
+    if (launch_step2_fft(tc, Zhat, Zop, pb.count, 0, P, s) != FTK_OK) {
+      msg = "Step 2: tensor map encoding failed";
+      return FTK_ECUDA;
+    }
     if (prof) prof(plan, 2, 1, s);
   } else {
     if (prof) prof(plan, 1, 0, s);
     launch_step1_tc(tc, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
+    if (tc.sync_debug) {
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) {
+        msg = std::string("Step 1: ") + cudaGetErrorString(e);
+        return FTK_ECUDA;
+      }
+    }
     if (prof) prof(plan, 2, 0, s);
-    launch_step2_fft(tc, Zhat, Zop, pb.count, 1, P, s);
+    if (launch_step2_fft(tc, Zhat, Zop, pb.count, 1, P, s) != FTK_OK) {
+      msg = "Step 2: tensor map encoding failed";
+      return FTK_ECUDA;
+    }
     if (prof) prof(plan, 2, 1, s);
+  }
+  if (tc.sync_debug) {  // FTK_SYNC_DEBUG=1: attribute an asynchronous fault to its step
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      msg = std::string("Steps 1-2: ") + cudaGetErrorString(e);
+      return FTK_ECUDA;
+    }
   }
   if (prof) prof(plan, 3, 0, s);
   launch_step3_tc(tc, Zop, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
   if (prof) prof(plan, 3, 1, s);
+  if (tc.sync_debug) {
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      msg = std::string("Step 3: ") + cudaGetErrorString(e);
+      return FTK_ECUDA;
+    }
+  }
   return FTK_OK;
 }
 

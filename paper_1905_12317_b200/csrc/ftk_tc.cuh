@@ -32,16 +32,13 @@ struct TcPlan {
   // Step-2 work blocks (and the layout of Zhat'), mirrors S2Blocks in ftk_tc.cu
   struct {
     int nb;
-    long long zpair;
-    int zs[16], ze[16], g0[16], ng[16], W[16];
-    long long off[16];
+    int zs[16], ze[16], g0[16], ng[16];
     int used[16], lone[16];
-  } s2_blocks;                  // Step-2 work blocks and the layout of Zhat' (S2Blocks in ftk_tc.cu)
-  int* d_termoff = nullptr;     // Step 1: per term block-region offset
-  int* d_termpk = nullptr;      // Step 1: per term W | u << 4 | nz << 8
+  } s2_blocks;                  // Step-2 work blocks (S2Blocks in ftk_tc.cu)
   float2* d_s2tw = nullptr;  // Step-2 four-step twiddle tables
   int64_t n_tm = 0;
   int num_sms = 148;
+  bool sync_debug = false;  // FTK_SYNC_DEBUG=1: synchronize after each step (fault attribution)
 };
 
 typedef void (*prof_cb_t)(void* plan, int cls, int end, cudaStream_t s);
