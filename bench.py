@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--templates", type=int, default=0)
     ap.add_argument("--n-gamma", type=int, default=0,
                     help="rotations per (pair, shift); 0 = n_psi (the configs). > n_psi: zero-padded Step 2 (NEXT-3)")
+    ap.add_argument("--marginal-tau", type=float, default=0.0,
+                    help="> 0: time the marginalization epilogue (log sum exp(X / tau) per pair, NEXT-3) instead "
+                         "of max / argmax (1 GPU; not the headline metric)")
     return ap.parse_args()
 
 
@@ -221,6 +224,8 @@ def main():
     def step():
         plan.load_images(imgs, stream=stream)
         plan.load_templates(tpls, stream=stream)
+        if args.marginal_tau > 0:
+            return plan.align_marginal(args.marginal_tau, stream=stream)
         if world > 1:
             return pkg.distributed_align(plan, stream=stream)
         return plan.align(stream=stream)["best"]
@@ -261,53 +266,72 @@ def main():
     total_ips = float(ni) * nj * n_t * n_gamma
     value = total_ips * args.steps / (dt_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (largest device time in the timed region)
-    dom = max(("step1", "step3"), key=lambda c: kt_acc.get(c, [0, 0])[0])
-    dom_ms, dom_cnt = kt_acc.get(dom, [0.0, 0])
+    # ---- roofline of each hot-path kernel; the dominant one (largest device time in the timed region)
+    #      is the line's "roofline"
     info = plan.info
     pairs_local = ni * info["n_templates_local"]
-    if dom == "step3":
-        flops = 2.0 * n_t * n_gamma * info["K3"] * pairs_local            # real GEMM, K = 2 H_plus - H0
-    else:
-        flops = 8.0 * cfg.n_psi * info["H_plus"] * cfg.n_k * pairs_local  # complex GEMM over k_m
-    flops_per_launch = flops * args.steps / max(dom_cnt, 1)
-    avg_launch_s = dom_ms / max(dom_cnt, 1) / 1e3
-    achieved = flops_per_launch / avg_launch_s / 1e12 if avg_launch_s > 0 else None
     peaks = measured_peaks()
-    if engine == pkg.ENGINE_TC:
-        bound, peak_src = "tensor", "measured bf16 sustained (MEASURED_PEAKS.json)"
-        peak = peaks["bf16_tflops_sustained"] if peaks else 1400.0
-        if not peaks:
-            peak_src = "fallback 1.4 PF/s sustained (B200_PROFILING.md)"
-    else:
-        bound = "alu"
-        mhz = (peaks or {}).get("sm_max_mhz", 1965.0)
-        peak = 148 * 128 * 2 * mhz * 1e6 / 1e12   # fp32 FMA lanes x 2 flop x clock
-        peak_src = "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz"
-    issued = None
-    if engine == pkg.ENGINE_TC and dom == "step3":
-        rows = 128 * info["s3_rtiles"]
-        issued_flops = 3.0 * 2.0 * rows * info["s3_cols"] * info["K3p"] * pairs_local * args.steps / max(dom_cnt, 1)
-        issued = issued_flops / avg_launch_s / 1e12 if avg_launch_s > 0 else None
-    traffic = None
-    try:  # DRAM bytes per pair of this kernel from the committed ncu capture (same config only)
+    try:  # DRAM bytes per pair of each kernel from the committed ncu captures (same config only)
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        if tj.get("config") == cfg.name and dom in tj.get("bytes_per_pair", {}):
-            traffic = tj["bytes_per_pair"][dom] * pairs_local * args.steps / max(dom_cnt, 1)
     except (OSError, ValueError):
+        tj = {}
+
+    def roof(kern):
+        k_ms, k_cnt = kt_acc.get(kern, [0.0, 0])
+        avg_s = k_ms / max(k_cnt, 1) / 1e3
+        per_launch = pairs_local * args.steps / max(k_cnt, 1)     # pairs one launch processes
         traffic = None
-    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "tensor_issued_tflops": issued,
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_unit": "bytes/launch",
-                "traffic_algorithmic": (4.0 * 128 * info["s3_rtiles"] * info["K3p"] * pairs_local * args.steps
-                                        / max(dom_cnt, 1)) if dom == "step3" else None,
-                "kernel": dom,
-                "launches": dom_cnt, "avg_launch_ms": avg_launch_s * 1e3, "peak_source": peak_src,
-                "flops_per_launch": flops_per_launch,
-                "note": "achieved = algorithmic flops 2*N_t*n_psi*K3 per pair (minimal real Step-3 GEMM) / launch time; "
-                        "tensor_issued_tflops counts the MMAs actually issued (bf16x3 = 3 products, +-delta symmetry "
-                        "halves the rows, tile padding)"
-                if engine == pkg.ENGINE_TC else "algorithmic flops on CUDA cores"}
+        if tj.get("config") == cfg.name and kern in tj.get("bytes_per_pair", {}):
+            traffic = tj["bytes_per_pair"][kern] * per_launch
+        r = {"kernel": kern, "launches": k_cnt, "avg_launch_ms": avg_s * 1e3, "traffic": traffic,
+             "traffic_unit": "bytes/launch"}
+        if kern == "step2":
+            # HBM-bound: read Zhat' (n_psi x H_plus complex fp32), write the Step-3 operand (n_gamma x K3
+            # real columns, bf16 hi + lo)
+            byts = (8.0 * cfg.n_psi * info["H_plus"] + 4.0 * n_gamma * info["K3"]) * per_launch
+            peak = peaks["hbm_gbs"] if peaks else 7000.0
+            achieved = byts / avg_s / 1e9 if avg_s > 0 else None
+            r.update({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                      "bytes_per_launch": byts,
+                      "peak_source": "measured HBM copy GB/s (MEASURED_PEAKS.json)" if peaks
+                      else "fallback 7000 GB/s (B200_PROFILING.md)",
+                      "note": "algorithmic bytes per pair 8 n_psi H_plus (read Zhat') + 4 n_gamma K3 (write bf16 hi/lo)"})
+        else:
+            if kern == "step3":
+                flops = 2.0 * n_t * n_gamma * info["K3"] * per_launch           # real GEMM, K = 2 H_plus - H0
+            else:
+                flops = 8.0 * cfg.n_psi * info["H_plus"] * cfg.n_k * per_launch  # complex GEMM over k_m
+            achieved = flops / avg_s / 1e12 if avg_s > 0 else None
+            if engine == pkg.ENGINE_TC:
+                bound, peak_src = "tensor", "measured bf16 sustained (MEASURED_PEAKS.json)"
+                peak = peaks["bf16_tflops_sustained"] if peaks else 1400.0
+                if not peaks:
+                    peak_src = "fallback 1.4 PF/s sustained (B200_PROFILING.md)"
+            else:
+                bound = "alu"
+                mhz = (peaks or {}).get("sm_max_mhz", 1965.0)
+                peak = 148 * 128 * 2 * mhz * 1e6 / 1e12   # fp32 FMA lanes x 2 flop x clock
+                peak_src = "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz"
+            r.update({"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "flops_per_launch": flops,
+                      "peak_source": peak_src})
+            if engine == pkg.ENGINE_TC and kern == "step3":
+                rows = 128 * info["s3_rtiles"]
+                issued = 3.0 * 2.0 * rows * info["s3_cols"] * info["K3p"] * per_launch
+                r["tensor_issued_tflops"] = issued / avg_s / 1e12 if avg_s > 0 else None
+                r["traffic_algorithmic"] = 4.0 * 128 * info["s3_rtiles"] * info["K3p"] * per_launch
+                r["note"] = ("achieved = algorithmic flops 2*N_t*n_gamma*K3 per pair (minimal real Step-3 GEMM) / launch "
+                             "time; tensor_issued_tflops counts the MMAs actually issued (bf16x3 = 3 products, +-delta "
+                             "symmetry halves the rows, tile padding)")
+            elif kern == "step1":
+                r["note"] = "achieved = algorithmic flops 8 n_psi H_plus n_k per pair (complex Step-1 GEMM) / launch time"
+        r["frac"] = (r["achieved"] / r["peak"]) if r.get("achieved") else None
+        return r
+
+    kerns = [k2 for k2 in ("step1", "step2", "step3") if kt_acc.get(k2, [0, 0])[1] > 0]
+    dom = max(kerns, key=lambda c: kt_acc[c][0]) if kerns else "step3"
+    roofline = roof(dom)
+    roofline["all_kernels"] = {k2: {f: roof(k2).get(f) for f in ("bound", "achieved", "peak", "unit", "frac",
+                                                                   "avg_launch_ms")} for k2 in kerns}
     launches = sum(v[1] for v in kt_acc.values())
 
     # ---- end to end through the C ABI from pinned host buffers
@@ -367,7 +391,9 @@ def main():
                            "N_im": ni, "N_tm": nj, "N_t": n_t, "eps": cfg.eps, "H": info["H"],
                            "H_plus": info["H_plus"], "K3": info["K3"], "engine": args.engine,
                            "parallelism": f"template-shard x{world}", "l2": "inputs (6+ GB FB arrays) exceed L2",
-                           "step": "load FFT (images+templates) + Steps 1-3 + argmax (+ all-gather/merge)"},
+                           "step": "load FFT (images+templates) + Steps 1-3 + argmax (+ all-gather/merge)"
+                           if args.marginal_tau <= 0 else
+                           f"load FFT + Steps 1-3 + log-marginal epilogue (tau = {args.marginal_tau})"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks,
                 "kernel_ms": {k2: v[0] / args.steps for k2, v in kt_acc.items()}}

@@ -147,6 +147,18 @@ ftk_status_t ftk_fb_coeffs(ftk_plan_t plan, int which, int64_t first, int64_t co
 ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best, float* landscape,
                        int64_t landscape_capacity, void* stream);
 
+/* Marginalization epilogue (the Bayesian use of the whole landscape, PAPER.md
+ * P:73-74 "an integral of a probability distribution over shifts and angles is used to marginalize
+ * the likelihood"): Steps 1-3 as in ftk_align, with the Step-3 epilogue replaced by
+ *   log_marginal[i][j] = log sum_{t < N_t, r < n_gamma} exp(X_ij(delta_t, gamma_r) / tau)
+ * (uniform weights on the caller's shift list and the rotation grid; add log of the prior weights
+ * outside).  tau > 0 (units of X), finite, else FTK_EINVAL.  log_marginal: device float
+ * [N_im][N_tm_local] (j = local template index; rank r's block starts at its template offset),
+ * caller-allocated, fully overwritten.  Accuracy: |delta L| <= max |delta X| / tau + fp32 rounding.
+ * Tensor-core engine only (FTK_EINVAL on engine 1).  Asynchronous on `stream`.  Errors: FTK_EINVAL,
+ * FTK_ESTATE (missing load / host-only plan), FTK_ECUDA. */
+ftk_status_t ftk_align_marginal(ftk_plan_t plan, double tau, float* log_marginal, void* stream);
+
 /* Full landscapes for selected pairs (sampled parity at large configs).  img_idx / tpl_idx:
  * device int32 [n_pairs] (template index LOCAL to this rank); out: device float [n_pairs][N_t][n_psi]. */
 ftk_status_t ftk_landscape_pairs(ftk_plan_t plan, const int32_t* img_idx, const int32_t* tpl_idx, int n_pairs,

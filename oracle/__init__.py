@@ -13,7 +13,7 @@ Modules
   fb           Fourier-Bessel coefficients by the periodic trapezoid rule   (Eq. aqkcalc)
   kernel_svd   per-ell operator SVD of J_ell(delta k), two discretizations  (Eq. Jsvd, Remark r:svd P:801-811,
                global relabel + eps truncation                               Eqs. svdtrunc/svdobjective P:822-893)
-  ftk          FTK Steps 1-3 literally (Eq. fbk3), cyclic q
+  ftk          FTK Steps 1-3 literally (Eq. fbk3), cyclic q; log-marginal over the grid
   brute        direct evaluation of the discretized bandlimited inner product (Eq. Xdg P:293-298 with Eq. Fdk)
   closed_form  exact (2 pi)^2 <R_gamma T_delta A, B> for Gaussian-blob images (Eq. planch)
   bounds       Lemma 2 / Theorem 1 rank bounds, empirical fit, RMS error bound

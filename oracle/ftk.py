@@ -89,3 +89,19 @@ def ftk_best(a, b, plan: OraclePlan, chunk_i: int = 4, chunk_j: int = 16, n_gamm
                     best_v[i0 + ii] = v[ii]
                     best_idx[i0 + ii] = (j[ii] + j0, t[ii], r[ii])
     return best_v, best_idx
+
+
+def log_marginal(X, tau):
+    """Marginalization over the alignment grid ("sampling this
+    entire landscape is necessary in a Bayesian framework, where an integral of a probability
+    distribution over shifts and angles is used to marginalize the likelihood").  Uniform weights on
+    the shift list and the rotation grid (reading R22):
+        L = log sum_{t, r} exp(Re X(delta_t, gamma_r) / tau)        per (image, template) pair.
+    X [..., N_t, n_gamma] (complex or real); tau > 0.  Evaluated as the textbook log-sum-exp
+    m + log sum exp(X / tau - m) with m the maximum of X / tau (no overflow)."""
+    if not tau > 0:
+        raise ValueError("tau must be positive")
+    R = np.real(np.asarray(X, dtype=np.complex128 if np.iscomplexobj(X) else np.float64)) / tau
+    m = R.max(axis=(-2, -1), keepdims=True)
+    s = np.exp(R - m).sum(axis=(-2, -1), keepdims=True)
+    return (m + np.log(s))[..., 0, 0]

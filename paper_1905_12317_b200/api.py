@@ -155,6 +155,15 @@ class FTKPlan:
                                  _stream_ptr(stream)), self._p)
         return out
 
+    def align_marginal(self, tau: float, stream=None, out=None):
+        """ftk_align_marginal: float32 [N_im, N_tm_local] device tensor of log sum_{t,r} exp(X / tau)."""
+        import torch
+        NI, NJ = self.info["n_images"], self.info["n_templates_local"]
+        res = out if out is not None else torch.empty((NI, NJ), dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(self._L.ftk_align_marginal(self._p, float(tau), C.c_void_p(res.data_ptr()), _stream_ptr(stream)),
+               self._p)
+        return res
+
     def landscape_pairs(self, img_idx, tpl_idx, stream=None):
         import torch
         dev = f"cuda:{self.device}"

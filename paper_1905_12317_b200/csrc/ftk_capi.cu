@@ -524,27 +524,11 @@ static size_t bytes_per_pair(ftk_plan_t plan) {
   return tc_bytes_per_pair(plan->tc, P);
 }
 
-ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best, float* landscape,
-                       int64_t landscape_capacity, void* stream) {
-  if (!plan || !best) return FTK_EINVAL;
-  if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
-  if (!plan->have_images || !plan->have_templates)
-    return fail(plan, FTK_ESTATE, "ftk_align called before ftk_load_images and ftk_load_templates");
-  CK(cudaSetDevice(plan->device));
-  cudaStream_t s = (cudaStream_t)stream;
+// All pair blocks of the (images x local templates) job through run_block (workspace-sized blocks).
+static ftk_status_t run_blocks(ftk_plan_t plan, unsigned long long* img_keys, unsigned long long* pair_keys,
+                               float* landscape, cudaStream_t s) {
   const DevPlan P = devplan(plan);
   const int64_t NI = plan->n_im, NJ = plan->n_tm_local;
-  if (landscape && landscape_capacity < NI * NJ * P.N_t * (int64_t)P.n_gamma)
-    return fail(plan, FTK_ECAPACITY, "landscape buffer too small");
-  if (plan->keys_cap < NI * (pair_best ? NJ + 1 : 1)) {
-    cudaFree(plan->d_keys);
-    plan->d_keys = nullptr;
-    plan->keys_cap = NI * (NJ + 1);
-    CK(cudaMalloc(&plan->d_keys, plan->keys_cap * sizeof(unsigned long long)));
-  }
-  unsigned long long* img_keys = plan->d_keys;
-  unsigned long long* pair_keys = pair_best ? plan->d_keys + NI : nullptr;
-  CK(cudaMemsetAsync(plan->d_keys, 0, NI * (pair_best ? NJ + 1 : 1) * sizeof(unsigned long long), s));
   if (NJ > 0) {
     const size_t per = bytes_per_pair(plan);
     size_t wsb = plan->ws_bytes;
@@ -581,6 +565,34 @@ ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best,
       }
     }
   }
+  return FTK_OK;
+}
+
+ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best, float* landscape,
+                       int64_t landscape_capacity, void* stream) {
+  if (!plan || !best) return FTK_EINVAL;
+  if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
+  if (!plan->have_images || !plan->have_templates)
+    return fail(plan, FTK_ESTATE, "ftk_align called before ftk_load_images and ftk_load_templates");
+  CK(cudaSetDevice(plan->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevPlan P = devplan(plan);
+  const int64_t NI = plan->n_im, NJ = plan->n_tm_local;
+  if (landscape && landscape_capacity < NI * NJ * P.N_t * (int64_t)P.n_gamma)
+    return fail(plan, FTK_ECAPACITY, "landscape buffer too small");
+  if (plan->keys_cap < NI * (pair_best ? NJ + 1 : 1)) {
+    cudaFree(plan->d_keys);
+    plan->d_keys = nullptr;
+    plan->keys_cap = NI * (NJ + 1);
+    CK(cudaMalloc(&plan->d_keys, plan->keys_cap * sizeof(unsigned long long)));
+  }
+  unsigned long long* img_keys = plan->d_keys;
+  unsigned long long* pair_keys = pair_best ? plan->d_keys + NI : nullptr;
+  CK(cudaMemsetAsync(plan->d_keys, 0, NI * (pair_best ? NJ + 1 : 1) * sizeof(unsigned long long), s));
+  {
+    const ftk_status_t st = run_blocks(plan, img_keys, pair_keys, landscape, s);
+    if (st != FTK_OK) return st;
+  }
   const bool host_out = !is_device_ptr(best);
   if (plan->best_tmp_cap < NI) {
     cudaFree(plan->d_best_tmp);
@@ -597,6 +609,26 @@ ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best,
     CK(cudaMemcpyAsync(best, plan->d_best_tmp, NI * sizeof(ftk_best_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
   }
+  return FTK_OK;
+}
+
+ftk_status_t ftk_align_marginal(ftk_plan_t plan, double tau, float* log_marginal, void* stream) {
+  if (!plan || !log_marginal) return FTK_EINVAL;
+  if (!(tau > 0.0) || !std::isfinite(tau)) return fail(plan, FTK_EINVAL, "tau must be positive and finite");
+  if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
+  if (!plan->have_images || !plan->have_templates)
+    return fail(plan, FTK_ESTATE, "ftk_align_marginal called before ftk_load_images and ftk_load_templates");
+  if (plan->engine != 0) return fail(plan, FTK_EINVAL, "the marginalization epilogue runs on the tensor-core engine");
+  if (!is_device_ptr(log_marginal)) return fail(plan, FTK_EINVAL, "log_marginal must be a device pointer");
+  CK(cudaSetDevice(plan->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  plan->tc.marg = log_marginal;
+  plan->tc.marg_scale = (float)(1.4426950408889634 / tau);
+  const ftk_status_t st = run_blocks(plan, nullptr, nullptr, nullptr, s);
+  plan->tc.marg = nullptr;
+  plan->tc.marg_scale = 0.f;
+  if (st != FTK_OK) return st;
+  CK(cudaGetLastError());
   return FTK_OK;
 }
 

@@ -61,8 +61,24 @@ struct S3Params {
   unsigned long long* img_keys;
   unsigned long long* pair_keys;
   float* land;
+  float* marg;     // MODE 1: [N_im][n_tm_local] log sum_{t,r} exp(X / tau)
+  float msc;       // MODE 1: log2(e) / tau
   unsigned long long* trace;  // nullable (FTK_S3_TRACE=1): wait / busy cycle counters of CTA 0
 };
+
+__device__ __forceinline__ float ex2_approx(float x) {  // 2^x, one MUFU op (2^-inf = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// (m, s) pairs of a scaled log-sum-exp in base 2: value = m + log2(s); m = -inf means "empty"
+__device__ __forceinline__ void lse2_merge(float& m, float& s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  if (mn != -INFINITY) {
+    s = s * ex2_approx(m - mn) + s2 * ex2_approx(m2 - mn);
+    m = mn;
+  }
+}
 
 struct S3Smem {
   uint64_t y_bar;
@@ -94,6 +110,11 @@ __device__ __forceinline__ void tc_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
 
+// MODE 0: fused max / argmax (the north-star epilogue).  MODE 1: marginalization epilogue (SURVEY 8(f)
+// NEXT-3; the Bayesian use of the full landscape): per pair
+//   L = log sum_{t, r} exp(X(delta_t, gamma_r) / tau),
+// accumulated per thread as a base-2 running (max, scaled sum) and merged per warp and per pair.
+template <int MODE>
 __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   extern __shared__ __align__(1024) uint8_t s3_raw[];
   S3Smem& S = *reinterpret_cast<S3Smem*>(s3_raw);
@@ -257,6 +278,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
       uint32_t bkf = 0xffffffffu;   // ... and its key (T << 24 | column << 7 | row)
       float bve = -INFINITY;        // exact record (slow groups)
       uint32_t bfe = 0xffffffffu;
+      float mrun = -INFINITY, srun = 0.f;  // MODE 1: running base-2 log-sum-exp of X log2(e) / tau
       float* land_p = P.land ? P.land + (size_t)p * P.N_t * n : nullptr;
       for (int T = 0; T < NRT; ++T) {
         const int r = T * 128 + row;
@@ -304,7 +326,74 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) o2[k] = 0u;
           }
-          if (active) {
+          if (MODE == 1 && active) {
+            // pass 1: the chunk's maximum of X = max(E + O, E - O) = E + |O| over valid columns (the
+            // group test is warp-uniform: fast groups have 8 paired, non-padding columns)
+            float cmk[8];  // per-k partial maxima (short dependency chains)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cmk[k] = -INFINITY;
+#pragma unroll
+            for (int g8 = 0; g8 < 5; ++g8) {
+              if (8 * g8 >= hw) break;
+              const int cl = clb + 8 * g8;
+              float ev[8], ov[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                ev[k] = __uint_as_float(g8 < 2 ? e0[8 * g8 + k] : (g8 < 4 ? e1[8 * (g8 - 2) + k] : e2[k]));
+                ov[k] = __uint_as_float(g8 < 2 ? o0[8 * g8 + k] : (g8 < 4 ? o1[8 * (g8 - 2) + k] : o2[k]));
+              }
+              if (s_fast[cl >> 3]) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) cmk[k] = fmaxf(cmk[k], ev[k] + fabsf(ov[k]));
+              } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  if (s_rep[cl + k] >= 0) cmk[k] = fmaxf(cmk[k], ev[k] + ov[k]);
+                  if (s_part[cl + k] >= 0) cmk[k] = fmaxf(cmk[k], ev[k] - ov[k]);
+                }
+              }
+            }
+            float cm = fmaxf(fmaxf(fmaxf(cmk[0], cmk[1]), fmaxf(cmk[2], cmk[3])),
+                             fmaxf(fmaxf(cmk[4], cmk[5]), fmaxf(cmk[6], cmk[7])));
+            if (cm != -INFINITY) {
+              cm *= P.msc;
+              if (cm > mrun) {
+                srun *= ex2_approx(mrun - cm);
+                mrun = cm;
+              }
+              // pass 2: sum of 2^(X log2(e) / tau - m) over both signs of delta (per-k partial sums)
+              float sk[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) sk[k] = 0.f;
+              const float nm = -mrun, sc = P.msc;
+#pragma unroll
+              for (int g8 = 0; g8 < 5; ++g8) {
+                if (8 * g8 >= hw) break;
+                const int cl = clb + 8 * g8;
+                float ev[8], ov[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  ev[k] = __uint_as_float(g8 < 2 ? e0[8 * g8 + k] : (g8 < 4 ? e1[8 * (g8 - 2) + k] : e2[k]));
+                  ov[k] = __uint_as_float(g8 < 2 ? o0[8 * g8 + k] : (g8 < 4 ? o1[8 * (g8 - 2) + k] : o2[k]));
+                }
+                if (s_fast[cl >> 3]) {
+#pragma unroll
+                  for (int k = 0; k < 8; ++k) {
+                    // X(+delta) log2(e) / tau - m and X(-delta) log2(e) / tau - m
+                    sk[k] += ex2_approx(fmaf(ev[k] + ov[k], sc, nm)) + ex2_approx(fmaf(ev[k] - ov[k], sc, nm));
+                  }
+                } else {
+#pragma unroll
+                  for (int k = 0; k < 8; ++k) {
+                    if (s_rep[cl + k] >= 0) sk[k] += ex2_approx(fmaf(ev[k] + ov[k], sc, nm));   // else padding
+                    if (s_part[cl + k] >= 0) sk[k] += ex2_approx(fmaf(ev[k] - ov[k], sc, nm));  // else no -delta
+                  }
+                }
+              }
+              srun += ((sk[0] + sk[1]) + (sk[2] + sk[3])) + ((sk[4] + sk[5]) + (sk[6] + sk[7]));
+            }
+          }
+          if (MODE == 0 && active) {
             const uint32_t kb = ((uint32_t)T << 24) | ((uint32_t)clb << 7) | (uint32_t)row;
 #pragma unroll
             for (int g8 = 0; g8 < 5; ++g8) {
@@ -354,8 +443,19 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         }
       }
       // per-pair reduction over the warp; the resolver merges the 8 warps' records
+      if (MODE == 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float m2 = __shfl_xor_sync(0xffffffffu, mrun, o);
+          const float s2 = __shfl_xor_sync(0xffffffffu, srun, o);
+          lse2_merge(mrun, srun, m2, s2);
+        }
+        bvf = mrun;
+        bve = srun;
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
+        if (MODE == 1) break;
         const float v2 = __shfl_xor_sync(0xffffffffu, bvf, o);
         const uint32_t k2 = __shfl_xor_sync(0xffffffffu, bkf, o);
         if (better(v2, k2, bvf, bkf)) {
@@ -392,6 +492,19 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
     for (int p = p_begin; p < p_end; ++p, ++it) {
       const int rb = it & 1;
       mbar_wait_lazy(&S.red_full[rb], (it >> 1) & 1, 200);
+      if (MODE == 1) {
+        float m = S.red_v[rb][0], sm = S.red_ve[rb][0];
+        for (int w = 1; w < 8; ++w) lse2_merge(m, sm, S.red_v[rb][w], S.red_ve[rb][w]);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&S.red_empty[rb]);
+          int i, j;
+          pair_of(P.pb, p, i, j);
+          P.marg[(size_t)i * P.n_tm_local + j] = (m + log2f(sm)) * 0.6931471805599453f;
+        }
+        __syncwarp();
+        continue;
+      }
       float v = S.red_v[rb][0], ve = S.red_ve[rb][0];
       uint32_t key = S.red_k[rb][0], fe = S.red_fe[rb][0];
       for (int w = 1; w < 8; ++w) {
@@ -1414,7 +1527,8 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   cudaMemcpy(tc.d_colfast, colfast.data(), colfast.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(tc.d_Ysm, yimg.data(), yimg.size() * 2, cudaMemcpyHostToDevice);
   tc.s3_smem = s3_smem_bytes(ncol_g, K3p, tc.NS);
-  cudaFuncSetAttribute(k_step3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.s3_smem);
+  cudaFuncSetAttribute(k_step3_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.s3_smem);
+  cudaFuncSetAttribute(k_step3_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.s3_smem);
   if (pm.n_k % 16 != 0 || pm.n_k > 128) {
     msg = "tensor-core engine: n_k must be a multiple of 16 and <= 128";
     return FTK_EINVAL;
@@ -1602,7 +1716,12 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
     cudaMemsetAsync(d_trace, 0, 16 * sizeof(unsigned long long), s);
     prm.trace = d_trace;
   }
-  k_step3_tc<<<cpg * tc.G, S3_THREADS, tc.s3_smem, s>>>(prm);
+  prm.marg = tc.marg;
+  prm.msc = tc.marg_scale;
+  if (tc.marg)
+    k_step3_tc<1><<<cpg * tc.G, S3_THREADS, tc.s3_smem, s>>>(prm);
+  else
+    k_step3_tc<0><<<cpg * tc.G, S3_THREADS, tc.s3_smem, s>>>(prm);
   if (prm.trace) {
     unsigned long long h[16];
     cudaMemcpyAsync(h, d_trace, sizeof h, cudaMemcpyDeviceToHost, s);

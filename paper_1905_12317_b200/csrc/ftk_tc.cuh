@@ -38,7 +38,12 @@ struct TcPlan {
   float2* d_s2tw = nullptr;  // Step-2 four-step twiddle tables
   int64_t n_tm = 0;
   int num_sms = 148;
-  bool sync_debug = false;  // FTK_SYNC_DEBUG=1: synchronize after each step (fault attribution)
+  bool sync_debug = false;
+  // Step-3 epilogue of the next tc_run_block calls: marg == nullptr -> max / argmax (MODE 0); else the
+  // marginalization epilogue (MODE 1) writes log sum exp(X / tau) per pair to marg[i][j], marg_scale =
+  // log2(e) / tau
+  float* marg = nullptr;
+  float marg_scale = 0.f;  // FTK_SYNC_DEBUG=1: synchronize after each step (fault attribution)
 };
 
 typedef void (*prof_cb_t)(void* plan, int cls, int end, cudaStream_t s);

@@ -250,3 +250,88 @@ def test_n_gamma_option_errors(pkg):
         with pytest.raises(pkg.FTKError):
             make(pkg, cfg, engine, n_gamma=ng)
 
+
+
+# ---------------------------------------------------------------- marginalization epilogue (NEXT-3, R22)
+def _marg_check(Lg, X, na, nb, tau):
+    """|L_gpu - L_oracle| <= max |dX| / tau + fp32 rounding, max |dX| <= 1e-4 ||A|| ||B|| (north star)."""
+    Lo = ftk.log_marginal(X, tau)
+    tol = TOL * na[:, None] * nb[None, :] / tau + 1e-5 * np.maximum(1.0, np.abs(Lo))
+    err = np.abs(Lg - Lo)
+    assert np.all(err <= tol), (err.max(), (err / tol).max())
+
+
+@pytest.mark.parametrize("name,ni,nj,shift_filter,mult", [
+    ("tiny", 4, 4, None, 1),
+    ("tiny", 3, 5, "half", 1),     # shifts without a -delta partner + padding columns: the exact path
+    ("tiny", 2, 3, None, 2),       # n_gamma = 2 n_psi (reading R21)
+    ("c2", 6, 40, None, 1),
+    ("c3", 3, 20, None, 1),
+])
+def test_marginal_vs_oracle(pkg, name, ni, nj, shift_filter, mult):
+    cfg = synth.config(name)
+    sh = synth.shift_list(cfg)
+    if shift_filter == "half":
+        sh = sh[sh[:, 1] >= -0.25]
+    ng = mult * cfg.n_psi
+    p = pkg.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), sh, cfg.eps, n_k=cfg.n_k, n_psi=cfg.n_psi, device=0,
+                    n_gamma=ng if mult > 1 else 0)
+    k, w = p.radial()
+    imgs, _ = synth.draw_items(cfg, "images", range(ni), k)
+    tpls, _ = synth.draw_items(cfg, "templates", range(nj), k)
+    p.load_images(torch.from_numpy(imgs).cuda())
+    p.load_templates(torch.from_numpy(tpls).cuda())
+    oplan = ks.build_plan(cfg.n, cfg.K, synth.delta_max(cfg), sh, cfg.eps, cfg.n_k, cfg.n_psi, n_nodes=96) \
+        if shift_filter else oracle_plan(cfg)
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), oplan, n_gamma=ng))
+    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+    scale = float(np.median(na[:, None] * nb[None, :]))
+    for f in (0.01, 0.1, 1.0):
+        tau = f * scale
+        Lg = p.align_marginal(tau).cpu().numpy()
+        assert Lg.shape == (ni, nj)
+        _marg_check(Lg, X, na, nb, tau)
+    # the max / argmax epilogue is unaffected by a preceding marginal call
+    check_best(pkg.best_to_numpy(p.align()["best"]), X, na, nb)
+
+
+def test_marginal_full_size_sampled(pkg):
+    """c5 sizes (256 images x 512 templates, the bench's Step-3 launch shape): sampled pairs vs the oracle."""
+    cfg = synth.config("c5")
+    p = make(pkg, cfg, 0)
+    k, w = p.radial()
+    ni, nj = 256, 512
+    imgs, _ = synth.draw_items(cfg, "images", range(ni), k, backend="torch", device="cuda")
+    tpls, _ = synth.draw_items(cfg, "templates", range(nj), k, backend="torch", device="cuda")
+    p.load_images(imgs)
+    p.load_templates(tpls)
+    ii, jj = np.array([0, 255, 17]), np.array([511, 0, 300])
+    xs = imgs[torch.as_tensor(ii, device="cuda")].cpu().numpy()
+    ys = tpls[torch.as_tensor(jj, device="cuda")].cpu().numpy()
+    na, nb = fb.discrete_norm(xs, w), fb.discrete_norm(ys, w)
+    tau = 0.05 * float(np.median(na * nb))
+    Lg = p.align_marginal(tau).cpu().numpy()
+    assert np.all(np.isfinite(Lg))
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(xs), fb.fb_coeffs(ys), oracle_plan(cfg)))
+    for n in range(3):
+        Lo = ftk.log_marginal(X[n, n], tau)
+        assert abs(Lg[ii[n], jj[n]] - Lo) <= TOL * na[n] * nb[n] / tau + 1e-5 * max(1.0, abs(Lo))
+
+
+def test_marginal_errors(pkg):
+    cfg = synth.config("tiny")
+    p = make(pkg, cfg, 0)
+    k, _ = p.radial()
+    x, _ = synth.draw_items(cfg, "images", range(2), k)
+    with pytest.raises(pkg.FTKError):          # before the loads
+        p.align_marginal(1.0)
+    p.load_images(torch.from_numpy(x).cuda())
+    p.load_templates(torch.from_numpy(x).cuda())
+    for bad in (0.0, -1.0, float("inf"), float("nan")):
+        with pytest.raises(pkg.FTKError):
+            p.align_marginal(bad)
+    ps = make(pkg, cfg, 1)
+    ps.load_images(torch.from_numpy(x).cuda())
+    ps.load_templates(torch.from_numpy(x).cuda())
+    with pytest.raises(pkg.FTKError):          # SIMT engine: max / argmax only
+        ps.align_marginal(1.0)

@@ -245,3 +245,62 @@ def test_n_gamma_planted_off_grid_rotation_recovered():
     X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(x), fb.fb_coeffs(y), plan, n_gamma=ng))[0, 0]
     t0 = int(np.argmin(np.sum(plan.shifts ** 2, axis=1)))     # delta = 0
     assert int(np.argmax(X[t0])) == (ng - r0) % ng
+
+
+# ---------------------------------------------------------------- marginalization (NEXT-3, reading R22)
+def test_log_marginal_closed_forms():
+    """log sum_{t,r} exp(X / tau) against closed forms: a constant landscape gives c / tau + log(N_t n_gamma);
+    a two-level landscape (k cells at c1, scattered over both axes) gives log(k e^{c1/tau} + (N - k) e^{c2/tau});
+    no overflow at X / tau = 1000; Jensen / Hoeffding bounds log N + mean / tau <= L <= that + (max - min)^2 / 8 tau^2;
+    and the tau -> 0 limit tau L -> max X within tau log N."""
+    rng = np.random.default_rng(5)
+    shape = (3, 2, 49, 64)
+    N = 49 * 64
+    c = rng.normal(size=(3, 2))
+    X = np.broadcast_to(c[:, :, None, None], shape).copy()
+    for tau in (0.01, 0.3, 7.0):
+        L = ftk.log_marginal(X, tau)
+        assert L.shape == (3, 2)
+        assert np.allclose(L, c / tau + math.log(N), rtol=0, atol=1e-12 * (1 + np.abs(c).max() / tau))
+    X2 = np.full((49, 64), -0.4)
+    cells = rng.choice(N, size=37, replace=False)
+    X2.reshape(-1)[cells] = 0.9
+    for tau in (0.05, 1.0):
+        want = math.log(37 * math.exp(0.9 / tau) + (N - 37) * math.exp(-0.4 / tau))
+        assert abs(ftk.log_marginal(X2, tau) - want) < 1e-12 * abs(want)
+    assert abs(ftk.log_marginal(np.full((7, 8), 1000.0), 1.0) - (1000.0 + math.log(56))) < 1e-9
+    Xr = rng.normal(size=(49, 64))
+    for tau in (0.5, 3.0, 40.0):
+        L = ftk.log_marginal(Xr, tau)
+        lo = math.log(N) + Xr.mean() / tau
+        assert lo - 1e-12 <= L <= lo + (Xr.max() - Xr.min()) ** 2 / (8 * tau * tau) + 1e-12
+    for tau in (1e-2, 1e-3):
+        assert Xr.max() <= tau * ftk.log_marginal(Xr, tau) <= Xr.max() + tau * math.log(N) + 1e-12
+    # complex input: the real part is used (Re X, P:838)
+    assert abs(ftk.log_marginal(X2 + 1j, 1.0) - ftk.log_marginal(X2, 1.0)) < 1e-14
+
+
+def test_log_marginal_through_ftk(tiny):
+    """Through the FTK landscapes: a zero image gives log(N_t n_psi) exactly; rotating the template by a
+    grid angle leaves L unchanged (X'(t, r) = X(t, r - j) permutes the grid); and L of the FTK landscape
+    is within max |X_FTK - X_exact| / tau of L of the exact Gaussian landscape (closed form, Eq. planch
+    P:207-212; log-sum-exp is 1-Lipschitz in the sup norm)."""
+    cfg, plan, imgs, tpls, pi, pt = tiny
+    b = fb.fb_coeffs(tpls[:2])
+    X0 = ftk.ftk_landscapes(np.zeros_like(fb.fb_coeffs(imgs[:1])), b, plan)
+    assert np.allclose(ftk.log_marginal(X0, 0.1), math.log(len(plan.shifts) * cfg.n_psi), rtol=0, atol=1e-12)
+    a = fb.fb_coeffs(imgs[:1])
+    b_rot = fb.fb_coeffs(np.roll(tpls[:1], 9, axis=-1))
+    L1 = ftk.log_marginal(ftk.ftk_landscapes(a, b[:1], plan), 0.05)
+    L2 = ftk.log_marginal(ftk.ftk_landscapes(a, b_rot, plan), 0.05)
+    assert abs(L1 - L2) < 1e-10 * abs(L1)
+    i, j = 1, 3
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs[i:i + 1]), fb.fb_coeffs(tpls[j:j + 1]), plan))[0, 0]
+    Xc = np.array([[closed_form.gaussian_ip(pi, pt, i, j, plan.shifts[t], 2 * math.pi * r / cfg.n_psi)
+                    for r in range(cfg.n_psi)] for t in range(len(plan.shifts))])
+    dmax = np.max(np.abs(X - Xc))
+    na, nb = fb.discrete_norm(imgs, plan.w), fb.discrete_norm(tpls, plan.w)
+    assert dmax < 3e-3 * na[i] * nb[j]
+    for tau in (0.02, 0.2, 2.0):
+        tau_abs = tau * na[i] * nb[j]
+        assert abs(ftk.log_marginal(X, tau_abs) - ftk.log_marginal(Xc, tau_abs)) <= dmax / tau_abs + 1e-12
