@@ -1187,24 +1187,30 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
       }
     }
     __syncthreads();
-    // ---- write out the block's word groups as core-matrix rows; words no term writes are zero
+    // ---- write out the block's word groups as core-matrix rows; words no term writes are zero.
+    //      Thread = (row, part): per (group, r-tile) one 16-byte store; 8-row runs are contiguous 128 B.
     {
       const int ng = B.ng[b];
       const uint32_t used = (uint32_t)B.used[b];  // bit grp * 4 + w
-      uint8_t* base = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)g0 * 128;
-      for (int idx = threadIdx.x; idx < ng * NRT * 2 * 128; idx += blockDim.x) {
-        const int row = idx & 127, rest = idx >> 7;
-        const int part = rest & 1, T = (rest >> 1) % NRT, grp = (rest >> 1) / NRT;
-        const int r = T * 128 + row;
-        uint32_t v4[4] = {0u, 0u, 0u, 0u};
-        if (r < n) {
-          const int pi = r + r / E;
-          const uint32_t* sp = stg + (size_t)((grp * 2 + part) * 4) * RS + pi;
+      const int row = threadIdx.x & 127, part = threadIdx.x >> 7;
+      uint8_t* dst = Zop + (size_t)pr * NRT * 128 * P.K3p * 4 + (size_t)g0 * 128 + (size_t)part * NWG * 2048 +
+                     (size_t)(row >> 3) * NWG * 128 + (row & 7) * 16;
+      for (int grp = 0; grp < ng; ++grp) {
+        const uint32_t um = used >> (grp * 4);
+        const uint32_t* sp = stg + (size_t)((grp * 2 + part) * 4) * RS;
 #pragma unroll
-          for (int w = 0; w < 4; ++w) v4[w] = ((used >> (grp * 4 + w)) & 1) ? sp[w * RS] : 0u;
+        for (int T = 0; T < (n + 127) / 128; ++T) {
+          const int r = T * 128 + row;
+          uint4 v = make_uint4(0u, 0u, 0u, 0u);
+          if (r < n) {
+            const int pi = r + r / E;
+            v.x = (um & 1u) ? sp[pi] : 0u;
+            v.y = (um & 2u) ? sp[RS + pi] : 0u;
+            v.z = (um & 4u) ? sp[2 * RS + pi] : 0u;
+            v.w = (um & 8u) ? sp[3 * RS + pi] : 0u;
+          }
+          *reinterpret_cast<uint4*>(dst + (size_t)T * 2 * NWG * 2048 + (size_t)grp * 128) = v;
         }
-        *reinterpret_cast<uint4*>(base + (size_t)((T * 2 + part) * NWG) * 2048 + (size_t)(row >> 3) * NWG * 128 +
-                                  (size_t)grp * 128 + (row & 7) * 16) = make_uint4(v4[0], v4[1], v4[2], v4[3]);
       }
     }
     __syncthreads();  // the staging area becomes transpose scratch again
