@@ -226,7 +226,8 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
   // columns: one per ell = 0 term; (Re, Im) pairs of the even ell > 0 terms on even columns; the odd-ell
   // pairs from column Ke (a multiple of 16).  Every group of 8 columns holds whole terms (Step 2 writes
   // column groups) and Y_zeta(-delta) = (-1)^ell Y_zeta(delta) splits X(+-delta) = E(delta) +- O(delta)
-  // between the two blocks (the tensor-core Step 3 evaluates half of a symmetric shift list).
+  // between the two blocks (the tensor-core Step 3 evaluates half of a symmetric shift list).  The
+  // tensor-core engine then moves whole Step-2 blocks (tc_term_order) so that each fits one TMA window.
   std::vector<int> zplus;
   for (int pass = 0; pass < 3; ++pass)
     for (int z = 0; z < pm.H; ++z) {
@@ -258,6 +259,25 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
       }
     }
     c += (l == 0) ? 1 : 2;
+  }
+  if (plan->engine == 0) {  // tensor-core engine: term order with every Step-2 block in one TMA window
+    std::string msg;
+    std::vector<int> perm;
+    if (tc_term_order(ell, col, plan->K3p, perm, msg) != FTK_OK) {
+      plan->err = msg;
+      fprintf(stderr, "ftk_plan_create: %s\n", msg.c_str());
+      return bail(FTK_EINVAL);
+    }
+    std::vector<int> ell2, col2;
+    std::vector<float> g2;
+    for (int z : perm) {
+      ell2.push_back(ell[z]);
+      col2.push_back(col[z]);
+      g2.insert(g2.end(), g.begin() + (size_t)z * pm.n_k, g.begin() + (size_t)(z + 1) * pm.n_k);
+    }
+    ell.swap(ell2);
+    col.swap(col2);
+    g.swap(g2);
   }
   std::vector<int> pads;
   for (int k = 0; k < plan->K3p; ++k)

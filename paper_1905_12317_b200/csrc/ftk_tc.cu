@@ -917,13 +917,7 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 //   DIF across the warp with shfl_xor (output index d lands on lane bitrev5(d)).
 // Output words are staged per (group, part, word) in padded rows (index r + r / E: conflict-free) and
 // written out as contiguous 2 KB row blocks.
-struct S2Blocks {      // Step-2 work blocks: 1 or 2 consecutive word groups holding <= 8 terms
-  int nb;
-  int zs[16], ze[16];  // term range of block b
-  int g0[16], ng[16];  // first word group, number of groups
-  int used[16];        // words (bit grp * 4 + w) written by some term
-  int lone[16];        // terms (bit z - zs) with ell = 0 and no neighbour in their word
-};
+using S2Blocks = S2BlockTable;
 // Step-2 row buffer: [p][8 terms] complex (64-byte rows) in the TMA SWIZZLE_64B layout: the 16-byte
 // chunk c of row p sits at chunk c ^ ((p >> 1) & 3), which makes the warps' column reads conflict-free.
 constexpr int S2_SMAX = 8;
@@ -998,7 +992,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int E>
-__global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
+__global__ void __launch_bounds__(256, 3) k_step2_fft(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
                                                       int npair, int formB, DevPlan P, S2Blocks B,
                                                       const float2* __restrict__ twtab,
                                                       const __grid_constant__ CUtensorMap zmap) {
@@ -1007,9 +1001,9 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
   constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
   constexpr int RS = n + n / E;  // padded staging row (words): index r + r / E
   const int n_in = P.n_psi;     // input rows (cyclic q)
-  // [rows: 2 x n_in x S2_SMAX complex][stg: 16 x RS words; also the warps' n-slot transpose scratch][mbarrier]
+  // [rows: n_in x S2_SMAX complex][stg: 16 x RS words; also the warps' n-slot transpose scratch][mbarrier]
   float2* rows = reinterpret_cast<float2*>(s2raw);
-  const size_t rows_bytes = (size_t)2 * n_in * S2_SMAX * 8;
+  const size_t rows_bytes = (size_t)n_in * S2_SMAX * 8;
   uint32_t* stg = reinterpret_cast<uint32_t*>(s2raw + rows_bytes);
   uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 16 * RS);
   // warp index made provably warp-uniform (shfl from lane 0) so the shuffles below sit in convergent code
@@ -1047,21 +1041,19 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
   const int per = (total + gridDim.x - 1) / gridDim.x;
   const int i_beg = blockIdx.x * per;
   const int i_end = min(total, i_beg + per);
-  // Form B input: the block's term columns of the pair's n_psi rows of Zhat' [pair][p][Hs] as 2-D TMA
-  // boxes (8 x 256, zero fill beyond Hs) into the swizzled [p][8] row buffers.  A box must start on a
-  // 16-byte boundary (an odd 8-byte column start faults), so the window starts at the even column
-  // zs & ~1 and takes a second 8-column box when the block's terms reach past it.  Form A (explicit
-  // pairs, Zhat [pair][zeta][q]): cp.async gather into the same layout
+  // Form B input: the aligned 8-term window [zs & ~1, +8) holding the block's terms, for the pair's n_psi
+  // rows of Zhat' [pair][p][Hs], as 2-D TMA boxes (8 x 256, zero fill beyond Hs) into the swizzled [p][8]
+  // row buffer.  A box must start on a 16-byte boundary (an odd 8-byte column start faults); the device
+  // term order (tc_term_order) puts every block inside one such window.  Form A (explicit pairs,
+  // Zhat [pair][zeta][q]): cp.async gather into the same layout
   auto issue = [&](int it) {
     const int bi = it % B.nb, pi2 = it / B.nb;
     if (formB) {
       if (threadIdx.x == 0) {
         const int box = n_in < 256 ? n_in : 256;
-        const int x0 = B.zs[bi] & ~1, nbox = (B.ze[bi] - x0 > 8) ? 2 : 1;
-        mbar_arrive_expect_tx(bar, (uint32_t)(n_in * 64 * nbox));
-        for (int h = 0; h < nbox; ++h)
-          for (int k = 0; k < n_in; k += box)
-            tma_load_2d(s2raw + (size_t)(h * n_in + k) * 64, &zmap, x0 + 8 * h, pi2 * n_in + k, bar);
+        mbar_arrive_expect_tx(bar, (uint32_t)n_in * 64u);
+        for (int k = 0; k < n_in; k += box)
+          tma_load_2d(s2raw + (size_t)k * 64, &zmap, B.zs[bi] & ~1, pi2 * n_in + k, bar);
       }
     } else {
       const int zs = B.zs[bi], nz = B.ze[bi] - zs;
@@ -1098,8 +1090,7 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
       l = P.ell[z];
       col = P.col[z];
       const int e = formB ? (zs & 1) + zz : zz;  // window column of this term
-      const float2* rb = rows + (size_t)(e >> 3) * n_in * S2_SMAX;
-      auto at = [&](int p) { return rb[s2_slot(p, e & 7)]; };
+      auto at = [&](int p) { return rows[s2_slot(p, e)]; };
       // Form B: Z(r) w^{ell r} = DFT of the cyclically shifted row Zhat'(q - ell) (reading R5)
       if (n_in == n) {
         const int q0 = formB ? ((lane - l) & (n - 1)) : lane;
@@ -1219,7 +1210,7 @@ __global__ void __launch_bounds__(256, 2) k_step2_fft(const float2* __restrict__
 
 static size_t step2_smem(int n_in, int n) {  // n_in = n_psi input rows, n = n_gamma >= n_in FFT length
   const int E = n / 32;
-  return (size_t)2 * n_in * S2_SMAX * 8 + (size_t)16 * (n + n / E) * 4 + 16;
+  return (size_t)n_in * S2_SMAX * 8 + (size_t)16 * (n + n / E) * 4 + 16;
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1238,7 +1229,6 @@ static PFN_encodeTiled get_encode_tiled() {
   return fn;
 }
 
-static_assert(sizeof(S2Blocks) == sizeof(TcPlan::s2_blocks), "S2Blocks must mirror TcPlan::s2_blocks");
 
 // Zhat' [pair][p][Hs] as a 2-D tensor of 8-byte elements (rows = pair * n_psi + p), 8 x 256 boxes,
 // 64-byte swizzle (the layout s2_slot() reads)
@@ -1268,7 +1258,16 @@ static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, 
             B.nb * npair < 2 * tc.num_sms ? B.nb * npair : 2 * tc.num_sms);
   const size_t smem = step2_smem(P.n_psi, P.n_gamma);
   const int items = B.nb * npair;
-  dim3 grid(items < 2 * tc.num_sms ? items : 2 * tc.num_sms);
+  int occ = 2;  // resident CTAs per SM (registers <= 80 at E <= 16; shared memory decides)
+  switch (P.n_gamma) {
+    case 64: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2_fft<2>, 256, smem); break;
+    case 128: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2_fft<4>, 256, smem); break;
+    case 256: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2_fft<8>, 256, smem); break;
+    case 512: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2_fft<16>, 256, smem); break;
+    default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2_fft<32>, 256, smem); break;
+  }
+  occ = std::max(1, std::min(occ, 4));
+  dim3 grid(items < occ * tc.num_sms ? items : occ * tc.num_sms);
   switch (P.n_gamma) {
     case 64: k_step2_fft<2><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
     case 128: k_step2_fft<4><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
@@ -1411,6 +1410,100 @@ int tc_selftest(double* err_ts, double* err_ss, std::string& msg) {
 }
 
 // ---------------------------------------------------------------- engine plumbing
+// Step-2 work blocks: 1 or 2 consecutive word groups (8 Step-3 columns each) holding <= 8 whole terms,
+// each a contiguous range of the device term order.
+int s2_block_table(const std::vector<int>& ell, const std::vector<int>& col, int K3p, S2BlockTable& t,
+                   std::string& msg) {
+  std::memset(&t, 0, sizeof t);
+  const int ngroups = K3p / 8;
+  std::vector<int> tg(ngroups, 0);
+  for (int z = 0; z < (int)col.size(); ++z) {
+    tg[col[z] / 8]++;
+    if (ell[z] > 0 && (col[z] & 1)) {
+      msg = "tensor-core engine: an ell > 0 term on an odd column";
+      return FTK_EINVAL;
+    }
+  }
+  int nb = 0;
+  for (int g = 0; g < ngroups;) {
+    const int ng = (g + 1 < ngroups && tg[g] + tg[g + 1] <= 8) ? 2 : 1;
+    if (nb >= 16 || tg[g] > 8) {
+      msg = "tensor-core engine: unsupported Step-2 block structure";
+      return FTK_EINVAL;
+    }
+    int zs = -1, ze = -1;
+    for (int z = 0; z < (int)col.size(); ++z)
+      if (col[z] / 8 >= g && col[z] / 8 < g + ng) {
+        if (zs < 0) zs = z;
+        if (ze >= 0 && z != ze) {
+          msg = "tensor-core engine: Step-2 block terms not contiguous";
+          return FTK_EINVAL;
+        }
+        ze = z + 1;
+      }
+    if (zs < 0) zs = ze = 0;
+    int used = 0, lone = 0;
+    for (int z = zs; z < ze; ++z) {
+      const int kl = col[z] - 8 * g;
+      used |= 1 << (kl >> 1);
+      if (ell[z] == 0) {
+        bool nbr = false;
+        for (int z2 = zs; z2 < ze; ++z2) nbr = nbr || (z2 != z && ell[z2] == 0 && col[z2] == (col[z] ^ 1));
+        if (!nbr) lone |= 1 << (z - zs);
+      }
+    }
+    t.zs[nb] = zs;
+    t.ze[nb] = ze;
+    t.g0[nb] = g;
+    t.ng[nb] = ng;
+    t.used[nb] = used;
+    t.lone[nb] = lone;
+    ++nb;
+    g += ng;
+  }
+  t.nb = nb;
+  return FTK_OK;
+}
+
+// Device term order for the tensor-core engine: the blocks of s2_block_table moved as units so that each
+// lies in one aligned 8-term window [zs & ~1, (zs & ~1) + 8) of a Zhat' row (a 2-D TMA box must start on a
+// 16-byte boundary), i.e. a block starting at an odd term index holds <= 7 terms.  Greedy in block order
+// (Step 1 writes runs of consecutive terms: the closer to the column order, the fewer split runs), taking
+// the first remaining block that fits the current parity; if that gets stuck, even-sized blocks first,
+// then the odd ones (alternating parities, <= 7 terms each).  perm[new z] = old z.
+int tc_term_order(const std::vector<int>& ell, const std::vector<int>& col, int K3p, std::vector<int>& perm,
+                  std::string& msg) {
+  S2BlockTable t;
+  if (s2_block_table(ell, col, K3p, t, msg) != FTK_OK) return FTK_EINVAL;
+  const int nb = t.nb;
+  std::vector<int> order;
+  std::vector<bool> done(nb, false);
+  int S = 0;
+  for (int k = 0; k < nb; ++k) {
+    int pick = -1;
+    for (int bi = 0; bi < nb && pick < 0; ++bi)
+      if (!done[bi] && (!(S & 1) || t.ze[bi] - t.zs[bi] <= 7)) pick = bi;
+    if (pick < 0) break;
+    done[pick] = true;
+    order.push_back(pick);
+    S += t.ze[pick] - t.zs[pick];
+  }
+  if ((int)order.size() < nb) {
+    order.clear();
+    for (int pass = 0; pass < 2; ++pass)
+      for (int bi = 0; bi < nb; ++bi)
+        if (((t.ze[bi] - t.zs[bi]) & 1) == pass) order.push_back(bi);
+  }
+  perm.clear();
+  for (int bi : order)
+    for (int z = t.zs[bi]; z < t.ze[bi]; ++z) perm.push_back(z);
+  if (perm.size() != col.size()) {
+    msg = "tensor-core engine: Step-2 blocks do not cover the terms";
+    return FTK_EINVAL;
+  }
+  return FTK_OK;
+}
+
 int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, const std::vector<int>& ell,
                  const std::vector<int>& col, const std::vector<float>& Y3, int K3p, int Ke, int n_gamma,
                  std::string& msg) {
@@ -1542,58 +1635,15 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   tc.KCH = (2 * pm.n_k) % 64 == 0 ? 64 : 32;
   tc.NKCH = 2 * pm.n_k / tc.KCH;
   cudaFuncSetAttribute(k_step1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
-  // Step-2 blocks: 1 or 2 consecutive word groups (8 Step-3 columns each) holding <= 8 whole terms; the
-  // device term order makes the terms of consecutive columns consecutive (column map in ftk_capi.cu).
+  // Step-2 blocks (s2_block_table); the device term order (tc_term_order, applied in ftk_capi.cu) puts
+  // every block's terms in one aligned 8-term window of a Zhat' row (one TMA box)
   {
-    std::memset(&tc.s2_blocks, 0, sizeof tc.s2_blocks);
-    const int ngroups = K3p / 8;
-    std::vector<int> tg(ngroups, 0);
-    for (int z = 0; z < (int)col.size(); ++z) {
-      tg[col[z] / 8]++;
-      if (ell[z] > 0 && (col[z] & 1)) {
-        msg = "tensor-core engine: an ell > 0 term on an odd column";
+    if (s2_block_table(ell, col, K3p, tc.s2_blocks, msg) != FTK_OK) return FTK_EINVAL;
+    for (int bi = 0; bi < tc.s2_blocks.nb; ++bi)
+      if ((tc.s2_blocks.zs[bi] & 1) + tc.s2_blocks.ze[bi] - tc.s2_blocks.zs[bi] > 8) {
+        msg = "tensor-core engine: a Step-2 block does not fit its 8-term window (term order)";
         return FTK_EINVAL;
       }
-    }
-    int nb = 0;
-    for (int g = 0; g < ngroups;) {
-      const int ng = (g + 1 < ngroups && tg[g] + tg[g + 1] <= 8) ? 2 : 1;
-      if (nb >= 16 || tg[g] > 8) {
-        msg = "tensor-core engine: unsupported Step-2 block structure";
-        return FTK_EINVAL;
-      }
-      int zs = -1, ze = -1;
-      for (int z = 0; z < (int)col.size(); ++z)
-        if (col[z] / 8 >= g && col[z] / 8 < g + ng) {
-          if (zs < 0) zs = z;
-          if (ze >= 0 && z != ze) {
-            msg = "tensor-core engine: Step-2 block terms not contiguous";
-            return FTK_EINVAL;
-          }
-          ze = z + 1;
-        }
-      if (zs < 0) zs = ze = 0;
-      const int nz = ze - zs;
-      int used = 0, lone = 0;
-      for (int z = zs; z < ze; ++z) {
-        const int kl = col[z] - 8 * g;
-        used |= 1 << (kl >> 1);
-        if (ell[z] == 0) {
-          bool nbr = false;
-          for (int z2 = zs; z2 < ze; ++z2) nbr = nbr || (z2 != z && ell[z2] == 0 && col[z2] == (col[z] ^ 1));
-          if (!nbr) lone |= 1 << (z - zs);
-        }
-      }
-      tc.s2_blocks.zs[nb] = zs;
-      tc.s2_blocks.ze[nb] = ze;
-      tc.s2_blocks.g0[nb] = g;
-      tc.s2_blocks.ng[nb] = ng;
-      tc.s2_blocks.used[nb] = used;
-      tc.s2_blocks.lone[nb] = lone;
-      ++nb;
-      g += ng;
-    }
-    tc.s2_blocks.nb = nb;
     {  // Step-2 twiddle tables: [c][a] w_n^{a c} and [d'][a] w_32^{(a % L) d'}, E = n / 32, L = 32 / E
       const int n = n_gamma, E = n / 32, L = 32 / E;
       std::vector<float2> tw((size_t)2 * E * 32);
@@ -1622,7 +1672,8 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   if (tc.sync_debug)
     for (int bi = 0; bi < tc.s2_blocks.nb; ++bi)
       fprintf(stderr, "s2 block %d: terms [%d,%d) groups %d+%d used %x lone %x\n", bi, tc.s2_blocks.zs[bi],
-              tc.s2_blocks.ze[bi], tc.s2_blocks.g0[bi], tc.s2_blocks.ng[bi], tc.s2_blocks.used[bi], tc.s2_blocks.lone[bi]);
+              tc.s2_blocks.ze[bi], tc.s2_blocks.g0[bi], tc.s2_blocks.ng[bi], tc.s2_blocks.used[bi],
+              tc.s2_blocks.lone[bi]);
   tc.ready = true;
   return FTK_OK;
 }

@@ -10,6 +10,15 @@
 
 namespace ftk {
 
+// Step-2 work blocks: 1 or 2 consecutive 8-column word groups of the Step-3 operand holding <= 8 terms
+struct S2BlockTable {
+  int nb;
+  int zs[16], ze[16];  // term range of block b (device term order)
+  int g0[16], ng[16];  // first word group, number of groups
+  int used[16];        // words (bit grp * 4 + w) written by some term
+  int lone[16];        // terms (bit z - zs) with ell = 0 and no neighbour in their word
+};
+
 struct TcPlan {
   static constexpr int MAXG = 16;  // max rep-groups (Y slices) of Step 3
   bool ready = false;
@@ -29,12 +38,7 @@ struct TcPlan {
   uint8_t* d_Aop = nullptr;    // images, bf16 hi/lo split, Step-1 K-major tiles [p][tile][kchunk][part]...
   size_t aop_bytes = 0;
   int NIT = 0, KCH = 64, NKCH = 0;
-  // Step-2 work blocks (and the layout of Zhat'), mirrors S2Blocks in ftk_tc.cu
-  struct {
-    int nb;
-    int zs[16], ze[16], g0[16], ng[16];
-    int used[16], lone[16];
-  } s2_blocks;                  // Step-2 work blocks (S2Blocks in ftk_tc.cu)
+  S2BlockTable s2_blocks;     // Step-2 work blocks
   float2* d_s2tw = nullptr;  // Step-2 four-step twiddle tables
   int64_t n_tm = 0;
   int num_sms = 148;
@@ -48,6 +52,11 @@ struct TcPlan {
 
 typedef void (*prof_cb_t)(void* plan, int cls, int end, cudaStream_t s);
 
+int s2_block_table(const std::vector<int>& ell, const std::vector<int>& col, int K3p, S2BlockTable& t,
+                   std::string& msg);
+// Device term order for the tensor-core engine (see ftk_tc.cu); perm[new z] = old z.
+int tc_term_order(const std::vector<int>& ell, const std::vector<int>& col, int K3p, std::vector<int>& perm,
+                  std::string& msg);
 int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, const std::vector<int>& ell,
                  const std::vector<int>& col, const std::vector<float>& Y3, int K3p, int Ke, int n_gamma,
                  std::string& msg);

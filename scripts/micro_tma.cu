@@ -37,7 +37,9 @@ typedef CUresult (*PFN)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, co
                         const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                         CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int main() {
+int main(int argc, char** argv) {
+  const bool u32 = argc > 1 && std::strcmp(argv[1], "u32") == 0;  // 4-byte elements, x in floats
+  printf("element: %s\n", u32 ? "UINT32 (box 16 x rows, x = 2 x0)" : "UINT64 (box 8 x rows)");
   void* fp = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
@@ -55,13 +57,13 @@ int main() {
     cudaMalloc(&o, c.n_in * 8 * 8);
     cudaMemcpy(d, h.data(), ne * 8, cudaMemcpyHostToDevice);
     alignas(64) CUtensorMap m;
-    const cuuint64_t dims[2] = {(cuuint64_t)c.Hs, (cuuint64_t)c.npair * c.n_in};
+    const cuuint64_t dims[2] = {(cuuint64_t)(u32 ? 2 * c.Hs : c.Hs), (cuuint64_t)c.npair * c.n_in};
     const cuuint64_t strides[1] = {(cuuint64_t)c.Hs * 8};
-    const cuuint32_t box[2] = {8u, (cuuint32_t)(c.n_in < 256 ? c.n_in : 256)};
+    const cuuint32_t box[2] = {u32 ? 16u : 8u, (cuuint32_t)(c.n_in < 256 ? c.n_in : 256)};
     const cuuint32_t es[2] = {1u, 1u};
-    CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, d, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    CUresult r = enc(&m, u32 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, d, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    k<<<1, 256, c.n_in * 64>>>(m, c.n_in, c.x0, c.pair, o, nullptr);
+    k<<<1, 256, c.n_in * 64>>>(m, c.n_in, u32 ? 2 * c.x0 : c.x0, c.pair, o, nullptr);
     cudaError_t e = cudaDeviceSynchronize();
     int bad = -1;
     if (e == cudaSuccess) {
