@@ -16,6 +16,7 @@ Modules
   ftk          FTK Steps 1-3 literally (Eq. fbk3), cyclic q; log-marginal over the grid
   brute        direct evaluation of the discretized bandlimited inner product (Eq. Xdg P:293-298 with Eq. Fdk)
   closed_form  exact (2 pi)^2 <R_gamma T_delta A, B> for Gaussian-blob images (Eq. planch)
+  pixels       pixel images -> polar Fourier samples, the trapezoid sum of Eq. Ahattrap evaluated directly
   bounds       Lemma 2 / Theorem 1 rank bounds, empirical fit, RMS error bound
 
 Parity status: every function here is pinned by tests in tests/test_oracle_*.py

@@ -256,3 +256,35 @@ def make_polar_set(cfg: Config, k_nodes, mode: str = "independent", noise: bool 
     imgs, _ = draw_items(cfg, "images", range(ni), k_nodes, mode, noise, backend, device)
     tpls, _ = draw_items(cfg, "templates", range(nt), k_nodes, "independent", noise, backend, device)
     return imgs, tpls
+
+
+def pixel_images(params, n: int, noise_sd: float = 0.0, seeds: Optional[Sequence] = None):
+    """Blob images sampled at pixel centres: A[i][j] = sum_b amp_b exp(-((x_i - cx_b)^2 + (y_j - cy_b)^2) / 2 sig_b^2)
+    with x_i = i - n/2, y_j = j - n/2 px (PAPER.md P:309-312 with the [-1, 1]^2 box in px units, DESIGN R23).
+    Optional i.i.d. real Gaussian pixel noise of std `noise_sd` (one rng per item from `seeds`).
+    Returns float32 [N_items, n, n] (i slow, j fast)."""
+    x = np.arange(n, dtype=np.float64) - n / 2.0
+    n_items = params["cx"].shape[0]
+    out = np.empty((n_items, n, n), dtype=np.float32)
+    for r in range(n_items):
+        cx, cy, sig, amp = params["cx"][r], params["cy"][r], params["sigma"][r], params["amp"][r]
+        gx = np.exp(-(x[None, :] - cx[:, None]) ** 2 / (2.0 * sig[:, None] ** 2))  # [B, n] over i
+        gy = np.exp(-(x[None, :] - cy[:, None]) ** 2 / (2.0 * sig[:, None] ** 2))  # [B, n] over j
+        img = np.einsum("b,bi,bj->ij", amp, gx, gy)
+        if noise_sd > 0.0:
+            img = img + noise_sd * np.random.default_rng(seeds[r]).standard_normal((n, n))
+        out[r] = img.astype(np.float32)
+    return out
+
+
+def draw_pixel_items(cfg: Config, kind: str, items: Sequence[int], mode: str = "independent", noise: bool = True):
+    """Pixel images of the config's blob items (same blobs as draw_items) with pixel-domain white noise at
+    the config's SNR (||noise||^2 = ||signal||^2 / SNR over the n x n samples; unit-norm signals).
+    Returns (pixels float32 [N, n, n], params)."""
+    p = blob_params(cfg, kind, items, mode)
+    sd = 0.0
+    if noise and math.isfinite(cfg.snr):
+        sd = math.sqrt(1.0 / (cfg.snr * cfg.n * cfg.n))
+    stream = 4 if kind == "templates" else 5
+    seeds = [[cfg.seed, stream, it] for it in items]
+    return pixel_images(p, cfg.n, sd, seeds), p
