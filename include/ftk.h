@@ -132,6 +132,26 @@ ftk_status_t ftk_plan_factors(ftk_plan_t plan, double* G, double* Y);
 ftk_status_t ftk_load_images(ftk_plan_t plan, const void* polar_c64, int64_t N, int is_device, void* stream);
 ftk_status_t ftk_load_templates(ftk_plan_t plan, const void* polar_c64, int64_t N_total, int is_device, void* stream);
 
+/* Pixel front end (PAPER.md Sec. "Conversion of discrete input images to the Fourier
+ * domain", Eq. Ahattrap, evaluated with a 2-D type-2 NUFFT as in P:531-541):
+ *   Ahat(k_m, psi_p) = sum_{i,j < n} A[i][j] exp(-i k_m ((i - n/2) cos psi_p + (j - n/2) sin psi_p))
+ * in pixel units (the paper's box [-1, 1]^2 with dx = 2/n, rescaled so that dx = 1 px; R23),
+ * psi_p = 2 pi p / n_psi, k_m = the plan's radial nodes (rad/px).  NUFFT: upsampling 2, exponential-of-
+ * semicircle kernel of width 7 (relative error ~1e-6 of sum |A|), fp32 arithmetic.
+ *   pixels : float32 [N][n][n] (i slow, j fast), n = the plan's image size; host (is_device = 0, copied
+ *            in chunks) or device (is_device = 1).  The caller keeps ownership.
+ *   ftk_polar_from_pixels: out_c64 = device complex64 [N][n_k][n_psi] (the layout ftk_load_* takes).
+ *   ftk_load_images_pixels / ftk_load_templates_pixels: same as ftk_load_images / ftk_load_templates
+ *            from pixels (templates: N_total global, this rank keeps its shard); the polar samples are
+ *            not materialized beyond one chunk.
+ * Errors: FTK_EINVAL (null pointer, N <= 0, n not a power of two, out not a device pointer),
+ * FTK_ESTATE (host-only plan), FTK_ENOMEM, FTK_ECUDA.  Asynchronous on `stream`. */
+ftk_status_t ftk_polar_from_pixels(ftk_plan_t plan, const float* pixels, int64_t N, int is_device, void* out_c64,
+                                   void* stream);
+ftk_status_t ftk_load_images_pixels(ftk_plan_t plan, const float* pixels, int64_t N, int is_device, void* stream);
+ftk_status_t ftk_load_templates_pixels(ftk_plan_t plan, const float* pixels, int64_t N_total, int is_device,
+                                       void* stream);
+
 /* Copy Fourier-Bessel coefficients a(k_m; q) of loaded items [first, first+count) to out_c64
  * (device, [count][n_k][n_psi] complex64, q fastest, q cyclic).  which: 0 images, 1 local templates. */
 ftk_status_t ftk_fb_coeffs(ftk_plan_t plan, int which, int64_t first, int64_t count, void* out_c64, void* stream);

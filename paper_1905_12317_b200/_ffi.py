@@ -44,6 +44,9 @@ SYMBOLS = {
     "ftk_align": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "ftk_landscape_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "ftk_align_marginal": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]),
+    "ftk_polar_from_pixels": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]),
+    "ftk_load_images_pixels": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
+    "ftk_load_templates_pixels": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
     "ftk_merge_bests": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]),
     "ftk_merge_bests_host": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
     "ftk_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),

@@ -118,6 +118,38 @@ class FTKPlan:
     def load_templates(self, polar, stream=None):
         self._load(self._L.ftk_load_templates, polar, stream)
 
+    # ---------------- pixel front end (Eq. Ahattrap by a type-2 NUFFT)
+    def _pixels(self, x):
+        import torch
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(np.ascontiguousarray(x.astype(np.float32, copy=False)))
+        n = self.info["n"]
+        assert x.dtype == torch.float32 and x.dim() == 3 and x.shape[1] == n and x.shape[2] == n, \
+            f"pixels must be float32 [N][{n}][{n}]"
+        return x.contiguous()
+
+    def polar_from_pixels(self, pixels, stream=None):
+        """complex64 [N, n_k, n_psi] device tensor of Ahat(k_m, psi_p) from float32 [N, n, n] pixels."""
+        import torch
+        x = self._pixels(pixels)
+        out = torch.empty((x.shape[0], self.info["n_k"], self.info["n_psi"]), dtype=torch.complex64,
+                          device=f"cuda:{self.device}")
+        _check(self._L.ftk_polar_from_pixels(self._p, C.c_void_p(x.data_ptr()), x.shape[0], 1 if x.is_cuda else 0,
+                                             C.c_void_p(out.data_ptr()), _stream_ptr(stream)), self._p)
+        return out
+
+    def load_images_pixels(self, pixels, stream=None):
+        x = self._pixels(pixels)
+        _check(self._L.ftk_load_images_pixels(self._p, C.c_void_p(x.data_ptr()), x.shape[0], 1 if x.is_cuda else 0,
+                                              _stream_ptr(stream)), self._p)
+        self._refresh()
+
+    def load_templates_pixels(self, pixels, stream=None):
+        x = self._pixels(pixels)
+        _check(self._L.ftk_load_templates_pixels(self._p, C.c_void_p(x.data_ptr()), x.shape[0],
+                                                 1 if x.is_cuda else 0, _stream_ptr(stream)), self._p)
+        self._refresh()
+
     def fb_coeffs(self, which: int, first: int, count: int, stream=None):
         import torch
         out = torch.empty((count, self.info["n_k"], self.info["n_psi"]), dtype=torch.complex64,

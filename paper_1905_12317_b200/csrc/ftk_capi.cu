@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -47,6 +48,10 @@ struct ftk_plan_s {
   int64_t best_tmp_cap = 0;
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
+  // pixel front end (NEXT-2): NUFFT plan and its chunk scratch
+  NuPlan nu;
+  void* d_nu = nullptr;
+  size_t nu_bytes = 0;
   // profiling
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[5];
@@ -330,6 +335,8 @@ void ftk_plan_destroy(ftk_plan_t plan) {
     cudaFree(plan->d_keys);
     cudaFree(plan->d_best_tmp);
     cudaFree(plan->d_stage);
+    cudaFree(plan->d_nu);
+    nu_plan_free(plan->nu);
     tc_plan_free(plan->tc);
     for (int c = 0; c < 5; ++c)
       for (auto& e : plan->ev[c]) {
@@ -432,7 +439,53 @@ static ftk_status_t load_set(ftk_plan_t plan, const void* polar, int64_t first, 
   return FTK_OK;
 }
 
-ftk_status_t ftk_load_images(ftk_plan_t plan, const void* polar_c64, int64_t N, int is_device, void* stream) {
+// Pixel images [first, first + count) -> polar samples (NUFFT, Eq. Ahattrap) -> either the caller's polar
+// buffer (fb == nullptr) or, through the ring FFT, FB coefficients at fb.  Chunked through plan->d_nu.
+static ftk_status_t pixels_chunked(ftk_plan_t plan, const float* pixels, int64_t first, int64_t count, int is_device,
+                                   float2* polar_out, float2* fb, cudaStream_t s) {
+  const DevPlan P = devplan(plan);
+  if (!plan->nu.ready) {
+    std::string msg;
+    const int st = nu_plan_init(plan->nu, plan->pm.n, plan->pm.k, 7, msg);
+    if (st != FTK_OK) return fail(plan, (ftk_status_t)st, msg);
+  }
+  const int n = plan->pm.n;
+  const size_t pix_bytes = (size_t)n * n * sizeof(float);
+  const size_t polar_bytes = (size_t)P.n_k * P.n_psi * sizeof(float2);
+  const size_t per = nu_scratch_bytes_per_image(plan->nu) + (fb ? polar_bytes : 0) + (is_device ? 0 : pix_bytes);
+  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(count, std::max<size_t>(per, (size_t)512 << 20) / per));
+  if (const char* e = std::getenv("FTK_NU_CHUNK"))  // tests: force small chunks (ragged chunk boundaries)
+    chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, std::atoll(e)));
+  if (plan->nu_bytes < (size_t)chunk * per) {
+    cudaFree(plan->d_nu);
+    plan->d_nu = nullptr;
+    plan->nu_bytes = 0;
+    CK(cudaMalloc(&plan->d_nu, (size_t)chunk * per));
+    plan->nu_bytes = (size_t)chunk * per;
+  }
+  uint8_t* base = reinterpret_cast<uint8_t*>(plan->d_nu);
+  void* scratch = base;
+  float2* pol_tmp = reinterpret_cast<float2*>(base + (size_t)chunk * nu_scratch_bytes_per_image(plan->nu));
+  float* pix_tmp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(pol_tmp) + (fb ? (size_t)chunk * polar_bytes : 0));
+  for (int64_t c0 = 0; c0 < count; c0 += chunk) {
+    const int64_t nc = std::min(chunk, count - c0);
+    const float* src = pixels + (first + c0) * (int64_t)n * n;
+    if (!is_device) {
+      CK(cudaMemcpyAsync(pix_tmp, src, nc * pix_bytes, cudaMemcpyHostToDevice, s));
+      src = pix_tmp;
+    }
+    float2* pol = fb ? pol_tmp : polar_out + c0 * (int64_t)P.n_k * P.n_psi;
+    prof_begin(plan, 0, s);
+    launch_polar_from_pixels(plan->nu, src, nc, pol, P.n_psi, scratch, s);
+    if (fb) launch_ring_fft(pol, fb + c0 * (int64_t)P.n_k * P.n_psi, nc, P, s);
+    prof_end(plan, 0, s);
+    CK(cudaGetLastError());
+  }
+  return FTK_OK;
+}
+
+static ftk_status_t load_images_any(ftk_plan_t plan, const void* polar_c64, int64_t N, int is_device, void* stream,
+                                    bool pixels) {
   if (!plan) return FTK_EINVAL;
   if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
   if (!polar_c64 || N <= 0) return fail(plan, FTK_EINVAL, "ftk_load_images: null pointer or N <= 0");
@@ -445,7 +498,9 @@ ftk_status_t ftk_load_images(ftk_plan_t plan, const void* polar_c64, int64_t N, 
     CK(cudaMalloc(&plan->d_A, bytes));
   }
   plan->n_im = N;
-  ftk_status_t st = load_set(plan, polar_c64, 0, N, is_device, plan->d_A, s);
+  ftk_status_t st = pixels ? pixels_chunked(plan, reinterpret_cast<const float*>(polar_c64), 0, N, is_device, nullptr,
+                                            plan->d_A, s)
+                           : load_set(plan, polar_c64, 0, N, is_device, plan->d_A, s);
   if (st != FTK_OK) return st;
   if (plan->engine == 0) {
     std::string msg;
@@ -456,7 +511,8 @@ ftk_status_t ftk_load_images(ftk_plan_t plan, const void* polar_c64, int64_t N, 
   return FTK_OK;
 }
 
-ftk_status_t ftk_load_templates(ftk_plan_t plan, const void* polar_c64, int64_t N_total, int is_device, void* stream) {
+static ftk_status_t load_templates_any(ftk_plan_t plan, const void* polar_c64, int64_t N_total, int is_device,
+                                       void* stream, bool pixels) {
   if (!plan) return FTK_EINVAL;
   if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
   if (!polar_c64 || N_total <= 0) return fail(plan, FTK_EINVAL, "ftk_load_templates: null pointer or N <= 0");
@@ -477,7 +533,9 @@ ftk_status_t ftk_load_templates(ftk_plan_t plan, const void* polar_c64, int64_t 
   plan->n_tm_local = nl;
   plan->tm_off = lo;
   if (nl > 0) {
-    ftk_status_t st = load_set(plan, polar_c64, lo, nl, is_device, plan->d_B, s);
+    ftk_status_t st = pixels ? pixels_chunked(plan, reinterpret_cast<const float*>(polar_c64), lo, nl, is_device,
+                                              nullptr, plan->d_B, s)
+                             : load_set(plan, polar_c64, lo, nl, is_device, plan->d_B, s);
     if (st != FTK_OK) return st;
     if (plan->engine == 0) {
       std::string msg;
@@ -487,6 +545,31 @@ ftk_status_t ftk_load_templates(ftk_plan_t plan, const void* polar_c64, int64_t 
   }
   plan->have_templates = true;
   return FTK_OK;
+}
+
+ftk_status_t ftk_load_images(ftk_plan_t plan, const void* polar_c64, int64_t N, int is_device, void* stream) {
+  return load_images_any(plan, polar_c64, N, is_device, stream, false);
+}
+ftk_status_t ftk_load_templates(ftk_plan_t plan, const void* polar_c64, int64_t N_total, int is_device, void* stream) {
+  return load_templates_any(plan, polar_c64, N_total, is_device, stream, false);
+}
+ftk_status_t ftk_load_images_pixels(ftk_plan_t plan, const float* pixels, int64_t N, int is_device, void* stream) {
+  return load_images_any(plan, pixels, N, is_device, stream, true);
+}
+ftk_status_t ftk_load_templates_pixels(ftk_plan_t plan, const float* pixels, int64_t N_total, int is_device,
+                                       void* stream) {
+  return load_templates_any(plan, pixels, N_total, is_device, stream, true);
+}
+
+ftk_status_t ftk_polar_from_pixels(ftk_plan_t plan, const float* pixels, int64_t N, int is_device, void* out_c64,
+                                   void* stream) {
+  if (!plan) return FTK_EINVAL;
+  if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
+  if (!pixels || !out_c64 || N <= 0) return fail(plan, FTK_EINVAL, "ftk_polar_from_pixels: null pointer or N <= 0");
+  if (!is_device_ptr(out_c64)) return fail(plan, FTK_EINVAL, "ftk_polar_from_pixels: out must be a device pointer");
+  CK(cudaSetDevice(plan->device));
+  return pixels_chunked(plan, pixels, 0, N, is_device, reinterpret_cast<float2*>(out_c64), nullptr,
+                        (cudaStream_t)stream);
 }
 
 ftk_status_t ftk_fb_coeffs(ftk_plan_t plan, int which, int64_t first, int64_t count, void* out_c64, void* stream) {

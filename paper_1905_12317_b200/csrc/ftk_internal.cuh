@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+#include <vector>
+
 #include "../../include/ftk.h"
 
 namespace ftk {
@@ -91,5 +94,21 @@ void launch_step3_simt(const float* Z3, const PairBlock& pb, const DevPlan& P, i
 void launch_finalize(const unsigned long long* keys, int64_t n, int N_t, int n_psi, ftk_best_t* out, cudaStream_t s);
 void launch_merge(const ftk_best_t* gathered, int world, int64_t n, ftk_best_t* out, cudaStream_t s);
 void launch_fb_export(const float2* fb, int64_t first, int64_t count, int n_k, int n_psi, float2* out, cudaStream_t s);
+
+// ---------------- pixel front end (ftk_nufft.cu): Eq. Ahattrap by a 2-D type-2 NUFFT ----------------
+struct NuPlan {
+  int n = 0, nf = 0, lognf = 0, w = 7, n_k = 0;  // pixels per side, fine grid 2n, kernel width
+  double beta = 0;                                // ES kernel shape 2.30 w
+  float* d_corr = nullptr;                        // [n] 1 / phihat(i - n/2)
+  float2* d_twf = nullptr;                        // [nf/2] e^{-2 pi i j / nf}
+  float* d_k = nullptr;                           // [n_k] radial nodes (rad/px)
+  bool ready = false;
+};
+int nu_plan_init(NuPlan& nu, int n, const std::vector<double>& k, int w, std::string& msg);
+void nu_plan_free(NuPlan& nu);
+size_t nu_scratch_bytes_per_image(const NuPlan& nu);
+// pix: device float [count][n][n]; polar: device complex [count][n_k][n_psi]; scratch >= count x per-image bytes
+void launch_polar_from_pixels(const NuPlan& nu, const float* pix, int64_t count, float2* polar, int n_psi,
+                              void* scratch, cudaStream_t s);
 
 }  // namespace ftk
