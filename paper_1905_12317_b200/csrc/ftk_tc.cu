@@ -34,6 +34,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "ftk_fft.cuh"
 #include "ftk_sm100.cuh"
@@ -63,6 +64,7 @@ struct S3Params {
   float* land;
   float* marg;     // MODE 1: [N_im][n_tm_local] log sum_{t,r} exp(X / tau)
   float msc;       // MODE 1: log2(e) / tau
+  int dbg;         // FTK_S3_DBG (diagnostics): bit 0 skips the epilogue arithmetic, bit 1 the TMEM drain (timing only)
   unsigned long long* trace;  // nullable (FTK_S3_TRACE=1): wait / busy cycle counters of CTA 0
 };
 
@@ -108,6 +110,74 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint4& v) {
 // SMEM -> TMEM: 128 rows x 32 bytes (two K-adjacent canonical core matrices per 8-row group)
 __device__ __forceinline__ void tc_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
+struct S3MmaArgs {
+  uint32_t tmem, acol0, ybase, sbase, ypart, rt_part, SBO;
+  int NCH, nch, NRT, NS, K3p, ke_steps, p_begin, p_end;
+  S3Smem* S;
+};
+
+// Step-3 MMA issue loop (one thread): per (pair, r-tile) the A slot copies (tcgen05.cp, in order with the
+// MMAs), per chunk 3 x KS MMAs M128 x NCH x K16 into E (k-steps < ke) / O.  KS = K3p / 16 at compile time
+// (KS = 0: runtime loop, for unusual widths).  tr: total, stage-wait and D-buffer-wait cycles.
+template <int KS>
+__device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[3]) {
+  S3Smem& S = *a.S;
+  const uint32_t idesc = idesc_bf16_f32(128, a.NCH);
+  const int ksteps = KS > 0 ? KS : a.K3p / 16, halfk = a.K3p / 2, ke = a.ke_steps;
+  uint32_t g_a = 0, g_d = 0;
+  const long long tr0 = clock64();
+  for (int p = a.p_begin; p < a.p_end; ++p) {
+    for (int T = 0; T < a.NRT; ++T, ++g_a) {
+      const int ab = g_a & 1, s = g_a % a.NS;
+      long long t1 = clock64();
+      mbar_wait(&S.st_full[s], (g_a / a.NS) & 1);
+      tr[1] += clock64() - t1;
+      tc_fence_after();
+      const uint32_t a_hi0 = a.tmem + a.acol0 + (uint32_t)(ab * a.K3p);
+      // staging -> TMEM A slot (after the MMAs that last read this slot: in-order tensor pipe)
+      const uint32_t src = a.sbase + (uint32_t)s * 2u * a.rt_part;
+      for (int part = 0; part < 2; ++part)
+        for (int j = 0; j < ksteps; ++j)
+          tc_cp_128x256b(a_hi0 + (uint32_t)(part * halfk + 8 * j),
+                         smem_desc_kmajor_noswz(src + part * a.rt_part + j * 256, 128, a.SBO));
+      tc_commit(&S.st_empty[s]);
+      for (int c = 0; c < a.nch; ++c, ++g_d) {
+        const int db = g_d & 1;
+        t1 = clock64();
+        mbar_wait(&S.d_empty[db], ((g_d >> 1) & 1) ^ 1);
+        tr[2] += clock64() - t1;
+        tc_fence_after();
+        const uint32_t dE = a.tmem + (uint32_t)(db * 2 * a.NCH), dO = dE + (uint32_t)a.NCH;
+        const uint32_t bch = a.ybase + (uint32_t)(c * (a.NCH / 8)) * a.SBO;
+        const uint64_t bh0 = smem_desc_kmajor_noswz(bch, 128, a.SBO);
+        const uint64_t bl0 = smem_desc_kmajor_noswz(bch + a.ypart, 128, a.SBO);
+        if constexpr (KS > 0) {
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            const uint32_t d = ks >= ke ? dO : dE;
+            const uint32_t acc0 = (ks == 0 || ks == ke) ? 0u : 1u;
+            const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + (uint32_t)halfk;
+            mma_bf16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);  // +256 B per k-step
+            mma_bf16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_bf16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+          }
+        } else {
+          for (int ks = 0; ks < ksteps; ++ks) {
+            const uint32_t d = ks >= ke ? dO : dE;
+            const uint32_t acc0 = (ks == 0 || ks == ke) ? 0u : 1u;
+            const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + (uint32_t)halfk;
+            mma_bf16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);
+            mma_bf16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_bf16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+          }
+        }
+        tc_commit(&S.d_full[db]);
+      }
+    }
+  }
+  tr[0] = clock64() - tr0;
 }
 
 // MODE 0: fused max / argmax (the north-star epilogue).  MODE 1: marginalization epilogue (SURVEY 8(f)
@@ -173,74 +243,39 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   const int p_end = min(count, p_begin + per);
 
   if (warp == 0) {
-    // ---------------- Y image of the group -> SMEM (once); then A copies + MMAs
-    const uint32_t ybytes = 2u * ypart;
+    // ---------------- Y image of the group -> SMEM (once); then A copies + MMAs, all from one elected
+    // lane.  The k-step loop is unrolled at compile time (s3_mma_loop<KS>): a runtime-trip-count loop
+    // around tcgen05.mma measured ~500 extra cycles per chunk (scripts/micro_s3.cu).
     if (elect_one()) {
+      const uint32_t ybytes = 2u * ypart;
       mbar_arrive_expect_tx(&S.y_bar, ybytes);
       const uint8_t* ysrc = P.Ysm + P.g_yoff[grp];
       for (uint32_t o = 0; o < ybytes; o += 32768u) {
         const uint32_t b = min(32768u, ybytes - o);
         bulk_g2s(ys + o, ysrc + o, b, &S.y_bar);
       }
-    }
-    __syncwarp();
-    mbar_wait(&S.y_bar, 0);
-    const uint32_t idesc = idesc_bf16_f32(128, NCH);
-    const uint32_t ybase = smem_u32(ys), sbase = smem_u32(stg);
-    const int ksteps = K3p / 16, ke_steps = P.Ke / 16, halfk = K3p / 2;
-    uint32_t g_a = 0, g_d = 0;
-    long long tr0 = clock64(), tr_a = 0, tr_d = 0;
-    for (int p = p_begin; p < p_end; ++p) {
-      for (int T = 0; T < NRT; ++T, ++g_a) {
-        const int ab = g_a & 1, s = g_a % NS;
-        long long t1 = clock64();
-        mbar_wait(&S.st_full[s], (g_a / NS) & 1);
-        tr_a += clock64() - t1;
-        tc_fence_after();
-        const uint32_t a_hi0 = tmem + acol0 + (uint32_t)(ab * K3p);
-        if (elect_one()) {
-          // staging -> TMEM A slot (after the MMAs that last read this slot: in-order tensor pipe)
-          const uint32_t src = sbase + (uint32_t)s * 2u * rt_part;
-          for (int part = 0; part < 2; ++part)
-            for (int j = 0; j < ksteps; ++j)
-              tc_cp_128x256b(a_hi0 + (uint32_t)(part * halfk + 8 * j),
-                             smem_desc_kmajor_noswz(src + part * rt_part + j * 256, 128, SBO));
-          tc_commit(&S.st_empty[s]);
-        }
-        __syncwarp();
-        for (int c = 0; c < nch; ++c, ++g_d) {
-          const int db = g_d & 1;
-          long long t2 = clock64();
-          mbar_wait(&S.d_empty[db], ((g_d >> 1) & 1) ^ 1);
-          tr_d += clock64() - t2;
-          tc_fence_after();
-          const uint32_t dE = tmem + (uint32_t)(db * 2 * NCH), dO = dE + (uint32_t)NCH;
-          const uint32_t bch = ybase + (uint32_t)(c * (NCH / 8)) * SBO;
-          const uint64_t bh0 = smem_desc_kmajor_noswz(bch, 128, SBO);
-          const uint64_t bl0 = smem_desc_kmajor_noswz(bch + ypart, 128, SBO);
-          if (elect_one()) {
-            for (int ks = 0; ks < ksteps; ++ks) {
-              const bool odd = ks >= ke_steps;
-              const uint32_t d = odd ? dO : dE;
-              const uint32_t acc0 = (odd ? ks > ke_steps : ks > 0) ? 1u : 0u;
-              const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + (uint32_t)halfk;
-              const uint64_t b_hi = bh0 + (uint64_t)(ks * 16), b_lo = bl0 + (uint64_t)(ks * 16);  // +256 B
-              mma_bf16_ts(d, a_hi, b_hi, idesc, acc0);
-              mma_bf16_ts(d, a_hi, b_lo, idesc, 1u);
-              mma_bf16_ts(d, a_lo, b_hi, idesc, 1u);
-            }
-            tc_commit(&S.d_full[db]);
-          }
-          __syncwarp();
-        }
+      mbar_wait(&S.y_bar, 0);
+      S3MmaArgs a{tmem, acol0, smem_u32(ys), smem_u32(stg), ypart, rt_part, SBO, NCH, nch, NRT, NS, K3p, P.Ke / 16,
+                  p_begin, p_end, &S};
+      long long tr[3] = {0, 0, 0};
+      switch (K3p / 16) {
+        case 2: s3_mma_loop<2>(a, tr); break;
+        case 3: s3_mma_loop<3>(a, tr); break;
+        case 4: s3_mma_loop<4>(a, tr); break;
+        case 5: s3_mma_loop<5>(a, tr); break;
+        case 6: s3_mma_loop<6>(a, tr); break;
+        case 7: s3_mma_loop<7>(a, tr); break;
+        case 8: s3_mma_loop<8>(a, tr); break;
+        default: s3_mma_loop<0>(a, tr); break;
+      }
+      if (P.trace && blockIdx.x == 0) {
+        P.trace[0] = tr[0];
+        P.trace[1] = tr[1];
+        P.trace[2] = tr[2];
+        P.trace[3] = p_end - p_begin;
       }
     }
-    if (P.trace && blockIdx.x == 0 && lane == 0) {
-      P.trace[0] = clock64() - tr0;
-      P.trace[1] = tr_a;
-      P.trace[2] = tr_d;
-      P.trace[3] = p_end - p_begin;
-    }
+    __syncwarp();
   } else if (warp == 1) {
     // ---------------- producer: one bulk copy per (pair, r-tile) into the staging ring
     if (lane == 0) {
@@ -286,8 +321,12 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         for (int c = 0; c < nch; ++c, ++g_d) {
           const int db = g_d & 1;
           long long te = clock64();
-          if (warp == 2) mbar_wait(&S.d_full[db], (g_d >> 1) & 1);
-          named_bar(3, 256);
+          if (P.dbg & 4) {  // (diagnostics) one poller + named barrier
+            if (warp == 2) mbar_wait(&S.d_full[db], (g_d >> 1) & 1);
+            named_bar(3, 256);
+          } else {
+            mbar_wait(&S.d_full[db], (g_d >> 1) & 1);  // every epilogue warp (suspending try_wait)
+          }
           tr_e += clock64() - te;
           te = clock64();
           tc_fence_after();
@@ -299,33 +338,137 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           uint32_t* e1 = e01 + 16;
           uint32_t* o0 = o01;
           uint32_t* o1 = o01 + 16;
-          if (active) {
-            if (hw > 16) {
-              tmem_ld32(base, e01);
-            } else {
-              tmem_ld16(base, *reinterpret_cast<uint32_t(*)[16]>(e01));
-            }
-            if (hw > 32) tmem_ld8(base + 32, e2);
-            if (has_odd) {
-              if (hw > 16) {
-                tmem_ld32(base + NCH, o01);
-              } else {
-                tmem_ld16(base + NCH, *reinterpret_cast<uint32_t(*)[16]>(o01));
-              }
-              if (hw > 32) tmem_ld8(base + NCH + 32, o2);
-            }
-            tmem_wait_ld();
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&S.d_empty[db]);
-          tr_x += clock64() - te;
           if (!has_odd) {
 #pragma unroll
             for (int k = 0; k < 16; ++k) o0[k] = o1[k] = 0u;
 #pragma unroll
             for (int k = 0; k < 8; ++k) o2[k] = 0u;
           }
+          // MODE 0 (fast groups): per 8-column group, the best E + |O| = max(X(+delta), X(-delta)) and its
+          // group key; slow groups (padding / unpaired shifts / landscape output) take the exact path
+          const uint32_t kb = ((uint32_t)T << 24) | ((uint32_t)clb << 7) | (uint32_t)row;
+          auto grp0 = [&](auto G) {
+            constexpr int g8 = decltype(G)::value;
+            if (MODE != 0 || !active || (P.dbg & 1) || 8 * g8 >= hw) return;
+            uint32_t e[8], o[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              e[k] = g8 < 2 ? e0[8 * g8 + k] : (g8 < 4 ? e1[8 * (g8 - 2) + k] : e2[k]);
+              o[k] = g8 < 2 ? o0[8 * g8 + k] : (g8 < 4 ? o1[8 * (g8 - 2) + k] : o2[k]);
+            }
+            if (8 * g8 < nfast) {
+              float v[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(e[k]) + fabsf(__uint_as_float(o[k]));
+              const float m = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+              const bool upd = m > bvf;
+              bvf = upd ? m : bvf;
+              bkf = upd ? kb + ((uint32_t)(8 * g8) << 7) : bkf;
+            } else if (r < n) {
+              const int cl = clb + 8 * g8;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int tp = s_rep[cl + k], tm = s_part[cl + k];
+                if (tp < 0) continue;
+                const float ev = __uint_as_float(e[k]), ov = __uint_as_float(o[k]);
+                const float xp = ev + ov;
+                const uint32_t fp = (uint32_t)tp * (uint32_t)n + (uint32_t)r;
+                if (better(xp, fp, bve, bfe)) {
+                  bve = xp;
+                  bfe = fp;
+                }
+                if (land_p) land_p[(size_t)tp * n + r] = xp;
+                if (tm >= 0) {
+                  const float xm = ev - ov;
+                  const uint32_t fm = (uint32_t)tm * (uint32_t)n + (uint32_t)r;
+                  if (better(xm, fm, bve, bfe)) {
+                    bve = xm;
+                    bfe = fm;
+                  }
+                  if (land_p) land_p[(size_t)tm * n + r] = xm;
+                }
+              }
+            }
+          };
+          // all-fast half chunks (the common case): branch-free over the groups [G0, G1) so the FADD / max
+          // chains of different groups interleave; the serial compare-select only per group maximum
+          const bool allfast = MODE == 0 && active && !(P.dbg & 1) && nfast >= hw;
+          auto fast_range = [&](auto G0, auto G1) {
+            constexpr int g0 = decltype(G0)::value, g1 = decltype(G1)::value;
+            float m[5];
+#pragma unroll
+            for (int g8 = g0; g8 < g1; ++g8) {
+              float v[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const uint32_t ek = g8 < 2 ? e0[8 * g8 + k] : (g8 < 4 ? e1[8 * (g8 - 2) + k] : e2[k]);
+                const uint32_t ok = g8 < 2 ? o0[8 * g8 + k] : (g8 < 4 ? o1[8 * (g8 - 2) + k] : o2[k]);
+                v[k] = __uint_as_float(ek) + fabsf(__uint_as_float(ok));
+              }
+              m[g8] = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+            }
+#pragma unroll
+            for (int g8 = g0; g8 < g1; ++g8) {
+              const bool upd = m[g8] > bvf;
+              bvf = upd ? m[g8] : bvf;
+              bkf = upd ? kb + ((uint32_t)(8 * g8) << 7) : bkf;
+            }
+          };
+          auto phase1 = [&]() {
+            if (allfast && hw >= 16) {
+              fast_range(std::integral_constant<int, 0>{}, std::integral_constant<int, 2>{});
+            } else if (allfast) {
+              fast_range(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{});
+            } else {
+              grp0(std::integral_constant<int, 0>{});
+              grp0(std::integral_constant<int, 1>{});
+            }
+          };
+          auto phase2 = [&]() {
+            if (allfast && hw == 40) {
+              fast_range(std::integral_constant<int, 2>{}, std::integral_constant<int, 5>{});
+            } else if (allfast && hw == 32) {
+              fast_range(std::integral_constant<int, 2>{}, std::integral_constant<int, 4>{});
+            } else if (allfast && hw == 24) {
+              fast_range(std::integral_constant<int, 2>{}, std::integral_constant<int, 3>{});
+            } else if (!(allfast && hw <= 16)) {
+              grp0(std::integral_constant<int, 2>{});
+              grp0(std::integral_constant<int, 3>{});
+              grp0(std::integral_constant<int, 4>{});
+            }
+          };
+          // two-phase drain: columns [0, 16) first; the rest is loaded while MODE 0 processes them
+          // (tcgen05.wait::ld waits for all of a thread's loads; the empty asm "+r" ties each register to
+          // the wait so no use is scheduled before it)
+          const bool ld = active && !(P.dbg & 2);
+          if (ld) {
+            tmem_ld16(base, *reinterpret_cast<uint32_t(*)[16]>(e0));
+            if (has_odd) tmem_ld16(base + NCH, *reinterpret_cast<uint32_t(*)[16]>(o0));
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) asm volatile("" : "+r"(e0[k]), "+r"(o0[k]));
+            if (hw > 16) {
+              tmem_ld16(base + 16, *reinterpret_cast<uint32_t(*)[16]>(e1));
+              if (has_odd) tmem_ld16(base + NCH + 16, *reinterpret_cast<uint32_t(*)[16]>(o1));
+            }
+            if (hw > 32) {
+              tmem_ld8(base + 32, e2);
+              if (has_odd) tmem_ld8(base + NCH + 32, o2);
+            }
+          }
+          phase1();
+          if (ld) {
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) asm volatile("" : "+r"(e1[k]), "+r"(o1[k]));
+#pragma unroll
+            for (int k = 0; k < 8; ++k) asm volatile("" : "+r"(e2[k]), "+r"(o2[k]));
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.d_empty[db]);
+          tr_x += clock64() - te;
+          phase2();
           if (MODE == 1 && active) {
             // pass 1: the chunk's maximum of X = max(E + O, E - O) = E + |O| over valid columns (the
             // group test is warp-uniform: fast groups have 8 paired, non-padding columns)
@@ -391,53 +534,6 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
                 }
               }
               srun += ((sk[0] + sk[1]) + (sk[2] + sk[3])) + ((sk[4] + sk[5]) + (sk[6] + sk[7]));
-            }
-          }
-          if (MODE == 0 && active) {
-            const uint32_t kb = ((uint32_t)T << 24) | ((uint32_t)clb << 7) | (uint32_t)row;
-#pragma unroll
-            for (int g8 = 0; g8 < 5; ++g8) {
-              if (8 * g8 >= hw) break;
-              uint32_t e[8], o[8];
-#pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                e[k] = g8 < 2 ? e0[8 * g8 + k] : (g8 < 4 ? e1[8 * (g8 - 2) + k] : e2[k]);
-                o[k] = g8 < 2 ? o0[8 * g8 + k] : (g8 < 4 ? o1[8 * (g8 - 2) + k] : o2[k]);
-              }
-              if (8 * g8 < nfast) {
-                float v[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(e[k]) + fabsf(__uint_as_float(o[k]));
-                const float m = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
-                                      fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
-                const bool upd = m > bvf;
-                bvf = upd ? m : bvf;
-                bkf = upd ? kb + ((uint32_t)(8 * g8) << 7) : bkf;
-              } else if (r < n) {
-                const int cl = clb + 8 * g8;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                  const int tp = s_rep[cl + k], tm = s_part[cl + k];
-                  if (tp < 0) continue;
-                  const float ev = __uint_as_float(e[k]), ov = __uint_as_float(o[k]);
-                  const float xp = ev + ov;
-                  const uint32_t fp = (uint32_t)tp * (uint32_t)n + (uint32_t)r;
-                  if (better(xp, fp, bve, bfe)) {
-                    bve = xp;
-                    bfe = fp;
-                  }
-                  if (land_p) land_p[(size_t)tp * n + r] = xp;
-                  if (tm >= 0) {
-                    const float xm = ev - ov;
-                    const uint32_t fm = (uint32_t)tm * (uint32_t)n + (uint32_t)r;
-                    if (better(xm, fm, bve, bfe)) {
-                      bve = xm;
-                      bfe = fm;
-                    }
-                    if (land_p) land_p[(size_t)tm * n + r] = xm;
-                  }
-                }
-              }
             }
           }
         }
@@ -1772,6 +1868,10 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
     if (!d_trace) cudaMalloc(&d_trace, 16 * sizeof(unsigned long long));
     cudaMemsetAsync(d_trace, 0, 16 * sizeof(unsigned long long), s);
     prm.trace = d_trace;
+  }
+  {
+    const char* e = std::getenv("FTK_S3_DBG");
+    prm.dbg = e ? std::atoi(e) : 0;
   }
   prm.marg = tc.marg;
   prm.msc = tc.marg_scale;
