@@ -735,6 +735,62 @@ struct S1Smem {
   uint32_t tmem_base;
 };
 
+struct S1MmaArgs {
+  uint32_t tmem, sbase, stage_bytes, part_bytes, SBO;
+  int KCH, NKCH, nk, units, nit;
+  S1Smem* S;
+};
+
+// Step-1 MMA issue loop (one thread): per unit the generated A operand (TMEM) against every image tile,
+// per stage KS = KCH / 16 k-steps x 3 bf16 products (compile-time unrolled: a runtime loop around
+// tcgen05.mma costs ~500 cycles per stage, scripts/micro_s3.cu).  tr: total, A-wait, acc-wait, stage-wait.
+template <int KS>
+__device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&tr)[4]) {
+  S1Smem& S = *a.S;
+  const uint32_t idesc = idesc_bf16_f32(128, 128);
+  uint32_t g_st = 0, g_acc = 0, g_u = 0;
+  const long long tr0 = clock64();
+  for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++g_u) {
+    long long t1 = clock64();
+    mbar_wait(&S.a_full, g_u & 1);
+    tr[1] += clock64() - t1;
+    tc_fence_after();
+    for (int t = 0; t < a.nit; ++t, ++g_acc) {
+      const int ab = g_acc & 1;
+      t1 = clock64();
+      mbar_wait(&S.acc_empty[ab], ((g_acc >> 1) & 1) ^ 1);
+      tr[2] += clock64() - t1;
+      tc_fence_after();
+      const uint32_t d = a.tmem + 256 + (uint32_t)(ab * 128);
+      for (int kc = 0; kc < a.NKCH; ++kc, ++g_st) {
+        const int s = g_st % S1_STAGES;
+        t1 = clock64();
+        mbar_wait(&S.st_full[s], (g_st / S1_STAGES) & 1);
+        tr[3] += clock64() - t1;
+        tc_fence_after();
+        const uint32_t st = a.sbase + s * a.stage_bytes;
+        const uint64_t bh0 = smem_desc_kmajor_noswz(st, 128, a.SBO);
+        const uint64_t bl0 = smem_desc_kmajor_noswz(st + a.part_bytes, 128, a.SBO);
+        const uint32_t a_hi0 = a.tmem + (uint32_t)(kc * (KS * 8));
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8);
+          const uint32_t a_lo = a_hi + (uint32_t)a.nk;
+          const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+          mma_bf16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc);  // +256 B per k-step
+          mma_bf16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
+          mma_bf16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+        }
+        tc_commit(&S.st_empty[s]);
+      }
+      tc_commit(&S.acc_full[ab]);
+    }
+    tc_commit(&S.a_empty);
+  }
+  tr[0] = clock64() - tr0;
+  return g_u;
+}
+
 __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
   extern __shared__ __align__(1024) uint8_t s1_raw[];
   S1Smem& S = *reinterpret_cast<S1Smem*>(s1_raw);
@@ -785,54 +841,21 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(128, 128);
-      const uint32_t sbase = smem_u32(stages);
-      const uint32_t part_bytes = 128u * P.KCH * 2u;
-      const uint32_t SBO = (uint32_t)(P.KCH / 8) * 128u;
-      uint32_t g_st = 0, g_acc = 0, g_u = 0;
-      long long tr0 = clock64(), tra = 0, trc = 0, trs = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++g_u) {
-        long long t1 = clock64();
-        mbar_wait(&S.a_full, g_u & 1);
-        tra += clock64() - t1;
-        tc_fence_after();
-        for (int t = 0; t < nit; ++t, ++g_acc) {
-          const int ab = g_acc & 1;
-          t1 = clock64();
-          mbar_wait(&S.acc_empty[ab], ((g_acc >> 1) & 1) ^ 1);
-          trc += clock64() - t1;
-          tc_fence_after();
-          const uint32_t d = tmem + 256 + (uint32_t)(ab * 128);
-          for (int kc = 0; kc < P.NKCH; ++kc, ++g_st) {
-            const int s = g_st % S1_STAGES;
-            t1 = clock64();
-            mbar_wait(&S.st_full[s], (g_st / S1_STAGES) & 1);
-            trs += clock64() - t1;
-            tc_fence_after();
-            const uint32_t st = sbase + s * stage_bytes;
-            for (int ks = 0; ks < P.KCH / 16; ++ks) {
-              const uint32_t a_hi = tmem + (uint32_t)(kc * (P.KCH / 2) + ks * 8);
-              const uint32_t a_lo = a_hi + (uint32_t)nk;
-              const uint64_t b_hi = smem_desc_kmajor_noswz(st + ks * 256, 128, SBO);
-              const uint64_t b_lo = smem_desc_kmajor_noswz(st + part_bytes + ks * 256, 128, SBO);
-              const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
-              mma_bf16_ts(d, a_hi, b_hi, idesc, acc);
-              mma_bf16_ts(d, a_hi, b_lo, idesc, 1u);
-              mma_bf16_ts(d, a_lo, b_hi, idesc, 1u);
-            }
-            tc_commit(&S.st_empty[s]);
-          }
-          tc_commit(&S.acc_full[ab]);
-        }
-        tc_commit(&S.a_empty);
-      }
+    // ---------------- MMA issuer (one elected lane; the k-steps of a stage unrolled at compile time)
+    if (elect_one()) {
+      S1MmaArgs a{tmem, smem_u32(stages), stage_bytes, 128u * P.KCH * 2u, (uint32_t)(P.KCH / 8) * 128u, P.KCH,
+                  P.NKCH, nk, units, nit, &S};
+      long long tr[4] = {0, 0, 0, 0};
+      uint32_t g_u = 0;
+      if (P.KCH == 64)
+        g_u = s1_mma_loop<4>(a, tr);
+      else
+        g_u = s1_mma_loop<2>(a, tr);
       if (P.trace && blockIdx.x == 0) {
-        P.trace[0] = clock64() - tr0;
-        P.trace[1] = tra;
-        P.trace[2] = trc;
-        P.trace[3] = trs;
+        P.trace[0] = tr[0];
+        P.trace[1] = tr[1];
+        P.trace[2] = tr[2];
+        P.trace[3] = tr[3];
         P.trace[4] = g_u;
       }
     }
