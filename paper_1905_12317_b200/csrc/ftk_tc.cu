@@ -1349,6 +1349,14 @@ static PFN_encodeTiled get_encode_tiled() {
 }
 
 
+static CUtensorMapL2promotion s2_l2_promotion() {  // FTK_S2_L2PROMO = 0 / 64 / 128 / 256 (diagnostics)
+  const char* e = std::getenv("FTK_S2_L2PROMO");
+  const int v = e ? std::atoi(e) : 64;  // 64: 17 % less DRAM read than 128 at c5, same time
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                          : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+}
+
 // Zhat' [pair][p][Hs] as a 2-D tensor of 8-byte elements (rows = pair * n_psi + p), 8 x 256 boxes,
 // 64-byte swizzle (the layout s2_slot() reads)
 static int make_zmap(CUtensorMap* m, const float2* Zhat, int npair, const DevPlan& P) {
@@ -1359,7 +1367,7 @@ static int make_zmap(CUtensorMap* m, const float2* Zhat, int npair, const DevPla
   const cuuint32_t box[2] = {8u, (cuuint32_t)(P.n_psi < 256 ? P.n_psi : 256)};
   const cuuint32_t es[2] = {1u, 1u};
   const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<float2*>(Zhat), dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, s2_l2_promotion(),
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? FTK_OK : FTK_ECUDA;
 }
