@@ -52,6 +52,9 @@ struct ftk_plan_s {
   NuPlan nu;
   void* d_nu = nullptr;
   size_t nu_bytes = 0;
+  // marginalization partials (G > 1 rep-groups)
+  void* d_marg_part = nullptr;
+  size_t marg_part_bytes = 0;
   // profiling
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[5];
@@ -336,6 +339,7 @@ void ftk_plan_destroy(ftk_plan_t plan) {
     cudaFree(plan->d_best_tmp);
     cudaFree(plan->d_stage);
     cudaFree(plan->d_nu);
+    cudaFree(plan->d_marg_part);
     nu_plan_free(plan->nu);
     tc_plan_free(plan->tc);
     for (int c = 0; c < 5; ++c)
@@ -727,8 +731,23 @@ ftk_status_t ftk_align_marginal(ftk_plan_t plan, double tau, float* log_marginal
   cudaStream_t s = (cudaStream_t)stream;
   plan->tc.marg = log_marginal;
   plan->tc.marg_scale = (float)(1.4426950408889634 / tau);
-  const ftk_status_t st = run_blocks(plan, nullptr, nullptr, nullptr, s);
+  plan->tc.marg_part = nullptr;
+  plan->tc.marg_np = plan->n_im * plan->n_tm_local;
+  if (plan->tc.G > 1 && plan->tc.marg_np > 0) {  // per-rep-group partials, merged below
+    const size_t need = (size_t)plan->tc.G * plan->tc.marg_np * sizeof(float2);
+    if (plan->marg_part_bytes < need) {
+      cudaFree(plan->d_marg_part);
+      plan->d_marg_part = nullptr;
+      plan->marg_part_bytes = 0;
+      CK(cudaMalloc(&plan->d_marg_part, need));
+      plan->marg_part_bytes = need;
+    }
+    plan->tc.marg_part = reinterpret_cast<float2*>(plan->d_marg_part);
+  }
+  ftk_status_t st = run_blocks(plan, nullptr, nullptr, nullptr, s);
+  if (st == FTK_OK) tc_marg_finalize(plan->tc, s);
   plan->tc.marg = nullptr;
+  plan->tc.marg_part = nullptr;
   plan->tc.marg_scale = 0.f;
   if (st != FTK_OK) return st;
   CK(cudaGetLastError());

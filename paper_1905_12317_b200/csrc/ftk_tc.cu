@@ -63,6 +63,8 @@ struct S3Params {
   unsigned long long* pair_keys;
   float* land;
   float* marg;     // MODE 1: [N_im][n_tm_local] log sum_{t,r} exp(X / tau)
+  float2* marg_part;  // MODE 1 with G > 1: [G][N_im][n_tm_local] base-2 (max, sum) partials
+  long long marg_np;
   float msc;       // MODE 1: log2(e) / tau
   int dbg;         // FTK_S3_DBG (diagnostics): bit 0 skips the epilogue arithmetic, bit 1 the TMEM drain (timing only)
   unsigned long long* trace;  // nullable (FTK_S3_TRACE=1): wait / busy cycle counters of CTA 0
@@ -596,7 +598,11 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           mbar_arrive(&S.red_empty[rb]);
           int i, j;
           pair_of(P.pb, p, i, j);
-          P.marg[(size_t)i * P.n_tm_local + j] = (m + log2f(sm)) * 0.6931471805599453f;
+          const size_t ij = (size_t)i * P.n_tm_local + j;
+          if (P.marg_part)
+            P.marg_part[(size_t)grp * (size_t)P.marg_np + ij] = make_float2(m, sm);
+          else
+            P.marg[ij] = (m + log2f(sm)) * 0.6931471805599453f;
         }
         __syncwarp();
         continue;
@@ -1905,6 +1911,8 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
     prm.dbg = e ? std::atoi(e) : 0;
   }
   prm.marg = tc.marg;
+  prm.marg_part = tc.marg_part;
+  prm.marg_np = tc.marg_np;
   prm.msc = tc.marg_scale;
   if (tc.marg)
     k_step3_tc<1><<<cpg * tc.G, S3_THREADS, tc.s3_smem, s>>>(prm);
@@ -1917,6 +1925,22 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
     fprintf(stderr, "s3trace pairs=%llu total=%llu mma_wait_stage=%llu mma_wait_dempty=%llu epi_wait_dfull=%llu "
             "epi_drain=%llu\n", h[3], h[0], h[1], h[2], h[4], h[5]);
   }
+}
+
+__global__ void k_marg_finalize(const float2* __restrict__ part, int G, long long np, float* __restrict__ out) {
+  const long long ij = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (ij >= np) return;
+  float m = -INFINITY, sm = 0.f;
+  for (int g = 0; g < G; ++g) {
+    const float2 v = part[(size_t)g * np + ij];
+    lse2_merge(m, sm, v.x, v.y);
+  }
+  out[ij] = (m + log2f(sm)) * 0.6931471805599453f;
+}
+
+void tc_marg_finalize(const TcPlan& tc, cudaStream_t s) {
+  if (!tc.marg_part || tc.marg_np <= 0) return;
+  k_marg_finalize<<<(unsigned)((tc.marg_np + 255) / 256), 256, 0, s>>>(tc.marg_part, tc.G, tc.marg_np, tc.marg);
 }
 
 void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const PairBlock& pb, const DevPlan& P,

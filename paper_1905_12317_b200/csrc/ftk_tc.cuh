@@ -47,10 +47,18 @@ struct TcPlan {
   // marginalization epilogue (MODE 1) writes log sum exp(X / tau) per pair to marg[i][j], marg_scale =
   // log2(e) / tau
   float* marg = nullptr;
-  float marg_scale = 0.f;  // FTK_SYNC_DEBUG=1: synchronize after each step (fault attribution)
+  float marg_scale = 0.f;
+  // G > 1 rep-groups: each group's CTAs see only part of the shifts, so MODE 1 writes per-group base-2
+  // (max, sum) partials to marg_part[group][i][j] (marg_np = N_im x n_tm_local) and tc_marg_finalize
+  // merges them into marg
+  float2* marg_part = nullptr;
+  int64_t marg_np = 0;
 };
 
 typedef void (*prof_cb_t)(void* plan, int cls, int end, cudaStream_t s);
+
+// log-sum-exp merge of the G rep-group partials of ftk_align_marginal (see TcPlan::marg_part)
+void tc_marg_finalize(const TcPlan& tc, cudaStream_t s);
 
 int s2_block_table(const std::vector<int>& ell, const std::vector<int>& col, int K3p, S2BlockTable& t,
                    std::string& msg);

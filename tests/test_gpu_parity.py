@@ -295,17 +295,20 @@ def test_marginal_vs_oracle(pkg, name, ni, nj, shift_filter, mult):
     check_best(pkg.best_to_numpy(p.align()["best"]), X, na, nb)
 
 
-def test_marginal_full_size_sampled(pkg):
-    """c5 sizes (256 images x 512 templates, the bench's Step-3 launch shape): sampled pairs vs the oracle."""
-    cfg = synth.config("c5")
+@pytest.mark.parametrize("name,ni,nj", [("c5", 256, 512), ("c4", 96, 160)])
+def test_marginal_full_size_sampled(pkg, name, ni, nj):
+    """c5 sizes (256 images x 512 templates, the bench's Step-3 launch shape) and c4 (3209 shifts: several
+    Step-3 rep-groups, whose per-group partials are merged by a finalize kernel): sampled pairs vs the oracle."""
+    cfg = synth.config(name)
     p = make(pkg, cfg, 0)
     k, w = p.radial()
-    ni, nj = 256, 512
+    if name == "c4":
+        assert p.info["s3_groups"] > 1
     imgs, _ = synth.draw_items(cfg, "images", range(ni), k, backend="torch", device="cuda")
     tpls, _ = synth.draw_items(cfg, "templates", range(nj), k, backend="torch", device="cuda")
     p.load_images(imgs)
     p.load_templates(tpls)
-    ii, jj = np.array([0, 255, 17]), np.array([511, 0, 300])
+    ii, jj = np.array([0, ni - 1, 17]), np.array([nj - 1, 0, 100])
     xs = imgs[torch.as_tensor(ii, device="cuda")].cpu().numpy()
     ys = tpls[torch.as_tensor(jj, device="cuda")].cpu().numpy()
     na, nb = fb.discrete_norm(xs, w), fb.discrete_norm(ys, w)
