@@ -263,3 +263,33 @@ def distributed_align(plan: FTKPlan, group=None, stream=None):
     import torch.distributed as dist
     local = plan.align(stream=stream)["best"]
     return gather_and_merge(local, group=group, stream=stream)
+
+
+def gather_marginal(local, n_tm_total: int, group=None):
+    """All-gather per-rank float32 [N_im, N_tm_local] log-marginals (template shards in shard_range order)
+    into the full [N_im, N_tm_total] matrix on every rank (NCCL for CUDA tensors, gloo for CPU)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if world == 1:
+        return local
+    rank = dist.get_rank(group)
+    ni = local.shape[0]
+    width = max(hi - lo for lo, hi in (shard_range(r, world, n_tm_total) for r in range(world)))
+    pad = torch.full((ni, width), float("-inf"), dtype=torch.float32, device=local.device)
+    lo, hi = shard_range(rank, world, n_tm_total)
+    pad[:, : hi - lo] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad.contiguous(), group=group)
+    out = torch.empty((ni, n_tm_total), dtype=torch.float32, device=local.device)
+    for r in range(world):
+        lo, hi = shard_range(r, world, n_tm_total)
+        out[:, lo:hi] = parts[r][:, : hi - lo]
+    return out
+
+
+def distributed_align_marginal(plan: FTKPlan, tau: float, group=None, stream=None):
+    """Template-sharded marginalization (ftk_align_marginal on this rank's shard) gathered to the full
+    [N_im, N_tm] matrix of log sum_{t,r} exp(X / tau) on every rank."""
+    local = plan.align_marginal(tau, stream=stream)
+    return gather_marginal(local, plan.info["n_templates_total"], group=group)

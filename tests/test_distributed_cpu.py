@@ -70,3 +70,40 @@ def test_two_rank_gloo_merge_matches_single_rank(world, nj):
         assert p.exitcode == 0
     for rank, merged in res:
         assert np.array_equal(merged, ref), (rank, merged, ref)
+
+
+def _worker_marg(rank, world, port, X, tau, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import paper_1905_12317_b200 as pkg
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = pkg.shard_range(rank, world, X.shape[1])
+    local = torch.from_numpy(ftk.log_marginal(X[:, lo:hi], tau).astype(np.float32).reshape(X.shape[0], hi - lo))
+    full = pkg.gather_marginal(local, X.shape[1])
+    q.put((rank, np.asarray(full)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nj", [(2, 5), (3, 7), (3, 2)])
+def test_gloo_gather_marginal_matches_single_rank(world, nj):
+    """Template-sharded log-marginals (NEXT-3) gathered over a gloo group equal the single-rank matrix,
+    including ranks that own no template (world > N_tm)."""
+    cfg = synth.config("tiny")
+    plan = ks.build_plan(cfg.n, cfg.K, synth.delta_max(cfg), synth.shift_list(cfg), cfg.eps, cfg.n_k, cfg.n_psi)
+    imgs, _ = synth.draw_items(cfg, "images", range(3), plan.k)
+    tpls, _ = synth.draw_items(cfg, "templates", range(nj), plan.k)
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), plan))
+    tau = 0.1
+    ref = ftk.log_marginal(X, tau).astype(np.float32)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_marg, args=(r, world, port, X, tau, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, full in res:
+        assert np.array_equal(full, ref), (rank, full, ref)
