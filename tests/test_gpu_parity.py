@@ -216,7 +216,7 @@ def test_tc_selftest(pkg):
     assert ets.value < 1e-4 and ess.value < 1e-4, (ets.value, ess.value)
 
 
-@pytest.mark.parametrize("name,mult", [("tiny", 2), ("c2", 4)])
+@pytest.mark.parametrize("name,mult", [("tiny", 2), ("c2", 4), ("c3", 4)])
 def test_n_gamma_more_rotations(pkg, name, mult):
     """n_gamma = mult * n_psi rotations (zero-padded Step 2, reading R21): full landscapes, per-image
     bests and the explicit-pair path against the oracle evaluated at the same angles."""
