@@ -1050,6 +1050,25 @@ __device__ __forceinline__ int s2_slot(int p, int zz) {  // complex index of (ro
   return p * 8 + ((((zz >> 1) ^ (p >> 1)) & 3) << 1) + (zz & 1);
 }
 
+// packed fp32x2 arithmetic (sm_100a FADD2 / FFMA2: one instruction for both components)
+__device__ __forceinline__ unsigned long long f2_u64(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+__device__ __forceinline__ float2 u64_f2(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u64(a)), "l"(f2_u64(b)));
+  return u64_f2(d);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u64(a)), "l"(f2_u64(b)));
+  return u64_f2(d);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_u64(a)), "l"(f2_u64(b)), "l"(f2_u64(c)));
+  return u64_f2(d);
+}
+
 __device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -1099,8 +1118,8 @@ __device__ __forceinline__ void dft_regs(float2 (&x)[E]) {
 #pragma unroll
       for (int j = 0; j < s; ++j) {
         const float2 u = x[rv(blk + j)], v = cmul_w32(x[rv(blk + j + s)], j * (32 / (2 * s)));
-        x[rv(blk + j)] = make_float2(u.x + v.x, u.y + v.y);
-        x[rv(blk + j + s)] = make_float2(u.x - v.x, u.y - v.y);
+        x[rv(blk + j)] = add2(u, v);
+        x[rv(blk + j + s)] = sub2(u, v);
       }
     }
   }
@@ -1264,7 +1283,7 @@ __global__ void __launch_bounds__(256, 3) k_step2_fft(const float2* __restrict__
           for (int c = 0; c < E; ++c) {
             const float px = __shfl_xor_sync(0xffffffffu, x[c].x, h);
             const float py = __shfl_xor_sync(0xffffffffu, x[c].y, h);
-            x[c] = cmulf(make_float2(fmaf(sg, x[c].x, px), fmaf(sg, x[c].y, py)), wc[s]);
+            x[c] = cmulf(fma2(make_float2(sg, sg), x[c], make_float2(px, py)), wc[s]);
           }
         }
       }
