@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
     const int hw = NCH / 2;         // columns per epilogue warp (multiple of 8, <= 40)
     const bool has_odd = P.Ke < K3p;
     uint32_t g_d = 0, it = 0;
-    long long tr_e = 0, tr_x = 0;
+    long long tr_e = 0, tr_x = 0, tr_p[4] = {0, 0, 0, 0};
     for (int p = p_begin; p < p_end; ++p, ++it) {
       float bvf = -INFINITY;        // fast record: best E + |O| ...
       uint32_t bkf = 0xffffffffu;   // ... and its key (T << 24 | column << 7 | row)
@@ -449,6 +449,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
             tmem_wait_ld();
 #pragma unroll
             for (int k = 0; k < 16; ++k) asm volatile("" : "+r"(e0[k]), "+r"(o0[k]));
+            if (P.trace) tr_p[0] += clock64() - te;
             if (hw > 16) {
               tmem_ld16(base + 16, *reinterpret_cast<uint32_t(*)[16]>(e1));
               if (has_odd) tmem_ld16(base + NCH + 16, *reinterpret_cast<uint32_t(*)[16]>(o1));
@@ -458,7 +459,9 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
               if (has_odd) tmem_ld8(base + NCH + 32, o2);
             }
           }
+          long long tq = P.trace ? clock64() : 0;
           phase1();
+          if (P.trace) { const long long t2 = clock64(); tr_p[1] += t2 - tq; tq = t2; }
           if (ld) {
             tmem_wait_ld();
 #pragma unroll
@@ -470,7 +473,9 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&S.d_empty[db]);
           tr_x += clock64() - te;
+          if (P.trace) { const long long t2 = clock64(); tr_p[2] += t2 - tq; tq = t2; }
           phase2();
+          if (P.trace) tr_p[3] += clock64() - tq;
           if (MODE == 1 && active) {
             // pass 1: the chunk's maximum of X = max(E + O, E - O) = E + |O| over valid columns (the
             // group test is warp-uniform: fast groups have 8 paired, non-padding columns)
@@ -581,6 +586,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
     if (P.trace && blockIdx.x == 0 && lane == 0 && warp == 2) {
       P.trace[4] = tr_e;
       P.trace[5] = tr_x;
+      for (int k = 0; k < 4; ++k) P.trace[6 + k] = tr_p[k];
     }
   } else {
     // ---------------- resolver (warp 10): merge the 8 partial records; exact (shift, sign) of the pair's
@@ -1942,7 +1948,8 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
     cudaMemcpyAsync(h, d_trace, sizeof h, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     fprintf(stderr, "s3trace pairs=%llu total=%llu mma_wait_stage=%llu mma_wait_dempty=%llu epi_wait_dfull=%llu "
-            "epi_drain=%llu\n", h[3], h[0], h[1], h[2], h[4], h[5]);
+            "epi_drain=%llu epi_ld1=%llu epi_g01=%llu epi_wait2=%llu epi_g234=%llu\n", h[3], h[0], h[1], h[2], h[4],
+            h[5], h[6], h[7], h[8], h[9]);
   }
 }
 
