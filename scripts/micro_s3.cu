@@ -10,6 +10,10 @@
 
 using namespace ftk::sm100;
 
+__device__ __forceinline__ void cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
 __device__ __forceinline__ void wait_mode(uint64_t* bar, uint32_t parity, int mode) {
   if (mode == 0) {
     mbar_wait(bar, parity);
@@ -30,7 +34,7 @@ __device__ __forceinline__ void wait_mode(uint64_t* bar, uint32_t parity, int mo
   }
 }
 
-__global__ void __launch_bounds__(128, 1) k_s3(int chunks, int N, int K3p, int Ke, int nch, int prods, int bfixed,
+__global__ void __launch_bounds__(288, 1) k_s3(int chunks, int N, int K3p, int Ke, int nch, int prods, int bfixed,
                                                int wmode, int NB, int flags, unsigned long long* cyc) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar[4];
@@ -58,6 +62,27 @@ __global__ void __launch_bounds__(128, 1) k_s3(int chunks, int N, int K3p, int K
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+  }
+  if (warp >= 1 && (flags & 8192)) {  // TMEM loader warps: 8 warps (two per lane quarter) read D-buffer columns
+    const int q = warp & 3, hh = (warp - 1) >> 2;
+    uint32_t acc = 0;
+    for (int it = 0; it < chunks; ++it) {
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((it & 1) * 2 * N + hh * (N / 2));
+      uint32_t r[16];
+      for (int c0 = 0; c0 + 16 <= N / 2; c0 += 16) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                     : "r"(base + c0));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                     : "r"(base + N + c0));
+        tmem_wait_ld();
+        for (int k = 0; k < 16; ++k) acc ^= r[k];
+      }
+    }
+    if (acc == 0x12345u) cyc[296] = acc;
   }
   if (warp == 0) {
     const uint32_t idesc = idesc_bf16_f32(128, N);
@@ -90,6 +115,12 @@ __global__ void __launch_bounds__(128, 1) k_s3(int chunks, int N, int K3p, int K
           const uint32_t db = (uint32_t)(c & 1);
           if (c >= 2 && !(flags & 4)) mbar_wait(&bar[db], (uint32_t)(((c >> 1) - 1) & 1));
           tc_fence_after();
+          if ((flags & 16384) && c % 5 == 0) {  // A slot refill per "r-tile" (every 5 chunks), 2 parts x 6 cp
+            const uint32_t slot = a_hi0 + (uint32_t)(((c / 5) & 1) * 96);
+            for (int part = 0; part < 2; ++part)
+              for (int j = 0; j < 6; ++j)
+                cp_128x256b(slot + (uint32_t)(part * 48 + 8 * j), smem_desc_kmajor_noswz(ybase + part * 24576 + j * 256, 128, SBO));
+          }
           const uint32_t dE = tmem + db * 2u * (uint32_t)N, dO = dE + (uint32_t)N;
           const uint32_t bch = ybase + (uint32_t)(cc * (N / 8)) * SBO;
           cc = (cc + 1 == nch) ? 0 : cc + 1;
@@ -200,19 +231,19 @@ __global__ void __launch_bounds__(128, 1) k_s3(int chunks, int N, int K3p, int K
 
 int main() {
   unsigned long long* d;
-  cudaMalloc(&d, 296 * sizeof(unsigned long long));
+  cudaMalloc(&d, 300 * sizeof(unsigned long long));
   unsigned long long h[296];
   const int K3p = 96, chunks = 2000;
   struct Cfg { int N, NB, prods, ks, flags, bfixed; };
   // flags: 1 = no fence::after_thread_sync, 2 = no per-chunk commit (only the last NB), 4 = no wait
   // dm (flags bits 3-5): 1 one D always accumulate; 2 one D, reset per chunk; 3 switching D, always accumulate
-  const Cfg cfgs[] = {{80, 2, 3, 6, 1024, 0}, {80, 2, 3, 6, 1024 | 2048, 0}, {80, 2, 3, 6, 64, 0}};
+  const Cfg cfgs[] = {{80, 2, 3, 6, 1024, 0}, {80, 2, 3, 6, 1024 | 16384, 0}, {80, 2, 3, 6, 1024 | 16384 | 8192, 0}};
   for (const Cfg& c : cfgs) {
     const int N = c.N, nch = 400 / N + 1;
     const int K3 = 16 * c.ks;
     const size_t smem = (size_t)2 * N * nch * K3p * 2;
     cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_s3<<<148, 128, smem>>>(chunks, N, K3, K3 / 2 > 16 ? (K3 / 32) * 16 : K3, nch, c.prods, c.bfixed, 1, c.NB, c.flags, d);
+    k_s3<<<148, (c.flags & 8192) ? 288 : 128, smem>>>(chunks, N, K3, K3 / 2 > 16 ? (K3 / 32) * 16 : K3, nch, c.prods, c.bfixed, 1, c.NB, c.flags, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       printf("err %s\n", cudaGetErrorString(e));
