@@ -118,6 +118,7 @@ struct S3MmaArgs {
   uint32_t tmem, acol0, ybase, sbase, ypart, rt_part, SBO;
   int NCH, nch, NRT, NS, K3p, ke_steps, p_begin, p_end;
   S3Smem* S;
+  unsigned long long* trace;  // CTA 0 only (FTK_S3_TRACE): per-chunk timestamps
 };
 
 // Step-3 MMA issue loop (one thread): per (pair, r-tile) the A slot copies (tcgen05.cp, in order with the
@@ -151,6 +152,7 @@ __device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[
         mbar_wait(&S.d_empty[db], ((g_d >> 1) & 1) ^ 1);
         tr[2] += clock64() - t1;
         tc_fence_after();
+        if (a.trace && g_d < 64) a.trace[16 + 4 * g_d] = clock64();
         const uint32_t dE = a.tmem + (uint32_t)(db * 2 * a.NCH), dO = dE + (uint32_t)a.NCH;
         const uint32_t bch = a.ybase + (uint32_t)(c * (a.NCH / 8)) * a.SBO;
         const uint64_t bh0 = smem_desc_kmajor_noswz(bch, 128, a.SBO);
@@ -176,6 +178,7 @@ __device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[
           }
         }
         tc_commit(&S.d_full[db]);
+        if (a.trace && g_d < 64) a.trace[16 + 4 * g_d + 1] = clock64();
       }
     }
   }
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
       }
       mbar_wait(&S.y_bar, 0);
       S3MmaArgs a{tmem, acol0, smem_u32(ys), smem_u32(stg), ypart, rt_part, SBO, NCH, nch, NRT, NS, K3p, P.Ke / 16,
-                  p_begin, p_end, &S};
+                  p_begin, p_end, &S, (P.trace && blockIdx.x == 0) ? P.trace : nullptr};
       long long tr[3] = {0, 0, 0};
       switch (K3p / 16) {
         case 2: s3_mma_loop<2>(a, tr); break;
@@ -331,6 +334,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           }
           tr_e += clock64() - te;
           te = clock64();
+          if (P.trace && blockIdx.x == 0 && warp == 2 && lane == 0 && g_d < 64) P.trace[16 + 4 * g_d + 2] = te;
           tc_fence_after();
           const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(db * 2 * NCH + h * hw);
           const int clb = c * NCH + h * hw;  // first column of this warp's half chunk
@@ -472,6 +476,9 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&S.d_empty[db]);
+          if (P.trace && blockIdx.x == 0 && warp == 2 && lane == 0 && g_d < 64) P.trace[16 + 4 * g_d + 3] = clock64();
+          if (P.trace && blockIdx.x == 0 && lane == 0 && g_d >= 16 && g_d < 24)
+            P.trace[16 + 4 * 64 + (g_d - 16) * 8 + (warp - 2)] = clock64();
           tr_x += clock64() - te;
           if (P.trace) { const long long t2 = clock64(); tr_p[2] += t2 - tq; tq = t2; }
           phase2();
@@ -1927,8 +1934,8 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
   static unsigned long long* d_trace = nullptr;  // diagnostics: FTK_S3_TRACE=1 prints CTA 0's counters
   const char* tenv = std::getenv("FTK_S3_TRACE");
   if (tenv && tenv[0] == '1') {
-    if (!d_trace) cudaMalloc(&d_trace, 16 * sizeof(unsigned long long));
-    cudaMemsetAsync(d_trace, 0, 16 * sizeof(unsigned long long), s);
+    if (!d_trace) cudaMalloc(&d_trace, (16 + 4 * 64 + 64) * sizeof(unsigned long long));
+    cudaMemsetAsync(d_trace, 0, (16 + 4 * 64 + 64) * sizeof(unsigned long long), s);
     prm.trace = d_trace;
   }
   {
@@ -1944,12 +1951,28 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
   else
     k_step3_tc<0><<<cpg * tc.G, S3_THREADS, tc.s3_smem, s>>>(prm);
   if (prm.trace) {
-    unsigned long long h[16];
+    unsigned long long h[16 + 4 * 64 + 64];
     cudaMemcpyAsync(h, d_trace, sizeof h, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     fprintf(stderr, "s3trace pairs=%llu total=%llu mma_wait_stage=%llu mma_wait_dempty=%llu epi_wait_dfull=%llu "
             "epi_drain=%llu epi_ld1=%llu epi_g01=%llu epi_wait2=%llu epi_g234=%llu\n", h[3], h[0], h[1], h[2], h[4],
             h[5], h[6], h[7], h[8], h[9]);
+    // per-chunk timeline of CTA 0 (chunks 8..63): MMA issue start / end (after commit), epilogue d_full seen /
+    // buffer released, relative to the issue start of the chunk
+    for (int c = 0; c < 63; ++c) {
+      const unsigned long long* t = h + 16 + 4 * c;
+      if (!t[0]) break;
+      fprintf(stderr, "s3chunk %d: issue %lld  full %lld  release %lld  next-issue %lld\n", c, (long long)(t[1] - t[0]),
+              (long long)(t[2] - t[0]), (long long)(t[3] - t[0]), (long long)(t[4] - t[0]));
+    }
+    fprintf(stderr, "s3chunk avg issue interval chunks 0..62: %lld\n",
+            (long long)(h[16 + 4 * 62] - h[16]) / 62);
+    for (int c = 16; c < 24; ++c) {  // per-warp release times (warps 2..9) relative to the chunk's issue start
+      fprintf(stderr, "s3rel %d:", c);
+      for (int w = 0; w < 8; ++w)
+        fprintf(stderr, " %lld", (long long)(h[16 + 4 * 64 + (c - 16) * 8 + w] - h[16 + 4 * c]));
+      fprintf(stderr, "\n");
+    }
   }
 }
 
