@@ -338,3 +338,24 @@ def test_marginal_errors(pkg):
     ps.load_templates(torch.from_numpy(x).cuda())
     with pytest.raises(pkg.FTKError):          # SIMT engine: max / argmax only
         ps.align_marginal(1.0)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_small_workspace_many_blocks(pkg, engine):
+    """A 16 MB workspace at c3 forces one-template pair blocks over ragged 128-image tiles (140 = 128 + 12):
+    per-image bests and per-pair maxima still match the oracle."""
+    cfg = synth.config("c3")
+    p = make(pkg, cfg, engine, workspace_bytes=16 << 20)
+    k, w = p.radial()
+    ni, nj = 140, 6
+    imgs, _ = synth.draw_items(cfg, "images", range(ni), k)
+    tpls, _ = synth.draw_items(cfg, "templates", range(nj), k)
+    p.load_images(torch.from_numpy(imgs).cuda())
+    p.load_templates(torch.from_numpy(tpls).cuda())
+    res = p.align(pair_best=True)
+    torch.cuda.synchronize()
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), oracle_plan(cfg)))
+    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+    check_best(pkg.best_to_numpy(res["best"]), X, na, nb)
+    pb = pkg.best_to_numpy(res["pair_best"].reshape(-1, 4)).reshape(ni, nj)
+    assert np.all(np.abs(pb["value"] - X.max(axis=(2, 3))) <= TOL * na[:, None] * nb[None, :])
