@@ -124,7 +124,7 @@ struct S3MmaArgs {
 // Step-3 MMA issue loop (one thread): per (pair, r-tile) the A slot copies (tcgen05.cp, in order with the
 // MMAs), per chunk 3 x KS MMAs M128 x NCH x K16 into E (k-steps < ke) / O.  KS = K3p / 16 at compile time
 // (KS = 0: runtime loop, for unusual widths).  tr: total, stage-wait and D-buffer-wait cycles.
-template <int KS>
+template <int KS, bool TR>
 __device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[3]) {
   S3Smem& S = *a.S;
   const uint32_t idesc = idesc_bf16_f32(128, a.NCH);
@@ -152,7 +152,9 @@ __device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[
         mbar_wait(&S.d_empty[db], ((g_d >> 1) & 1) ^ 1);
         tr[2] += clock64() - t1;
         tc_fence_after();
-        if (a.trace && g_d < 64) a.trace[16 + 4 * g_d] = clock64();
+        if constexpr (TR) {  // (FTK_S3_TRACE) compile-time: a runtime branch here slows the MMA issue
+          if (g_d < 64) a.trace[16 + 4 * g_d] = clock64();
+        }
         const uint32_t dE = a.tmem + (uint32_t)(db * 2 * a.NCH), dO = dE + (uint32_t)a.NCH;
         const uint32_t bch = a.ybase + (uint32_t)(c * (a.NCH / 8)) * a.SBO;
         const uint64_t bh0 = smem_desc_kmajor_noswz(bch, 128, a.SBO);
@@ -178,7 +180,9 @@ __device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[
           }
         }
         tc_commit(&S.d_full[db]);
-        if (a.trace && g_d < 64) a.trace[16 + 4 * g_d + 1] = clock64();
+        if constexpr (TR) {
+          if (g_d < 64) a.trace[16 + 4 * g_d + 1] = clock64();
+        }
       }
     }
   }
@@ -263,15 +267,19 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
       S3MmaArgs a{tmem, acol0, smem_u32(ys), smem_u32(stg), ypart, rt_part, SBO, NCH, nch, NRT, NS, K3p, P.Ke / 16,
                   p_begin, p_end, &S, (P.trace && blockIdx.x == 0) ? P.trace : nullptr};
       long long tr[3] = {0, 0, 0};
-      switch (K3p / 16) {
-        case 2: s3_mma_loop<2>(a, tr); break;
-        case 3: s3_mma_loop<3>(a, tr); break;
-        case 4: s3_mma_loop<4>(a, tr); break;
-        case 5: s3_mma_loop<5>(a, tr); break;
-        case 6: s3_mma_loop<6>(a, tr); break;
-        case 7: s3_mma_loop<7>(a, tr); break;
-        case 8: s3_mma_loop<8>(a, tr); break;
-        default: s3_mma_loop<0>(a, tr); break;
+      if (a.trace) {
+        s3_mma_loop<0, true>(a, tr);
+      } else {
+        switch (K3p / 16) {
+          case 2: s3_mma_loop<2, false>(a, tr); break;
+          case 3: s3_mma_loop<3, false>(a, tr); break;
+          case 4: s3_mma_loop<4, false>(a, tr); break;
+          case 5: s3_mma_loop<5, false>(a, tr); break;
+          case 6: s3_mma_loop<6, false>(a, tr); break;
+          case 7: s3_mma_loop<7, false>(a, tr); break;
+          case 8: s3_mma_loop<8, false>(a, tr); break;
+          default: s3_mma_loop<0, false>(a, tr); break;
+        }
       }
       if (P.trace && blockIdx.x == 0) {
         P.trace[0] = tr[0];
@@ -312,7 +320,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
     const int hw = NCH / 2;         // columns per epilogue warp (multiple of 8, <= 40)
     const bool has_odd = P.Ke < K3p;
     uint32_t g_d = 0, it = 0;
-    long long tr_e = 0, tr_x = 0, tr_p[4] = {0, 0, 0, 0};
+    long long tr_e = 0, tr_x = 0;
     for (int p = p_begin; p < p_end; ++p, ++it) {
       float bvf = -INFINITY;        // fast record: best E + |O| ...
       uint32_t bkf = 0xffffffffu;   // ... and its key (T << 24 | column << 7 | row)
@@ -334,7 +342,6 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           }
           tr_e += clock64() - te;
           te = clock64();
-          if (P.trace && blockIdx.x == 0 && warp == 2 && lane == 0 && g_d < 64) P.trace[16 + 4 * g_d + 2] = te;
           tc_fence_after();
           const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(db * 2 * NCH + h * hw);
           const int clb = c * NCH + h * hw;  // first column of this warp's half chunk
@@ -453,7 +460,6 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
             tmem_wait_ld();
 #pragma unroll
             for (int k = 0; k < 16; ++k) asm volatile("" : "+r"(e0[k]), "+r"(o0[k]));
-            if (P.trace) tr_p[0] += clock64() - te;
             if (hw > 16) {
               tmem_ld16(base + 16, *reinterpret_cast<uint32_t(*)[16]>(e1));
               if (has_odd) tmem_ld16(base + NCH + 16, *reinterpret_cast<uint32_t(*)[16]>(o1));
@@ -463,9 +469,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
               if (has_odd) tmem_ld8(base + NCH + 32, o2);
             }
           }
-          long long tq = P.trace ? clock64() : 0;
           phase1();
-          if (P.trace) { const long long t2 = clock64(); tr_p[1] += t2 - tq; tq = t2; }
           if (ld) {
             tmem_wait_ld();
 #pragma unroll
@@ -476,13 +480,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&S.d_empty[db]);
-          if (P.trace && blockIdx.x == 0 && warp == 2 && lane == 0 && g_d < 64) P.trace[16 + 4 * g_d + 3] = clock64();
-          if (P.trace && blockIdx.x == 0 && lane == 0 && g_d >= 16 && g_d < 24)
-            P.trace[16 + 4 * 64 + (g_d - 16) * 8 + (warp - 2)] = clock64();
           tr_x += clock64() - te;
-          if (P.trace) { const long long t2 = clock64(); tr_p[2] += t2 - tq; tq = t2; }
           phase2();
-          if (P.trace) tr_p[3] += clock64() - tq;
           if (MODE == 1 && active) {
             // pass 1: the chunk's maximum of X = max(E + O, E - O) = E + |O| over valid columns (the
             // group test is warp-uniform: fast groups have 8 paired, non-padding columns)
@@ -593,7 +592,6 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
     if (P.trace && blockIdx.x == 0 && lane == 0 && warp == 2) {
       P.trace[4] = tr_e;
       P.trace[5] = tr_x;
-      for (int k = 0; k < 4; ++k) P.trace[6 + k] = tr_p[k];
     }
   } else {
     // ---------------- resolver (warp 10): merge the 8 partial records; exact (shift, sign) of the pair's
@@ -1955,24 +1953,15 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
     cudaMemcpyAsync(h, d_trace, sizeof h, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     fprintf(stderr, "s3trace pairs=%llu total=%llu mma_wait_stage=%llu mma_wait_dempty=%llu epi_wait_dfull=%llu "
-            "epi_drain=%llu epi_ld1=%llu epi_g01=%llu epi_wait2=%llu epi_g234=%llu\n", h[3], h[0], h[1], h[2], h[4],
-            h[5], h[6], h[7], h[8], h[9]);
-    // per-chunk timeline of CTA 0 (chunks 8..63): MMA issue start / end (after commit), epilogue d_full seen /
-    // buffer released, relative to the issue start of the chunk
+            "epi_drain=%llu\n", h[3], h[0], h[1], h[2], h[4], h[5]);
+    // per-chunk MMA issue timeline of CTA 0 (issue duration, interval to the next chunk's issue)
     for (int c = 0; c < 63; ++c) {
       const unsigned long long* t = h + 16 + 4 * c;
-      if (!t[0]) break;
-      fprintf(stderr, "s3chunk %d: issue %lld  full %lld  release %lld  next-issue %lld\n", c, (long long)(t[1] - t[0]),
-              (long long)(t[2] - t[0]), (long long)(t[3] - t[0]), (long long)(t[4] - t[0]));
+      if (!t[0] || !t[4]) break;
+      fprintf(stderr, "s3chunk %d: issue %lld  next-issue %lld\n", c, (long long)(t[1] - t[0]), (long long)(t[4] - t[0]));
     }
-    fprintf(stderr, "s3chunk avg issue interval chunks 0..62: %lld\n",
-            (long long)(h[16 + 4 * 62] - h[16]) / 62);
-    for (int c = 16; c < 24; ++c) {  // per-warp release times (warps 2..9) relative to the chunk's issue start
-      fprintf(stderr, "s3rel %d:", c);
-      for (int w = 0; w < 8; ++w)
-        fprintf(stderr, " %lld", (long long)(h[16 + 4 * 64 + (c - 16) * 8 + w] - h[16 + 4 * c]));
-      fprintf(stderr, "\n");
-    }
+    if (h[16] && h[16 + 4 * 62]) fprintf(stderr, "s3chunk avg issue interval chunks 0..62: %lld\n", (long long)(h[16 + 4 * 62] - h[16]) / 62);
+
   }
 }
 
