@@ -952,7 +952,6 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
       s1_unit(u, P.NCT, p, ct);
       const int nvalid = min(128, 2 * (P.F - ct * 64));
       // this lane's two complex columns cc = lane, lane + 32 -> offsets (template jl, term z) in Zhat'
-      // this lane's two complex columns cc = lane, lane + 32 -> offsets (template jl, term z) in Zhat'
       long long coff[2];
       bool cval[2];
 #pragma unroll
