@@ -482,7 +482,54 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           if (lane == 0) mbar_arrive(&S.d_empty[db]);
           tr_x += clock64() - te;
           phase2();
-          if (MODE == 1 && active) {
+          // MODE 1, all-fast half chunks: branch-free over NG compile-time groups
+          auto marg_fast = [&](auto NGc) {
+            constexpr int NG = decltype(NGc)::value;
+            float cmk[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cmk[k] = -INFINITY;
+#pragma unroll
+            for (int g8 = 0; g8 < NG; ++g8)
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const float ev = __uint_as_float(g8 < 2 ? e0[8 * g8 + k] : (g8 < 4 ? e1[8 * (g8 - 2) + k] : e2[k]));
+                const float ov = __uint_as_float(g8 < 2 ? o0[8 * g8 + k] : (g8 < 4 ? o1[8 * (g8 - 2) + k] : o2[k]));
+                cmk[k] = fmaxf(cmk[k], ev + fabsf(ov));
+              }
+            float cm = fmaxf(fmaxf(fmaxf(cmk[0], cmk[1]), fmaxf(cmk[2], cmk[3])),
+                             fmaxf(fmaxf(cmk[4], cmk[5]), fmaxf(cmk[6], cmk[7])));
+            cm *= P.msc;
+            if (cm > mrun) {
+              srun *= ex2_approx(mrun - cm);
+              mrun = cm;
+            }
+            const float nm = -mrun, sc = P.msc;
+            float sk[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sk[k] = 0.f;
+#pragma unroll
+            for (int g8 = 0; g8 < NG; ++g8)
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const float ev = __uint_as_float(g8 < 2 ? e0[8 * g8 + k] : (g8 < 4 ? e1[8 * (g8 - 2) + k] : e2[k]));
+                const float ov = __uint_as_float(g8 < 2 ? o0[8 * g8 + k] : (g8 < 4 ? o1[8 * (g8 - 2) + k] : o2[k]));
+                sk[k] += ex2_approx(fmaf(ev + ov, sc, nm)) + ex2_approx(fmaf(ev - ov, sc, nm));
+              }
+            srun += ((sk[0] + sk[1]) + (sk[2] + sk[3])) + ((sk[4] + sk[5]) + (sk[6] + sk[7]));
+          };
+          bool marg_done = false;
+          if (MODE == 1 && active && nfast >= hw) {
+            marg_done = true;
+            switch (hw >> 3) {
+              case 5: marg_fast(std::integral_constant<int, 5>{}); break;
+              case 4: marg_fast(std::integral_constant<int, 4>{}); break;
+              case 3: marg_fast(std::integral_constant<int, 3>{}); break;
+              case 2: marg_fast(std::integral_constant<int, 2>{}); break;
+              case 1: marg_fast(std::integral_constant<int, 1>{}); break;
+              default: marg_done = false; break;
+            }
+          }
+          if (MODE == 1 && active && !marg_done) {
             // pass 1: the chunk's maximum of X = max(E + O, E - O) = E + |O| over valid columns (the
             // group test is warp-uniform: fast groups have 8 paired, non-padding columns)
             float cmk[8];  // per-k partial maxima (short dependency chains)
