@@ -1209,7 +1209,10 @@ __global__ void __launch_bounds__(256, 3) k_step2_fft(const float2* __restrict__
   uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 16 * RS);
   // warp index made provably warp-uniform (shfl from lane 0) so the shuffles below sit in convergent code
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-  float2* scr = reinterpret_cast<float2*>(stg) + warp * n;  // 8 warps x n complex <= 16 x RS words
+  // transpose scratch: 8 warps x E rows of (32 + L) complex (row padding L makes both the row-wise stores and
+  // the strided loads conflict-free and the indices compile-time offsets); 8 E (32 + L) complex = 16 RS words
+  constexpr int SROW = 32 + 32 / E;
+  float2* scr = reinterpret_cast<float2*>(stg) + warp * E * SROW;
   const int total = npair * B.nb;
   const int Hp = P.H_plus;
   const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
@@ -1321,12 +1324,12 @@ __global__ void __launch_bounds__(256, 3) k_step2_fft(const float2* __restrict__
       //     that lane (c = lane / L, h = lane % L) holds a = L i + h, i < E; then (A2) an E-point DFT over i
       //     in registers, (B2) twiddle w_32^{h d'}, (C2) an L-point DIF across the L lanes of each c.
 #pragma unroll
-      for (int c = 0; c < E; ++c) scr[c * 32 + ((lane + c) & 31)] = x[rv(c)];
+      for (int c = 0; c < E; ++c) scr[c * SROW + lane] = x[rv(c)];
       __syncwarp();
       {
         const int cq = lane / L, hq = lane % L;
 #pragma unroll
-        for (int i = 0; i < E; ++i) x[i] = scr[cq * 32 + ((L * i + hq + cq) & 31)];
+        for (int i = 0; i < E; ++i) x[i] = scr[cq * SROW + L * i + hq];
       }
       dft_regs<E>(x);  // (A2): natural order in x[rv(d')]
       if constexpr (L > 1) {
