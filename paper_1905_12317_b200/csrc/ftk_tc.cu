@@ -794,7 +794,7 @@ __device__ __forceinline__ void s1_unit(int u, int NCT, int& p, int& ct) {
 
 struct S1Smem {
   uint64_t st_full[S1_STAGES], st_empty[S1_STAGES];
-  uint64_t a_full, a_empty;
+  uint64_t a_full[2], a_empty[2];  // per generation round (see s1_rounds)
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
 };
@@ -814,20 +814,30 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
   const uint32_t idesc = idesc_bf16_f32(128, 128);
   uint32_t g_st = 0, g_acc = 0, g_u = 0;
   const long long tr0 = clock64();
+  // generation rounds: R = 2 when the K' chunks split by radial halves (NKCH % 4 == 0): round r fills the
+  // chunks kc with (kc mod NKCH/2) in [r NKCH/4, (r+1) NKCH/4), i.e. m in [r n_k/2, (r+1) n_k/2)
+  const int R = (a.NKCH % 4 == 0) ? 2 : 1;
+  const int hq = a.NKCH / 2, qq = a.NKCH / 4;
+  auto round_of = [&](int kc) { return R == 2 ? ((kc % hq) >= qq ? 1 : 0) : 0; };
   for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++g_u) {
-    long long t1 = clock64();
-    mbar_wait(&S.a_full, g_u & 1);
-    tr[1] += clock64() - t1;
-    tc_fence_after();
+    bool got0 = false, got1 = false;
     for (int t = 0; t < a.nit; ++t, ++g_acc) {
       const int ab = g_acc & 1;
-      t1 = clock64();
+      long long t1 = clock64();
       mbar_wait(&S.acc_empty[ab], ((g_acc >> 1) & 1) ^ 1);
       tr[2] += clock64() - t1;
       tc_fence_after();
       const uint32_t d = a.tmem + 256 + (uint32_t)(ab * 128);
       for (int kc = 0; kc < a.NKCH; ++kc, ++g_st) {
         const int s = g_st % S1_STAGES;
+        const int rr = round_of(kc);
+        if (rr == 0 ? !got0 : !got1) {  // the generated operand chunk of this round (first tile of a unit)
+          t1 = clock64();
+          mbar_wait(&S.a_full[rr], g_u & 1);
+          tr[1] += clock64() - t1;
+          tc_fence_after();
+          if (rr == 0) got0 = true; else got1 = true;
+        }
         t1 = clock64();
         mbar_wait(&S.st_full[s], (g_st / S1_STAGES) & 1);
         tr[3] += clock64() - t1;
@@ -846,10 +856,12 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
           mma_bf16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
         }
         tc_commit(&S.st_empty[s]);
+        // last tile: a round's chunks are free once its last stage has been read
+        if (t == a.nit - 1 && (R == 1 ? kc == a.NKCH - 1 : (kc == a.NKCH - 1 || kc == hq + qq - 1)))
+          tc_commit(&S.a_empty[R == 1 ? 0 : (kc == a.NKCH - 1 ? 1 : 0)]);
       }
       tc_commit(&S.acc_full[ab]);
     }
-    tc_commit(&S.a_empty);
   }
   tr[0] = clock64() - tr0;
   return g_u;
@@ -868,8 +880,10 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
       mbar_init(&S.st_full[i], 1);
       mbar_init(&S.st_empty[i], 1);
     }
-    mbar_init(&S.a_full, 8);
-    mbar_init(&S.a_empty, 1);
+    for (int r = 0; r < 2; ++r) {
+      mbar_init(&S.a_full[r], 8);
+      mbar_init(&S.a_empty[r], 1);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.acc_full[i], 1);
       mbar_init(&S.acc_empty[i], 128);
@@ -933,9 +947,10 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
     const int mh = (warp - 2) >> 2;  // radial half
     const uint32_t base = tmem + ((uint32_t)(q * 32) << 16);
     const int half = nk / 2;  // u32 columns per K' half
-    // (n_k < 32: a half would be narrower than one 16-node STTM step; the first-half warps do all nodes)
-    const int m_beg = nk >= 32 ? mh * half : 0;
-    const int m_end = nk >= 32 ? m_beg + half : (mh == 0 ? nk : 0);
+    // generation rounds (as in s1_mma_loop): R = 2 -> round r covers m in [r n_k/2, (r+1) n_k/2), each warp of
+    // the quarter pair a quarter of n_k; R = 1 -> each warp half of n_k (n_k < 32: a half would be
+    // narrower than one 16-node STTM step; the first-half warps do all nodes)
+    const int R = (P.NKCH % 4 == 0) ? 2 : 1;
     uint32_t g_u = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++g_u) {
       int p, ct;
@@ -950,7 +965,16 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
       const int qt = valid ? ((p + __ldg(P.ell + z)) & (n - 1)) : 0;
       const float2* brow = P.B + ((size_t)(P.j0 + jl) * n + qt) * nk;
       const float* grow = P.g + (size_t)z * nk;
-      mbar_wait(&S.a_empty, (g_u & 1) ^ 1);
+      for (int rnd = 0; rnd < R; ++rnd) {
+      int m_beg, m_end;
+      if (R == 2) {
+        m_beg = rnd * half + mh * (nk / 4);
+        m_end = m_beg + nk / 4;
+      } else {
+        m_beg = nk >= 32 ? mh * half : 0;
+        m_end = nk >= 32 ? m_beg + half : (mh == 0 ? nk : 0);
+      }
+      mbar_wait(&S.a_empty[rnd], (g_u & 1) ^ 1);
       tc_fence_after();
       for (int m0 = m_beg; m0 < m_end; m0 += 32) {
         float4 bb[2][8];
@@ -986,7 +1010,8 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.a_full);
+      if (lane == 0) mbar_arrive(&S.a_full[rnd]);
+      }
     }
   } else {
     // ---------------- epilogue: accumulator [128 rows (j,zeta,part)] x [128 images] -> Zhat'
