@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--templates", type=int, default=0)
     ap.add_argument("--n-gamma", type=int, default=0,
                     help="rotations per (pair, shift); 0 = n_psi (the configs). > n_psi: zero-padded Step 2 (NEXT-3)")
+    ap.add_argument("--pixels", action="store_true",
+                    help="inputs are n x n pixel images; each step runs the NUFFT front end (Eq. Ahattrap, NEXT-2) "
+                         "before Steps 1-3 (no e2e / cpu_baseline legs)")
     ap.add_argument("--marginal-tau", type=float, default=0.0,
                     help="> 0: time the marginalization epilogue (log sum exp(X / tau) per pair, NEXT-3) instead "
                          "of max / argmax (1 GPU; not the headline metric)")
@@ -216,14 +219,23 @@ def main():
     n_gamma = plan.info["n_gamma"]
     k, w = plan.radial()
     # synthetic inputs generated on the device (seeded), resident in HBM
-    imgs, _ = synth.draw_items(cfg, "images", range(ni), k, backend="torch", device=dev)
-    tpls, _ = synth.draw_items(cfg, "templates", range(nj), k, backend="torch", device=dev)
+    if args.pixels:
+        imgs, _ = synth.draw_pixel_items(cfg, "images", range(ni), backend="torch", device=dev)
+        tpls, _ = synth.draw_pixel_items(cfg, "templates", range(nj), backend="torch", device=dev)
+        args.no_e2e = args.no_cpu_baseline = True
+    else:
+        imgs, _ = synth.draw_items(cfg, "images", range(ni), k, backend="torch", device=dev)
+        tpls, _ = synth.draw_items(cfg, "templates", range(nj), k, backend="torch", device=dev)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
 
     def step():
-        plan.load_images(imgs, stream=stream)
-        plan.load_templates(tpls, stream=stream)
+        if args.pixels:
+            plan.load_images_pixels(imgs, stream=stream)
+            plan.load_templates_pixels(tpls, stream=stream)
+        else:
+            plan.load_images(imgs, stream=stream)
+            plan.load_templates(tpls, stream=stream)
         if args.marginal_tau > 0:
             return plan.align_marginal(args.marginal_tau, stream=stream)
         if world > 1:
@@ -391,6 +403,8 @@ def main():
                            "N_im": ni, "N_tm": nj, "N_t": n_t, "eps": cfg.eps, "H": info["H"],
                            "H_plus": info["H_plus"], "K3": info["K3"], "engine": args.engine,
                            "parallelism": f"template-shard x{world}", "l2": "inputs (6+ GB FB arrays) exceed L2",
+                           "input": (f"pixels {cfg.n}x{cfg.n} float32 (NUFFT front end in the step)" if args.pixels
+                                     else "polar Fourier samples complex64 [N][n_k][n_psi]"),
                            "step": "load FFT (images+templates) + Steps 1-3 + argmax (+ all-gather/merge)"
                            if args.marginal_tau <= 0 else
                            f"load FFT + Steps 1-3 + log-marginal epilogue (tau = {args.marginal_tau})"},

@@ -277,7 +277,33 @@ def pixel_images(params, n: int, noise_sd: float = 0.0, seeds: Optional[Sequence
     return out
 
 
-def draw_pixel_items(cfg: Config, kind: str, items: Sequence[int], mode: str = "independent", noise: bool = True):
+def pixel_images_torch(params, n: int, noise_sd: float = 0.0, seed: int = 0, device=None, chunk: int = 256):
+    """pixel_images on the GPU (torch, float64 arithmetic, float32 result); noise from one device
+    generator seeded with `seed` (a different realization than the numpy path)."""
+    import torch
+    dev = torch.device(device if device is not None else "cuda")
+    x = torch.arange(n, dtype=torch.float64, device=dev) - n / 2.0
+    n_items = params["cx"].shape[0]
+    out = torch.empty((n_items, n, n), dtype=torch.float32, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    for s0 in range(0, n_items, chunk):
+        e = slice(s0, min(s0 + chunk, n_items))
+        cx = torch.as_tensor(params["cx"][e], device=dev)
+        cy = torch.as_tensor(params["cy"][e], device=dev)
+        sig = torch.as_tensor(params["sigma"][e], device=dev)
+        amp = torch.as_tensor(params["amp"][e], device=dev)
+        gx = torch.exp(-(x[None, None, :] - cx[:, :, None]) ** 2 / (2.0 * sig[:, :, None] ** 2))  # [I, B, n]
+        gy = torch.exp(-(x[None, None, :] - cy[:, :, None]) ** 2 / (2.0 * sig[:, :, None] ** 2))
+        img = torch.einsum("ib,ibx,iby->ixy", amp, gx, gy)
+        if noise_sd > 0.0:
+            img = img + noise_sd * torch.randn(img.shape, generator=g, device=dev, dtype=torch.float64)
+        out[e] = img.to(torch.float32)
+    return out
+
+
+def draw_pixel_items(cfg: Config, kind: str, items: Sequence[int], mode: str = "independent", noise: bool = True,
+                     backend: str = "numpy", device=None):
     """Pixel images of the config's blob items (same blobs as draw_items) with pixel-domain white noise at
     the config's SNR (||noise||^2 = ||signal||^2 / SNR over the n x n samples; unit-norm signals).
     Returns (pixels float32 [N, n, n], params)."""
@@ -286,5 +312,7 @@ def draw_pixel_items(cfg: Config, kind: str, items: Sequence[int], mode: str = "
     if noise and math.isfinite(cfg.snr):
         sd = math.sqrt(1.0 / (cfg.snr * cfg.n * cfg.n))
     stream = 4 if kind == "templates" else 5
+    if backend == "torch":
+        return pixel_images_torch(p, cfg.n, sd, seed=cfg.seed * 1000003 + stream, device=device), p
     seeds = [[cfg.seed, stream, it] for it in items]
     return pixel_images(p, cfg.n, sd, seeds), p
