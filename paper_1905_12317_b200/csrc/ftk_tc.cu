@@ -43,6 +43,18 @@
 namespace ftk {
 using namespace sm100;
 
+// Diagnostics (wait-cycle counters, FTK_S1_TRACE / FTK_S3_TRACE, FTK_S3_DBG) are compiled in only with
+// -DFTK_DIAG=1 (build.py: FTK_DIAG=1 in the environment): clock reads and runtime checks inside the MMA
+// and epilogue loops measurably slow them down.
+#ifndef FTK_DIAG
+#define FTK_DIAG 0
+#endif
+constexpr bool kDiag = FTK_DIAG != 0;
+__device__ __forceinline__ long long diag_clock() {
+  if constexpr (kDiag) return clock64();
+  return 0;
+}
+
 constexpr int S3_WARPS = 11;
 constexpr int S3_THREADS = S3_WARPS * 32;
 constexpr int S3_MAXG = TcPlan::MAXG;
@@ -130,13 +142,13 @@ __device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[
   const uint32_t idesc = idesc_bf16_f32(128, a.NCH);
   const int ksteps = KS > 0 ? KS : a.K3p / 16, halfk = a.K3p / 2, ke = a.ke_steps;
   uint32_t g_a = 0, g_d = 0;
-  const long long tr0 = clock64();
+  const long long tr0 = diag_clock();
   for (int p = a.p_begin; p < a.p_end; ++p) {
     for (int T = 0; T < a.NRT; ++T, ++g_a) {
       const int ab = g_a & 1, s = g_a % a.NS;
-      long long t1 = clock64();
+      long long t1 = diag_clock();
       mbar_wait(&S.st_full[s], (g_a / a.NS) & 1);
-      tr[1] += clock64() - t1;
+      tr[1] += diag_clock() - t1;
       tc_fence_after();
       const uint32_t a_hi0 = a.tmem + a.acol0 + (uint32_t)(ab * a.K3p);
       // staging -> TMEM A slot (after the MMAs that last read this slot: in-order tensor pipe)
@@ -148,12 +160,12 @@ __device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[
       tc_commit(&S.st_empty[s]);
       for (int c = 0; c < a.nch; ++c, ++g_d) {
         const int db = g_d & 1;
-        t1 = clock64();
+        t1 = diag_clock();
         mbar_wait(&S.d_empty[db], ((g_d >> 1) & 1) ^ 1);
-        tr[2] += clock64() - t1;
+        tr[2] += diag_clock() - t1;
         tc_fence_after();
         if constexpr (TR) {  // (FTK_S3_TRACE) compile-time: a runtime branch here slows the MMA issue
-          if (g_d < 64) a.trace[16 + 4 * g_d] = clock64();
+          if (g_d < 64) a.trace[16 + 4 * g_d] = diag_clock();
         }
         const uint32_t dE = a.tmem + (uint32_t)(db * 2 * a.NCH), dO = dE + (uint32_t)a.NCH;
         const uint32_t bch = a.ybase + (uint32_t)(c * (a.NCH / 8)) * a.SBO;
@@ -181,12 +193,12 @@ __device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[
         }
         tc_commit(&S.d_full[db]);
         if constexpr (TR) {
-          if (g_d < 64) a.trace[16 + 4 * g_d + 1] = clock64();
+          if (g_d < 64) a.trace[16 + 4 * g_d + 1] = diag_clock();
         }
       }
     }
   }
-  tr[0] = clock64() - tr0;
+  tr[0] = diag_clock() - tr0;
 }
 
 // MODE 0: fused max / argmax (the north-star epilogue).  MODE 1: marginalization epilogue (SURVEY 8(f)
@@ -333,15 +345,15 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         const bool active = T * 128 + q * 32 < n;  // warp-uniform: lane quarters beyond n_psi idle
         for (int c = 0; c < nch; ++c, ++g_d) {
           const int db = g_d & 1;
-          long long te = clock64();
-          if (P.dbg & 4) {  // (diagnostics) one poller + named barrier
+          long long te = diag_clock();
+          if (kDiag && (P.dbg & 4)) {  // (diagnostics) one poller + named barrier
             if (warp == 2) mbar_wait(&S.d_full[db], (g_d >> 1) & 1);
             named_bar(3, 256);
           } else {
             mbar_wait(&S.d_full[db], (g_d >> 1) & 1);  // every epilogue warp (suspending try_wait)
           }
-          tr_e += clock64() - te;
-          te = clock64();
+          tr_e += diag_clock() - te;
+          te = diag_clock();
           tc_fence_after();
           const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(db * 2 * NCH + h * hw);
           const int clb = c * NCH + h * hw;  // first column of this warp's half chunk
@@ -362,7 +374,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           const uint32_t kb = ((uint32_t)T << 24) | ((uint32_t)clb << 7) | (uint32_t)row;
           auto grp0 = [&](auto G) {
             constexpr int g8 = decltype(G)::value;
-            if (MODE != 0 || !active || (P.dbg & 1) || 8 * g8 >= hw) return;
+            if (MODE != 0 || !active || (kDiag && (P.dbg & 1)) || 8 * g8 >= hw) return;
             uint32_t e[8], o[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -405,7 +417,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           };
           // all-fast half chunks (the common case): branch-free over the groups [G0, G1) so the FADD / max
           // chains of different groups interleave; the serial compare-select only per group maximum
-          const bool allfast = MODE == 0 && active && !(P.dbg & 1) && nfast >= hw;
+          const bool allfast = MODE == 0 && active && !(kDiag && (P.dbg & 1)) && nfast >= hw;
           auto fast_range = [&](auto G0, auto G1) {
             constexpr int g0 = decltype(G0)::value, g1 = decltype(G1)::value;
             float m[5];
@@ -453,7 +465,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           // two-phase drain: columns [0, 16) first; the rest is loaded while MODE 0 processes them
           // (tcgen05.wait::ld waits for all of a thread's loads; the empty asm "+r" ties each register to
           // the wait so no use is scheduled before it)
-          const bool ld = active && !(P.dbg & 2);
+          const bool ld = active && !(kDiag && (P.dbg & 2));
           if (ld) {
             tmem_ld16(base, *reinterpret_cast<uint32_t(*)[16]>(e0));
             if (has_odd) tmem_ld16(base + NCH, *reinterpret_cast<uint32_t(*)[16]>(o0));
@@ -480,7 +492,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&S.d_empty[db]);
-          tr_x += clock64() - te;
+          tr_x += diag_clock() - te;
           phase2();
           // MODE 1, all-fast half chunks: branch-free over NG compile-time groups
           auto marg_fast = [&](auto NGc) {
@@ -813,7 +825,7 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
   S1Smem& S = *a.S;
   const uint32_t idesc = idesc_bf16_f32(128, 128);
   uint32_t g_st = 0, g_acc = 0, g_u = 0;
-  const long long tr0 = clock64();
+  const long long tr0 = diag_clock();
   // generation rounds: R = 2 when the K' chunks split by radial halves (NKCH % 4 == 0): round r fills the
   // chunks kc with (kc mod NKCH/2) in [r NKCH/4, (r+1) NKCH/4), i.e. m in [r n_k/2, (r+1) n_k/2)
   const int R = (a.NKCH % 4 == 0) ? 2 : 1;
@@ -823,24 +835,24 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
     bool got0 = false, got1 = false;
     for (int t = 0; t < a.nit; ++t, ++g_acc) {
       const int ab = g_acc & 1;
-      long long t1 = clock64();
+      long long t1 = diag_clock();
       mbar_wait(&S.acc_empty[ab], ((g_acc >> 1) & 1) ^ 1);
-      tr[2] += clock64() - t1;
+      tr[2] += diag_clock() - t1;
       tc_fence_after();
       const uint32_t d = a.tmem + 256 + (uint32_t)(ab * 128);
       for (int kc = 0; kc < a.NKCH; ++kc, ++g_st) {
         const int s = g_st % S1_STAGES;
         const int rr = round_of(kc);
         if (rr == 0 ? !got0 : !got1) {  // the generated operand chunk of this round (first tile of a unit)
-          t1 = clock64();
+          t1 = diag_clock();
           mbar_wait(&S.a_full[rr], g_u & 1);
-          tr[1] += clock64() - t1;
+          tr[1] += diag_clock() - t1;
           tc_fence_after();
           if (rr == 0) got0 = true; else got1 = true;
         }
-        t1 = clock64();
+        t1 = diag_clock();
         mbar_wait(&S.st_full[s], (g_st / S1_STAGES) & 1);
-        tr[3] += clock64() - t1;
+        tr[3] += diag_clock() - t1;
         tc_fence_after();
         const uint32_t st = a.sbase + s * a.stage_bytes;
         const uint64_t bh0 = smem_desc_kmajor_noswz(st, 128, a.SBO);
@@ -863,7 +875,7 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
       tc_commit(&S.acc_full[ab]);
     }
   }
-  tr[0] = clock64() - tr0;
+  tr[0] = diag_clock() - tr0;
   return g_u;
 }
 
@@ -2004,7 +2016,7 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
   if (cpg > pb.count) cpg = pb.count;
   if (cpg < 1) cpg = 1;
   static unsigned long long* d_trace = nullptr;  // diagnostics: FTK_S3_TRACE=1 prints CTA 0's counters
-  const char* tenv = std::getenv("FTK_S3_TRACE");
+  const char* tenv = kDiag ? std::getenv("FTK_S3_TRACE") : nullptr;  // needs a -DFTK_DIAG=1 build
   if (tenv && tenv[0] == '1') {
     if (!d_trace) cudaMalloc(&d_trace, (16 + 4 * 64 + 64) * sizeof(unsigned long long));
     cudaMemsetAsync(d_trace, 0, (16 + 4 * 64 + 64) * sizeof(unsigned long long), s);
@@ -2079,7 +2091,7 @@ void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const Pair
   const int units = P.n_psi * prm.NCT;
   const int grid = units < tc.num_sms ? units : tc.num_sms;
   static unsigned long long* d_trace = nullptr;  // diagnostics: FTK_S1_TRACE=1 prints CTA 0's counters
-  const char* tenv = std::getenv("FTK_S1_TRACE");
+  const char* tenv = kDiag ? std::getenv("FTK_S1_TRACE") : nullptr;  // needs a -DFTK_DIAG=1 build
   prm.trace = nullptr;
   if (tenv && tenv[0] == '1') {
     if (!d_trace) cudaMalloc(&d_trace, 16 * sizeof(unsigned long long));
