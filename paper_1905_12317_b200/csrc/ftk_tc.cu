@@ -1229,12 +1229,13 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int E>
+template <int E, bool FB>  // FB: Form B input (the tensor-core Step 1) at compile time
 __global__ void __launch_bounds__(256, 3) k_step2_fft(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
-                                                      int npair, int formB, DevPlan P, S2Blocks B,
+                                                      int npair, DevPlan P, S2Blocks B,
                                                       const float2* __restrict__ twtab,
                                                       const __grid_constant__ CUtensorMap zmap) {
   extern __shared__ __align__(1024) uint8_t s2raw[];
+  constexpr bool formB = FB;
   constexpr int n = 32 * E;  // FFT length = n_gamma (>= n_psi; zero-padded input, reading R21)
   constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
   constexpr int RS = n + n / E;  // padded staging row (words): index r + r / E
@@ -1507,22 +1508,19 @@ static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, 
             B.nb * npair < 2 * tc.num_sms ? B.nb * npair : 2 * tc.num_sms);
   const size_t smem = step2_smem(P.n_psi, P.n_gamma);
   const int items = B.nb * npair;
-  int occ = 2;  // resident CTAs per SM (registers <= 80 at E <= 16; shared memory decides)
+  auto run = [&](auto kern) {
+    int occ = 2;  // resident CTAs per SM (registers <= 80 at E <= 16; shared memory decides)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+    occ = std::max(1, std::min(occ, 4));
+    dim3 grid(items < occ * tc.num_sms ? items : occ * tc.num_sms);
+    kern<<<grid, 256, smem, s>>>(Zhat, Zop, npair, P, B, tc.d_s2tw, zmap);
+  };
   switch (P.n_gamma) {
-    case 64: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2_fft<2>, 256, smem); break;
-    case 128: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2_fft<4>, 256, smem); break;
-    case 256: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2_fft<8>, 256, smem); break;
-    case 512: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2_fft<16>, 256, smem); break;
-    default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step2_fft<32>, 256, smem); break;
-  }
-  occ = std::max(1, std::min(occ, 4));
-  dim3 grid(items < occ * tc.num_sms ? items : occ * tc.num_sms);
-  switch (P.n_gamma) {
-    case 64: k_step2_fft<2><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
-    case 128: k_step2_fft<4><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
-    case 256: k_step2_fft<8><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
-    case 512: k_step2_fft<16><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
-    default: k_step2_fft<32><<<grid, 256, smem, s>>>(Zhat, Zop, npair, formB, P, B, tc.d_s2tw, zmap); break;
+    case 64: formB ? run(k_step2_fft<2, true>) : run(k_step2_fft<2, false>); break;
+    case 128: formB ? run(k_step2_fft<4, true>) : run(k_step2_fft<4, false>); break;
+    case 256: formB ? run(k_step2_fft<8, true>) : run(k_step2_fft<8, false>); break;
+    case 512: formB ? run(k_step2_fft<16, true>) : run(k_step2_fft<16, false>); break;
+    default: formB ? run(k_step2_fft<32, true>) : run(k_step2_fft<32, false>); break;
   }
   return FTK_OK;
 }
@@ -1910,11 +1908,16 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       cudaMemcpy(tc.d_s2tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice);
     }
     const int sm2 = (int)step2_smem(pm.n_psi, n_gamma);
-    cudaFuncSetAttribute(k_step2_fft<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    cudaFuncSetAttribute(k_step2_fft<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
   }
   const char* sdbg = std::getenv("FTK_SYNC_DEBUG");
   tc.sync_debug = sdbg && sdbg[0] == '1';
