@@ -17,12 +17,13 @@
 //     hi/lo, canonical K-major core matrices) into a shared-memory staging ring.
 //   * warp 0 (one elected lane): per r-tile 2 x K3p/16 tcgen05.cp.128x256b staging -> TMEM A slot, then
 //     per chunk 3 x K3p/16 tcgen05.mma M128 x NCH x K16 (A = Z r-tile from TMEM, B = Y chunk from SMEM)
-//     into the E / O accumulators of one of two TMEM buffers.  cp and mma execute in issue order, so
-//     the A slots need no barriers.
-//   * warps 2-9: epilogue -- per chunk, tcgen05.ld of this warp's E and O columns into registers and
-//     immediate release of the TMEM buffer; then per thread the running max of E + |O| =
-//     max(E + O, E - O) and its 8-column group (branch-free); per pair the partial records go to the
-//     resolver through shared memory (no CTA-wide barrier).
+//     into the E / O accumulators of one of two TMEM buffers, the k-steps unrolled at compile time
+//     (s3_mma_loop<KS>).  cp and mma execute in issue order, so the A slots need no barriers.
+//   * warps 2-9: epilogue -- per chunk, tcgen05.ld of this warp's E and O columns into registers in two
+//     phases (columns [0, 16) first, the rest loaded while those are reduced) and release of the TMEM
+//     buffer; per thread the running max of E + |O| = max(E + O, E - O) and its 8-column group
+//     (branch-free over all-fast half chunks); per pair the partial records go to the resolver through
+//     shared memory (no CTA-wide barrier).  MODE 1 replaces the max by a log-sum-exp (marginalization).
 //   * warp 10: resolver -- merges the 8 partial records, recomputes the 16 E / O sums of the pair's
 //     winning group in fp32 from the same bf16 operands to recover the exact (shift, sign), one
 //     packed-key atomicMax per pair.
