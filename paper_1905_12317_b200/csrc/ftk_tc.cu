@@ -781,7 +781,7 @@ static size_t s3_smem_bytes(int ncol, int K3p, int NS) {
 // Real GEMM per p with K' = 2 n_k:  rows (j, zeta, part) of the GENERATED operand c (A, in TMEM):
 //   Re-row = [c_r | -c_i],  Im-row = [c_i | c_r];  columns = images, B = [a_r | a_i] (pre-split, SMEM).
 // Output Zhat' [pair][p][Hs] complex (pair = il * nj + jl within the block; Hs = H_plus rounded up to even).
-constexpr int S1_THREADS = 14 * 32;
+constexpr int S1_THREADS = 18 * 32;  // 0 producer, 1 MMA, 2-9 generators, 10-17 epilogue
 constexpr int S1_STAGES = 4;
 
 struct S1Params {
@@ -880,7 +880,7 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
   return g_u;
 }
 
-__global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
+__global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
   extern __shared__ __align__(1024) uint8_t s1_raw[];
   S1Smem& S = *reinterpret_cast<S1Smem*>(s1_raw);
   uint8_t* stages = s1_raw + 1024;                                   // S1_STAGES x stage_bytes
@@ -899,7 +899,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.acc_full[i], 1);
-      mbar_init(&S.acc_empty[i], 128);
+      mbar_init(&S.acc_empty[i], 256);
     }
     fence_barrier_init();
   }
@@ -1030,7 +1030,8 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
     // ---------------- epilogue: accumulator [128 rows (j,zeta,part)] x [128 images] -> Zhat'
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int ew = warp - 10;  // 0..3
+    const int ew = warp - 10;  // 0..7
+    const int eh = ew >> 2;    // image half of the TMEM columns this warp drains
     uint32_t g_acc = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int p, ct;
@@ -1052,7 +1053,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
         mbar_wait(&S.acc_full[ab], (g_acc >> 1) & 1);
         tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + 256 + (uint32_t)(ab * 128);
-        for (int c0 = 0; c0 < 128; c0 += 16) {
+        for (int c0 = 64 * eh; c0 < 64 * eh + 64; c0 += 16) {
           uint32_t r16[16];
           tmem_ld16(base + c0, r16);
           tmem_wait_ld();
@@ -1061,10 +1062,10 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
         }
         tc_fence_before();
         mbar_arrive(&S.acc_empty[ab]);
-        named_bar(2, 128);
+        named_bar(2, 256);
         // write-out: image ii, complex column cc = (template jl, term z) -> Zhat'[pair (il, jl)][p][z]
         // (runs of consecutive terms of one pair row)
-        for (int ii = ew; ii < 128; ii += 4) {
+        for (int ii = ew; ii < 128; ii += 8) {
           const int il = t * 128 + ii;  // local image index within the block
           if (il >= P.ni) continue;
           float2* dst = P.Zhat + ((size_t)il * P.nj * n + p) * P.Hs;
@@ -1072,7 +1073,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_step1_tc(S1Params P) {
           for (int h = 0; h < 2; ++h)
             if (cval[h]) dst[coff[h]] = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
         }
-        named_bar(2, 128);
+        named_bar(2, 256);
       }
     }
   }
