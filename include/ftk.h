@@ -101,6 +101,8 @@ typedef struct {
   int s3_groups;             /* engine 0: rep-groups (Y slices resident in shared memory) */
   int s3_rtiles;             /* engine 0: 128-row rotation tiles per pair (MMA M) */
   int n_gamma;               /* rotations per (pair, shift): gamma_r = 2 pi r / n_gamma */
+  int n_tau;                 /* CTF plans (ftk_plan_create_ctf): number of filters; 0 for plain plans */
+  int N_t_base;              /* the caller's shift count; N_t = N_t_base * max(n_tau, 1) shift entries */
 } ftk_plan_info_t;
 
 /* Build the plan (host, double precision, untimed per P:1321): radial rule, per-ell operator SVD of
@@ -111,6 +113,28 @@ typedef struct {
  * On error *out is NULL. */
 ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double* shifts_xy_px,
                              int N_t, double eps, const ftk_plan_opts_t* opts, ftk_plan_t* out);
+
+/* The plan's radial rule without building a plan (host only): k_m, w_m for n_k nodes on [0, k_max],
+ * k_max = 2 pi K / n rad/px (reading R1), radial_rule as in ftk_plan_opts_t (sum w = k_max^2/2).
+ * k_out, w_out: caller-allocated host double[n_k].  Used to evaluate CTF filters on the nodes before
+ * ftk_plan_create_ctf.  Errors: FTK_EINVAL (bad argument), FTK_ENUMERIC. */
+ftk_status_t ftk_radial_rule(int n, double K, int n_k, int radial_rule, double* k_out, double* w_out);
+
+/* CTF-parameterized factorized kernel (Sec. 6 "Other 2D kernels"; SURVEY 8(f)
+ * NEXT-4; DESIGN reading R24).  The translation kernel times a family of radial filters (contrast
+ * transfer functions, one per defocus tau) is factorized as
+ *     F(delta, k) c_tau(|k|) ~= sum_zeta Y_zeta(delta, tau) G_zeta(k),   G_zeta(k) = G_zeta(|k|) e^{i ell psi},
+ * per Bessel order ell by one SVD over rows (x_i, tau) (Gauss-Jacobi(0,1) nodes in x = K|delta|, weight 1
+ * per tau) and columns k_m (the plan's radial rule, weight w_m); Sigma > eps kept.  Alignment then
+ * evaluates X(delta_t, gamma_r, tau) = <R_gamma T_delta A, c_tau B> for every filter: the same Steps 1-3
+ * with the shift list replaced by the n_tau * N_t "virtual shifts" v = tau * N_t + t (tau-major), so
+ * ftk_best_t.shift_idx, landscapes and marginals index v.
+ * filters: host double[n_tau][n_k], the real filter values c_tau(k_m) at this plan's radial nodes (see
+ * ftk_radial_rule; any real radial filter — the library does not fix a CTF model).  Other arguments and
+ * errors as ftk_plan_create; FTK_EINVAL also for n_tau <= 0, filters == NULL, non-finite filter values. */
+ftk_status_t ftk_plan_create_ctf(int n, double K, double delta_max_px, const double* shifts_xy_px, int N_t,
+                                 int n_tau, const double* filters, double eps, const ftk_plan_opts_t* opts,
+                                 ftk_plan_t* out);
 
 void ftk_plan_destroy(ftk_plan_t plan);
 

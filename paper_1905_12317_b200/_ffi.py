@@ -23,7 +23,7 @@ class PlanInfo(C.Structure):
                 ("engine", C.c_int), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
                 ("K3p", C.c_int), ("n_rep", C.c_int), ("s3_cols", C.c_int),
                 ("s3_nch", C.c_int), ("s3_groups", C.c_int), ("s3_rtiles", C.c_int),
-                ("n_gamma", C.c_int)]
+                ("n_gamma", C.c_int), ("n_tau", C.c_int), ("N_t_base", C.c_int)]
 
 
 class Best(C.Structure):
@@ -33,6 +33,9 @@ class Best(C.Structure):
 SYMBOLS = {
     "ftk_plan_create": (C.c_int, [C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_int, C.c_double,
                                   C.POINTER(PlanOpts), C.POINTER(C.c_void_p)]),
+    "ftk_plan_create_ctf": (C.c_int, [C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                      C.c_double, C.POINTER(PlanOpts), C.POINTER(C.c_void_p)]),
+    "ftk_radial_rule": (C.c_int, [C.c_int, C.c_double, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "ftk_plan_destroy": (None, [C.c_void_p]),
     "ftk_plan_query": (C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
     "ftk_plan_radial": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),

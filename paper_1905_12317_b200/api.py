@@ -50,19 +50,41 @@ def best_to_numpy(t) -> np.ndarray:
     return np.ascontiguousarray(a).view(BEST_DTYPE).reshape(-1)
 
 
+def radial_rule(n: int, K: float, n_k: int = 0, rule: int = 0):
+    """ftk_radial_rule: the radial nodes/weights (k_m, w_m) a plan with these arguments uses (host)."""
+    L = _ffi.lib()
+    n_k = n_k if n_k > 0 else int(round(K))
+    k, w = np.empty(n_k), np.empty(n_k)
+    st = L.ftk_radial_rule(n, float(K), n_k, rule, k.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p))
+    if st != 0:
+        raise FTKError(st, "ftk_radial_rule failed")
+    return k, w
+
+
 class FTKPlan:
-    """One FTK plan (ftk_plan_create) bound to one CUDA device (or host-only with device=-1)."""
+    """One FTK plan (ftk_plan_create) bound to one CUDA device (or host-only with device=-1).
+
+    filters: optional real array [n_tau, n_k] of radial filters (CTFs) on the plan's radial nodes
+    (radial_rule()); then the plan is ftk_plan_create_ctf's CTF-parameterized kernel and every result
+    indexes the virtual shift v = tau * N_t + t (split_ctf_index)."""
 
     def __init__(self, n: int, K: float, delta_max: float, shifts, eps: float, *, n_k: int = 0, n_psi: int = 0,
                  radial_rule: int = 0, device: int = 0, rank: int = 0, world: int = 1, engine: int = ENGINE_TC,
-                 svd_nodes: int = 0, workspace_bytes: int = 0, n_gamma: int = 0):
+                 svd_nodes: int = 0, workspace_bytes: int = 0, n_gamma: int = 0, filters=None):
         self._L = _ffi.lib()
         sh = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(-1, 2))
         opts = _ffi.PlanOpts(n_k, n_psi, radial_rule, device, rank, world, engine, svd_nodes, workspace_bytes,
                              n_gamma)
         out = C.c_void_p()
-        st = self._L.ftk_plan_create(n, float(K), float(delta_max), sh.ctypes.data_as(C.c_void_p), sh.shape[0],
-                                     float(eps), C.byref(opts), C.byref(out))
+        if filters is None:
+            st = self._L.ftk_plan_create(n, float(K), float(delta_max), sh.ctypes.data_as(C.c_void_p), sh.shape[0],
+                                         float(eps), C.byref(opts), C.byref(out))
+        else:
+            f = np.ascontiguousarray(np.asarray(filters, dtype=np.float64))
+            f = f.reshape(1, -1) if f.ndim == 1 else f
+            st = self._L.ftk_plan_create_ctf(n, float(K), float(delta_max), sh.ctypes.data_as(C.c_void_p),
+                                             sh.shape[0], f.shape[0], f.ctypes.data_as(C.c_void_p), float(eps),
+                                             C.byref(opts), C.byref(out))
         if st != 0:
             raise FTKError(st, "ftk_plan_create failed")
         self._p = out
@@ -80,6 +102,12 @@ class FTKPlan:
         if p:
             self._L.ftk_plan_destroy(p)
             self._p = None
+
+    def split_ctf_index(self, v):
+        """Virtual shift index v -> (shift t, filter tau) for CTF plans ((v, 0) for plain plans)."""
+        v = np.asarray(v)
+        nb = self.info["N_t_base"]
+        return v % nb, v // nb
 
     # ---------------- plan queries (host)
     def radial(self):

@@ -158,11 +158,13 @@ int ftk_version(void) { return 100; }
 
 const char* ftk_last_error(ftk_plan_t plan) { return plan ? plan->err.c_str() : ""; }
 
-ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double* shifts_xy_px, int N_t, double eps,
-                             const ftk_plan_opts_t* opts, ftk_plan_t* out) {
+static ftk_status_t plan_create_impl(int n, double K, double delta_max_px, const double* shifts_xy_px, int N_t,
+                                     int n_tau, const double* filters, double eps, const ftk_plan_opts_t* opts,
+                                     ftk_plan_t* out) {
   if (!out) return FTK_EINVAL;
   *out = nullptr;
-  if (!shifts_xy_px || N_t <= 0) return FTK_EINVAL;
+  if (!shifts_xy_px || N_t <= 0 || n_tau < 0 || (n_tau > 0 && !filters)) return FTK_EINVAL;
+  if (n_tau > 0 && (long long)N_t * n_tau > (1LL << 30)) return FTK_EINVAL;
   ftk_plan_t plan = new (std::nothrow) ftk_plan_s();
   if (!plan) return FTK_ENOMEM;
   ftk_plan_opts_t o;
@@ -173,12 +175,23 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
   pm.K_cycles = K;
   pm.delta_max = delta_max_px;
   pm.eps = eps;
-  pm.N_t = N_t;
   pm.n_k = o.n_k > 0 ? o.n_k : (int)std::lround(K);
   pm.n_psi = o.n_psi > 0 ? o.n_psi : 4 * (int)std::lround(K);
   pm.rule = o.radial_rule;
   pm.svd_nodes = o.svd_nodes > 0 ? o.svd_nodes : 96;
-  pm.shifts.assign(shifts_xy_px, shifts_xy_px + 2 * (size_t)N_t);
+  if (n_tau > 0) {
+    // CTF-parameterized kernel (reading R24): virtual shift v = tau * N_t + t, tau-major
+    pm.n_tau = n_tau;
+    pm.N_base = N_t;
+    pm.filt.assign(filters, filters + (size_t)n_tau * pm.n_k);
+    pm.N_t = N_t * n_tau;
+    pm.shifts.clear();
+    for (int ta = 0; ta < n_tau; ++ta) pm.shifts.insert(pm.shifts.end(), shifts_xy_px, shifts_xy_px + 2 * (size_t)N_t);
+  } else {
+    pm.N_t = N_t;
+    pm.shifts.assign(shifts_xy_px, shifts_xy_px + 2 * (size_t)N_t);
+  }
+  N_t = pm.N_t;
   plan->device = o.device;
   plan->world = o.world > 0 ? o.world : 1;
   plan->rank = o.rank;
@@ -321,6 +334,31 @@ ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double*
   return FTK_OK;
 }
 
+ftk_status_t ftk_plan_create(int n, double K, double delta_max_px, const double* shifts_xy_px, int N_t, double eps,
+                             const ftk_plan_opts_t* opts, ftk_plan_t* out) {
+  return plan_create_impl(n, K, delta_max_px, shifts_xy_px, N_t, 0, nullptr, eps, opts, out);
+}
+
+ftk_status_t ftk_plan_create_ctf(int n, double K, double delta_max_px, const double* shifts_xy_px, int N_t,
+                                 int n_tau, const double* filters, double eps, const ftk_plan_opts_t* opts,
+                                 ftk_plan_t* out) {
+  if (n_tau <= 0) {
+    if (out) *out = nullptr;
+    return FTK_EINVAL;
+  }
+  return plan_create_impl(n, K, delta_max_px, shifts_xy_px, N_t, n_tau, filters, eps, opts, out);
+}
+
+ftk_status_t ftk_radial_rule(int n, double K, int n_k, int radial_rule, double* k_out, double* w_out) {
+  if (n <= 0 || !(K > 0) || n_k <= 0 || n_k > 1024 || (radial_rule != 0 && radial_rule != 1) || !k_out || !w_out)
+    return FTK_EINVAL;
+  std::vector<double> k, w;
+  if (!radial_rule_nodes(n_k, 2.0 * M_PI * K / n, radial_rule, k, w)) return FTK_ENUMERIC;
+  std::memcpy(k_out, k.data(), n_k * sizeof(double));
+  std::memcpy(w_out, w.data(), n_k * sizeof(double));
+  return FTK_OK;
+}
+
 void ftk_plan_destroy(ftk_plan_t plan) {
   if (!plan) return;
   if (plan->device >= 0) {
@@ -381,6 +419,8 @@ ftk_status_t ftk_plan_query(ftk_plan_t plan, ftk_plan_info_t* info) {
   info->K3p = plan->K3p;
   info->n_rep = plan->engine == 0 ? plan->tc.n_rep : plan->pm.N_t;
   info->n_gamma = plan->n_gamma;
+  info->n_tau = pm.n_tau;
+  info->N_t_base = pm.n_tau > 0 ? pm.N_base : pm.N_t;
   info->s3_cols = plan->engine == 0 ? plan->tc.ncol : plan->pm.N_t;
   info->s3_nch = plan->engine == 0 ? plan->tc.NCH : 0;
   info->s3_groups = plan->engine == 0 ? plan->tc.G : 0;

@@ -222,6 +222,22 @@ bool svd_jacobi(int m, int n, std::vector<double>& A, std::vector<double>& S, st
   return conv;
 }
 
+bool radial_rule_nodes(int n_k, double k_max, int rule, std::vector<double>& k, std::vector<double>& w) {
+  std::vector<double> t, om;
+  if (rule == 0) {
+    gauss_legendre(n_k, t, om);
+  } else if (!gauss_jacobi(n_k, 0.0, 1.0, t, om)) {
+    return false;
+  }
+  k.resize(n_k);
+  w.resize(n_k);
+  for (int m = 0; m < n_k; ++m) {
+    k[m] = 0.5 * k_max * (1.0 + t[m]);
+    w[m] = rule == 0 ? om[m] * 0.5 * k_max * k[m] : om[m] * 0.25 * k_max * k_max;
+  }
+  return true;
+}
+
 namespace {
 struct Kept {
   int ell, eta;
@@ -255,26 +271,9 @@ int PlanMath::build() {
   const double a = 2.0 * kPi * W;
 
   // ---- radial rule
-  std::vector<double> t, om;
-  if (rule == 0) {
-    gauss_legendre(n_k, t, om);
-    k.resize(n_k);
-    w.resize(n_k);
-    for (int m = 0; m < n_k; ++m) {
-      k[m] = 0.5 * k_max * (1.0 + t[m]);
-      w[m] = om[m] * 0.5 * k_max * k[m];
-    }
-  } else {
-    if (!gauss_jacobi(n_k, 0.0, 1.0, t, om)) {
-      error = "Gauss-Jacobi radial rule: QL iteration failed";
-      return FTK_ENUMERIC;
-    }
-    k.resize(n_k);
-    w.resize(n_k);
-    for (int m = 0; m < n_k; ++m) {
-      k[m] = 0.5 * k_max * (1.0 + t[m]);
-      w[m] = om[m] * 0.25 * k_max * k_max;
-    }
+  if (!radial_rule_nodes(n_k, k_max, rule, k, w)) {
+    error = "Gauss-Jacobi radial rule: QL iteration failed";
+    return FTK_ENUMERIC;
   }
   {
     double sw = 0;
@@ -285,8 +284,20 @@ int PlanMath::build() {
     }
   }
 
-  // ---- Nystrom nodes (Gauss-Jacobi(0,1) on [0,a] and [0,1])
-  const int N = svd_nodes;
+  const bool ctf = n_tau > 0;
+  if (ctf && ((int)filt.size() != n_tau * n_k || N_base <= 0 || N_base * n_tau != N_t)) {
+    error = "ftk_plan_create_ctf: filter table / shift list size mismatch";
+    return FTK_EINVAL;
+  }
+  for (double x : filt)
+    if (!std::isfinite(x)) {
+      error = "ftk_plan_create_ctf: non-finite filter value";
+      return FTK_EINVAL;
+    }
+
+  // ---- Nystrom nodes (Gauss-Jacobi(0,1) on [0,a] and [0,1]).  CTF mode: the k side is the radial
+  // rule itself (the filters are known only on k_m), so the x side needs N n_tau >= n_k rows.
+  const int N = ctf ? std::max(svd_nodes, (n_k + n_tau - 1) / n_tau) : svd_nodes;
   std::vector<double> tj, oj;
   if (!gauss_jacobi(N, 0.0, 1.0, tj, oj)) {
     error = "Gauss-Jacobi Nystrom nodes: QL iteration failed";
@@ -303,17 +314,30 @@ int PlanMath::build() {
   }
   const double calH = std::max(kPi * std::exp(2.0) * W, std::log(2.0 * kPi * W / eps)) + 1.5;  // Theorem 1
   const int Lc = std::min(400, (int)std::ceil(2.0 * calH));
-  std::vector<double> Jtab((size_t)N * N * (Lc + 1));
+  // CTF mode: y_m = k_m / K with weights w_m / K^2 (the same y dy measure, sum 1/2); rows (x_i, tau)
+  // with weight 1 per tau, so the discarded tail bounds every filter's error (reading R24).
+  const int NY = ctf ? n_k : N;
+  const int NR = ctf ? N * n_tau : N;
+  std::vector<double> ymv(NY), symv(NY);
+  for (int j = 0; j < NY; ++j) {
+    ymv[j] = ctf ? k[j] / k_max : ys[j];
+    symv[j] = ctf ? std::sqrt(w[j]) / k_max : swy[j];
+  }
+  std::vector<double> Jtab((size_t)N * NY * (Lc + 1));
   for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N; ++j) bessel_j_all(xs[i] * ys[j], Lc, &Jtab[((size_t)i * N + j) * (Lc + 1)]);
+    for (int j = 0; j < NY; ++j) bessel_j_all(xs[i] * ymv[j], Lc, &Jtab[((size_t)i * NY + j) * (Lc + 1)]);
 
   std::vector<Kept> kept;
   sigma_all.clear();
   for (int ell = 0; ell <= Lc; ++ell) {
-    std::vector<double> M((size_t)N * N), S, Vm;
-    for (int j = 0; j < N; ++j)
-      for (int i = 0; i < N; ++i) M[(size_t)j * N + i] = swx[i] * Jtab[((size_t)i * N + j) * (Lc + 1) + ell] * swy[j];
-    if (!svd_jacobi(N, N, M, S, Vm)) {
+    std::vector<double> M((size_t)NR * NY), S, Vm;
+    for (int j = 0; j < NY; ++j)
+      for (int r = 0; r < NR; ++r) {
+        const int i = r % N, ta = r / N;
+        const double cf = ctf ? filt[(size_t)ta * n_k + j] : 1.0;
+        M[(size_t)j * NR + r] = swx[i] * Jtab[((size_t)i * NY + j) * (Lc + 1) + ell] * cf * symv[j];
+      }
+    if (!svd_jacobi(NR, NY, M, S, Vm)) {
       error = "one-sided Jacobi SVD did not converge";
       return FTK_ENUMERIC;
     }
@@ -324,20 +348,20 @@ int PlanMath::build() {
       }
     sigma_all.push_back(S);
     int nk = 0;
-    for (int e = 0; e < N; ++e) {
+    for (int e = 0; e < NY; ++e) {
       if (!(S[e] > eps)) break;
       ++nk;
       Kept kp;
       kp.ell = ell;
       kp.eta = e;
       kp.sigma = S[e];
-      kp.Ux.assign(&M[(size_t)e * N], &M[(size_t)e * N] + N);
-      kp.Vy.assign(&Vm[(size_t)e * N], &Vm[(size_t)e * N] + N);
+      kp.Ux.assign(&M[(size_t)e * NR], &M[(size_t)e * NR] + NR);
+      kp.Vy.assign(&Vm[(size_t)e * NY], &Vm[(size_t)e * NY] + NY);
       // sign convention: largest-|v| node value positive (products U Sigma V are sign-free)
       int jm = 0;
       double best = -1;
-      for (int j = 0; j < N; ++j) {
-        double v = std::fabs(kp.Vy[j] / swy[j]);
+      for (int j = 0; j < NY; ++j) {
+        double v = std::fabs(kp.Vy[j] / symv[j]);
         if (v > best) { best = v; jm = j; }
       }
       if (kp.Vy[jm] < 0) {
@@ -382,19 +406,43 @@ int PlanMath::build() {
   };
   // v at y_m = k_m / k_max
   std::vector<double> Jb(ell_max + 1);
-  std::vector<double> Jym((size_t)n_k * N * (ell_max + 1));
+  const int NJ = ctf ? 0 : N;  // plain-mode Nystrom tables only
+  std::vector<double> Jym((size_t)n_k * NJ * (ell_max + 1));
   for (int m = 0; m < n_k; ++m)
-    for (int i = 0; i < N; ++i) bessel_j_all(xs[i] * (k[m] / k_max), ell_max, &Jym[((size_t)m * N + i) * (ell_max + 1)]);
-  std::vector<double> Jxt((size_t)N_t * N * (ell_max + 1));
+    for (int i = 0; i < NJ; ++i) bessel_j_all(xs[i] * (k[m] / k_max), ell_max, &Jym[((size_t)m * N + i) * (ell_max + 1)]);
+  std::vector<double> Jxt((size_t)N_t * NJ * (ell_max + 1));
   std::vector<double> dd(N_t), ww(N_t);
   for (int tt = 0; tt < N_t; ++tt) {
     dd[tt] = std::hypot(shifts[2 * tt], shifts[2 * tt + 1]);
     ww[tt] = std::atan2(shifts[2 * tt + 1], shifts[2 * tt]);
-    for (int j = 0; j < N; ++j) bessel_j_all(k_max * dd[tt] * ys[j], ell_max, &Jxt[((size_t)tt * N + j) * (ell_max + 1)]);
+    for (int j = 0; j < NJ; ++j) bessel_j_all(k_max * dd[tt] * ys[j], ell_max, &Jxt[((size_t)tt * N + j) * (ell_max + 1)]);
   }
   G.assign((size_t)H * n_k, 0.0);
   Y.assign((size_t)N_t * H, 0.0);
-  for (int z = 0; z < H; ++z) {
+  if (ctf) {
+    // k side: v(y_m) = V_m / sqrt(wy_m) directly on the radial nodes; (delta, tau) side by the Nystrom
+    // extension u(x, tau) = (1/s) sum_m J_ell(x y_m) c_tau(k_m) sqrt(wy_m) V_m at x = K |delta_t|.
+    std::vector<double> Jt((size_t)N_base * n_k * (ell_max + 1));
+    for (int tt = 0; tt < N_base; ++tt)
+      for (int m = 0; m < n_k; ++m) bessel_j_all(k_max * dd[tt] * ymv[m], ell_max, &Jt[((size_t)tt * n_k + m) * (ell_max + 1)]);
+    for (int z = 0; z < H; ++z) {
+      const Term& tm = terms[z];
+      const int L = std::abs(tm.ell);
+      const Kept& kp = find_kept(L, tm.eta);
+      const double par = (tm.ell < 0 && (L & 1)) ? -1.0 : 1.0;
+      for (int m = 0; m < n_k; ++m) G[(size_t)z * n_k + m] = tm.sigma * par * (kp.Vy[m] / symv[m]) / k_max;
+      for (int tt = 0; tt < N_t; ++tt) {
+        const int tb = tt % N_base, ta = tt / N_base;
+        double acc = 0;
+        for (int m = 0; m < n_k; ++m)
+          acc += Jt[((size_t)tb * n_k + m) * (ell_max + 1) + L] * filt[(size_t)ta * n_k + m] * symv[m] * kp.Vy[m];
+        const double U = k_max * acc / kp.sigma;
+        const double ph = -tm.ell * (ww[tt] + 0.5 * kPi);
+        Y[(size_t)tt * H + z] = std::complex<double>(U * std::cos(ph), U * std::sin(ph));
+      }
+    }
+  }
+  for (int z = 0; z < (ctf ? 0 : H); ++z) {
     const Term& tm = terms[z];
     const int L = std::abs(tm.ell);
     const Kept& kp = find_kept(L, tm.eta);
@@ -438,7 +486,8 @@ int PlanMath::build() {
           for (int l = 0; l <= 2 * ell_max; ++l) fs += c[l] * eil[(size_t)l * n_psi + p];
           const double psi = 2.0 * kPi * p / n_psi;
           const double ph = -k[m] * (shifts[2 * tt] * std::cos(psi) + shifts[2 * tt + 1] * std::sin(psi));
-          worst = std::max(worst, std::abs(std::complex<double>(std::cos(ph), std::sin(ph)) - fs));
+          const double cf = ctf ? filt[(size_t)(tt / N_base) * n_k + m] : 1.0;
+          worst = std::max(worst, std::abs(cf * std::complex<double>(std::cos(ph), std::sin(ph)) - fs));
         }
       }
     }

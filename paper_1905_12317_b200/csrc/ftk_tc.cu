@@ -1782,7 +1782,8 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       const double x = pm.shifts[2 * t], y = pm.shifts[2 * t + 1];
       if (x != 0.0 || y != 0.0) {
         for (int u = t + 1; u < pm.N_t; ++u)
-          if (!taken[u] && std::fabs(pm.shifts[2 * u] + x) <= 1e-12 * (1.0 + std::fabs(x)) &&
+          if (!taken[u] && (pm.n_tau == 0 || u / pm.N_base == t / pm.N_base) &&  // same filter (CTF)
+              std::fabs(pm.shifts[2 * u] + x) <= 1e-12 * (1.0 + std::fabs(x)) &&
               std::fabs(pm.shifts[2 * u + 1] + y) <= 1e-12 * (1.0 + std::fabs(y))) {
             mate = u;
             taken[u] = 1;

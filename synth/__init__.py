@@ -7,5 +7,5 @@ polar grid whose radial nodes are passed in by the caller, or samples them at pi
 """
 from .workloads import (  # noqa: F401
     CONFIGS, Config, config, shift_list, delta_max, draw_items, blob_params,
-    polar_samples, add_noise, make_polar_set, planted_truth, pixel_images, draw_pixel_items,
+    polar_samples, add_noise, make_polar_set, planted_truth, pixel_images, draw_pixel_items, ctf_filters,
 )

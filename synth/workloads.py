@@ -316,3 +316,24 @@ def draw_pixel_items(cfg: Config, kind: str, items: Sequence[int], mode: str = "
         return pixel_images_torch(p, cfg.n, sd, seed=cfg.seed * 1000003 + stream, device=device), p
     seeds = [[cfg.seed, stream, it] for it in items]
     return pixel_images(p, cfg.n, sd, seeds), p
+
+
+def ctf_filters(k_nodes, defocus_A, pixel_A: float = 4.0, kv: float = 300.0, cs_mm: float = 2.7,
+                amp_contrast: float = 0.07, bfactor_A2: float = 0.0):
+    """Isotropic weak-phase CTFs (the model of Mindell & Grigorieff, which PAPER.md P:1397-1399 cites for
+    the defocus parametrization) on radial nodes k [rad/px], one row per defocus [Angstrom]:
+        c(s) = -(sqrt(1 - A^2) sin chi(s) + A cos chi(s)) exp(-B s^2 / 4),
+        chi(s) = pi lambda dF s^2 - (pi/2) Cs lambda^3 s^4,   s = k / (2 pi pixel_A)  [1/Angstrom],
+    lambda the relativistic electron wavelength at kv.  An INPUT generator (the filters are inputs of
+    the CTF-parameterized kernel, reading R24); nothing of the method's arithmetic lives here."""
+    k = np.asarray(k_nodes, dtype=np.float64)
+    V = kv * 1e3
+    lam = 12.2643247 / math.sqrt(V * (1.0 + 0.978466e-6 * V))
+    cs = cs_mm * 1e7
+    s = k / (2.0 * math.pi * pixel_A)
+    out = []
+    for df in np.atleast_1d(np.asarray(defocus_A, dtype=np.float64)):
+        chi = math.pi * lam * df * s ** 2 - 0.5 * math.pi * cs * lam ** 3 * s ** 4
+        c = -(math.sqrt(1.0 - amp_contrast ** 2) * np.sin(chi) + amp_contrast * np.cos(chi))
+        out.append(c * np.exp(-bfactor_A2 * s ** 2 / 4.0))
+    return np.stack(out)

@@ -92,3 +92,52 @@ def test_merge_host_tie_break(ftk):
     assert vals[0] == 1.0 and out[0, 1] == 3          # equal values -> smaller template
     assert vals[1] == 2.0 and tuple(out[1, 1:]) == (9, 0, 5)   # equal template -> smaller shift
     assert vals[2] == 0.5 and out[2, 1] == 1          # missing record (-1) loses
+
+
+@pytest.mark.parametrize("name,defoci", [("tiny", [8000.0, 15000.0, 22000.0, 30000.0]), ("c2", [10000.0, 20000.0])])
+def test_host_ctf_plan_matches_oracle(ftk, name, defoci):
+    """ftk_plan_create_ctf (reading R24) vs oracle.ctf: same terms, Sigma and rank-1 factors on the virtual
+    shift list; ftk_radial_rule == the oracle's rule."""
+    from oracle import ctf
+    cfg = synth.config(name)
+    sh = synth.shift_list(cfg)
+    k, w = ftk.radial_rule(cfg.n, cfg.K, cfg.n_k, 0)
+    ko, wo = quadrature.radial_rule(cfg.n_k, cfg.k_max)
+    assert np.max(np.abs(k - ko)) < 1e-13 and np.max(np.abs(w - wo)) < 1e-12 * np.max(wo)
+    f = synth.ctf_filters(k, defoci)
+    p = ftk.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), sh, cfg.eps, n_k=cfg.n_k, n_psi=cfg.n_psi, device=-1,
+                    filters=f)
+    op = ctf.build_plan_ctf(cfg.n, cfg.K, synth.delta_max(cfg), sh, cfg.eps, cfg.n_k, cfg.n_psi,
+                            synth.ctf_filters(ko, defoci), n_nodes=96)
+    assert p.info["n_tau"] == len(defoci) and p.info["N_t_base"] == len(sh)
+    assert p.info["N_t"] == len(defoci) * len(sh) and p.info["H"] == op.H
+    ell, eta, sig = p.terms()
+    assert list(ell) == [t.ell for t in op.terms] and list(eta) == [t.eta for t in op.terms]
+    assert np.max(np.abs(sig - np.array([t.sigma for t in op.terms]))) < 1e-10
+    G, Y = p.factors()
+    for z in range(op.H):
+        P1 = np.outer(Y[:, z], G[z])
+        P2 = np.outer(op.Y[:, z], op.G[z])
+        assert np.max(np.abs(P1 - P2)) < 1e-8 * max(1.0, np.max(np.abs(P2)))
+    assert abs(p.info["certificate"] - ctf.kernel_certificate_ctf(op, f)) < 1e-9
+    t, tau = p.split_ctf_index(np.array([0, len(sh) + 3, p.info["N_t"] - 1]))
+    assert list(t) == [0, 3, len(sh) - 1] and list(tau) == [0, 1, len(defoci) - 1]
+
+
+def test_host_ctf_plan_errors(ftk):
+    cfg = synth.config("tiny")
+    sh = synth.shift_list(cfg)
+    bad = np.ones((2, cfg.n_k))
+    bad[1, 3] = np.nan
+    with pytest.raises(ftk.FTKError) as e:
+        ftk.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), sh, cfg.eps, n_k=16, n_psi=64, device=-1, filters=bad)
+    assert e.value.status == 1
+    L = ftk.lib()
+    import ctypes as C
+    out = C.c_void_p()
+    shp = np.ascontiguousarray(sh)
+    st = L.ftk_plan_create_ctf(cfg.n, cfg.K, synth.delta_max(cfg), shp.ctypes.data_as(C.c_void_p), len(sh), 0,
+                               None, cfg.eps, None, C.byref(out))
+    assert st == 1 and not out.value
+    k = np.empty(4)
+    assert L.ftk_radial_rule(cfg.n, cfg.K, 4, 7, k.ctypes.data_as(C.c_void_p), k.ctypes.data_as(C.c_void_p)) == 1
