@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--marginal-tau", type=float, default=0.0,
                     help="> 0: time the marginalization epilogue (log sum exp(X / tau) per pair, NEXT-3) instead "
                          "of max / argmax (1 GPU; not the headline metric)")
+    ap.add_argument("--ctf-defoci", default="",
+                    help="comma-separated defoci [Angstrom]: CTF-parameterized kernel (NEXT-4, reading R24); "
+                         "the metric counts every (pair, shift, rotation, defocus) (no e2e / cpu_baseline legs)")
     return ap.parse_args()
 
 
@@ -214,8 +217,14 @@ def main():
     shifts = synth.shift_list(cfg)
     n_t = shifts.shape[0]
     engine = pkg.ENGINE_TC if args.engine == "tc" else pkg.ENGINE_SIMT
+    defoci = [float(x) for x in args.ctf_defoci.split(",") if x.strip()]
+    filters = None
+    if defoci:
+        filters = synth.ctf_filters(pkg.radial_rule(cfg.n, cfg.K, cfg.n_k, 0)[0], defoci)
+        n_t *= len(defoci)                      # virtual shifts (tau, t)
+        args.no_e2e = args.no_cpu_baseline = True
     plan = pkg.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), shifts, cfg.eps, n_k=cfg.n_k, n_psi=cfg.n_psi,
-                       device=local, rank=rank, world=world, engine=engine, n_gamma=args.n_gamma)
+                       device=local, rank=rank, world=world, engine=engine, n_gamma=args.n_gamma, filters=filters)
     n_gamma = plan.info["n_gamma"]
     k, w = plan.radial()
     # synthetic inputs generated on the device (seeded), resident in HBM
@@ -402,6 +411,8 @@ def main():
                            "n_gamma": n_gamma,
                            "N_im": ni, "N_tm": nj, "N_t": n_t, "eps": cfg.eps, "H": info["H"],
                            "H_plus": info["H_plus"], "K3": info["K3"], "engine": args.engine,
+                           **({"ctf_defoci_A": defoci, "n_tau": len(defoci),
+                               "ctf_model": "weak-phase, 300 kV, Cs 2.7 mm, A 0.07, 4 A/px"} if defoci else {}),
                            "parallelism": f"template-shard x{world}", "l2": "inputs (6+ GB FB arrays) exceed L2",
                            "input": (f"pixels {cfg.n}x{cfg.n} float32 (NUFFT front end in the step)" if args.pixels
                                      else "polar Fourier samples complex64 [N][n_k][n_psi]"),
