@@ -129,3 +129,32 @@ def test_ctf_width_limit(pkg):
     p.load_templates(torch.from_numpy(tpls).cuda())
     X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), op))
     _check_best(pkg.best_to_numpy(p.align()["best"]), X, fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w))
+
+
+def test_ctf_n_gamma_and_sharding(pkg):
+    """CTF plan with n_gamma = 2 n_psi (reading R21) vs the oracle at the same angles, and 2 template shards
+    (run one after the other on one GPU) merged with ftk_merge_bests equal to the 1-rank result bitwise."""
+    cfg = synth.config("tiny")
+    ng = 2 * cfg.n_psi
+    p, op = _plans(pkg, cfg, DEF2, 0, n_gamma=ng)
+    k, w = p.radial()
+    imgs, _ = synth.draw_items(cfg, "images", range(3), k)
+    tpls, _ = synth.draw_items(cfg, "templates", range(4), k)
+    p.load_images(torch.from_numpy(imgs).cuda())
+    p.load_templates(torch.from_numpy(tpls).cuda())
+    res = p.align(landscape=True)
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), op, n_gamma=ng))
+    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+    L = res["landscape"].cpu().numpy()
+    assert L.shape == X.shape
+    assert np.max(np.abs(L - X) / (na[:, None, None, None] * nb[None, :, None, None])) <= TOL
+    _check_best(pkg.best_to_numpy(res["best"]), X, na, nb)
+    b1 = pkg.best_to_numpy(res["best"])
+    recs = []
+    for rank in range(2):
+        pr, _ = _plans(pkg, cfg, DEF2, 0, n_gamma=ng, rank=rank, world=2)
+        pr.load_images(torch.from_numpy(imgs).cuda())
+        pr.load_templates(torch.from_numpy(tpls).cuda())
+        recs.append(pr.align()["best"])
+    m = pkg.best_to_numpy(pkg.merge_bests(torch.cat(recs), 2, 3))
+    assert np.array_equal(m.view(np.int32), b1.view(np.int32))
