@@ -51,6 +51,13 @@ using namespace sm100;
 #define FTK_DIAG 0
 #endif
 constexpr bool kDiag = FTK_DIAG != 0;
+#ifndef FTK_S1_HINT
+#define FTK_S1_HINT 2
+#endif
+// Step-1 L2 cache policies: bit 1 (default): image-operand stages evict_last (the 8 modes in flight stay
+// L2-resident under the Zhat' write stream: c3 Step 1 -14 %, c3 x 2 defoci -5 %, c5 unchanged);
+// bit 0: Zhat' stores evict_first (c3 +8-13 %, rejected); bit 2: template rows evict_last (experiment)
+constexpr int kS1Hint = FTK_S1_HINT;
 __device__ __forceinline__ long long diag_clock() {
   if constexpr (kDiag) return clock64();
   return 0;
@@ -925,7 +932,10 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
             mbar_wait(&S.st_empty[s], ((g_st / S1_STAGES) & 1) ^ 1);
             mbar_arrive_expect_tx(&S.st_full[s], stage_bytes);
             const uint8_t* src = P.Aop + (((size_t)p * P.NIT + it0 + t) * P.NKCH + kc) * stage_bytes;
-            bulk_g2s(stages + s * stage_bytes, src, stage_bytes, &S.st_full[s]);
+            if constexpr ((kS1Hint & 2) != 0)
+              bulk_g2s_hint(stages + s * stage_bytes, src, stage_bytes, &S.st_full[s], l2_policy_evict_last());
+            else
+              bulk_g2s(stages + s * stage_bytes, src, stage_bytes, &S.st_full[s]);
           }
         }
       }
@@ -964,6 +974,7 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
     // the quarter pair a quarter of n_k; R = 1 -> each warp half of n_k (n_k < 32: a half would be
     // narrower than one 16-node STTM step; the first-half warps do all nodes)
     const int R = (P.NKCH % 4 == 0) ? 2 : 1;
+    const uint64_t pol_b = (kS1Hint & 4) ? l2_policy_evict_last() : 0;
     uint32_t g_u = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++g_u) {
       int p, ct;
@@ -998,7 +1009,10 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
           for (int e = 0; e < 8; ++e) {
             const int m = m0 + 16 * s2 + 2 * e;
             const bool ok = valid && m < m_end;
-            bb[s2][e] = ok ? __ldg(reinterpret_cast<const float4*>(brow + m)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            if constexpr ((kS1Hint & 4) != 0)
+              bb[s2][e] = ok ? ldg_f4_hint(reinterpret_cast<const float4*>(brow + m), pol_b) : make_float4(0.f, 0.f, 0.f, 0.f);
+            else
+              bb[s2][e] = ok ? __ldg(reinterpret_cast<const float4*>(brow + m)) : make_float4(0.f, 0.f, 0.f, 0.f);
             gg[s2][e] = ok ? __ldg(reinterpret_cast<const float2*>(grow + m)) : make_float2(0.f, 0.f);
           }
 #pragma unroll
@@ -1032,6 +1046,7 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
     const int row = q * 32 + lane;
     const int ew = warp - 10;  // 0..7
     const int eh = ew >> 2;    // image half of the TMEM columns this warp drains
+    const uint64_t pol_st = (kS1Hint & 1) ? l2_policy_evict_first() : 0;
     uint32_t g_acc = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int p, ct;
@@ -1071,7 +1086,13 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
           float2* dst = P.Zhat + ((size_t)il * P.nj * n + p) * P.Hs;
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            if (cval[h]) dst[coff[h]] = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
+            if (cval[h]) {
+              const float2 v = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
+              if constexpr ((kS1Hint & 1) != 0)
+                st_f2_hint(dst + coff[h], v, pol_st);
+              else
+                dst[coff[h]] = v;
+            }
         }
         named_bar(2, 256);
       }
