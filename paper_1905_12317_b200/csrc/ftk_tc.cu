@@ -298,6 +298,12 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
           case 6: s3_mma_loop<6, false>(a, tr); break;
           case 7: s3_mma_loop<7, false>(a, tr); break;
           case 8: s3_mma_loop<8, false>(a, tr); break;
+          case 9: s3_mma_loop<9, false>(a, tr); break;    // K3p > 128: CTF plans
+          case 10: s3_mma_loop<10, false>(a, tr); break;
+          case 11: s3_mma_loop<11, false>(a, tr); break;
+          case 12: s3_mma_loop<12, false>(a, tr); break;
+          case 13: s3_mma_loop<13, false>(a, tr); break;
+          case 14: s3_mma_loop<14, false>(a, tr); break;
           default: s3_mma_loop<0, false>(a, tr); break;
         }
       }
@@ -1778,9 +1784,11 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
                  const std::vector<int>& col, const std::vector<float>& Y3, int K3p, int Ke, int n_gamma,
                  std::string& msg) {
   tc_plan_free(tc);
-  if (K3p % 16 != 0 || K3p > 128) {
+  // TMEM: two A slots (K3p columns each) + two D buffers of E and O (4 NCH columns) <= 512, NCH >= 16.
+  // K3p <= 128 keeps NCH >= 64 (full-rate MMAs); wider contractions (CTF plans) run with narrower chunks.
+  if (K3p % 16 != 0 || K3p > 224) {
     msg = "tensor-core engine: Step-3 width " + std::to_string(K3p) + " (K3 = 2 H_plus - H0 = " +
-          std::to_string(pm.K3) + " plus block padding) exceeds 128 (use engine=1)";
+          std::to_string(pm.K3) + " plus block padding) exceeds 224 (use engine=1)";
     return FTK_EINVAL;
   }
   if (pm.n_psi % 64 != 0 || pm.n_psi > 1024) {

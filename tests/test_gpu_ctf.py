@@ -112,23 +112,36 @@ def test_ctf_marginal(pkg):
 
 
 def test_ctf_width_limit(pkg):
-    """c3 x 4 defoci needs K3p = 224 > 128: the tensor-core engine refuses (FTK_EINVAL), the SIMT
-    engine runs it."""
-    cfg = synth.config("c3")
+    """c5 x 4 defoci needs K3p = 288 > 224: the tensor-core engine refuses (FTK_EINVAL)."""
+    cfg = synth.config("c5")
     k, _ = pkg.radial_rule(cfg.n, cfg.K, cfg.n_k, 0)
     f = synth.ctf_filters(k, DEF4)
     with pytest.raises(pkg.FTKError) as e:
         pkg.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), synth.shift_list(cfg), cfg.eps, n_k=cfg.n_k,
                     n_psi=cfg.n_psi, device=0, engine=0, filters=f)
     assert e.value.status == 1
-    p, op = _plans(pkg, cfg, DEF4, 1)
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("name,defoci,ni,nj", [("c3", DEF4, 3, 7), ("c5", DEF2, 2, 3)])
+def test_ctf_wide_step3(pkg, engine, name, defoci, ni, nj):
+    """Contractions wider than 128 (c3 x 4 defoci: K3p = 224, Step-3 chunks of N = 16; c5 x 2: K3p = 160,
+    N = 32) on both engines vs the oracle, with sampled landscapes."""
+    cfg = synth.config(name)
+    p, op = _plans(pkg, cfg, defoci, engine)
+    assert p.info["K3p"] > 128
     k, w = p.radial()
-    imgs, _ = synth.draw_items(cfg, "images", range(2), k)
-    tpls, _ = synth.draw_items(cfg, "templates", range(3), k)
+    imgs, _ = synth.draw_items(cfg, "images", range(ni), k)
+    tpls, _ = synth.draw_items(cfg, "templates", range(nj), k)
     p.load_images(torch.from_numpy(imgs).cuda())
     p.load_templates(torch.from_numpy(tpls).cuda())
     X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), op))
-    _check_best(pkg.best_to_numpy(p.align()["best"]), X, fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w))
+    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+    _check_best(pkg.best_to_numpy(p.align()["best"]), X, na, nb)
+    ii, jj = np.array([0, ni - 1]), np.array([nj - 1, 0])
+    Lp = p.landscape_pairs(ii, jj).cpu().numpy()
+    for n in range(2):
+        assert np.max(np.abs(Lp[n] - X[ii[n], jj[n]])) <= TOL * na[ii[n]] * nb[jj[n]]
 
 
 def test_ctf_n_gamma_and_sharding(pkg):
