@@ -1259,7 +1259,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int E, bool FB>  // FB: Form B input (the tensor-core Step 1) at compile time
-__global__ void __launch_bounds__(256, 3) k_step2_fft(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
+__global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
                                                       int npair, DevPlan P, S2Blocks B,
                                                       const float2* __restrict__ twtab,
                                                       const __grid_constant__ CUtensorMap zmap) {
