@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--marginal-tau", type=float, default=0.0,
                     help="> 0: time the marginalization epilogue (log sum exp(X / tau) per pair, NEXT-3) instead "
                          "of max / argmax (1 GPU; not the headline metric)")
+    ap.add_argument("--eps", type=float, default=0.0, help="override the config's eps (debug only)")
     ap.add_argument("--ctf-defoci", default="",
                     help="comma-separated defoci [Angstrom]: CTF-parameterized kernel (NEXT-4, reading R24); "
                          "the metric counts every (pair, shift, rotation, defocus) (no e2e / cpu_baseline legs)")
@@ -211,7 +212,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = f"cuda:{local}"
-    cfg = synth.config(args.config)
+    cfg = synth.config(args.config, **({"eps": args.eps} if args.eps > 0 else {}))
     ni = args.images or cfg.N_im
     nj = args.templates or cfg.N_tm
     shifts = synth.shift_list(cfg)
