@@ -54,6 +54,7 @@ def parse():
                     help="> 0: time the marginalization epilogue (log sum exp(X / tau) per pair, NEXT-3) instead "
                          "of max / argmax (1 GPU; not the headline metric)")
     ap.add_argument("--eps", type=float, default=0.0, help="override the config's eps (debug only)")
+    ap.add_argument("--workspace-gb", type=float, default=0.0, help="fixed pair-block workspace (debug only)")
     ap.add_argument("--ctf-defoci", default="",
                     help="comma-separated defoci [Angstrom]: CTF-parameterized kernel (NEXT-4, reading R24); "
                          "the metric counts every (pair, shift, rotation, defocus) (no e2e / cpu_baseline legs)")
@@ -225,7 +226,8 @@ def main():
         n_t *= len(defoci)                      # virtual shifts (tau, t)
         args.no_e2e = args.no_cpu_baseline = True
     plan = pkg.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), shifts, cfg.eps, n_k=cfg.n_k, n_psi=cfg.n_psi,
-                       device=local, rank=rank, world=world, engine=engine, n_gamma=args.n_gamma, filters=filters)
+                       device=local, rank=rank, world=world, engine=engine, n_gamma=args.n_gamma, filters=filters,
+                       workspace_bytes=int(args.workspace_gb * (1 << 30)))
     n_gamma = plan.info["n_gamma"]
     k, w = plan.radial()
     # synthetic inputs generated on the device (seeded), resident in HBM
