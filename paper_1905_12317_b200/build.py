@@ -18,6 +18,8 @@ HEADERS = ["ftk_plan_math.h", "ftk_internal.cuh", "ftk_tc.cuh", "ftk_sm100.cuh",
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"]
+if os.environ.get("FTK_S1_PLO"):  # (experiment) Step-1 modes interleaved in the unit order
+    FLAGS += ["-DFTK_S1_PLO=" + os.environ["FTK_S1_PLO"]]
 if os.environ.get("FTK_S1_HINT"):  # (experiment) Step-1 L2 cache hints
     FLAGS += ["-DFTK_S1_HINT=" + os.environ["FTK_S1_HINT"]]
 if os.environ.get("FTK_DIAG") == "1":  # wait-cycle counters / trace / FTK_S3_DBG (remove _build/ to switch)

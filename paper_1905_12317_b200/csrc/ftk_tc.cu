@@ -812,10 +812,14 @@ struct S1Params {
 // Unit order: u -> (mode p, column tile ct) with p = 8 p_hi + p_lo, p_lo fastest, then ct, then p_hi.
 // The ~148 units in flight then share 8 image-operand modes (L2-resident) and write 8 consecutive
 // p-rows of each of their pairs' Zhat' rows together (contiguous runs merged in L2).
+#ifndef FTK_S1_PLO
+#define FTK_S1_PLO 8
+#endif
 __device__ __forceinline__ void s1_unit(int u, int NCT, int& p, int& ct) {
-  const int p_lo = u & 7, rest = u >> 3;
+  constexpr int PLO = FTK_S1_PLO;
+  const int p_lo = u % PLO, rest = u / PLO;
   ct = rest % NCT;
-  p = (rest / NCT) * 8 + p_lo;
+  p = (rest / NCT) * PLO + p_lo;
 }
 
 struct S1Smem {
