@@ -805,7 +805,7 @@ struct S1Params {
   float2* Zhat;         // [pair][p][Hs]
   int i0, ni, j0, nj;   // block (i0 multiple of 128)
   int n, n_k, Hp, Hs, KCH, NKCH, NIT;  // NIT = image tiles per mode in Aop
-  int F, NCT;           // F = nj * Hp flattened (j, zeta) columns, NCT = ceil(F / 64)
+  int F, NCT;           // F = nj * Hs flattened (j, zeta slot) columns (pad slots written as zeros), NCT = ceil(F / 64)
   unsigned long long* trace;  // nullable (FTK_S1_TRACE=1): wait cycle counters of CTA 0
 };
 
@@ -990,12 +990,15 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
       int p, ct;
       s1_unit(u, P.NCT, p, ct);
       const int f = ct * 64 + c;
-      const bool valid = f < P.F;
       int jl = 0, z = 0;
-      if (valid) {
-        jl = f / P.Hp;
-        z = f - jl * P.Hp;
+      if (f < P.F) {
+        jl = f / P.Hs;
+        z = f - jl * P.Hs;
       }
+      // slots z >= Hp (the Zhat' row padding, Hs > Hp) get zero operand rows, so the epilogue writes whole
+      // rows: a never-written slot leaves a partial 32-byte sector in every row, which L2 must complete by a
+      // DRAM read-modify-write (that made Step 1 2x slower whenever Hs > Hp)
+      const bool valid = f < P.F && z < P.Hp;
       const int qt = valid ? ((p + __ldg(P.ell + z)) & (n - 1)) : 0;
       const float2* brow = P.B + ((size_t)(P.j0 + jl) * n + qt) * nk;
       const float* grow = P.g + (size_t)z * nk;
@@ -1069,8 +1072,8 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
       for (int h = 0; h < 2; ++h) {
         const int cc = lane + 32 * h;
         const int f = ct * 64 + cc;
-        const int jl = f / P.Hp, z = f - jl * P.Hp;
-        cval[h] = 2 * cc < nvalid;
+        const int jl = f / P.Hs, z = f - jl * P.Hs;
+        cval[h] = 2 * cc < nvalid;  // pad slots included (zeros)
         coff[h] = (long long)jl * n * P.Hs + z;
       }
       for (int t = 0; t < nit; ++t, ++g_acc) {
@@ -2125,7 +2128,7 @@ void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const Pair
   prm.KCH = tc.KCH;
   prm.NKCH = tc.NKCH;
   prm.NIT = tc.NIT;
-  prm.F = pb.nj * P.H_plus;
+  prm.F = pb.nj * P.Hs;  // (template, slot) columns, pad slots included
   prm.NCT = (prm.F + 63) / 64;
   const int units = P.n_psi * prm.NCT;
   const int grid = units < tc.num_sms ? units : tc.num_sms;
