@@ -793,7 +793,8 @@ static size_t s3_smem_bytes(int ncol, int K3p, int NS) {
 // so that Zhat_zeta(q) = Zhat'_zeta(q - ell) and Step 2 applies e^{-i ell gamma_r} after the FFT.
 // Real GEMM per p with K' = 2 n_k:  rows (j, zeta, part) of the GENERATED operand c (A, in TMEM):
 //   Re-row = [c_r | -c_i],  Im-row = [c_i | c_r];  columns = images, B = [a_r | a_i] (pre-split, SMEM).
-// Output Zhat' [pair][p][Hs] complex (pair = il * nj + jl within the block; Hs = H_plus rounded up to even).
+// Output Zhat' [pair][p][Hs] complex (pair = il * nj + jl within the block; Hs = H_plus rounded up to even, the
+// pad slot written as zero so that every 32-byte sector of a row is written in full).
 constexpr int S1_THREADS = 18 * 32;  // 0 producer, 1 MMA, 2-9 generators, 10-17 epilogue
 constexpr int S1_STAGES = 4;
 
