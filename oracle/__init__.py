@@ -18,6 +18,8 @@ Modules
   closed_form  exact (2 pi)^2 <R_gamma T_delta A, B> for Gaussian-blob images (Eq. planch)
   pixels       pixel images -> polar Fourier samples, the trapezoid sum of Eq. Ahattrap evaluated directly
   bounds       Lemma 2 / Theorem 1 rank bounds, empirical fit, RMS error bound
+  ctf          CTF-parameterized kernel (Sec. 6, DESIGN reading R24): the filtered brute force and the
+               joint (delta, tau) factorization per ell
 
 Parity status: every function here is pinned by tests in tests/test_oracle_*.py
 (see DESIGN.md "Oracle pins"); none is "parity unpinned".
