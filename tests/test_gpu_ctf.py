@@ -171,3 +171,24 @@ def test_ctf_n_gamma_and_sharding(pkg):
         recs.append(pr.align()["best"])
     m = pkg.best_to_numpy(pkg.merge_bests(torch.cat(recs), 2, 3))
     assert np.array_equal(m.view(np.int32), b1.view(np.int32))
+
+
+def test_ctf_wide_marginal(pkg):
+    """Marginalization epilogue (MODE 1) with the narrow Step-3 chunks of a wide CTF plan (c3 x 4 defoci,
+    K3p = 224, N = 16)."""
+    cfg = synth.config("c3")
+    p, op = _plans(pkg, cfg, DEF4, 0)
+    assert p.info["K3p"] > 128
+    k, w = p.radial()
+    imgs, _ = synth.draw_items(cfg, "images", range(3), k)
+    tpls, _ = synth.draw_items(cfg, "templates", range(5), k)
+    p.load_images(torch.from_numpy(imgs).cuda())
+    p.load_templates(torch.from_numpy(tpls).cuda())
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), op))
+    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+    for f in (0.02, 0.5):
+        tau = f * float(np.median(na[:, None] * nb[None, :]))
+        Lg = p.align_marginal(tau).cpu().numpy()
+        Lo = ftk.log_marginal(X, tau)
+        tol = TOL * na[:, None] * nb[None, :] / tau + 1e-5 * np.maximum(1.0, np.abs(Lo))
+        assert np.all(np.abs(Lg - Lo) <= tol)
