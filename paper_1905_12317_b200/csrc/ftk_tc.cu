@@ -839,7 +839,9 @@ struct S1MmaArgs {
 // Step-1 MMA issue loop (one thread): per unit the generated A operand (TMEM) against every image tile,
 // per stage KS = KCH / 16 k-steps x 3 bf16 products (compile-time unrolled: a runtime loop around
 // tcgen05.mma costs ~500 cycles per stage, scripts/micro_s3.cu).  tr: total, A-wait, acc-wait, stage-wait.
-template <int KS>
+// NK = NKCH at compile time (1, 2, 4; 0 = runtime): the k-chunk loop is then unrolled, which avoids the
+// per-iteration cost of a runtime loop around tcgen05.mma (see the Step-3 note in DESIGN.md)
+template <int KS, int NK>
 __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&tr)[4]) {
   S1Smem& S = *a.S;
   const uint32_t idesc = idesc_bf16_f32(128, 128);
@@ -847,8 +849,9 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
   const long long tr0 = diag_clock();
   // generation rounds: R = 2 when the K' chunks split by radial halves (NKCH % 4 == 0): round r fills the
   // chunks kc with (kc mod NKCH/2) in [r NKCH/4, (r+1) NKCH/4), i.e. m in [r n_k/2, (r+1) n_k/2)
-  const int R = (a.NKCH % 4 == 0) ? 2 : 1;
-  const int hq = a.NKCH / 2, qq = a.NKCH / 4;
+  const int nkch = NK > 0 ? NK : a.NKCH;
+  const int R = (nkch % 4 == 0) ? 2 : 1;
+  const int hq = nkch / 2, qq = nkch / 4;
   auto round_of = [&](int kc) { return R == 2 ? ((kc % hq) >= qq ? 1 : 0) : 0; };
   for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++g_u) {
     bool got0 = false, got1 = false;
@@ -859,37 +862,44 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
       tr[2] += diag_clock() - t1;
       tc_fence_after();
       const uint32_t d = a.tmem + 256 + (uint32_t)(ab * 128);
-      for (int kc = 0; kc < a.NKCH; ++kc, ++g_st) {
+      auto chunk = [&](const int kc) {
         const int s = g_st % S1_STAGES;
-        const int rr = round_of(kc);
-        if (rr == 0 ? !got0 : !got1) {  // the generated operand chunk of this round (first tile of a unit)
+          const int rr = round_of(kc);
+          if (rr == 0 ? !got0 : !got1) {  // the generated operand chunk of this round (first tile of a unit)
+            t1 = diag_clock();
+            mbar_wait(&S.a_full[rr], g_u & 1);
+            tr[1] += diag_clock() - t1;
+            tc_fence_after();
+            if (rr == 0) got0 = true; else got1 = true;
+          }
           t1 = diag_clock();
-          mbar_wait(&S.a_full[rr], g_u & 1);
-          tr[1] += diag_clock() - t1;
+          mbar_wait(&S.st_full[s], (g_st / S1_STAGES) & 1);
+          tr[3] += diag_clock() - t1;
           tc_fence_after();
-          if (rr == 0) got0 = true; else got1 = true;
-        }
-        t1 = diag_clock();
-        mbar_wait(&S.st_full[s], (g_st / S1_STAGES) & 1);
-        tr[3] += diag_clock() - t1;
-        tc_fence_after();
-        const uint32_t st = a.sbase + s * a.stage_bytes;
-        const uint64_t bh0 = smem_desc_kmajor_noswz(st, 128, a.SBO);
-        const uint64_t bl0 = smem_desc_kmajor_noswz(st + a.part_bytes, 128, a.SBO);
-        const uint32_t a_hi0 = a.tmem + (uint32_t)(kc * (KS * 8));
+          const uint32_t st = a.sbase + s * a.stage_bytes;
+          const uint64_t bh0 = smem_desc_kmajor_noswz(st, 128, a.SBO);
+          const uint64_t bl0 = smem_desc_kmajor_noswz(st + a.part_bytes, 128, a.SBO);
+          const uint32_t a_hi0 = a.tmem + (uint32_t)(kc * (KS * 8));
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8);
-          const uint32_t a_lo = a_hi + (uint32_t)a.nk;
-          const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
-          mma_bf16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc);  // +256 B per k-step
-          mma_bf16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
-          mma_bf16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
-        }
-        tc_commit(&S.st_empty[s]);
-        // last tile: a round's chunks are free once its last stage has been read
-        if (t == a.nit - 1 && (R == 1 ? kc == a.NKCH - 1 : (kc == a.NKCH - 1 || kc == hq + qq - 1)))
-          tc_commit(&S.a_empty[R == 1 ? 0 : (kc == a.NKCH - 1 ? 1 : 0)]);
+          for (int ks = 0; ks < KS; ++ks) {
+            const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8);
+            const uint32_t a_lo = a_hi + (uint32_t)a.nk;
+            const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+            mma_bf16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc);  // +256 B per k-step
+            mma_bf16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_bf16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+          }
+          tc_commit(&S.st_empty[s]);
+          // last tile: a round's chunks are free once its last stage has been read
+          if (t == a.nit - 1 && (R == 1 ? kc == nkch - 1 : (kc == nkch - 1 || kc == hq + qq - 1)))
+            tc_commit(&S.a_empty[R == 1 ? 0 : (kc == nkch - 1 ? 1 : 0)]);
+          ++g_st;
+      };
+      if constexpr (NK > 0) {
+#pragma unroll
+        for (int kc = 0; kc < NK; ++kc) chunk(kc);
+      } else {
+        for (int kc = 0; kc < nkch; ++kc) chunk(kc);
       }
       tc_commit(&S.acc_full[ab]);
     }
@@ -898,6 +908,9 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
   return g_u;
 }
 
+// NKC: the k-chunk count at compile time (4: n_k = 128, the c5 shape; 0: runtime), a separate instance so
+// that the unrolled MMA loop does not change the register allocation of the other shapes
+template <int NKC>
 __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
   extern __shared__ __align__(1024) uint8_t s1_raw[];
   S1Smem& S = *reinterpret_cast<S1Smem*>(s1_raw);
@@ -959,10 +972,11 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
                   P.NKCH, nk, units, nit, &S};
       long long tr[4] = {0, 0, 0, 0};
       uint32_t g_u = 0;
-      if (P.KCH == 64)
-        g_u = s1_mma_loop<4>(a, tr);
-      else
-        g_u = s1_mma_loop<2>(a, tr);
+      if (P.KCH == 64) {
+        g_u = s1_mma_loop<4, NKC>(a, tr);
+      } else {
+        g_u = s1_mma_loop<2, 0>(a, tr);
+      }
       if (P.trace && blockIdx.x == 0) {
         P.trace[0] = tr[0];
         P.trace[1] = tr[1];
@@ -1921,7 +1935,8 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   }
   tc.KCH = (2 * pm.n_k) % 64 == 0 ? 64 : 32;
   tc.NKCH = 2 * pm.n_k / tc.KCH;
-  cudaFuncSetAttribute(k_step1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
+  cudaFuncSetAttribute(k_step1_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
+  cudaFuncSetAttribute(k_step1_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
   // Step-2 blocks (s2_block_table); the device term order (tc_term_order, applied in ftk_capi.cu) puts
   // every block's terms in one aligned 8-term window of a Zhat' row (one TMA box)
   {
@@ -2141,7 +2156,10 @@ void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const Pair
     cudaMemsetAsync(d_trace, 0, 16 * sizeof(unsigned long long), s);
     prm.trace = d_trace;
   }
-  k_step1_tc<<<grid, S1_THREADS, s1_smem_bytes(tc), s>>>(prm);
+  if (tc.KCH == 64 && tc.NKCH == 4)
+    k_step1_tc<4><<<grid, S1_THREADS, s1_smem_bytes(tc), s>>>(prm);
+  else
+    k_step1_tc<0><<<grid, S1_THREADS, s1_smem_bytes(tc), s>>>(prm);
   if (prm.trace) {
     unsigned long long h[16];
     cudaMemcpyAsync(h, d_trace, sizeof h, cudaMemcpyDeviceToHost, s);
