@@ -42,7 +42,9 @@ def step2_rotations(Zhat, n_gamma=None):
 
 def ftk_landscapes(a, b, plan: OraclePlan, n_gamma=None):
     """a: FB coeffs of images [I, n_k, n_psi]; b: templates [J, n_k, n_psi] (complex).
-    Returns X [I, J, N_t, n_gamma] complex128 (n_gamma defaults to n_psi)."""
+    Returns X [I, J, N_t, n_gamma] complex128 (n_gamma defaults to n_psi).  The two contractions are
+    plain matrix products per pair (np.matmul, a library primitive), summed over m and zeta exactly as
+    Eq. fbk3 states."""
     a = np.asarray(a, dtype=np.complex128)
     b = np.asarray(b, dtype=np.complex128)
     I, J = a.shape[0], b.shape[0]
@@ -56,9 +58,9 @@ def ftk_landscapes(a, b, plan: OraclePlan, n_gamma=None):
         a_shift = np.roll(a, ell, axis=-1)                      # a_shift[..., q] = a[..., (q - ell) mod n]
         P = a_shift[:, None, :, :] * bc[None, :, :, :]          # [I, J, m, q]
         Gw = 2.0 * math.pi * plan.w[None, :] * plan.G[zs]       # [h, m]
-        Zhat[:, :, zs, :] = np.einsum("hm,ijmq->ijhq", Gw, P)   # Step 1
+        Zhat[:, :, zs, :] = np.matmul(Gw, P)                    # Step 1: sum_m Gw[h, m] P[i, j, m, q]
     Z = step2_rotations(Zhat, n_gamma)                          # Step 2
-    return np.einsum("th,ijhr->ijtr", plan.Y, Z)                # Step 3
+    return np.matmul(plan.Y, Z)                                 # Step 3: sum_h Y[t, h] Z[i, j, h, r]
 
 
 def best_per_image(X):
