@@ -122,6 +122,26 @@ def measured_peaks():
         return None
 
 
+def host_description():
+    """nproc, CPU model and the BLAS thread count the oracle runs with."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        import threadpoolctl
+        blas = [{"api": d.get("internal_api"), "threads": d.get("num_threads")}
+                for d in threadpoolctl.threadpool_info()]
+    except Exception:  # noqa: BLE001
+        blas = None
+    return {"nproc": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+            else None, "cpu_model": model, "blas": blas}
+
+
 def cpu_baseline(cfg, imgs_cpu, tpls_cpu, k_nodes, seconds_budget=15.0):
     """The float64 oracle (as it stands) on a bounded sample of the same workload, on this host's cores."""
     from oracle import fb, ftk, kernel_svd as ks
@@ -151,7 +171,8 @@ def cpu_baseline(cfg, imgs_cpu, tpls_cpu, k_nodes, seconds_budget=15.0):
         thr = os.cpu_count()
     return {"value": ips, "unit": "inner products/s", "cores": int(thr), "kind": "oracle",
             "sample": f"{cfg.name}: {done_pairs} (image, template) pairs x {n_t} shifts x {n_psi} rotations, "
-                      f"float64 numpy oracle (FB coeffs + plan excluded), {dt:.1f} s"}
+                      f"float64 numpy oracle (FB coeffs + plan excluded), {dt:.1f} s",
+            "host": host_description()}
 
 
 def run_reference(args):
@@ -191,7 +212,7 @@ def run_reference(args):
             "config": {"workload": cfg.name, "n": cfg.n, "n_k": cfg.n_k, "n_psi": cfg.n_psi, "N_t": n_t,
                        "eps": cfg.eps, "pairs_per_step": ni * nj},
             "cpu_baseline": {"value": value, "unit": "inner products/s", "cores": int(thr), "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "host": host_description()},
             "e2e": {"value": value, "unit": "inner products/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -210,8 +231,12 @@ def main():
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # the library's own NCCL communicator: ftk_align all-gathers + merges the per-image bests itself
+        # (torch.distributed only carries the 128-byte unique id)
+        comm = pkg.NcclComm.from_group(local)
     dev = f"cuda:{local}"
     cfg = synth.config(args.config, **({"eps": args.eps} if args.eps > 0 else {}))
     ni = args.images or cfg.N_im
@@ -227,7 +252,7 @@ def main():
         args.no_e2e = args.no_cpu_baseline = True
     plan = pkg.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), shifts, cfg.eps, n_k=cfg.n_k, n_psi=cfg.n_psi,
                        device=local, rank=rank, world=world, engine=engine, n_gamma=args.n_gamma, filters=filters,
-                       workspace_bytes=int(args.workspace_gb * (1 << 30)))
+                       workspace_bytes=int(args.workspace_gb * (1 << 30)), nccl_comm=comm)
     n_gamma = plan.info["n_gamma"]
     k, w = plan.radial()
     # synthetic inputs generated on the device (seeded), resident in HBM

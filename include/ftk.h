@@ -34,8 +34,11 @@
  *
  * Multi-GPU: every rank creates a plan with opts.rank/opts.world and calls the same sequence with
  * the same arguments.  Rank r keeps templates [floor(r N/W), floor((r+1) N/W)); ftk_align reports
- * GLOBAL template indices; the caller all-gathers the per-image records (NCCL over NVLink through
- * torch.distributed in the Python binding) and reduces them with ftk_merge_bests().
+ * GLOBAL template indices.  With opts.nccl_comm set (an NCCL communicator of the `world` ranks, e.g.
+ * from ftk_nccl_comm_create), ftk_align itself all-gathers the per-image records over NVLink/NVSwitch
+ * (one ncclAllGather of N_im x 16 B per rank) and merges them on the device with the same tie-break, so
+ * every rank returns the GLOBAL bests.  Without a communicator ftk_align returns this rank's shard-local
+ * bests and the caller may gather them itself and reduce with ftk_merge_bests().
  */
 #ifndef FTK_H_
 #define FTK_H_
@@ -58,12 +61,13 @@ typedef enum {
   FTK_ECUDA = 5,       /* CUDA runtime error (message holds cudaGetErrorString) */
   FTK_ESTATE = 6,      /* wrong call order (e.g. ftk_align before both loads; host-only plan) */
   FTK_ECAPACITY = 7,   /* an optional output buffer is too small, or an index does not fit */
-  FTK_ENODEV = 8       /* no CUDA device / device ordinal invalid */
+  FTK_ENODEV = 8,      /* no CUDA device / device ordinal invalid */
+  FTK_ENCCL = 9        /* NCCL unavailable or an NCCL call failed (message holds ncclGetErrorString) */
 } ftk_status_t;
 
 typedef struct {
   int n_k;              /* radial quadrature nodes; 0 -> round(K)  (configs: n_k = K) */
-  int n_psi;            /* angles per ring = number of rotations; 0 -> 4 round(K); power of two, 16..1024 */
+  int n_psi;            /* angles per ring; 0 -> 4 round(K); power of two, 64..1024 */
   int radial_rule;      /* 0 = Gauss-Legendre x k dk (configs), 1 = Gauss-Jacobi(0,1) (paper P:483-490) */
   int device;           /* CUDA ordinal; -1 = host-only plan: plan math + queries, no device memory */
   int rank, world;      /* template shard of this process; world <= 0 is treated as 1 */
@@ -76,6 +80,9 @@ typedef struct {
   int n_gamma;          /* rotations gamma_r = 2 pi r / n_gamma; 0 -> n_psi.  n_gamma > n_psi evaluates Step 2
                            as the zero-padded trigonometric sum (DESIGN reading R21); power of two,
                            n_psi <= n_gamma <= 1024, engine 0 only (engine 1 -> FTK_EINVAL) */
+  void* nccl_comm;      /* NULL, or an ncclComm_t of `world` ranks in which this process is `rank` (checked
+                           at plan creation, FTK_EINVAL on mismatch): ftk_align then returns global bests on
+                           every rank (see "Multi-GPU" above).  Not owned by the plan. */
 } ftk_plan_opts_t;
 
 /* One per-image (or per-pair) result, 16 bytes. */
@@ -83,7 +90,7 @@ typedef struct {
   float value;               /* Re X at the maximum */
   int32_t template_idx;      /* GLOBAL template index (-1 if no template was seen) */
   int32_t shift_idx;         /* index into the caller's shift list */
-  int32_t rot_idx;           /* r, gamma_r = 2 pi r / n_psi */
+  int32_t rot_idx;           /* r, gamma_r = 2 pi r / n_gamma (n_gamma = n_psi unless opts.n_gamma is set) */
 } ftk_best_t;
 
 typedef struct {
@@ -187,10 +194,14 @@ ftk_status_t ftk_fb_coeffs(ftk_plan_t plan, int which, int64_t first, int64_t co
  *   best      : [N_im] per-image best over this rank's templates (global indices); host or device
  *               pointer (detected); required.
  *   pair_best : nullable, device, [N_im][N_tm_local] per-pair maxima (template_idx global).
- *   landscape : nullable, device, float [N_im][N_tm_local][N_t][n_psi] = Re X; landscape_capacity is its
- *               element count (FTK_ECAPACITY if smaller).
+ *   landscape : nullable, device, float [N_im][N_tm_local][N_t][n_gamma] = Re X; landscape_capacity is its
+ *               element count (FTK_ECAPACITY if smaller, or if the workspace cannot hold a block spanning
+ *               all local templates).
+ * With opts.nccl_comm, `best` holds the GLOBAL bests on every rank (all-gather + device merge on `stream`;
+ * every rank must call ftk_align); pair_best and landscape stay rank-local.
  * The call is asynchronous on `stream` for device outputs; it synchronizes `stream` when `best` is
- * a host pointer.  Errors: FTK_ESTATE (missing load / host-only plan), FTK_ECAPACITY, FTK_ECUDA. */
+ * a host pointer.  Errors: FTK_ESTATE (missing load / host-only plan), FTK_ECAPACITY, FTK_ECUDA,
+ * FTK_ENCCL. */
 ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best, float* landscape,
                        int64_t landscape_capacity, void* stream);
 
@@ -206,10 +217,15 @@ ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best,
  * FTK_ESTATE (missing load / host-only plan), FTK_ECUDA. */
 ftk_status_t ftk_align_marginal(ftk_plan_t plan, double tau, float* log_marginal, void* stream);
 
-/* Full landscapes for selected pairs (sampled parity at large configs).  img_idx / tpl_idx:
- * device int32 [n_pairs] (template index LOCAL to this rank); out: device float [n_pairs][N_t][n_psi]. */
+/* Full landscapes for selected pairs (sampled parity at large configs): X_ij(delta_t, gamma_r) of Eq. fbk3
+ * for the pairs (img_idx[k], tpl_idx[k]).  img_idx / tpl_idx: int32 [n_pairs], host or device
+ * (template index LOCAL to this rank); out: device float [n_pairs][N_t][n_gamma], out_capacity = its
+ * element count (FTK_ECAPACITY if < n_pairs * N_t * n_gamma).  Engine 0 runs the production kernels
+ * (k_step1_tc over the pair's 128-image tile, k_step2_fft, k_step3_tc with landscape output).  Errors:
+ * FTK_EINVAL (null pointer, n_pairs <= 0, an index out of range), FTK_ESTATE, FTK_ECAPACITY, FTK_ECUDA.
+ * Synchronizes `stream` once (index validation); the kernels are asynchronous on it. */
 ftk_status_t ftk_landscape_pairs(ftk_plan_t plan, const int32_t* img_idx, const int32_t* tpl_idx, int n_pairs,
-                                 float* out, void* stream);
+                                 float* out, int64_t out_capacity, void* stream);
 
 /* Deterministic merge of per-rank results: out[i] = best of gathered[r][i] over r (max value, ties ->
  * smallest (template, shift, rot)).  Device pointers; gathered: [world][N_im].  The _host variant
@@ -227,6 +243,16 @@ ftk_status_t ftk_kernel_times(ftk_plan_t plan, double* ms /*[5]*/, int64_t* laun
  * one with A from shared memory, K-major, plus one with an MN-major B operand) against a host reference: writes the max
  * absolute errors (expected ~1e-6, fp32 accumulation of exactly representable bf16 products). */
 ftk_status_t ftk_tc_selftest(int device, double* err_ts, double* err_ss);
+
+/* NCCL communicator helpers (libnccl.so.2 is loaded at run time; FTK_ENCCL if absent).  The usual
+ * bootstrap: rank 0 calls ftk_nccl_unique_id, broadcasts the 128 bytes (any channel: torch.distributed,
+ * MPI, a file), every rank calls ftk_nccl_comm_create with cudaSetDevice already pointing at its GPU (or
+ * passes `device` >= 0), and passes the communicator in ftk_plan_opts_t.nccl_comm.  The caller owns the
+ * communicator (ftk_nccl_comm_destroy after the plans that use it).  Errors: FTK_EINVAL (null pointer,
+ * bad rank/world), FTK_ENODEV, FTK_ENCCL. */
+ftk_status_t ftk_nccl_unique_id(void* id_out /* 128 bytes */);
+ftk_status_t ftk_nccl_comm_create(const void* id /* 128 bytes */, int world, int rank, int device, void** comm_out);
+ftk_status_t ftk_nccl_comm_destroy(void* comm);
 
 const char* ftk_last_error(ftk_plan_t plan);   /* never NULL; "" when no error */
 const char* ftk_status_string(ftk_status_t s);

@@ -11,7 +11,7 @@ LIB_PATH = os.path.join(_HERE, "libftk.so")
 class PlanOpts(C.Structure):
     _fields_ = [("n_k", C.c_int), ("n_psi", C.c_int), ("radial_rule", C.c_int), ("device", C.c_int),
                 ("rank", C.c_int), ("world", C.c_int), ("engine", C.c_int), ("svd_nodes", C.c_int),
-                ("workspace_bytes", C.c_size_t), ("n_gamma", C.c_int)]
+                ("workspace_bytes", C.c_size_t), ("n_gamma", C.c_int), ("nccl_comm", C.c_void_p)]
 
 
 class PlanInfo(C.Structure):
@@ -45,7 +45,11 @@ SYMBOLS = {
     "ftk_load_templates": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
     "ftk_fb_coeffs": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
     "ftk_align": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
-    "ftk_landscape_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    "ftk_landscape_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64,
+                                      C.c_void_p]),
+    "ftk_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "ftk_nccl_comm_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "ftk_nccl_comm_destroy": (C.c_int, [C.c_void_p]),
     "ftk_align_marginal": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]),
     "ftk_polar_from_pixels": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]),
     "ftk_load_images_pixels": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),

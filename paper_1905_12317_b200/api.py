@@ -70,11 +70,13 @@ class FTKPlan:
 
     def __init__(self, n: int, K: float, delta_max: float, shifts, eps: float, *, n_k: int = 0, n_psi: int = 0,
                  radial_rule: int = 0, device: int = 0, rank: int = 0, world: int = 1, engine: int = ENGINE_TC,
-                 svd_nodes: int = 0, workspace_bytes: int = 0, n_gamma: int = 0, filters=None):
+                 svd_nodes: int = 0, workspace_bytes: int = 0, n_gamma: int = 0, filters=None, nccl_comm=None):
         self._L = _ffi.lib()
         sh = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(-1, 2))
+        comm = nccl_comm.handle if isinstance(nccl_comm, NcclComm) else nccl_comm
         opts = _ffi.PlanOpts(n_k, n_psi, radial_rule, device, rank, world, engine, svd_nodes, workspace_bytes,
-                             n_gamma)
+                             n_gamma, C.c_void_p(comm) if comm else None)
+        self._comm_ref = nccl_comm  # the communicator must outlive the plan
         out = C.c_void_p()
         if filters is None:
             st = self._L.ftk_plan_create(n, float(K), float(delta_max), sh.ctypes.data_as(C.c_void_p), sh.shape[0],
@@ -231,7 +233,7 @@ class FTKPlan:
         jj = torch.as_tensor(np.asarray(tpl_idx, dtype=np.int32), device=dev)
         out = torch.empty((ii.numel(), self.info["N_t"], self.info["n_gamma"]), dtype=torch.float32, device=dev)
         _check(self._L.ftk_landscape_pairs(self._p, C.c_void_p(ii.data_ptr()), C.c_void_p(jj.data_ptr()), ii.numel(),
-                                           C.c_void_p(out.data_ptr()), _stream_ptr(stream)), self._p)
+                                           C.c_void_p(out.data_ptr()), out.numel(), _stream_ptr(stream)), self._p)
         return out
 
     # ---------------- profiling
@@ -243,6 +245,48 @@ class FTKPlan:
         cnt = np.zeros(5, dtype=np.int64)
         _check(self._L.ftk_kernel_times(self._p, ms.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p)), self._p)
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}
+
+
+class NcclComm:
+    """An NCCL communicator created through the C ABI (ftk_nccl_unique_id / ftk_nccl_comm_create).  Pass it
+    as FTKPlan(nccl_comm=...): ftk_align then all-gathers and merges the per-image bests inside the library
+    and returns global bests on every rank.  torch.distributed only carries the 128-byte unique id."""
+
+    def __init__(self, world: int, rank: int, device: int, uid: bytes):
+        self._L = _ffi.lib()
+        assert len(uid) == 128
+        buf = C.create_string_buffer(uid, 128)
+        h = C.c_void_p()
+        _check(self._L.ftk_nccl_comm_create(buf, world, rank, device, C.byref(h)))
+        self.handle = h.value
+        self.world, self.rank = world, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_ffi.lib().ftk_nccl_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_group(cls, device: int, group=None):
+        """Collective over a torch.distributed group: rank 0 draws the id, the group broadcasts it."""
+        import torch
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        uid = cls.unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda(device)
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        return cls(world, rank, device, bytes(t.cpu().tolist()))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._L.ftk_nccl_comm_destroy(C.c_void_p(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        self.close()
 
 
 def merge_bests(gathered, world: int, n_im: int, out=None, stream=None):
@@ -285,11 +329,12 @@ def gather_and_merge(local, group=None, stream=None):
 
 
 def distributed_align(plan: FTKPlan, group=None, stream=None):
-    """Template-sharded alignment: local ftk_align on this rank's shard, all-gather of the per-image
-    records through torch.distributed (NCCL on GPUs, gloo on CPU), deterministic merge."""
-    import torch
-    import torch.distributed as dist
+    """Template-sharded alignment.  A plan created with nccl_comm gathers inside ftk_align (the library's
+    ncclAllGather + device merge): its result is already global.  Otherwise the per-image records are
+    all-gathered through torch.distributed (gloo on CPU) and merged with ftk_merge_bests."""
     local = plan.align(stream=stream)["best"]
+    if getattr(plan, "_comm_ref", None) is not None:
+        return local
     return gather_and_merge(local, group=group, stream=stream)
 
 

@@ -13,8 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libftk.so")
-SOURCES = ["ftk_plan_math.cpp", "ftk_simt.cu", "ftk_tc.cu", "ftk_nufft.cu", "ftk_capi.cu"]
-HEADERS = ["ftk_plan_math.h", "ftk_internal.cuh", "ftk_tc.cuh", "ftk_sm100.cuh", "ftk_fft.cuh", os.path.join("..", "..", "include", "ftk.h")]
+SOURCES = ["ftk_plan_math.cpp", "ftk_nccl.cpp", "ftk_simt.cu", "ftk_tc.cu", "ftk_nufft.cu", "ftk_capi.cu"]
+HEADERS = ["ftk_plan_math.h", "ftk_nccl.h", "ftk_internal.cuh", "ftk_tc.cuh", "ftk_sm100.cuh", "ftk_fft.cuh", os.path.join("..", "..", "include", "ftk.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"]
@@ -33,7 +33,9 @@ def _newer(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
+def build(verbose: bool = False, ptxas_verbose: bool = False, force: bool = False) -> str:
+    """Compile every source (all of them when force=True, else those newer than their object) and link
+    libftk.so."""
     os.makedirs(OUT_DIR, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
     objs = []
@@ -41,7 +43,7 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(OUT_DIR, src + ".o")
         objs.append(o)
-        if _newer(o, [s, __file__] + hdrs):
+        if force or _newer(o, [s, __file__] + hdrs):
             cmd = [NVCC] + ARCH + FLAGS + ["-c", s, "-o", o]
             if src.endswith(".cu"):
                 cmd += ["-x", "cu"]
@@ -55,8 +57,8 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
                 raise RuntimeError(f"nvcc failed on {src}")
             if verbose or ptxas_verbose:
                 sys.stderr.write(r.stderr)
-    if _newer(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+    if force or _newer(LIB, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

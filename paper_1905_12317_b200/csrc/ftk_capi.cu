@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "ftk_internal.cuh"
+#include "ftk_nccl.h"
 #include "ftk_plan_math.h"
 #include "ftk_tc.cuh"
 
@@ -19,6 +20,9 @@ using namespace ftk;
 struct ftk_plan_s {
   PlanMath pm;
   int device = -1, rank = 0, world = 1, engine = 0;
+  void* nccl_comm = nullptr;  // caller-owned ncclComm_t (opts.nccl_comm): ftk_align gathers global bests
+  ftk_best_t* d_gather = nullptr;  // [world][N_im] all-gathered records
+  int64_t gather_cap = 0;
   size_t ws_bytes = (size_t)1 << 30;
   bool ws_user = false;
   std::string err;
@@ -64,7 +68,7 @@ struct ftk_plan_s {
 namespace {
 
 const char* kStatusStr[] = {"FTK_OK",     "FTK_EINVAL", "FTK_ERANGE", "FTK_ENUMERIC", "FTK_ENOMEM",
-                            "FTK_ECUDA",  "FTK_ESTATE", "FTK_ECAPACITY", "FTK_ENODEV"};
+                            "FTK_ECUDA",  "FTK_ESTATE", "FTK_ECAPACITY", "FTK_ENODEV", "FTK_ENCCL"};
 
 ftk_status_t fail(ftk_plan_t p, ftk_status_t s, const std::string& msg) {
   if (p) p->err = msg;
@@ -151,7 +155,7 @@ extern "C" {
 
 const char* ftk_status_string(ftk_status_t s) {
   int i = (int)s;
-  return (i >= 0 && i <= 8) ? kStatusStr[i] : "FTK_UNKNOWN";
+  return (i >= 0 && i <= 9) ? kStatusStr[i] : "FTK_UNKNOWN";
 }
 
 int ftk_version(void) { return 100; }
@@ -196,6 +200,7 @@ static ftk_status_t plan_create_impl(int n, double K, double delta_max_px, const
   plan->world = o.world > 0 ? o.world : 1;
   plan->rank = o.rank;
   plan->engine = o.engine;
+  plan->nccl_comm = o.nccl_comm;
   plan->ws_bytes = o.workspace_bytes ? o.workspace_bytes : ((size_t)1 << 30);
   plan->ws_user = o.workspace_bytes != 0;
   auto bail = [&](ftk_status_t s) {
@@ -240,6 +245,14 @@ static ftk_status_t plan_create_impl(int n, double K, double delta_max_px, const
     return bail(FTK_ENODEV);
   }
   if (cudaSetDevice(plan->device) != cudaSuccess) return bail(FTK_ECUDA);
+  if (plan->nccl_comm) {
+    std::string msg;
+    const int cs = nccl_comm_check(plan->nccl_comm, plan->world, plan->rank, msg);
+    if (cs != FTK_OK) {
+      fprintf(stderr, "ftk_plan_create: %s\n", msg.c_str());
+      return bail((ftk_status_t)cs);
+    }
+  }
   // ---- device constants: ell >= 0 terms in zeta order
   std::vector<float> g, Y3((size_t)N_t * plan->K3p, 0.f);
   std::vector<int> ell, col;
@@ -375,6 +388,7 @@ void ftk_plan_destroy(ftk_plan_t plan) {
     cudaFree(plan->d_ws);
     cudaFree(plan->d_keys);
     cudaFree(plan->d_best_tmp);
+    cudaFree(plan->d_gather);
     cudaFree(plan->d_stage);
     cudaFree(plan->d_nu);
     cudaFree(plan->d_marg_part);
@@ -691,10 +705,13 @@ static ftk_status_t run_blocks(ftk_plan_t plan, unsigned long long* img_keys, un
     if (cap < 1) cap = 1;
     if (cap > (1 << 24)) cap = 1 << 24;
     int64_t nj = std::min<int64_t>(NJ, cap);
-    if (landscape && nj < NJ) return fail(plan, FTK_ECAPACITY, "landscape output needs workspace for a full template row");
     int64_t ni = std::max<int64_t>(1, std::min<int64_t>(NI, cap / nj));
-    ftk_status_t st = tc_block_shape(plan->tc, P, plan->engine, NI, NJ, cap, ni, nj);
+    ftk_status_t st = tc_block_shape(plan->tc, P, plan->engine, NI, NJ, cap, ni, nj, landscape != nullptr);
     if (st != FTK_OK) return fail(plan, st, "block shape");
+    // landscape rows are addressed as [image][template]: every block must span the full template range
+    // (checked after the engine's block shape, which may narrow nj)
+    if (landscape && nj < NJ)
+      return fail(plan, FTK_ECAPACITY, "landscape output needs workspace for a full template row");
     st = ensure_ws(plan, (size_t)(ni * nj) * per + 4096);
     if (st != FTK_OK) return st;
     for (int64_t i0 = 0; i0 < NI; i0 += ni) {
@@ -741,6 +758,7 @@ ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best,
     if (st != FTK_OK) return st;
   }
   const bool host_out = !is_device_ptr(best);
+  const bool gather = plan->nccl_comm != nullptr;  // world = 1 too (the collective path is then a copy)
   if (plan->best_tmp_cap < NI) {
     cudaFree(plan->d_best_tmp);
     plan->d_best_tmp = nullptr;
@@ -748,10 +766,30 @@ ftk_status_t ftk_align(ftk_plan_t plan, ftk_best_t* best, ftk_best_t* pair_best,
     plan->best_tmp_cap = NI;
   }
   prof_begin(plan, 4, s);
-  launch_finalize(img_keys, NI, P.N_t, P.n_gamma, host_out ? plan->d_best_tmp : best, s);
+  launch_finalize(img_keys, NI, P.N_t, P.n_gamma, (host_out || gather) ? plan->d_best_tmp : best, s);
   if (pair_best) launch_finalize(pair_keys, NI * NJ, P.N_t, P.n_gamma, pair_best, s);
   prof_end(plan, 4, s);
   CK(cudaGetLastError());
+  if (gather) {
+    // shard merge: all-gather the N_im x 16 B records of every rank over NVLink, then the
+    // deterministic device merge (max value, ties -> smallest (template, shift, rot)) into the output
+    if (plan->gather_cap < NI * plan->world) {
+      cudaFree(plan->d_gather);
+      plan->d_gather = nullptr;
+      plan->gather_cap = 0;
+      CK(cudaMalloc(&plan->d_gather, (size_t)NI * plan->world * sizeof(ftk_best_t)));
+      plan->gather_cap = NI * plan->world;
+    }
+    std::string msg;
+    const int gs = nccl_allgather_bests(plan->nccl_comm, plan->d_best_tmp, plan->d_gather, NI, s, msg);
+    if (gs != FTK_OK) return fail(plan, (ftk_status_t)gs, msg);
+    if (host_out) {
+      launch_merge(plan->d_gather, plan->world, NI, plan->d_best_tmp, s);
+    } else {
+      launch_merge(plan->d_gather, plan->world, NI, best, s);
+    }
+    CK(cudaGetLastError());
+  }
   if (host_out) {
     CK(cudaMemcpyAsync(best, plan->d_best_tmp, NI * sizeof(ftk_best_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -795,28 +833,54 @@ ftk_status_t ftk_align_marginal(ftk_plan_t plan, double tau, float* log_marginal
 }
 
 ftk_status_t ftk_landscape_pairs(ftk_plan_t plan, const int32_t* img_idx, const int32_t* tpl_idx, int n_pairs,
-                                 float* out, void* stream) {
+                                 float* out, int64_t out_capacity, void* stream) {
   if (!plan || !img_idx || !tpl_idx || !out || n_pairs <= 0) return FTK_EINVAL;
   if (plan->device < 0) return fail(plan, FTK_ESTATE, "host-only plan");
   if (!plan->have_images || !plan->have_templates) return fail(plan, FTK_ESTATE, "load images and templates first");
   CK(cudaSetDevice(plan->device));
   cudaStream_t s = (cudaStream_t)stream;
   const DevPlan P = devplan(plan);
+  const int64_t land_pp = (int64_t)P.N_t * P.n_gamma;
+  if (out_capacity < (int64_t)n_pairs * land_pp)
+    return fail(plan, FTK_ECAPACITY, "ftk_landscape_pairs: out holds fewer than n_pairs * N_t * n_gamma floats");
+  // indices: host or device arrays; validated on the host (an out-of-range index would address memory
+  // outside the loaded sets)
+  std::vector<int32_t> hi(n_pairs), hj(n_pairs);
+  CK(cudaMemcpyAsync(hi.data(), img_idx, n_pairs * sizeof(int32_t), cudaMemcpyDefault, s));
+  CK(cudaMemcpyAsync(hj.data(), tpl_idx, n_pairs * sizeof(int32_t), cudaMemcpyDefault, s));
+  CK(cudaStreamSynchronize(s));
+  for (int k = 0; k < n_pairs; ++k)
+    if (hi[k] < 0 || hi[k] >= plan->n_im || hj[k] < 0 || hj[k] >= plan->n_tm_local)
+      return fail(plan, FTK_EINVAL, "ftk_landscape_pairs: pair index out of range");
   const size_t per = bytes_per_pair(plan);
+  if (plan->engine == 0) {
+    ftk_status_t st = ensure_ws(plan, (size_t)128 * per + 4096);
+    if (st != FTK_OK) return st;
+    std::string msg;
+    const int ts = tc_landscape_pairs(plan->tc, P, plan->d_B, hi.data(), hj.data(), n_pairs, plan->n_im,
+                                      (int)plan->tm_off, (int)plan->n_tm_local, plan->d_ws, out, s, msg);
+    if (ts != FTK_OK) return fail(plan, (ftk_status_t)ts, msg);
+    return FTK_OK;
+  }
+  // SIMT engine: explicit pair blocks through run_block (device copies of the indices)
   int64_t cap = std::max<int64_t>(1, (int64_t)(plan->ws_bytes / per));
   const int64_t chunk = std::min<int64_t>(cap, n_pairs);
-  ftk_status_t st = ensure_ws(plan, (size_t)chunk * per + 4096);
+  ftk_status_t st = ensure_ws(plan, (size_t)chunk * per + 4096 + (size_t)2 * n_pairs * sizeof(int32_t));
   if (st != FTK_OK) return st;
+  int32_t* d_idx = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(plan->d_ws) + (size_t)chunk * per + 4096);
+  CK(cudaMemcpyAsync(d_idx, hi.data(), n_pairs * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_idx + n_pairs, hj.data(), n_pairs * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   for (int64_t p0 = 0; p0 < n_pairs; p0 += chunk) {
     PairBlock pb;
     pb.i0 = pb.j0 = 0;
     pb.ni = pb.nj = 1;
-    pb.li = img_idx + p0;
-    pb.lj = tpl_idx + p0;
+    pb.li = d_idx + p0;
+    pb.lj = d_idx + n_pairs + p0;
     pb.count = (int)std::min<int64_t>(chunk, n_pairs - p0);
-    st = run_block(plan, pb, nullptr, nullptr, out + p0 * (int64_t)P.N_t * P.n_gamma, s);
+    st = run_block(plan, pb, nullptr, nullptr, out + p0 * land_pp, s);
     if (st != FTK_OK) return st;
   }
+  CK(cudaStreamSynchronize(s));  // the host index copies must outlive the asynchronous uploads
   return FTK_OK;
 }
 
@@ -836,6 +900,29 @@ ftk_status_t ftk_merge_bests_host(const ftk_best_t* gathered, int world, int64_t
   }
   return FTK_OK;
 }
+
+ftk_status_t ftk_nccl_unique_id(void* id_out) {
+  if (!id_out) return FTK_EINVAL;
+  std::string msg;
+  const int st = nccl_unique_id(id_out, msg);
+  if (st != FTK_OK) fprintf(stderr, "ftk_nccl_unique_id: %s\n", msg.c_str());
+  return (ftk_status_t)st;
+}
+
+ftk_status_t ftk_nccl_comm_create(const void* id, int world, int rank, int device, void** comm_out) {
+  if (!id || !comm_out || world <= 0 || rank < 0 || rank >= world) return FTK_EINVAL;
+  *comm_out = nullptr;
+  if (device >= 0 && cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return FTK_ENODEV;
+  }
+  std::string msg;
+  const int st = nccl_comm_create(id, world, rank, comm_out, msg);
+  if (st != FTK_OK) fprintf(stderr, "ftk_nccl_comm_create: %s\n", msg.c_str());
+  return (ftk_status_t)st;
+}
+
+ftk_status_t ftk_nccl_comm_destroy(void* comm) { return (ftk_status_t)nccl_comm_destroy(comm); }
 
 ftk_status_t ftk_tc_selftest(int device, double* err_ts, double* err_ss) {
   if (!err_ts || !err_ss) return FTK_EINVAL;

@@ -29,8 +29,34 @@ __host__ __device__ inline void pair_of(const PairBlock& b, int p, int& i, int& 
   }
 }
 
-// Order-preserving float -> uint32 (larger float -> larger code).
+// Opt `func` into the device's full dynamic shared memory (227 KB on B200, minus its static shared
+// memory) on the CURRENT device, once per (call site, device).  The attribute belongs to the function
+// and the device, not to a plan, so it is never lowered to one plan's size (distinct plans, and plans
+// on different devices, stay independent).  `done` is a per-call-site device bit mask.
+inline void smem_optin(const void* func, unsigned long long& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done & bit) return;
+  int mx = 0;
+  cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, func) != cudaSuccess) return;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes) ==
+      cudaSuccess)
+    done |= bit;
+}
+#define FTK_SMEM_OPTIN(f)                  \
+  do {                                     \
+    static unsigned long long done_ = 0;   \
+    smem_optin((const void*)(f), done_);   \
+  } while (0)
+
+// Order-preserving float -> uint32 (larger float -> larger code).  -0.0 is mapped to +0.0 first, so the
+// packed-key atomics order values exactly as best_better() / the in-kernel comparisons do (-0 == +0,
+// ties broken by the index).
 __host__ __device__ inline uint32_t float_ord(float f) {
+  f = f + 0.0f;  // -0 + 0 = +0 (round to nearest)
   uint32_t u;
 #ifdef __CUDA_ARCH__
   u = __float_as_uint(f);

@@ -177,8 +177,8 @@ int nu_plan_init(NuPlan& nu, int n, const std::vector<double>& k, int w, std::st
   cudaMemcpy(nu.d_corr, corr.data(), n * sizeof(float), cudaMemcpyHostToDevice);
   cudaMemcpy(nu.d_twf, twf.data(), twf.size() * sizeof(float2), cudaMemcpyHostToDevice);
   cudaMemcpy(nu.d_k, kr.data(), kr.size() * sizeof(float), cudaMemcpyHostToDevice);
-  cudaFuncSetAttribute(k_nu_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_nu_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  FTK_SMEM_OPTIN(k_nu_rows);
+  FTK_SMEM_OPTIN(k_nu_cols);
   nu.ready = true;
   return FTK_OK;
 }

@@ -48,11 +48,7 @@ void launch_ring_fft(const float2* polar, float2* fb, int64_t n_items, const Dev
   if (n_items <= 0) return;
   const int rb = ring_rows_per_block(P.n_k, P.n_psi);
   const size_t smem = ((size_t)rb * P.n_psi + P.n_psi / 2) * sizeof(float2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_ring_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
-  }
+  FTK_SMEM_OPTIN(k_ring_fft);
   dim3 grid((unsigned)n_items, (P.n_k + rb - 1) / rb);
   k_ring_fft<<<grid, 256, smem, s>>>(polar, fb, P.n_k, P.n_psi, P.log2_psi, rb, P.tw);
 }
@@ -109,11 +105,7 @@ void launch_step1_simt(const float2* A, const float2* B, float2* Zhat, const Pai
   const int st = P.n_k + 1;
   const size_t smem = (size_t)(S1_QC + S1_QC + P.ell_max) * st * sizeof(float2) + (size_t)P.H_plus * P.n_k * 4 +
                       (size_t)P.H_plus * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_step1_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  FTK_SMEM_OPTIN(k_step1_simt);
   dim3 grid(pb.count, P.n_psi / S1_QC);
   k_step1_simt<<<grid, 256, smem, s>>>(A, B, Zhat, pb, P);
 }
@@ -151,11 +143,7 @@ __global__ void __launch_bounds__(256) k_step2_simt(const float2* __restrict__ Z
 
 void launch_step2_simt(const float2* Zhat, float* Z3, const PairBlock& pb, const DevPlan& P, cudaStream_t s) {
   const size_t smem = ((size_t)S2_ZB * P.n_psi + P.n_psi / 2) * sizeof(float2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_step2_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
-  }
+  FTK_SMEM_OPTIN(k_step2_simt);
   dim3 grid(pb.count, (P.H_plus + S2_ZB - 1) / S2_ZB);
   k_step2_simt<<<grid, 256, smem, s>>>(Zhat, Z3, pb, P);
 }
@@ -251,11 +239,7 @@ void launch_step3_simt(const float* Z3, const PairBlock& pb, const DevPlan& P, i
                        unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* landscape,
                        cudaStream_t s) {
   const size_t smem = (size_t)P.K3p * (S3_R + S3_T) * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_step3_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  FTK_SMEM_OPTIN(k_step3_simt);
   dim3 grid(pb.count, P.n_psi / S3_R);
   k_step3_simt<<<grid, 256, smem, s>>>(Z3, pb, P, tm_offset, img_keys, pair_keys, n_tm_local, landscape);
 }

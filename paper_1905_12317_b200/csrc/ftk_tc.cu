@@ -1176,12 +1176,12 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 
 // Step 2 for the tensor-core engine (Eq. fbk3 Step 2, Form B):
 //   Z_zeta(r) = e^{-2 pi i ell r / n} sum_p Zhat'_zeta(p) e^{-2 pi i p r / n},   (q = p + ell)
-// read from Zhat' [pair][p][Hs] (Form B, written by k_step1_tc) or Zhat [pair][zeta][q] (Form A, the
-// explicit-pair path); written as the Step-3 A operand rows (real columns of reading R13), bf16 hi/lo
-// packed in 32-bit words (two K columns per word), per (pair, r-tile, part) the canonical K-major core-matrix image [row/8][word group][8 rows x 16 B] that k_step3_tc bulk-copies and tcgen05.cp-s into TMEM.
-// Work item = (pair, block of two word groups = 16 Step-3 columns, <= 16 terms); persistent CTAs, two
-// per SM.  The item's input rows are gathered with 16-byte cp.async into a [p][18] shared-memory buffer,
-// one warp per term row.
+// read from Zhat' [pair][p][Hs] (Form B, written by k_step1_tc); written as the Step-3 A operand rows
+// (real columns of reading R13), bf16 hi/lo packed in 32-bit words (two K columns per word), per (pair,
+// r-tile, part) the canonical K-major core-matrix image [row/8][word group][8 rows x 16 B] that k_step3_tc
+// bulk-copies and tcgen05.cp-s into TMEM.
+// Work item = (pair, Step-2 block of <= 8 terms in one aligned 8-term window); persistent CTAs; the item's
+// input window arrives by 2-D TMA; one warp per term.
 // FFT: four-step decomposition n = 32 E, p = a + 32 b (a = lane), r = c + E d:
 //   (A) per lane an E-point DFT over b in registers, (B) twiddle w_n^{a c}, (C) a 32-point radix-2
 //   DIF across the warp with shfl_xor (output index d lands on lane bitrev5(d)).
@@ -1270,23 +1270,12 @@ __device__ __forceinline__ void dft_regs(float2 (&x)[E]) {
   }
 }
 
-__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <int E, bool FB>  // FB: Form B input (the tensor-core Step 1) at compile time
-__global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(const float2* __restrict__ Zhat, uint8_t* __restrict__ Zop,
+template <int E>
+__global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* __restrict__ Zop,
                                                       int npair, DevPlan P, S2Blocks B,
                                                       const float2* __restrict__ twtab,
                                                       const __grid_constant__ CUtensorMap zmap) {
   extern __shared__ __align__(1024) uint8_t s2raw[];
-  constexpr bool formB = FB;
   constexpr int n = 32 * E;  // FFT length = n_gamma (>= n_psi; zero-padded input, reading R21)
   constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
   constexpr int RS = n + n / E;  // padded staging row (words): index r + r / E
@@ -1303,7 +1292,6 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(const floa
   constexpr int SROW = 32 + 32 / E;
   float2* scr = reinterpret_cast<float2*>(stg) + warp * E * SROW;
   const int total = npair * B.nb;
-  const int Hp = P.H_plus;
   const int NWG = P.K3p / 8, NRT = (n + 127) / 128;
 
   // 32 = L x E: the 32-point DFT over the lane index runs as an E-point register DFT and an L-point
@@ -1334,26 +1322,17 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(const floa
   const int per = (total + gridDim.x - 1) / gridDim.x;
   const int i_beg = blockIdx.x * per;
   const int i_end = min(total, i_beg + per);
-  // Form B input: the aligned 8-term window [zs & ~1, +8) holding the block's terms, for the pair's n_psi
-  // rows of Zhat' [pair][p][Hs], as 2-D TMA boxes (8 x 256, zero fill beyond Hs) into the swizzled [p][8]
+  // input: the aligned 8-term window [zs & ~1, +8) holding the block's terms, for the pair's n_psi rows of
+  // Zhat' [pair][p][Hs] (Form B), as 2-D TMA boxes (8 x 256, zero fill beyond Hs) into the swizzled [p][8]
   // row buffer.  A box must start on a 16-byte boundary (an odd 8-byte column start faults); the device
-  // term order (tc_term_order) puts every block inside one such window.  Form A (explicit pairs,
-  // Zhat [pair][zeta][q]): cp.async gather into the same layout
+  // term order (tc_term_order) puts every block inside one such window.
   auto issue = [&](int it) {
     const int bi = it % B.nb, pi2 = it / B.nb;
-    if (formB) {
-      if (threadIdx.x == 0) {
-        const int box = n_in < 256 ? n_in : 256;
-        mbar_arrive_expect_tx(bar, (uint32_t)n_in * 64u);
-        for (int k = 0; k < n_in; k += box)
-          tma_load_2d(s2raw + (size_t)k * 64, &zmap, B.zs[bi] & ~1, pi2 * n_in + k, bar);
-      }
-    } else {
-      const int zs = B.zs[bi], nz = B.ze[bi] - zs;
-      const float2* src = Zhat + ((size_t)pi2 * Hp + zs) * n_in;
-      for (int z = 0; z < nz; ++z)
-        for (int q = threadIdx.x; q < n_in; q += blockDim.x) cp_async8(rows + s2_slot(q, z), src + (size_t)z * n_in + q);
-      cp_async_commit();
+    if (threadIdx.x == 0) {
+      const int box = n_in < 256 ? n_in : 256;
+      mbar_arrive_expect_tx(bar, (uint32_t)n_in * 64u);
+      for (int k = 0; k < n_in; k += box)
+        tma_load_2d(s2raw + (size_t)k * 64, &zmap, B.zs[bi] & ~1, pi2 * n_in + k, bar);
     }
   };
   if (threadIdx.x == 0) {
@@ -1366,13 +1345,8 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(const floa
   for (int item = i_beg; item < i_end; ++item) {
     const int b = item % B.nb, pr = item / B.nb;
     const int zs = B.zs[b], nz = B.ze[b] - zs, g0 = B.g0[b];
-    if (formB) {
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-    } else {
-      cp_async_wait<0>();
-      __syncthreads();
-    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
     // ---- each warp takes one term: load its row (cyclic shift by ell, zero padding to n)
     const int zz = warp;
     const bool act = zz < nz;
@@ -1382,11 +1356,11 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(const floa
       const int z = zs + zz;
       l = P.ell[z];
       col = P.col[z];
-      const int e = formB ? (zs & 1) + zz : zz;  // window column of this term
+      const int e = (zs & 1) + zz;  // window column of this term
       auto at = [&](int p) { return rows[s2_slot(p, e)]; };
       // Form B: Z(r) w^{ell r} = DFT of the cyclically shifted row Zhat'(q - ell) (reading R5)
       if (n_in == n) {
-        const int q0 = formB ? ((lane - l) & (n - 1)) : lane;
+        const int q0 = (lane - l) & (n - 1);
 #pragma unroll
         for (int bb = 0; bb < E; ++bb) x[bb] = at((q0 + 32 * bb) & (n - 1));
       } else {
@@ -1397,7 +1371,7 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(const floa
           const int qp = lane + 32 * bb;
           const int qc = qp < Qh ? qp : (qp > n - Qh ? qp - n + n_in : Qh);
           const float wgt = (qp < Qh || qp > n - Qh) ? 1.f : ((qp == Qh || qp == n - Qh) ? 0.5f : 0.f);
-          const int src = formB ? ((qc - l) & (n_in - 1)) : qc;
+          const int src = (qc - l) & (n_in - 1);
           const float2 v = at(src);
           x[bb] = make_float2(wgt * v.x, wgt * v.y);
         }
@@ -1546,13 +1520,13 @@ static int make_zmap(CUtensorMap* m, const float2* Zhat, int npair, const DevPla
   return r == CUDA_SUCCESS ? FTK_OK : FTK_ECUDA;
 }
 
-static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, int formB,
-                            const DevPlan& P, cudaStream_t s) {
+static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, const DevPlan& P,
+                            cudaStream_t s) {
   S2Blocks B;
   std::memcpy(&B, &tc.s2_blocks, sizeof B);
   alignas(64) CUtensorMap zmap;
   std::memset(&zmap, 0, sizeof zmap);
-  if (formB && make_zmap(&zmap, Zhat, npair, P) != FTK_OK) return FTK_ECUDA;
+  if (make_zmap(&zmap, Zhat, npair, P) != FTK_OK) return FTK_ECUDA;
   if (tc.sync_debug)
     fprintf(stderr, "step2: Zhat %p (mod 256 = %d) Hs %d npair %d n_psi %d n_gamma %d smem %zu grid %d\n", (const void*)Zhat,
             (int)((uintptr_t)Zhat & 255), P.Hs, npair, P.n_psi, P.n_gamma, step2_smem(P.n_psi, P.n_gamma),
@@ -1564,14 +1538,14 @@ static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
     occ = std::max(1, std::min(occ, 4));
     dim3 grid(items < occ * tc.num_sms ? items : occ * tc.num_sms);
-    kern<<<grid, 256, smem, s>>>(Zhat, Zop, npair, P, B, tc.d_s2tw, zmap);
+    kern<<<grid, 256, smem, s>>>(Zop, npair, P, B, tc.d_s2tw, zmap);
   };
   switch (P.n_gamma) {
-    case 64: formB ? run(k_step2_fft<2, true>) : run(k_step2_fft<2, false>); break;
-    case 128: formB ? run(k_step2_fft<4, true>) : run(k_step2_fft<4, false>); break;
-    case 256: formB ? run(k_step2_fft<8, true>) : run(k_step2_fft<8, false>); break;
-    case 512: formB ? run(k_step2_fft<16, true>) : run(k_step2_fft<16, false>); break;
-    default: formB ? run(k_step2_fft<32, true>) : run(k_step2_fft<32, false>); break;
+    case 64: run(k_step2_fft<2>); break;
+    case 128: run(k_step2_fft<4>); break;
+    case 256: run(k_step2_fft<8>); break;
+    case 512: run(k_step2_fft<16>); break;
+    default: run(k_step2_fft<32>); break;
   }
   return FTK_OK;
 }
@@ -1927,16 +1901,16 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   cudaMemcpy(tc.d_colfast, colfast.data(), colfast.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(tc.d_Ysm, yimg.data(), yimg.size() * 2, cudaMemcpyHostToDevice);
   tc.s3_smem = s3_smem_bytes(ncol_g, K3p, tc.NS);
-  cudaFuncSetAttribute(k_step3_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.s3_smem);
-  cudaFuncSetAttribute(k_step3_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc.s3_smem);
+  FTK_SMEM_OPTIN((k_step3_tc<0>));
+  FTK_SMEM_OPTIN((k_step3_tc<1>));
   if (pm.n_k % 16 != 0 || pm.n_k > 128) {
     msg = "tensor-core engine: n_k must be a multiple of 16 and <= 128";
     return FTK_EINVAL;
   }
   tc.KCH = (2 * pm.n_k) % 64 == 0 ? 64 : 32;
   tc.NKCH = 2 * pm.n_k / tc.KCH;
-  cudaFuncSetAttribute(k_step1_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
-  cudaFuncSetAttribute(k_step1_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1_smem_bytes(tc));
+  FTK_SMEM_OPTIN((k_step1_tc<0>));
+  FTK_SMEM_OPTIN((k_step1_tc<4>));
   // Step-2 blocks (s2_block_table); the device term order (tc_term_order, applied in ftk_capi.cu) puts
   // every block's terms in one aligned 8-term window of a Zhat' row (one TMA box)
   {
@@ -1963,16 +1937,11 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       cudaMemcpy(tc.d_s2tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice);
     }
     const int sm2 = (int)step2_smem(pm.n_psi, n_gamma);
-    cudaFuncSetAttribute(k_step2_fft<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    cudaFuncSetAttribute(k_step2_fft<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+    FTK_SMEM_OPTIN((k_step2_fft<2>));
+    FTK_SMEM_OPTIN((k_step2_fft<4>));
+    FTK_SMEM_OPTIN((k_step2_fft<8>));
+    FTK_SMEM_OPTIN((k_step2_fft<16>));
+    FTK_SMEM_OPTIN((k_step2_fft<32>));
   }
   const char* sdbg = std::getenv("FTK_SYNC_DEBUG");
   tc.sync_debug = sdbg && sdbg[0] == '1';
@@ -2029,10 +1998,18 @@ size_t tc_bytes_per_pair(const TcPlan& tc, const DevPlan& P) {
 }
 
 ftk_status_t tc_block_shape(const TcPlan&, const DevPlan&, int engine, int64_t NI, int64_t NJ, int64_t cap,
-                            int64_t& ni, int64_t& nj) {
+                            int64_t& ni, int64_t& nj, bool full_rows) {
   if (engine != 0) return FTK_OK;
   // image rows in multiples of 128 (Step-1 N tiles); as many as the workspace allows, up to 2048
   int64_t ni_t = std::min<int64_t>((NI + 127) / 128 * 128, 2048);
+  if (full_rows) {
+    // landscape output: every block spans all NJ templates, so the image rows shrink instead
+    while (ni_t > 128 && ni_t * NJ > cap) ni_t -= 128;
+    if (NI <= 128) ni_t = NI;
+    ni = std::min<int64_t>(ni_t, NI);
+    nj = ni_t * NJ <= cap ? NJ : std::max<int64_t>(1, cap / std::max<int64_t>(ni_t, 1));
+    return (ni < NI && ni % 128 != 0) ? FTK_EINVAL : FTK_OK;
+  }
   while (ni_t > 128 && ni_t * 1 > cap) ni_t -= 128;
   if (NI <= 128) ni_t = NI;
   ni = std::min<int64_t>(ni_t, NI);
@@ -2179,17 +2156,10 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
   float2* Zhat = reinterpret_cast<float2*>(ws);
   uint8_t* Zop = reinterpret_cast<uint8_t*>(Zhat + (size_t)pb.count * P.Hs * P.n_psi);
   if (pb.li) {
-    // explicit pair list (ftk_landscape_pairs): per-pair Step 1 on CUDA cores, then the same FFT
-    if (prof) prof(plan, 1, 0, s);
-    launch_step1_simt(A, B, Zhat, pb, P, s);
-    if (prof) prof(plan, 1, 1, s);
-    if (prof) prof(plan, 2, 0, s);
-    if (launch_step2_fft(tc, Zhat, Zop, pb.count, 0, P, s) != FTK_OK) {
-      msg = "Step 2: tensor map encoding failed";
-      return FTK_ECUDA;
-    }
-    if (prof) prof(plan, 2, 1, s);
-  } else {
+    msg = "tensor-core engine: explicit pair lists go through tc_landscape_pairs";
+    return FTK_EINVAL;
+  }
+  {
     if (prof) prof(plan, 1, 0, s);
     launch_step1_tc(tc, B, Zhat, pb, P, s);
     if (prof) prof(plan, 1, 1, s);
@@ -2201,7 +2171,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
       }
     }
     if (prof) prof(plan, 2, 0, s);
-    if (launch_step2_fft(tc, Zhat, Zop, pb.count, 1, P, s) != FTK_OK) {
+    if (launch_step2_fft(tc, Zhat, Zop, pb.count, P, s) != FTK_OK) {
       msg = "Step 2: tensor map encoding failed";
       return FTK_ECUDA;
     }
@@ -2225,6 +2195,60 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     }
   }
   return FTK_OK;
+}
+
+// ftk_landscape_pairs on the tensor-core engine: the production kernels on minimal blocks.  Pairs are
+// grouped by (128-image tile, template); per group one k_step1_tc launch over the tile x 1 template (the
+// Step-1 instance and block structure ftk_align runs), then per requested pair k_step2_fft (Form B) and
+// k_step3_tc on that single pair with landscape output (the exact epilogue path).
+int tc_landscape_pairs(TcPlan& tc, const DevPlan& P, const float2* B, const int32_t* h_img, const int32_t* h_tpl,
+                       int n_pairs, int64_t n_im, int tm_off, int n_tm_local, void* ws, float* out, cudaStream_t s,
+                       std::string& msg) {
+  if (!tc.ready) {
+    msg = "tensor-core engine not initialized";
+    return FTK_ESTATE;
+  }
+  std::vector<int> order(n_pairs);
+  for (int k = 0; k < n_pairs; ++k) order[k] = k;
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    const long long ka = (long long)(h_img[a] / 128) * n_tm_local + h_tpl[a];
+    const long long kb = (long long)(h_img[b] / 128) * n_tm_local + h_tpl[b];
+    return ka != kb ? ka < kb : a < b;
+  });
+  float2* Zhat = reinterpret_cast<float2*>(ws);
+  uint8_t* Zop = reinterpret_cast<uint8_t*>(Zhat + (size_t)128 * P.Hs * P.n_psi);
+  const size_t land_pp = (size_t)P.N_t * P.n_gamma;
+  for (int a = 0; a < n_pairs;) {
+    const int tile = h_img[order[a]] / 128, j = h_tpl[order[a]];
+    int b = a;
+    while (b < n_pairs && h_img[order[b]] / 128 == tile && h_tpl[order[b]] == j) ++b;
+    PairBlock pb1;
+    pb1.i0 = tile * 128;
+    pb1.ni = (int)std::min<int64_t>(128, n_im - pb1.i0);
+    pb1.j0 = j;
+    pb1.nj = 1;
+    pb1.li = pb1.lj = nullptr;
+    pb1.count = pb1.ni;
+    launch_step1_tc(tc, B, Zhat, pb1, P, s);
+    for (int c = a; c < b; ++c) {
+      const int k = order[c], i = h_img[k];
+      const float2* zp = Zhat + (size_t)(i - pb1.i0) * P.n_psi * P.Hs;
+      if (launch_step2_fft(tc, zp, Zop, 1, P, s) != FTK_OK) {
+        msg = "Step 2: tensor map encoding failed";
+        return FTK_ECUDA;
+      }
+      PairBlock pb3;
+      pb3.i0 = i;
+      pb3.ni = 1;
+      pb3.j0 = j;
+      pb3.nj = 1;
+      pb3.li = pb3.lj = nullptr;
+      pb3.count = 1;
+      launch_step3_tc(tc, Zop, pb3, P, tm_off, nullptr, nullptr, n_tm_local, out + (size_t)k * land_pp, s);
+    }
+    a = b;
+  }
+  return cudaGetLastError() == cudaSuccess ? FTK_OK : FTK_ECUDA;
 }
 
 }  // namespace ftk

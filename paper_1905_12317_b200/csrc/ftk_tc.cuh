@@ -73,8 +73,13 @@ int tc_prepare_images(TcPlan& tc, const float2* fb, int64_t n, const DevPlan& P,
 int tc_prepare_templates(TcPlan& tc, const float2* fb, int64_t n, const DevPlan& P, cudaStream_t s, std::string& msg);
 size_t tc_bytes_per_pair(const TcPlan& tc, const DevPlan& P);
 ftk_status_t tc_block_shape(const TcPlan& tc, const DevPlan& P, int engine, int64_t NI, int64_t NJ, int64_t cap,
-                            int64_t& ni, int64_t& nj);
+                            int64_t& ni, int64_t& nj, bool full_rows = false);
 int tc_selftest(double* err_ts, double* err_ss, std::string& msg);
+// ftk_landscape_pairs on the tensor-core engine (production Step-1/2/3 kernels on minimal blocks); h_img /
+// h_tpl: host copies of the pair indices (validated by the caller); ws >= 128 pairs of tc_bytes_per_pair
+int tc_landscape_pairs(TcPlan& tc, const DevPlan& P, const float2* B, const int32_t* h_img, const int32_t* h_tpl,
+                       int n_pairs, int64_t n_im, int tm_off, int n_tm_local, void* ws, float* out, cudaStream_t s,
+                       std::string& msg);
 int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2* A, const float2* B, void* ws,
                  size_t ws_size, int tm_off,
                  unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,

@@ -141,3 +141,16 @@ def test_host_ctf_plan_errors(ftk):
     assert st == 1 and not out.value
     k = np.empty(4)
     assert L.ftk_radial_rule(cfg.n, cfg.K, 4, 7, k.ctypes.data_as(C.c_void_p), k.ctypes.data_as(C.c_void_p)) == 1
+
+
+def test_nccl_unique_id_and_status(ftk):
+    """The NCCL glue loads libnccl.so.2 at run time; a unique id needs no GPU.  FTK_ENCCL has a name."""
+    import ctypes as C
+    L = ftk.lib()
+    assert L.ftk_status_string(9) == b"FTK_ENCCL"
+    buf = C.create_string_buffer(128)
+    assert L.ftk_nccl_unique_id(buf) == 0
+    assert any(buf.raw)
+    assert L.ftk_nccl_unique_id(None) == 1          # FTK_EINVAL
+    h = C.c_void_p()
+    assert L.ftk_nccl_comm_create(buf, 2, 5, -1, C.byref(h)) == 1   # rank >= world

@@ -1,0 +1,289 @@
+"""GPU parity of the PRODUCTION path (tensor-core engine, the kernels and block shapes bench.py times)
+against the float64 oracle, at BASELINE.json's full sizes (SURVEY 8(d) "parity sampling"
+Eq. fbk3, P:1324 consistency check).
+
+Which kernels each test runs (engine 0):
+  * test_landscape_pairs_32       k_step1_tc over each pair's 128-image tile, k_step2_fft (Form B),
+                                  k_step3_tc with landscape output (exact epilogue) -- 32 random pairs per
+                                  config, element-wise |dX| <= 1e-4 ||A|| ||B||.
+  * test_pair_best_every_pair     ftk_align as bench.py runs it (k_step1_tc, k_step2_fft, k_step3_tc with the
+                                  fast E + |O| epilogue and the resolver): value AND (shift, rot) of every
+                                  pair of a >= 2-image-tile subset vs the oracle (argmax: gap rule).
+  * test_image_bests_all_templates  per-image bests over ALL templates of the config (4 images at c3/c4,
+                                  1 image at c5) vs the oracle.
+  * test_bench_block_shape        c5 with 2100 images: one 2048-image Step-1 block (16 image tiles, the
+                                  bench's block) plus a ragged one; sampled pair maxima vs the oracle.
+  * test_nccl_single_rank         ftk_align with a 1-rank NCCL communicator (the library's all-gather +
+                                  device merge): bests equal the oracle's and, bitwise, the plain call.
+Argmax rule (reading R25): GPU and oracle argmax must agree unless the oracle's top-2 gap is
+within 2 x the tolerance (each side may be off by one tolerance).
+Set FTK_PARITY_LOG=path to write the max |dX| / (||A|| ||B||) per config as JSON.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import fb, ftk, kernel_svd as ks
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+_OPLANS = {}
+_STATS = {}
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as g
+    g.build()
+    import paper_1905_12317_b200 as p
+    return p
+
+
+@pytest.fixture(scope="module", autouse=True)
+def parity_log():
+    yield
+    path = os.environ.get("FTK_PARITY_LOG")
+    if path and _STATS:
+        with open(path, "w") as f:
+            json.dump(_STATS, f, indent=1, sort_keys=True)
+
+
+def note(key, val):
+    _STATS[key] = max(float(val), _STATS.get(key, 0.0))
+
+
+def oracle_plan(cfg):
+    if cfg.name not in _OPLANS:
+        _OPLANS[cfg.name] = ks.build_plan(cfg.n, cfg.K, synth.delta_max(cfg), synth.shift_list(cfg), cfg.eps,
+                                          cfg.n_k, cfg.n_psi, n_nodes=96)
+    return _OPLANS[cfg.name]
+
+
+def make(pkg, cfg, **kw):
+    return pkg.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), synth.shift_list(cfg), cfg.eps, n_k=cfg.n_k,
+                       n_psi=cfg.n_psi, device=0, engine=0, **kw)
+
+
+def load_gpu(pkg, cfg, ni, nj, **kw):
+    p = make(pkg, cfg, **kw)
+    k, w = p.radial()
+    imgs, _ = synth.draw_items(cfg, "images", range(ni), k, backend="torch", device="cuda")
+    tpls, _ = synth.draw_items(cfg, "templates", range(nj), k, backend="torch", device="cuda")
+    p.load_images(imgs)
+    p.load_templates(tpls)
+    return p, w, imgs, tpls
+
+
+def pair_stats(X):
+    """Per pair of X [I, J, N_t, n]: (max, t, r, top-2 gap); argmax ties -> smallest (t, r)."""
+    I, J = X.shape[:2]
+    flat = X.reshape(I, J, -1)
+    idx = np.argmax(flat, axis=2)
+    v = np.take_along_axis(flat, idx[..., None], 2)[..., 0]
+    part = np.partition(flat, -2, axis=2)
+    gap = part[..., -1] - part[..., -2]
+    t, r = np.unravel_index(idx, X.shape[2:])
+    return v, t, r, gap
+
+
+@pytest.mark.parametrize("name", ["tiny", "c2", "c3", "c4", "c5"])
+def test_landscape_pairs_32(pkg, name):
+    cfg = synth.config(name)
+    ni, nj = min(cfg.N_im, 300), min(cfg.N_tm, 300)
+    p, w, imgs, tpls = load_gpu(pkg, cfg, ni, nj)
+    rng = np.random.default_rng(7)
+    n = 32 if name != "tiny" else 16
+    ii = rng.integers(0, ni, n)
+    jj = rng.integers(0, nj, n)
+    Lp = p.landscape_pairs(ii, jj).cpu().numpy()
+    xs = imgs[torch.as_tensor(ii, device="cuda")].cpu().numpy()
+    ys = tpls[torch.as_tensor(jj, device="cuda")].cpu().numpy()
+    na, nb = fb.discrete_norm(xs, w), fb.discrete_norm(ys, w)
+    a, b = fb.fb_coeffs(xs), fb.fb_coeffs(ys)
+    worst = 0.0
+    for s in range(n):
+        X = np.real(ftk.ftk_landscapes(a[s:s + 1], b[s:s + 1], oracle_plan(cfg)))[0, 0]
+        worst = max(worst, np.max(np.abs(Lp[s] - X)) / (na[s] * nb[s]))
+    note(f"landscape_pairs_{name}", worst)
+    assert worst <= TOL, worst
+
+
+@pytest.mark.parametrize("name,ni,nj", [("c5", 130, 40), ("c4", 130, 8), ("c3", 160, 24)])
+def test_pair_best_every_pair(pkg, name, ni, nj):
+    """Every pair of a subset spanning 2 image tiles (128 + ragged): the fast E + |O| epilogue and the
+    resolver vs the oracle's per-pair maximum and its (shift, rotation).  c4 runs several Step-3 rep-groups."""
+    cfg = synth.config(name)
+    p, w, imgs, tpls = load_gpu(pkg, cfg, ni, nj)
+    if name == "c4":
+        assert p.info["s3_groups"] > 1
+    res = p.align(pair_best=True)
+    torch.cuda.synchronize()
+    pb = pkg.best_to_numpy(res["pair_best"].reshape(-1, 4)).reshape(ni, nj)
+    xs, ys = imgs.cpu().numpy(), tpls.cpu().numpy()
+    na, nb = fb.discrete_norm(xs, w), fb.discrete_norm(ys, w)
+    a, b = fb.fb_coeffs(xs), fb.fb_coeffs(ys)
+    worst, mism = 0.0, 0
+    for i in range(ni):
+        X = np.real(ftk.ftk_landscapes(a[i:i + 1], b, oracle_plan(cfg)))
+        v, t, r, gap = pair_stats(X)
+        tol = TOL * na[i] * nb
+        dv = np.abs(pb["value"][i] - v[0])
+        worst = max(worst, float(np.max(dv / (na[i] * nb))))
+        assert np.all(dv <= tol), (i, dv.max())
+        assert np.all(pb["template_idx"][i] == np.arange(nj))
+        clear = gap[0] > 2 * tol
+        ok = (pb["shift_idx"][i] == t[0]) & (pb["rot_idx"][i] == r[0])
+        assert np.all(ok | ~clear), (i, np.where(~ok & clear))
+        mism += int(np.sum(~ok))
+    note(f"pair_best_value_{name}", worst)
+    _STATS[f"pair_best_argmax_near_tie_{name}"] = mism
+
+
+@pytest.mark.parametrize("name,ni", [("c3", 4), ("c4", 4), ("c5", 1)])
+def test_image_bests_all_templates(pkg, name, ni):
+    """Per-image bests over ALL N_tm templates of the config (4 images at c3/c4, 1 at c5)."""
+    cfg = synth.config(name)
+    p, w, imgs, tpls = load_gpu(pkg, cfg, ni, cfg.N_tm)
+    best = pkg.best_to_numpy(p.align()["best"])
+    xs = imgs.cpu().numpy()
+    a, na = fb.fb_coeffs(xs), fb.discrete_norm(xs, w)
+    top = np.full((ni, 2), -np.inf)
+    arg = np.zeros((ni, 3), dtype=np.int64)
+    nb_all = np.empty(cfg.N_tm)
+    for j0 in range(0, cfg.N_tm, 64):
+        ys = tpls[j0:j0 + 64].cpu().numpy()
+        nb_all[j0:j0 + len(ys)] = fb.discrete_norm(ys, w)
+        X = np.real(ftk.ftk_landscapes(a, fb.fb_coeffs(ys), oracle_plan(cfg)))
+        flat = X.reshape(ni, -1)
+        part = np.partition(flat, -2, axis=1)[:, -2:]
+        for i in range(ni):
+            k = int(np.argmax(flat[i]))
+            if flat[i, k] > top[i, 0]:
+                top[i, 1] = max(top[i, 0], part[i, 0])
+                top[i, 0] = flat[i, k]
+                arg[i] = np.unravel_index(k, X.shape[1:])
+                arg[i, 0] += j0
+            else:
+                top[i, 1] = max(top[i, 1], flat[i, k])
+    for i in range(ni):
+        tol = TOL * na[i] * nb_all[arg[i, 0]]
+        assert abs(best["value"][i] - top[i, 0]) <= tol, (i, best["value"][i], top[i, 0])
+        note(f"image_best_value_{name}", abs(best["value"][i] - top[i, 0]) / (na[i] * nb_all[arg[i, 0]]))
+        if top[i, 0] - top[i, 1] > 2 * tol:
+            assert (best["template_idx"][i], best["shift_idx"][i], best["rot_idx"][i]) == tuple(arg[i])
+
+
+def test_bench_block_shape(pkg):
+    """c5 with 2100 images x 3 templates: the first pair block is the bench's 2048-image block (16 Step-1
+    image tiles per unit), the second a ragged 52-image block; 64 sampled pair maxima and their
+    (shift, rot) vs the oracle, and best[i] = lexicographic max_j pair_best[i, j] for all images."""
+    cfg = synth.config("c5")
+    ni, nj = 2100, 3
+    p, w, imgs, tpls = load_gpu(pkg, cfg, ni, nj)
+    res = p.align(pair_best=True)
+    torch.cuda.synchronize()
+    best = pkg.best_to_numpy(res["best"])
+    pb = pkg.best_to_numpy(res["pair_best"].reshape(-1, 4)).reshape(ni, nj)
+    jb = np.argmax(pb["value"], axis=1)
+    assert np.array_equal(best["value"], pb["value"][np.arange(ni), jb])
+    rng = np.random.default_rng(5)
+    ii = np.concatenate([[0, 127, 128, 2047, 2048, 2099], rng.integers(0, ni, 58)])
+    ys = tpls.cpu().numpy()
+    nb, b = fb.discrete_norm(ys, w), fb.fb_coeffs(ys)
+    worst = 0.0
+    for i in ii:
+        x = imgs[int(i):int(i) + 1].cpu().numpy()
+        na = fb.discrete_norm(x, w)[0]
+        X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(x), b, oracle_plan(cfg)))
+        v, t, r, gap = pair_stats(X)
+        for j in range(nj):
+            tol = TOL * na * nb[j]
+            assert abs(pb["value"][i, j] - v[0, j]) <= tol
+            worst = max(worst, abs(pb["value"][i, j] - v[0, j]) / (na * nb[j]))
+            if gap[0, j] > 2 * tol:
+                assert (pb["shift_idx"][i, j], pb["rot_idx"][i, j]) == (t[0, j], r[0, j])
+    note("bench_block_c5_pair_value", worst)
+
+
+def test_nccl_single_rank(pkg):
+    """opts.nccl_comm with a 1-rank communicator: ftk_align runs the library's ncclAllGather + device merge;
+    the bests equal the oracle's and are bitwise equal to the call without a communicator."""
+    cfg = synth.config("c2")
+    ni, nj = 6, 40
+    comm = pkg.NcclComm(1, 0, 0, pkg.NcclComm.unique_id())
+    p = make(pkg, cfg, nccl_comm=comm)
+    k, w = p.radial()
+    imgs, _ = synth.draw_items(cfg, "images", range(ni), k)
+    tpls, _ = synth.draw_items(cfg, "templates", range(nj), k)
+    p.load_images(torch.from_numpy(imgs).cuda())
+    p.load_templates(torch.from_numpy(tpls).cuda())
+    bg = pkg.best_to_numpy(p.align()["best"])
+    bh = p.align_host()                         # host output through the same gather
+    q = make(pkg, cfg)
+    q.load_images(torch.from_numpy(imgs).cuda())
+    q.load_templates(torch.from_numpy(tpls).cuda())
+    bl = pkg.best_to_numpy(q.align()["best"])
+    assert np.array_equal(bg.view(np.int32), bl.view(np.int32))
+    assert np.array_equal(bh.view(np.int32), bl.view(np.int32))
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), oracle_plan(cfg)))
+    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+    v, j, t, r, gap = ftk.best_per_image(X)
+    for i in range(ni):
+        tol = TOL * na[i] * nb[j[i]]
+        assert abs(bg["value"][i] - v[i]) <= tol
+        if gap[i] > 2 * tol:
+            assert (bg["template_idx"][i], bg["shift_idx"][i], bg["rot_idx"][i]) == (j[i], t[i], r[i])
+    del p
+    comm.close()
+    # a communicator whose size disagrees with the plan's world is refused at plan creation
+    comm2 = pkg.NcclComm(1, 0, 0, pkg.NcclComm.unique_id())
+    with pytest.raises(pkg.FTKError):
+        make(pkg, cfg, nccl_comm=comm2, rank=0, world=2)
+    comm2.close()
+
+
+def test_landscape_small_workspace(pkg):
+    """landscape output with a workspace too small for a full block -- the block shape
+    keeps every template in each block (or refuses with FTK_ECAPACITY); never overlapping rows."""
+    cfg = synth.config("c3")
+    ni, nj = 140, 6
+    p = make(pkg, cfg, workspace_bytes=16 << 20)
+    k, w = p.radial()
+    imgs, _ = synth.draw_items(cfg, "images", range(ni), k)
+    tpls, _ = synth.draw_items(cfg, "templates", range(nj), k)
+    p.load_images(torch.from_numpy(imgs).cuda())
+    p.load_templates(torch.from_numpy(tpls).cuda())
+    try:
+        L = p.align(landscape=True)["landscape"].cpu().numpy()
+    except pkg.FTKError as e:
+        assert e.status == 7  # FTK_ECAPACITY
+        return
+    X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), oracle_plan(cfg)))
+    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+    assert np.max(np.abs(L - X) / (na[:, None, None, None] * nb[None, :, None, None])) <= TOL
+
+
+def test_landscape_pairs_errors(pkg):
+    import ctypes as C
+    cfg = synth.config("tiny")
+    p = make(pkg, cfg)
+    k, _ = p.radial()
+    x, _ = synth.draw_items(cfg, "images", range(3), k)
+    p.load_images(torch.from_numpy(x).cuda())
+    p.load_templates(torch.from_numpy(x).cuda())
+    with pytest.raises(pkg.FTKError):
+        p.landscape_pairs([0, 5], [0, 1])        # image index out of range
+    with pytest.raises(pkg.FTKError):
+        p.landscape_pairs([0], [-1])             # template index out of range
+    ii = np.array([0, 1], dtype=np.int32)
+    out = torch.empty((2, p.info["N_t"], p.info["n_gamma"] - 1), dtype=torch.float32, device="cuda")
+    st = pkg.lib().ftk_landscape_pairs(p._p, C.c_void_p(ii.ctypes.data), C.c_void_p(ii.ctypes.data), 2,
+                                       C.c_void_p(out.data_ptr()), out.numel(), None)
+    assert st == 7                               # FTK_ECAPACITY: host indices accepted, buffer too small
