@@ -13,8 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libftk.so")
-SOURCES = ["ftk_plan_math.cpp", "ftk_nccl.cpp", "ftk_simt.cu", "ftk_tc.cu", "ftk_nufft.cu", "ftk_capi.cu"]
-HEADERS = ["ftk_plan_math.h", "ftk_nccl.h", "ftk_internal.cuh", "ftk_tc.cuh", "ftk_sm100.cuh", "ftk_fft.cuh", os.path.join("..", "..", "include", "ftk.h")]
+SOURCES = ["ftk_plan_math.cpp", "ftk_nccl.cpp", "ftk_simt.cu", "ftk_tc.cu", "ftk_s23.cu", "ftk_nufft.cu", "ftk_capi.cu"]
+HEADERS = ["ftk_plan_math.h", "ftk_nccl.h", "ftk_tc_dev.cuh", "ftk_internal.cuh", "ftk_tc.cuh", "ftk_sm100.cuh", "ftk_fft.cuh", os.path.join("..", "..", "include", "ftk.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"]

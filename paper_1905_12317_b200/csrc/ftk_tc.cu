@@ -40,6 +40,7 @@
 #include "ftk_fft.cuh"
 #include "ftk_sm100.cuh"
 #include "ftk_tc.cuh"
+#include "ftk_tc_dev.cuh"
 
 namespace ftk {
 using namespace sm100;
@@ -90,20 +91,6 @@ struct S3Params {
   unsigned long long* trace;  // nullable (FTK_S3_TRACE=1): wait / busy cycle counters of CTA 0
 };
 
-__device__ __forceinline__ float ex2_approx(float x) {  // 2^x, one MUFU op (2^-inf = 0)
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// (m, s) pairs of a scaled log-sum-exp in base 2: value = m + log2(s); m = -inf means "empty"
-__device__ __forceinline__ void lse2_merge(float& m, float& s, float m2, float s2) {
-  const float mn = fmaxf(m, m2);
-  if (mn != -INFINITY) {
-    s = s * ex2_approx(m - mn) + s2 * ex2_approx(m2 - mn);
-    m = mn;
-  }
-}
-
 struct S3Smem {
   uint64_t y_bar;
   uint64_t st_full[S3_MAXNS], st_empty[S3_MAXNS];
@@ -115,15 +102,6 @@ struct S3Smem {
 };
 static_assert(sizeof(S3Smem) <= 512, "S3Smem must fit below the column metadata");
 
-__device__ __forceinline__ bool better(float v, uint32_t f, float bv, uint32_t bf) {
-  return v > bv || (v == bv && f < bf);
-}
-
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-}
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint4& v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(v.x), "r"(v.y),
                "r"(v.z), "r"(v.w)
@@ -1188,88 +1166,6 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 // Output words are staged per (group, part, word) in padded rows (index r + r / E: conflict-free) and
 // written out as contiguous 2 KB row blocks.
 using S2Blocks = S2BlockTable;
-// Step-2 row buffer: [p][8 terms] complex (64-byte rows) in the TMA SWIZZLE_64B layout: the 16-byte
-// chunk c of row p sits at chunk c ^ ((p >> 1) & 3), which makes the warps' column reads conflict-free.
-constexpr int S2_SMAX = 8;
-__device__ __forceinline__ int s2_slot(int p, int zz) {  // complex index of (row p, term zz < 8)
-  return p * 8 + ((((zz >> 1) ^ (p >> 1)) & 3) << 1) + (zz & 1);
-}
-
-// packed fp32x2 arithmetic (sm_100a FADD2 / FFMA2: one instruction for both components)
-__device__ __forceinline__ unsigned long long f2_u64(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
-__device__ __forceinline__ float2 u64_f2(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-  unsigned long long d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u64(a)), "l"(f2_u64(b)));
-  return u64_f2(d);
-}
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
-  unsigned long long d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u64(a)), "l"(f2_u64(b)));
-  return u64_f2(d);
-}
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_u64(a)), "l"(f2_u64(b)), "l"(f2_u64(c)));
-  return u64_f2(d);
-}
-
-__device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
-  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-__device__ __forceinline__ float2 tw_full(const float2* tw, int j, int n) {  // e^{-2 pi i j / n}, 0 <= j < n
-  const float2 w = __ldg(tw + (j & (n / 2 - 1)));
-  return j < n / 2 ? w : make_float2(-w.x, -w.y);
-}
-
-// w_32^m = e^{-2 pi i m / 32}, m = 0..31 (cos, -sin): compile-time constants for the in-register DFTs
-__device__ constexpr float kW32c[32] = {
-    1.f, 0.98078528f, 0.92387953f, 0.83146961f, 0.70710678f, 0.55557023f, 0.38268343f, 0.19509032f,
-    0.f, -0.19509032f, -0.38268343f, -0.55557023f, -0.70710678f, -0.83146961f, -0.92387953f, -0.98078528f,
-    -1.f, -0.98078528f, -0.92387953f, -0.83146961f, -0.70710678f, -0.55557023f, -0.38268343f, -0.19509032f,
-    0.f, 0.19509032f, 0.38268343f, 0.55557023f, 0.70710678f, 0.83146961f, 0.92387953f, 0.98078528f};
-__device__ constexpr float kW32s[32] = {
-    0.f, -0.19509032f, -0.38268343f, -0.55557023f, -0.70710678f, -0.83146961f, -0.92387953f, -0.98078528f,
-    -1.f, -0.98078528f, -0.92387953f, -0.83146961f, -0.70710678f, -0.55557023f, -0.38268343f, -0.19509032f,
-    0.f, 0.19509032f, 0.38268343f, 0.55557023f, 0.70710678f, 0.83146961f, 0.92387953f, 0.98078528f,
-    1.f, 0.98078528f, 0.92387953f, 0.83146961f, 0.70710678f, 0.55557023f, 0.38268343f, 0.19509032f};
-
-// x * w_32^m for a compile-time m (after unrolling): the trivial rotations cost no multiplies
-__device__ __forceinline__ float2 cmul_w32(float2 x, int m) {
-  m &= 31;
-  if (m == 0) return x;
-  if (m == 8) return make_float2(x.y, -x.x);
-  if (m == 16) return make_float2(-x.x, -x.y);
-  if (m == 24) return make_float2(-x.y, x.x);
-  const float c = kW32c[m], sn = kW32s[m];
-  return make_float2(fmaf(x.x, c, -x.y * sn), fmaf(x.x, sn, x.y * c));
-}
-
-template <int E>
-__device__ __forceinline__ void dft_regs(float2 (&x)[E]) {
-  // radix-2 DIT over E <= 32 points with compile-time twiddles; x is addressed in bit-reversed order
-  // through rv() (a compile-time renaming), so the natural-order result ends up in x[rv(c)].
-  constexpr int LOG = (E == 32) ? 5 : (E == 16) ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));
-  auto rv = [](int i) {
-    int r = 0;
-#pragma unroll
-    for (int bb = 0; bb < LOG; ++bb) r |= ((i >> bb) & 1) << (LOG - 1 - bb);
-    return r;
-  };
-#pragma unroll
-  for (int s = 1; s < E; s *= 2) {
-#pragma unroll
-    for (int blk = 0; blk < E; blk += 2 * s) {
-#pragma unroll
-      for (int j = 0; j < s; ++j) {
-        const float2 u = x[rv(blk + j)], v = cmul_w32(x[rv(blk + j + s)], j * (32 / (2 * s)));
-        x[rv(blk + j)] = add2(u, v);
-        x[rv(blk + j + s)] = sub2(u, v);
-      }
-    }
-  }
-}
-
 template <int E>
 __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* __restrict__ Zop,
                                                       int npair, DevPlan P, S2Blocks B,
@@ -1479,23 +1375,6 @@ static size_t step2_smem(int n_in, int n) {  // n_in = n_psi input rows, n = n_g
   const int E = n / 32;
   return (size_t)n_in * S2_SMAX * 8 + (size_t)16 * (n + n / E) * 4 + 16;
 }
-
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static PFN_encodeTiled get_encode_tiled() {
-  static PFN_encodeTiled fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled>(p);
-  }
-  return fn;
-}
-
 
 static CUtensorMapL2promotion s2_l2_promotion() {  // FTK_S2_L2PROMO = 0 / 64 / 128 / 256 (diagnostics)
   const char* e = std::getenv("FTK_S2_L2PROMO");
@@ -1901,6 +1780,14 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   cudaMemcpy(tc.d_colfast, colfast.data(), colfast.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(tc.d_Ysm, yimg.data(), yimg.size() * 2, cudaMemcpyHostToDevice);
   tc.s3_smem = s3_smem_bytes(ncol_g, K3p, tc.NS);
+  {  // fused Steps 2 + 3 (ftk_s23.cu): opt-in (FTK_S23=1).  Measured slower than the separate k_step2_fft +
+     // k_step3_tc at c5 ("Fused Step 2+3"), so the default stays with the separate kernels
+    const char* e23 = std::getenv("FTK_S23");
+    if (e23 && e23[0] == '1') {
+      const int st = tc_s23_init(tc, pm.n_psi, n_gamma, rep, partner, Y3, K3p, msg);
+      if (st != FTK_OK) return st;
+    }
+  }
   FTK_SMEM_OPTIN((k_step3_tc<0>));
   FTK_SMEM_OPTIN((k_step3_tc<1>));
   if (pm.n_k % 16 != 0 || pm.n_k > 128) {
@@ -1955,6 +1842,7 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
 }
 
 void tc_plan_free(TcPlan& tc) {
+  tc_s23_free(tc);
   cudaFree(tc.d_s2tw);
   tc.d_s2tw = nullptr;
   cudaFree(tc.d_Ysm);
@@ -1994,6 +1882,7 @@ int tc_prepare_templates(TcPlan&, const float2*, int64_t, const DevPlan&, cudaSt
 }
 
 size_t tc_bytes_per_pair(const TcPlan& tc, const DevPlan& P) {
+  if (tc_s23_eligible(tc, P)) return (size_t)P.Hs * P.n_psi * sizeof(float2);  // fused: Zhat' only
   return (size_t)P.Hs * P.n_psi * sizeof(float2) + (size_t)tc.NRT * 128 * P.K3p * 4;
 }
 
@@ -2098,8 +1987,8 @@ __global__ void k_marg_finalize(const float2* __restrict__ part, int G, long lon
 }
 
 void tc_marg_finalize(const TcPlan& tc, cudaStream_t s) {
-  if (!tc.marg_part || tc.marg_np <= 0) return;
-  k_marg_finalize<<<(unsigned)((tc.marg_np + 255) / 256), 256, 0, s>>>(tc.marg_part, tc.G, tc.marg_np, tc.marg);
+  if (!tc.marg_part || tc.marg_np <= 0 || tc.marg_sets <= 0) return;
+  k_marg_finalize<<<(unsigned)((tc.marg_np + 255) / 256), 256, 0, s>>>(tc.marg_part, tc.marg_sets, tc.marg_np, tc.marg);
 }
 
 void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const PairBlock& pb, const DevPlan& P,
@@ -2170,6 +2059,23 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
         return FTK_ECUDA;
       }
     }
+    if (tc_s23_eligible(tc, P)) {  // fused Steps 2 + 3: Zhat' -> keys
+      if (prof) prof(plan, 3, 0, s);
+      const int st = launch_step23(tc, Zhat, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
+      if (prof) prof(plan, 3, 1, s);
+      if (st != FTK_OK) {
+        msg = "fused Step 2+3: launch failed (tensor map or configuration)";
+        return FTK_ECUDA;
+      }
+      if (tc.sync_debug) {
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+          msg = std::string("Steps 2+3: ") + cudaGetErrorString(e);
+          return FTK_ECUDA;
+        }
+      }
+      return FTK_OK;
+    }
     if (prof) prof(plan, 2, 0, s);
     if (launch_step2_fft(tc, Zhat, Zop, pb.count, P, s) != FTK_OK) {
       msg = "Step 2: tensor map encoding failed";
@@ -2233,6 +2139,20 @@ int tc_landscape_pairs(TcPlan& tc, const DevPlan& P, const float2* B, const int3
     for (int c = a; c < b; ++c) {
       const int k = order[c], i = h_img[k];
       const float2* zp = Zhat + (size_t)(i - pb1.i0) * P.n_psi * P.Hs;
+      if (tc_s23_eligible(tc, P)) {  // the fused kernel on this one pair
+        PairBlock pb3;
+        pb3.i0 = i;
+        pb3.ni = 1;
+        pb3.j0 = j;
+        pb3.nj = 1;
+        pb3.li = pb3.lj = nullptr;
+        pb3.count = 1;
+        if (launch_step23(tc, zp, pb3, P, tm_off, nullptr, nullptr, n_tm_local, out + (size_t)k * land_pp, s) != FTK_OK) {
+          msg = "fused Step 2+3: launch failed";
+          return FTK_ECUDA;
+        }
+        continue;
+      }
       if (launch_step2_fft(tc, zp, Zop, 1, P, s) != FTK_OK) {
         msg = "Step 2: tensor map encoding failed";
         return FTK_ECUDA;

@@ -53,9 +53,33 @@ struct TcPlan {
   // merges them into marg
   float2* marg_part = nullptr;
   int64_t marg_np = 0;
+  int marg_sets = 0;  // partial sets merged by tc_marg_finalize (G for k_step3_tc, 2 G' for k_step23)
+  // fused Steps 2 + 3 (ftk_s23.cu, k_step23): CTA pairs, rep-groups of its own (each CTA holds half of a
+  // group's Y image), FFT length F = n / D per rotation tile
+  bool s23_ready = false;
+  int s23_G = 0, s23_nch = 0, s23_NCH = 0, s23_F = 0, s23_D = 0, s23_ncol = 0;
+  int s23_col0[MAXG] = {0};
+  long long s23_yoff[MAXG] = {0};
+  long long s23_yhalf = 0;
+  int* d_s23_colrep = nullptr;
+  int* d_s23_colpart = nullptr;
+  uint8_t* d_s23_colfast = nullptr;
+  uint8_t* d_s23_Ysm = nullptr;
+  float2* d_s23_tw = nullptr;
+  size_t s23_smem = 0;
 };
 
 typedef void (*prof_cb_t)(void* plan, int cls, int end, cudaStream_t s);
+
+// fused Steps 2 + 3 (ftk_s23.cu).  tc_s23_init leaves s23_ready false (no error) for shapes it does not cover
+// (n_gamma != n_psi, n_psi outside {128, 256, 512}, Y halves that do not fit); those run k_step2_fft + k_step3_tc.
+int tc_s23_init(TcPlan& tc, int n_psi, int n_gamma, const std::vector<int>& rep, const std::vector<int>& partner,
+                const std::vector<float>& Y3, int K3p, std::string& msg);
+void tc_s23_free(TcPlan& tc);
+bool tc_s23_eligible(const TcPlan& tc, const DevPlan& P);
+int launch_step23(const TcPlan& tc, const float2* Zhat, const PairBlock& pb, const DevPlan& P, int tm_off,
+                  unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
+                  cudaStream_t s);
 
 // log-sum-exp merge of the G rep-group partials of ftk_align_marginal (see TcPlan::marg_part)
 void tc_marg_finalize(const TcPlan& tc, cudaStream_t s);
