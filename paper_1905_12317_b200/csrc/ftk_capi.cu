@@ -814,7 +814,9 @@ ftk_status_t ftk_align_marginal(ftk_plan_t plan, double tau, float* log_marginal
   // partial (max, sum) sets merged by tc_marg_finalize: k_step3_tc with G > 1 rep-groups writes one per
   // group; the fused k_step23 one per (group, CTA of the pair) (each CTA sees half of the rotations)
   const DevPlan P0 = devplan(plan);
-  plan->tc.marg_sets = tc_s23_eligible(plan->tc, P0) ? 2 * plan->tc.s23_G : (plan->tc.G > 1 ? plan->tc.G : 0);
+  plan->tc.marg_sets = (tc_s23_eligible(plan->tc, P0) || tc_s3v2_eligible(plan->tc, P0))
+                           ? 2 * plan->tc.s23_G
+                           : (plan->tc.G > 1 ? plan->tc.G : 0);
   if (plan->tc.marg_sets > 0 && plan->tc.marg_np > 0) {
     const size_t need = (size_t)plan->tc.marg_sets * plan->tc.marg_np * sizeof(float2);
     if (plan->marg_part_bytes < need) {

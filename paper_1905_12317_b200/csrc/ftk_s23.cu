@@ -91,6 +91,7 @@ static_assert(sizeof(S23Smem) <= 1024, "S23Smem");
 // FFT geometry: F = 16 V points per (term, tile), V values per lane, two terms per FFT warp (16 lanes each);
 // staging row index pi(i) = i + V (i / V^2) (conflict-free FFT writes), row stride RS = 16 (mod 32) words
 __host__ __device__ constexpr int s23_rs(int V) {
+  if (V == 0) return 0;
   return ((16 * V + V * (16 / V - 1) + 15) / 32) * 32 + 16 >= 16 * V + V * (16 / V - 1)
              ? ((16 * V + V * (16 / V - 1) + 15) / 32) * 32 + 16
              : ((16 * V + V * (16 / V - 1) + 15) / 32) * 32 + 48;
@@ -106,6 +107,11 @@ __host__ __device__ inline S23Layout s23_layout(int ncol, int nch, int NCH, int 
   const uint32_t meta_bytes = (uint32_t)ncol * 8u + (uint32_t)ncol / 8u + 2u * (uint32_t)nch + 64u;
   L.ys = up(L.meta + meta_bytes);
   const uint32_t ybytes = 2u * (uint32_t)nch * (uint32_t)(NCH / 2) * (uint32_t)K3p * 2u;
+  if (V == 0) {  // Step-3 only (operand tiles from k_step2_fft): two staging slots of one r-tile image (hi + lo)
+    L.inb = L.stg = up(L.ys + ybytes);
+    L.scr = L.total = up(L.stg + 2u * 2u * 128u * (uint32_t)K3p * 2u);
+    return L;
+  }
   L.inb = up(L.ys + ybytes);
   L.stg = up(L.inb + (uint32_t)S23_NIN * (uint32_t)n * 64u);
   L.scr = up(L.stg + 2u * (uint32_t)(K3p / 2) * (uint32_t)s23_rs(V) * 4u);
@@ -140,6 +146,8 @@ struct S23Params {
   unsigned long long* trace;  // diagnostics (kDiag23): [cta of cluster 0][16] cycle counters
   const void* zdbg;           // diagnostics: base of the block's Zhat' (FTK_S23_DBG bit 2)
   int Hs;
+  const uint8_t* Zop;         // ZS: k_step2_fft's r-tile images [pair][r-tile][part][128 x K3p bf16]
+  int NRT;                    // ZS: r-tiles per pair
   int dbg;                    // diagnostics (kDiag23, FTK_S23_DBG): bit 0 skips the FFT arithmetic, bit 1 the
                               // epilogue arithmetic (timing experiments; results are wrong by design)
 };
@@ -227,15 +235,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
     k_step23(const __grid_constant__ S23Params P, const __grid_constant__ CUtensorMap zmap) {
   extern __shared__ __align__(1024) uint8_t sraw[];
   S23Smem& S = *reinterpret_cast<S23Smem*>(sraw);
-  constexpr int F = 16 * V;          // FFT length per (term, tile)
-  constexpr int R = 16 / V;          // lanes per column group after the transpose
+  // V = 0: Step 3 only -- the A operand arrives as k_step2_fft's r-tile images (canonical K-major core matrices)
+  // and CTA h of the pair takes r-tile T = 2 s + h of unit s; V > 0: the fused FFT (F-point per tile)
+  constexpr bool ZS = V == 0;
+  constexpr int F = ZS ? 128 : 16 * V;  // rows per tile
+  constexpr int VV = ZS ? 8 : V;
+  constexpr int R = 16 / VV;            // lanes per column group after the transpose
   constexpr int LR = (R == 4) ? 2 : 1;
-  constexpr int RS = s23_rs(V);      // staging row stride (words)
-  constexpr int SR = 16 + R;         // transpose scratch row (complex)
+  constexpr int RS = s23_rs(V);         // staging row stride (words)
+  constexpr int SR = 16 + R;            // transpose scratch row (complex)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const uint32_t h = cluster_rank();
-  const int n = F * D, K3p = P.K3p, NCH = P.NCH, nch = P.nch;
-  constexpr int NT = D / 2;
+  const int n = ZS ? P.n : F * D, K3p = P.K3p, NCH = P.NCH, nch = P.nch;
+  const int NT = ZS ? P.NT : D / 2;
+  const uint32_t rt_part = 128u * (uint32_t)K3p * 2u;  // ZS: bytes of one part of an r-tile image
   const int G = P.G;
   const int cl = blockIdx.x >> 1;    // cluster index
   const int ncl = gridDim.x >> 1;
@@ -260,7 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < S23_NIN; ++i) {
       mbar_init(&S.in_full[i], 1);
-      mbar_init(&S.in_empty[i], 8);  // the slot's 4 FFT warps in each CTA
+      mbar_init(&S.in_empty[i], 8);  // fused: the slot's 4 FFT warps in each CTA; ZS: the 8 epilogue warps
     }
     mbar_init(&S.stg_full, 8);
     mbar_init(&S.stg_empty, 8);
@@ -287,7 +300,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
   }
   // staging starts zeroed: words no term writes (padding columns, the unused half of a lone ell = 0 word)
   // stay zero for the whole kernel
-  for (int w = threadIdx.x; w < 2 * KW * RS; w += blockDim.x) stg[w] = 0u;
+  if (!ZS)
+    for (int w = threadIdx.x; w < 2 * KW * RS; w += blockDim.x) stg[w] = 0u;
   if (warp == kWMma) tmem_alloc_cg2<512>(&S.tmem_base);
   if (warp == kWY && lane == 0) {  // this CTA's half of the group's Y image
     const uint32_t yb = (uint32_t)P.yhalf;
@@ -326,7 +340,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
   } else if (warp == kWTma) {
     // ---------------- TMA producer: the block's 8-term window, this CTA's n/2 rows, multicast to both CTAs
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtl));
-    if (lane == 0) {
+    if (lane == 0 && ZS) {
+      // r-tile images of k_step2_fft (one contiguous hi + lo image per (pair, r-tile)) into the staging ring
+      for (int u = 0; u < U; ++u) {
+        const int slot = u & 1;
+        const int p = p_begin + u / NT, T = 2 * (u % NT) + (int)h;
+        mbar_wait(&S.in_empty[slot], ((uint32_t)(u >> 1) & 1u) ^ 1u);
+        if (T < P.NRT) {
+          const uint32_t bytes = 2u * rt_part;
+          mbar_arrive_expect_tx(&S.in_full[slot], bytes);
+          const uint8_t* src = P.Zop + ((size_t)p * P.NRT + T) * bytes;
+          uint8_t* dst = reinterpret_cast<uint8_t*>(stg) + (size_t)slot * bytes;
+          for (uint32_t o = 0; o < bytes; o += 32768u) bulk_g2s(dst + o, src + o, min(32768u, bytes - o), &S.in_full[slot]);
+        } else {
+          mbar_arrive(&S.in_full[slot]);  // no such r-tile (odd NRT): the rows stay inactive
+        }
+      }
+    } else if (lane == 0) {
       uint32_t g = 0;
       const int half = n / 2;
       long long w_e = 0;
@@ -398,12 +428,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
     const int row = q * 32 + lane;         // tile row i
     const int hw = NCH / 2;                // columns per warp (multiple of 8)
     const bool has_odd = P.Ke < K3p;
-    const bool active = q * 32 < F;        // warp-uniform: rows >= F are padding
+    const bool active_f = q * 32 < F;      // warp-uniform: rows >= F are padding
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     const uint32_t a_full_cl0 = mapa_shared(&S.a_full[0], 0), a_full_cl1 = mapa_shared(&S.a_full[1], 0);
     const uint32_t d_empty_cl0 = mapa_shared(&S.d_empty[0], 0), d_empty_cl1 = mapa_shared(&S.d_empty[1], 0);
     const int wq = KW / 2;                 // words per part this warp copies: [eh wq, (eh + 1) wq)
     const int pi_row = row + V * (row / (V * V));
+    auto copy_stage_zs = [&](int v) {
+      // ZS: the r-tile image of unit v (staging slot v & 1, canonical K-major core matrices [part][row/8]
+      // [K3p/8][8 rows x 16 B]) -> TMEM A slot v & 1, 4 words (one 16-byte core row) per tcgen05.st
+      const int slot = v & 1;
+      const uint8_t* img = reinterpret_cast<const uint8_t*>(stg) + (size_t)slot * 2 * rt_part +
+                           (size_t)(row >> 3) * (K3p * 16) + (row & 7) * 16;
+#pragma unroll 1
+      for (int part = 0; part < 2; ++part)
+#pragma unroll 1
+        for (int w0 = eh * wq; w0 < (eh + 1) * wq; w0 += 4) {
+          const uint4 v4 = *reinterpret_cast<const uint4*>(img + (size_t)part * rt_part + (w0 / 4) * 128);
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(
+                           lane_base + acol0 + (uint32_t)(slot * K3p + part * KW + w0)),
+                       "r"(v4.x), "r"(v4.y), "r"(v4.z), "r"(v4.w)
+                       : "memory");
+        }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_cluster(slot ? a_full_cl1 : a_full_cl0);
+        mbar_arrive(&S.in_empty[slot]);
+      }
+    };
     auto copy_stage = [&](int slot) {
       // staging [part][word][RS] -> TMEM A slot (this warp's 32 rows, half of the words of each part)
       const bool ok = row < F;
@@ -432,8 +486,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
     };
     // prologue: units 0 and 1 into both A slots
     for (int u0 = 0; u0 < 2 && u0 < U; ++u0) {
-      mbar_wait(&S.stg_full, (uint32_t)u0 & 1u);
-      copy_stage(u0 & 1);
+      if (ZS) {
+        mbar_wait(&S.in_full[u0 & 1], 0u);
+        copy_stage_zs(u0);
+      } else {
+        mbar_wait(&S.stg_full, (uint32_t)u0 & 1u);
+        copy_stage(u0 & 1);
+      }
     }
     uint32_t g_d = 0, pit = 0;
     long long w_df = 0, w_sf = 0, w_ld = 0, w_cp = 0, w_pr = 0, w_rl = 0;
@@ -445,7 +504,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
       const int pl = u / NT, s = u - pl * NT;
       const int p = p_begin + pl;
       const int crot = 2 * s + (int)h;
-      const uint32_t r = (uint32_t)(D * row + crot);  // rotation of this thread's row
+      // rotation of this thread's row: fused r = D i + c; ZS r = 128 T + i (T = the r-tile, rows beyond n idle)
+      const uint32_t r = ZS ? (uint32_t)(128 * crot + row) : (uint32_t)(D * row + crot);
+      const bool active = ZS ? (128 * crot + q * 32 < n) : active_f;
       float* land_p = P.land ? P.land + (size_t)p * P.N_t * n : nullptr;
       int pi_img, pj_tm;
       pair_of(P.pb, p, pi_img, pj_tm);
@@ -594,10 +655,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
       // unit u's MMAs are complete (its last chunk's commit arrived): refill its A slot with unit u + 2
       if (u + 2 < U) {
         const long long t1 = clk23();
-        mbar_wait(&S.stg_full, (uint32_t)(u + 2) & 1u);
+        if (ZS)
+          mbar_wait(&S.in_full[u & 1], (uint32_t)((u + 2) >> 1) & 1u);
+        else
+          mbar_wait(&S.stg_full, (uint32_t)(u + 2) & 1u);
         w_sf += clk23() - t1;
         const long long t2 = clk23();
-        copy_stage(u & 1);
+        if (ZS)
+          copy_stage_zs(u + 2);
+        else
+          copy_stage(u & 1);
         w_cp += clk23() - t2;
       }
       if (s == NT - 1 && s23_flush(P, MODE, p, p_end, pi_img)) {
@@ -651,6 +718,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtl));
   } else if (warp < kWEpiFft) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegFft));
+    if constexpr (!ZS) {
     // ---------------- FFT warps: two terms of each Step-2 block per warp, one per 16-lane half.
     // F-point DFT of y_c over q1 = a + 16 b (a = lane % 16, b < V):
     //   (A) V-point DFT over b in registers, twiddle w_F^{a k1};  (T) transpose through the warp's scratch so
@@ -806,6 +874,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
       tr[13] = w_cb;
       tr[14] = w_ff;
     }
+    }  // !ZS
   }
   tc_fence_before();
   __syncthreads();
@@ -818,13 +887,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
 
 // ---------------------------------------------------------------- host side
 bool tc_s23_eligible(const TcPlan& tc, const DevPlan& P) { return tc.s23_ready && P.n_gamma == P.n_psi; }
+bool tc_s3v2_eligible(const TcPlan& tc, const DevPlan&) { return tc.s3v2_ready; }
 
+// Plan-time setup of the CTA-pair Step-3 kernels (k_step23): the Step-3-only variant (operand tiles from
+// k_step2_fft, any n_gamma) whenever its layout fits, and the fused Step 2+3 variant (n_gamma = n_psi in
+// {128, 256, 512}) when requested (fused = true) and its larger shared-memory layout fits with the same
+// rep-groups.  Leaves both off (no error) for shapes they do not cover: k_step3_tc then runs.
 int tc_s23_init(TcPlan& tc, int n_psi, int n_gamma, const std::vector<int>& rep, const std::vector<int>& partner,
-                const std::vector<float>& Y3, int K3p, std::string& msg) {
-  tc.s23_ready = false;
-  if (n_gamma != n_psi || (n_psi != 128 && n_psi != 256 && n_psi != 512)) return FTK_OK;  // separate kernels
+                const std::vector<float>& Y3, int K3p, bool fused, std::string& msg) {
+  tc.s23_ready = tc.s3v2_ready = false;
   const int n = n_psi;
-  const int F = std::min(128, n / 2), D = n / F, V = F / 16;
+  const bool fused_shape = fused && n_gamma == n_psi && (n_psi == 128 || n_psi == 256 || n_psi == 512);
+  const int F = std::min(128, n / 2), D = std::max(2, n / std::max(F, 1)), V = F / 16;
   // TMEM: two D buffers (E + O, NCH columns each) + two A slots (K3p columns) <= 512; NCH multiple of 16
   // (the epilogue drains a half chunk of up to 48 columns per warp: NCH <= 96)
   const int nmax = std::min(96, ((512 - 2 * K3p) / 4) / 16 * 16);
@@ -836,7 +910,7 @@ int tc_s23_init(TcPlan& tc, int n_psi, int n_gamma, const std::vector<int>& rep,
     const int rg = (n_rep + g - 1) / g;
     const int c = (rg + nmax - 1) / nmax;
     const int w = ((rg + c - 1) / c + 15) / 16 * 16;
-    const S23Layout LY = s23_layout(c * w, c, w, K3p, n, V);
+    const S23Layout LY = s23_layout(c * w, c, w, K3p, n_gamma, 0);
     if (LY.total <= smem_cap) {
       G = g;
       nch = c;
@@ -845,6 +919,7 @@ int tc_s23_init(TcPlan& tc, int n_psi, int n_gamma, const std::vector<int>& rep,
     }
   }
   if (G == 0) return FTK_OK;
+  const bool fused_fits = fused_shape && s23_layout(nch * NCH, nch, NCH, K3p, n, V).total <= smem_cap;
   const int rg = (n_rep + G - 1) / G;
   const int ncol_g = nch * NCH;
   tc.s23_G = G;
@@ -913,15 +988,23 @@ int tc_s23_init(TcPlan& tc, int n_psi, int n_gamma, const std::vector<int>& rep,
   cudaMemcpy(tc.d_s23_colfast, colfast.data(), colfast.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(tc.d_s23_Ysm, yimg.data(), yimg.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(tc.d_s23_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice);
-  const S23Layout LY = s23_layout(ncol_g, nch, NCH, K3p, n, V);
-  tc.s23_smem = LY.total;
+  tc.s3v2_smem = s23_layout(ncol_g, nch, NCH, K3p, n_gamma, 0).total;
+  tc.s23_smem = fused_fits ? s23_layout(ncol_g, nch, NCH, K3p, n, V).total : 0;
+  tc.s3v2_NRT = (n_gamma + 127) / 128;
   FTK_SMEM_OPTIN((k_step23<0, 8, 4>));
   FTK_SMEM_OPTIN((k_step23<0, 8, 2>));
   FTK_SMEM_OPTIN((k_step23<0, 4, 2>));
   FTK_SMEM_OPTIN((k_step23<1, 8, 4>));
   FTK_SMEM_OPTIN((k_step23<1, 8, 2>));
   FTK_SMEM_OPTIN((k_step23<1, 4, 2>));
-  tc.s23_ready = true;
+  FTK_SMEM_OPTIN((k_step23<0, 0, 2>));
+  FTK_SMEM_OPTIN((k_step23<1, 0, 2>));
+  tc.s23_ready = fused_fits;
+  {  // opt-in (FTK_S3V2=1): bit-identical to k_step3_tc but measured 2x slower at c5 (with
+     // two TMEM D buffers the cross-CTA release chain is longer than one chunk's MMAs)
+    const char* e = std::getenv("FTK_S3V2");
+    tc.s3v2_ready = e && e[0] == '1';
+  }
   return FTK_OK;
 }
 
@@ -935,18 +1018,20 @@ void tc_s23_free(TcPlan& tc) {
   tc.d_s23_colfast = nullptr;
   tc.d_s23_Ysm = nullptr;
   tc.d_s23_tw = nullptr;
-  tc.s23_ready = false;
+  tc.s23_ready = tc.s3v2_ready = false;
 }
 
-int launch_step23(const TcPlan& tc, const float2* Zhat, const PairBlock& pb, const DevPlan& P, int tm_off,
-                  unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
-                  cudaStream_t s) {
-  const int n = P.n_psi;
-  // Zhat' [pair][p][Hs] as a 2-D tensor of 8-byte elements (rows = pair * n + p), boxes of 8 terms x n/2 rows,
-  // 64-byte swizzle (the layout s2_slot() reads)
+// One launch of k_step23: zs = false -> fused Steps 2 + 3 from Zhat'; zs = true -> Step 3 only from k_step2_fft's
+// r-tile images Zop.
+static int launch_cg2(const TcPlan& tc, bool zs, const float2* Zhat, const uint8_t* Zop, const PairBlock& pb,
+                      const DevPlan& P, int tm_off, unsigned long long* img_keys, unsigned long long* pair_keys,
+                      int n_tm_local, float* land, cudaStream_t s) {
+  const int n = zs ? P.n_gamma : P.n_psi;
+  // fused: Zhat' [pair][p][Hs] as a 2-D tensor of 8-byte elements (rows = pair * n + p), boxes of 8 terms x n/2
+  // rows, 64-byte swizzle (the layout s2_slot() reads)
   alignas(64) CUtensorMap zmap;
   std::memset(&zmap, 0, sizeof zmap);
-  {
+  if (!zs) {
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) return FTK_ECUDA;
     const cuuint64_t dims[2] = {(cuuint64_t)P.Hs, (cuuint64_t)pb.count * n};
@@ -973,7 +1058,9 @@ int launch_step23(const TcPlan& tc, const float2* Zhat, const PairBlock& pb, con
   prm.n = n;
   prm.F = tc.s23_F;
   prm.D = tc.s23_D;
-  prm.NT = tc.s23_D / 2;
+  prm.NT = zs ? (tc.s3v2_NRT + 1) / 2 : tc.s23_D / 2;
+  prm.Zop = Zop;
+  prm.NRT = tc.s3v2_NRT;
   prm.K3p = P.K3p;
   prm.Ke = P.Ke;
   prm.N_t = P.N_t;
@@ -1011,10 +1098,13 @@ int launch_step23(const TcPlan& tc, const float2* Zhat, const PairBlock& pb, con
   ncl = std::min(ncl, pb.count * tc.s23_G);
   ncl = std::max(tc.s23_G, ncl / tc.s23_G * tc.s23_G);
   const dim3 grid(2 * ncl);
-  const size_t smem = tc.s23_smem;
+  const size_t smem = zs ? tc.s3v2_smem : tc.s23_smem;
   const int V = tc.s23_F / 16, D = tc.s23_D;
   auto go = [&](auto kern) { kern<<<grid, S23_THREADS, smem, s>>>(prm, zmap); };
-  if (tc.marg) {
+  if (zs) {
+    if (tc.marg) go(k_step23<1, 0, 2>);
+    else go(k_step23<0, 0, 2>);
+  } else if (tc.marg) {
     if (V == 8 && D == 4) go(k_step23<1, 8, 4>);
     else if (V == 8) go(k_step23<1, 8, 2>);
     else go(k_step23<1, 4, 2>);
@@ -1036,6 +1126,18 @@ int launch_step23(const TcPlan& tc, const float2* Zhat, const PairBlock& pb, con
     }
   }
   return cudaGetLastError() == cudaSuccess ? FTK_OK : FTK_ECUDA;
+}
+
+int launch_step23(const TcPlan& tc, const float2* Zhat, const PairBlock& pb, const DevPlan& P, int tm_off,
+                  unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
+                  cudaStream_t s) {
+  return launch_cg2(tc, false, Zhat, nullptr, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
+}
+
+int launch_step3_cg2(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, const DevPlan& P, int tm_off,
+                     unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
+                     cudaStream_t s) {
+  return launch_cg2(tc, true, nullptr, Zop, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
 }
 
 }  // namespace ftk

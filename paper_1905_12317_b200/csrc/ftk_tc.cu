@@ -1783,10 +1783,8 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   {  // fused Steps 2 + 3 (ftk_s23.cu): opt-in (FTK_S23=1).  Measured slower than the separate k_step2_fft +
      // k_step3_tc at c5 ("Fused Step 2+3"), so the default stays with the separate kernels
     const char* e23 = std::getenv("FTK_S23");
-    if (e23 && e23[0] == '1') {
-      const int st = tc_s23_init(tc, pm.n_psi, n_gamma, rep, partner, Y3, K3p, msg);
-      if (st != FTK_OK) return st;
-    }
+    const int st = tc_s23_init(tc, pm.n_psi, n_gamma, rep, partner, Y3, K3p, e23 && e23[0] == '1', msg);
+    if (st != FTK_OK) return st;
   }
   FTK_SMEM_OPTIN((k_step3_tc<0>));
   FTK_SMEM_OPTIN((k_step3_tc<1>));
@@ -2091,7 +2089,14 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     }
   }
   if (prof) prof(plan, 3, 0, s);
-  launch_step3_tc(tc, Zop, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
+  if (tc_s3v2_eligible(tc, P)) {
+    if (launch_step3_cg2(tc, Zop, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s) != FTK_OK) {
+      msg = "Step 3 (CTA pair): launch failed";
+      return FTK_ECUDA;
+    }
+  } else {
+    launch_step3_tc(tc, Zop, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
+  }
   if (prof) prof(plan, 3, 1, s);
   if (tc.sync_debug) {
     const cudaError_t e = cudaStreamSynchronize(s);
@@ -2164,7 +2169,15 @@ int tc_landscape_pairs(TcPlan& tc, const DevPlan& P, const float2* B, const int3
       pb3.nj = 1;
       pb3.li = pb3.lj = nullptr;
       pb3.count = 1;
-      launch_step3_tc(tc, Zop, pb3, P, tm_off, nullptr, nullptr, n_tm_local, out + (size_t)k * land_pp, s);
+      if (tc_s3v2_eligible(tc, P)) {
+        if (launch_step3_cg2(tc, Zop, pb3, P, tm_off, nullptr, nullptr, n_tm_local, out + (size_t)k * land_pp, s) !=
+            FTK_OK) {
+          msg = "Step 3 (CTA pair): launch failed";
+          return FTK_ECUDA;
+        }
+      } else {
+        launch_step3_tc(tc, Zop, pb3, P, tm_off, nullptr, nullptr, n_tm_local, out + (size_t)k * land_pp, s);
+      }
     }
     a = b;
   }

@@ -56,7 +56,10 @@ struct TcPlan {
   int marg_sets = 0;  // partial sets merged by tc_marg_finalize (G for k_step3_tc, 2 G' for k_step23)
   // fused Steps 2 + 3 (ftk_s23.cu, k_step23): CTA pairs, rep-groups of its own (each CTA holds half of a
   // group's Y image), FFT length F = n / D per rotation tile
-  bool s23_ready = false;
+  bool s23_ready = false;   // fused Steps 2 + 3 (opt-in, FTK_S23=1)
+  bool s3v2_ready = false;  // Step-3-only CTA-pair kernel (opt-in, FTK_S3V2=1)
+  size_t s3v2_smem = 0;
+  int s3v2_NRT = 0;
   int s23_G = 0, s23_nch = 0, s23_NCH = 0, s23_F = 0, s23_D = 0, s23_ncol = 0;
   int s23_col0[MAXG] = {0};
   long long s23_yoff[MAXG] = {0};
@@ -74,9 +77,14 @@ typedef void (*prof_cb_t)(void* plan, int cls, int end, cudaStream_t s);
 // fused Steps 2 + 3 (ftk_s23.cu).  tc_s23_init leaves s23_ready false (no error) for shapes it does not cover
 // (n_gamma != n_psi, n_psi outside {128, 256, 512}, Y halves that do not fit); those run k_step2_fft + k_step3_tc.
 int tc_s23_init(TcPlan& tc, int n_psi, int n_gamma, const std::vector<int>& rep, const std::vector<int>& partner,
-                const std::vector<float>& Y3, int K3p, std::string& msg);
+                const std::vector<float>& Y3, int K3p, bool fused, std::string& msg);
 void tc_s23_free(TcPlan& tc);
 bool tc_s23_eligible(const TcPlan& tc, const DevPlan& P);
+bool tc_s3v2_eligible(const TcPlan& tc, const DevPlan& P);
+// Step 3 on the CTA-pair kernel from k_step2_fft's operand images (same contract as launch_step3_tc)
+int launch_step3_cg2(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, const DevPlan& P, int tm_off,
+                     unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
+                     cudaStream_t s);
 int launch_step23(const TcPlan& tc, const float2* Zhat, const PairBlock& pb, const DevPlan& P, int tm_off,
                   unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
                   cudaStream_t s);

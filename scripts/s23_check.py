@@ -12,8 +12,10 @@ import synth  # noqa: E402
 import paper_1905_12317_b200 as pkg  # noqa: E402
 
 
-def run(cfg, ni, nj, fused):
-    os.environ["FTK_S23"] = "1" if fused else "0"  # fused kernel is opt-in
+def run(cfg, ni, nj, variant):
+    # variant: "old" k_step3_tc, "v2" the CTA-pair Step 3 (default), "fused" Steps 2 + 3 (opt-in)
+    os.environ["FTK_S23"] = "1" if variant == "fused" else "0"
+    os.environ["FTK_S3V2"] = "1" if variant == "v2" else "0"
     p = pkg.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), synth.shift_list(cfg), cfg.eps, n_k=cfg.n_k,
                     n_psi=cfg.n_psi, device=0)
     k, w = p.radial()
@@ -31,11 +33,12 @@ def run(cfg, ni, nj, fused):
     return pb, dt
 
 
-for name, ni, nj in [("c3", 200, 24), ("c2", 150, 40), ("c5", 260, 40), ("c4", 130, 8)]:
+for name, ni, nj in [("c3", 200, 24), ("c2", 150, 40), ("c5", 260, 40), ("c4", 130, 8), ("tiny", 4, 4)]:
     cfg = synth.config(name)
-    a, ta = run(cfg, ni, nj, False)
-    b, tb = run(cfg, ni, nj, True)
-    dv = np.abs(a["value"] - b["value"]).max() / np.abs(a["value"]).max()
-    same = np.mean((a["shift_idx"] == b["shift_idx"]) & (a["rot_idx"] == b["rot_idx"]))
-    print(f"{name}: max |dv|/max|v| = {dv:.2e}, argmax agreement {same:.4f}, time separate {ta*1e3:.1f} ms fused {tb*1e3:.1f} ms",
-          flush=True)
+    a, ta = run(cfg, ni, nj, "old")
+    for var in ("v2", "fused"):
+        b, tb = run(cfg, ni, nj, var)
+        dv = np.abs(a["value"] - b["value"]).max() / np.abs(a["value"]).max()
+        same = np.mean((a["shift_idx"] == b["shift_idx"]) & (a["rot_idx"] == b["rot_idx"]))
+        print(f"{name} {var}: max |dv|/max|v| = {dv:.2e}, argmax agreement {same:.4f}, time old {ta*1e3:.1f} ms "
+              f"{var} {tb*1e3:.1f} ms", flush=True)
