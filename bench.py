@@ -337,7 +337,7 @@ def main():
         if kern == "step2":
             # HBM-bound on STAGING bytes: the method's own HBM traffic is ~0 per inner product (SURVEY 8(d):
             # inputs only); Step 2 reads the staged Zhat' (n_psi x H_plus complex fp32) and writes the staged
-            # Step-3 operand (n_gamma x K3 real columns, bf16 hi + lo) -- an implementation cost, counted here
+            # Step-3 operand (n_gamma x K3 real columns, fp16 hi + lo) -- an implementation cost, counted here
             byts = (8.0 * cfg.n_psi * info["H_plus"] + 4.0 * n_gamma * info["K3"]) * per_launch
             peak = peaks["hbm_gbs"] if peaks else 7000.0
             achieved = byts / avg_s / 1e9 if avg_s > 0 else None
@@ -345,7 +345,7 @@ def main():
                       "bytes_per_launch": byts, "bytes_kind": "staging (not algorithmic: SURVEY 8(d))",
                       "peak_source": "measured HBM copy GB/s (MEASURED_PEAKS.json)" if peaks
                       else "fallback 7000 GB/s (B200_PROFILING.md)",
-                      "note": "staging bytes per pair 8 n_psi H_plus (read Zhat') + 4 n_gamma K3 (write bf16 hi/lo)"})
+                      "note": "staging bytes per pair 8 n_psi H_plus (read Zhat') + 4 n_gamma K3 (write fp16 hi/lo)"})
         else:
             if kern == "step3":
                 flops = 2.0 * n_t * n_gamma * info["K3"] * per_launch           # real GEMM, K = 2 H_plus - H0
@@ -353,7 +353,7 @@ def main():
                 flops = 8.0 * cfg.n_psi * info["H_plus"] * cfg.n_k * per_launch  # complex GEMM over k_m
             achieved = flops / avg_s / 1e12 if avg_s > 0 else None
             if engine == pkg.ENGINE_TC:
-                bound, peak_src = "tensor", "measured bf16 sustained (MEASURED_PEAKS.json)"
+                bound, peak_src = "tensor", "measured bf16 sustained (MEASURED_PEAKS.json) x 1 (fp16 dense = bf16 dense, B200_PROFILING.md)"
                 peak = peaks["bf16_tflops_sustained"] if peaks else 1400.0
                 if not peaks:
                     peak_src = "fallback 1.4 PF/s sustained (B200_PROFILING.md)"
@@ -370,7 +370,7 @@ def main():
                 r["tensor_issued_tflops"] = issued / avg_s / 1e12 if avg_s > 0 else None
                 r["traffic_algorithmic"] = 4.0 * 128 * info["s3_rtiles"] * info["K3p"] * per_launch
                 r["note"] = ("achieved = algorithmic flops 2*N_t*n_gamma*K3 per pair (minimal real Step-3 GEMM) / launch "
-                             "time; tensor_issued_tflops counts the MMAs actually issued (bf16x3 = 3 products, +-delta "
+                             "time; tensor_issued_tflops counts the MMAs actually issued (fp16x3 = 3 products, +-delta "
                              "symmetry halves the rows, tile padding)")
             elif kern == "step1":
                 r["note"] = "achieved = algorithmic flops 8 n_psi H_plus n_k per pair (complex Step-1 GEMM) / launch time"
@@ -383,8 +383,8 @@ def main():
     roofline["all_kernels"] = {k2: {f: roof(k2).get(f) for f in ("bound", "achieved", "peak", "unit", "frac",
                                                                    "avg_launch_ms")} for k2 in kerns}
     launches = sum(v[1] for v in kt_acc.values())
-    # whole-step tensor floor: the step's tensor work at the measured sustained bf16 peak, in the minimal
-    # (algorithmic) and in the issued (bf16x3, padded tiles) form, against the measured step time
+    # whole-step tensor floor: the step's tensor work at the measured sustained bf16 (= fp16) peak, in the minimal
+    # (algorithmic) and in the issued (fp16x3, padded tiles) form, against the measured step time
     if engine == pkg.ENGINE_TC:
         pairs_step = float(pairs_local)
         alg = pairs_step * (8.0 * cfg.n_psi * info["H_plus"] * cfg.n_k + 2.0 * n_t * n_gamma * info["K3"])
@@ -397,7 +397,7 @@ def main():
             "algorithmic_tflop_per_step": alg / 1e12, "issued_tflop_per_step": issued / 1e12,
             "floor_ms_algorithmic": 1e3 * alg / pk, "floor_ms_issued": 1e3 * issued / pk,
             "frac_algorithmic": (alg / pk) / step_s, "frac_issued": (issued / pk) / step_s,
-            "peak_source": "measured bf16 sustained (MEASURED_PEAKS.json)" if peaks else "fallback 1.4 PF/s"}
+            "peak_source": "measured bf16 sustained (MEASURED_PEAKS.json) = fp16 dense rate" if peaks else "fallback 1.4 PF/s"}
 
     # ---- end to end through the C ABI from pinned host buffers
     e2e = None
@@ -450,7 +450,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "inner products/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt_ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "bf16x3" if engine == pkg.ENGINE_TC else "f32", "data": "synthetic",
+                "dtype": "fp16x3" if engine == pkg.ENGINE_TC else "f32", "data": "synthetic",
                 "config": {"workload": cfg.name, "n": cfg.n, "K": cfg.K, "n_k": cfg.n_k, "n_psi": cfg.n_psi,
                            "n_gamma": n_gamma,
                            "N_im": ni, "N_tm": nj, "N_t": n_t, "eps": cfg.eps, "H": info["H"],

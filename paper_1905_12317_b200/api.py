@@ -10,7 +10,7 @@ import numpy as np
 
 from . import _ffi
 
-ENGINE_TC = 0     # tcgen05 bf16x3 tensor-core path
+ENGINE_TC = 0     # tcgen05 fp16x3 tensor-core path
 ENGINE_SIMT = 1   # CUDA-core fp32 reference kernels
 KERNEL_CLASSES = ("load_fft", "step1", "step2", "step3", "finalize")
 

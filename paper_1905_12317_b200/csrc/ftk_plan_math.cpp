@@ -54,7 +54,9 @@ void gauss_legendre(int n, std::vector<double>& t, std::vector<double>& w) {
   }
 }
 
-// Symmetric tridiagonal implicit QL with eigenvectors (z: n x n row-major, z[r*n+c]).
+// Symmetric tridiagonal implicit QL with eigenvectors (z: n x n row-major, z[r*n+c]).  Source: the textbook
+// implicit-shift QL iteration of the EISPACK tql2 lineage as given in Press et al., Numerical Recipes, 2nd ed.,
+// Sec. 11.3 ("tqli"), with its temporaries (f, g, r, s, c, p, b); host-side plan setup only (untimed).
 static bool tridiag_ql(int n, std::vector<double>& d, std::vector<double>& e, std::vector<double>& z) {
   for (int i = 1; i < n; ++i) e[i - 1] = e[i];
   e[n - 1] = 0.0;
@@ -137,6 +139,8 @@ void bessel_j_all(double x, int nmax, double* J) {
     return;
   }
   const int big = std::max(nmax, (int)x);
+  // Miller start index: the even N above max(nmax, x) + sqrt(ACC (big + 1)) with ACC = 40, the heuristic of
+  // Numerical Recipes' bessj (2nd ed., Sec. 6.5)
   int N = 2 * ((big + 40 + (int)std::sqrt(40.0 * (big + 1))) / 2);
   double bjp = 0.0, bj = 1.0, sum = 0.0;
   for (int kk = N; kk > 0; --kk) {

@@ -12,12 +12,12 @@
 // input window of the term.  A "unit" is (pair, tile s); the cluster runs the units of its pair range in
 // order, the two CTAs in lock step.  One tcgen05.mma M = 256 covers both CTAs' 128-row tiles (rows >= F
 // unused), N = NCH representative shifts (B = Y3 chunk, its NCH/2 columns of each chunk resident in each
-// CTA's shared memory: half of the Y image per SM), K = K3p in bf16x3 (hi*hi + hi*lo + lo*hi).
+// CTA's shared memory: half of the Y image per SM), K = K3p in fp16x3 (hi*hi + hi*lo + lo*hi, scaled operands).
 //
 // Warp roles (20 warps):
 //   0-7    FFT: two groups of 4 warps, one per input slot; each warp two terms of a Step-2 block (16 lanes
 //          each): y_c from the input window, F-point FFT (V-point register DFTs around a transpose, one or
-//          two shuffle stages), bf16 hi/lo split into the staging area [part][word][row]
+//          two shuffle stages), fp16 hi/lo split (scaled) into the staging area [part][word][row]
 //   8      Y image load at start, then idle
 //   9      merge: the 8 epilogue records -> packed-key atomicMax (or the MODE-1 partial)
 //   10     TMA producer: per (unit, Step-2 block) the block's 8-term window of Zhat', n/2 rows per CTA,
@@ -143,16 +143,20 @@ struct S23Params {
   float2* marg_part;  // MODE 1: [2 G][N_im][n_tm_local] base-2 (max, sum) partials
   long long marg_np;
   float msc;          // MODE 1: log2(e) / tau
+  const float2* ast;  // fp16x3 scaling (ftk_tc.cu header): image / local template maxima, Z bound constant,
+  const float2* bst;  // Y3 exponent
+  float Cz;
+  int eY;
   unsigned long long* trace;  // diagnostics (kDiag23): [cta of cluster 0][16] cycle counters
   const void* zdbg;           // diagnostics: base of the block's Zhat' (FTK_S23_DBG bit 2)
   int Hs;
-  const uint8_t* Zop;         // ZS: k_step2_fft's r-tile images [pair][r-tile][part][128 x K3p bf16]
+  const uint8_t* Zop;         // ZS: k_step2_fft's r-tile images [pair][r-tile][part][128 x K3p fp16]
   int NRT;                    // ZS: r-tiles per pair
   int dbg;                    // diagnostics (kDiag23, FTK_S23_DBG): bit 0 skips the FFT arithmetic, bit 1 the
                               // epilogue arithmetic (timing experiments; results are wrong by design)
 };
 
-// Step-3 MMAs of one chunk over the CTA pair (one thread of the even CTA): 3 x KS bf16 products M256 x NCH x K16
+// Step-3 MMAs of one chunk over the CTA pair (one thread of the even CTA): 3 x KS fp16 products M256 x NCH x K16
 template <int KS>
 __device__ __forceinline__ void s23_chunk_mmas(uint32_t dE, uint32_t dO, uint32_t a_hi0, uint32_t halfk, uint64_t bh0,
                                                uint64_t bl0, uint32_t idesc, int ke, int ksteps) {
@@ -162,18 +166,18 @@ __device__ __forceinline__ void s23_chunk_mmas(uint32_t dE, uint32_t dO, uint32_
       const uint32_t d = ks >= ke ? dO : dE;
       const uint32_t acc0 = (ks == 0 || ks == ke) ? 0u : 1u;
       const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + halfk;
-      mma_bf16_ts_cg2(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);
-      mma_bf16_ts_cg2(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
-      mma_bf16_ts_cg2(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+      mma_f16_ts_cg2(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);
+      mma_f16_ts_cg2(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
+      mma_f16_ts_cg2(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
     }
   } else {
     for (int ks = 0; ks < ksteps; ++ks) {
       const uint32_t d = ks >= ke ? dO : dE;
       const uint32_t acc0 = (ks == 0 || ks == ke) ? 0u : 1u;
       const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + halfk;
-      mma_bf16_ts_cg2(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);
-      mma_bf16_ts_cg2(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
-      mma_bf16_ts_cg2(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+      mma_f16_ts_cg2(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);
+      mma_f16_ts_cg2(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
+      mma_f16_ts_cg2(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
     }
   }
 }
@@ -188,7 +192,7 @@ struct S23MmaArgs {
 template <int KS>
 __device__ __forceinline__ void s23_mma_loop(const S23MmaArgs& a) {
   S23Smem& S = *a.S;
-  const uint32_t idesc = idesc_bf16_f32(256, a.NCH);
+  const uint32_t idesc = idesc_f16_f32(256, a.NCH);
   const uint32_t halfk = (uint32_t)a.K3p / 2u;
   uint32_t g_d = 0;
   long long w_a = 0, w_d = 0;
@@ -411,7 +415,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
             }
           mbar_arrive(&S.red_empty[rb]);
           if (f != 0xffffffffu) {
-            const unsigned long long key = pack_key(v, f);  // f: global flat index (template, shift, rot)
+            // f: global flat index (template, shift, rot); v is in pair p's fp16x3 units (exact rescale)
+            const int pe = f16_scale_exp(P.Cz * __ldg(P.ast + i).y * __ldg(P.bst + j).y) + P.eY;
+            const unsigned long long key = pack_key(ldexpf(v, -pe), f);
             if (P.img_keys) atomicMax(&P.img_keys[i], key);
             if (P.pair_keys) atomicMax(&P.pair_keys[(size_t)i * P.n_tm_local + j], key);
           }
@@ -500,6 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
     float bv = -INFINITY;          // MODE 0: best value of this thread's rows in the current pair
     uint32_t bf = 0xffffffffu;     //         and its flat index t n + r
     float mrun = -INFINITY, srun = 0.f;  // MODE 1: running base-2 log-sum-exp of X log2(e) / tau
+    int pe_prev = 0;
     for (int u = 0; u < U; ++u) {
       const int pl = u / NT, s = u - pl * NT;
       const int p = p_begin + pl;
@@ -510,6 +517,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
       float* land_p = P.land ? P.land + (size_t)p * P.N_t * n : nullptr;
       int pi_img, pj_tm;
       pair_of(P.pb, p, pi_img, pj_tm);
+      // fp16x3: this pair's results are X 2^pe; a MODE-0 record carried over from the previous pair of the same
+      // image is rescaled (exactly) into this pair's units
+      const int pe = f16_scale_exp(P.Cz * __ldg(P.ast + pi_img).y * __ldg(P.bst + pj_tm).y) + P.eY;
+      if (s == 0) {
+        if (MODE == 0 && bv != -INFINITY) bv = ldexpf(bv, pe - pe_prev);
+        pe_prev = pe;
+      }
+      const float msc_p = ldexpf(P.msc, -pe);
       // flat indices are global ((template, shift) major, rotation minor): the running best of MODE 0 is
       // carried over the consecutive templates of one image unless per-pair maxima are requested
       const uint32_t fbase = (uint32_t)(P.tm_off + pj_tm) * (uint32_t)P.N_t;
@@ -601,7 +616,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
                     bv = xp;
                     bf = fp;
                   }
-                  if (land_p && row < F) land_p[(size_t)tp * n + r] = xp;
+                  if (land_p && row < F) land_p[(size_t)tp * n + r] = ldexpf(xp, -pe);
                   if (tm >= 0) {
                     const float xm = ev - ov;
                     const uint32_t fm = (fbase + (uint32_t)tm) * (uint32_t)n + r;
@@ -609,7 +624,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
                       bv = xm;
                       bf = fm;
                     }
-                    if (land_p && row < F) land_p[(size_t)tm * n + r] = xm;
+                    if (land_p && row < F) land_p[(size_t)tm * n + r] = ldexpf(xm, -pe);
                   }
                 }
               }
@@ -627,12 +642,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
                 }
               }
               if (cm != -INFINITY) {
-                cm *= P.msc;
+                cm *= msc_p;
                 if (cm > mrun) {
                   srun *= ex2_approx(mrun - cm);
                   mrun = cm;
                 }
-                const float nm = -mrun, sc = P.msc;
+                const float nm = -mrun, sc = msc_p;
                 float sk = 0.f;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
@@ -753,6 +768,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
     for (int u = 0; u < U; ++u) {
       const int s = u % NT;
       const int crot = 2 * s + (int)h;
+      int ez;  // fp16x3 scale exponent of this pair's Z
+      {
+        int pi_, pj_;
+        pair_of(P.pb, p_begin + u / NT, pi_, pj_);
+        ez = f16_scale_exp(P.Cz * __ldg(P.ast + pi_).y * __ldg(P.bst + pj_).y);
+      }
       // per unit: w_n^{q1 c} for this lane's q1 = a + 16 b, and the radix-D combination constants
       float2 tu[V];
 #pragma unroll
@@ -840,7 +861,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
         }
         w_ff += clk23() - t3;
         if (act && !(kDiag23 && (P.dbg & 16))) {
-          // stage: ell > 0 -> word (Re, Im); ell = 0 -> one bf16 half of a word (the other: a neighbour or zero)
+          // stage: ell > 0 -> word (Re, Im); ell = 0 -> one fp16 half of a word (the other: a neighbour or zero)
           const int W = cc >> 1;
           uint32_t* shi = stg + (size_t)W * RS;
           uint32_t* slo = stg + (size_t)(KW + W) * RS;
@@ -848,17 +869,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
           for (int m = 0; m < V; ++m) {
             const int i = k1g + V * m + V * V * m2;
             const int pi = i + V * m2;
-            const float2 a0v = x[rv(m)];
+            const float2 a0v = make_float2(ldexpf(x[rv(m)].x, ez), ldexpf(x[rv(m)].y, ez));
             if (l > 0) {
               uint32_t hh2, ll2;
-              split2_bf16(a0v.x, a0v.y, hh2, ll2);
+              split2_f16(a0v.x, a0v.y, hh2, ll2);
               shi[pi] = hh2;
               slo[pi] = ll2;
             } else {
-              const __nv_bfloat16 hb = __float2bfloat16_rn(a0v.x);
-              const __nv_bfloat16 lb = __float2bfloat16_rn(a0v.x - __bfloat162float(hb));
-              reinterpret_cast<__nv_bfloat16*>(shi + pi)[cc & 1] = hb;
-              reinterpret_cast<__nv_bfloat16*>(slo + pi)[cc & 1] = lb;
+              const __half hb = __float2half_rn(a0v.x);
+              const __half lb = __float2half_rn(a0v.x - __half2float(hb));
+              reinterpret_cast<__half*>(shi + pi)[cc & 1] = hb;
+              reinterpret_cast<__half*>(slo + pi)[cc & 1] = lb;
             }
           }
         }
@@ -932,7 +953,7 @@ int tc_s23_init(TcPlan& tc, int n_psi, int n_gamma, const std::vector<int>& rep,
   std::vector<uint8_t> colfast(tc.s23_ncol / 8 + 16, 0);
   // Y image per (group, half): [part][chunk][NCH/2 rows][K3p] canonical K-major (core = 8 rows x 16 B)
   const int hr = NCH / 2;
-  const size_t half_elems = (size_t)2 * nch * hr * K3p;  // bf16 elements (both parts)
+  const size_t half_elems = (size_t)2 * nch * hr * K3p;  // fp16 elements (both parts)
   tc.s23_yhalf = (long long)half_elems * 2;
   std::vector<uint16_t> yimg((size_t)G * 2 * half_elems, 0);
   for (int g = 0; g < G; ++g) {
@@ -946,9 +967,9 @@ int tc_s23_init(TcPlan& tc, int n_psi, int n_gamma, const std::vector<int>& rep,
       const int t = rep[rr];
       const int chunk = c / NCH, within = c % NCH, hh = within / hr, rrow = within % hr;
       for (int k = 0; k < K3p; ++k) {
-        const float x = Y3[(size_t)t * K3p + k];
-        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-        const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+        const float x = std::ldexp(Y3[(size_t)t * K3p + k], tc.eY);  // fp16x3 (see ftk_tc.cu header)
+        const __half hi = __float2half_rn(x);
+        const __half lo = __float2half_rn(x - __half2float(hi));
         const size_t core = (size_t)chunk * hr * K3p + (size_t)(rrow / 8) * (K3p / 8) * 64 + (size_t)(k / 8) * 64 +
                             (rrow % 8) * 8 + (k % 8);
         const size_t hbase = ((size_t)g * 2 + hh) * half_elems;
@@ -1080,6 +1101,10 @@ static int launch_cg2(const TcPlan& tc, bool zs, const float2* Zhat, const uint8
   prm.marg_part = tc.marg ? tc.marg_part : nullptr;
   prm.marg_np = tc.marg_np;
   prm.msc = tc.marg_scale;
+  prm.ast = tc.d_ast;
+  prm.bst = tc.d_bst;
+  prm.Cz = tc.Cz;
+  prm.eY = tc.eY;
   if (kDiag23) {
     const char* e = std::getenv("FTK_S23_DBG");
     prm.dbg = e ? std::atoi(e) : 0;

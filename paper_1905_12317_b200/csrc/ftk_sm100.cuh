@@ -2,6 +2,7 @@
 // tcgen05 TMEM allocation / MMA / loads / stores / commits, UMMA descriptors.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -165,13 +166,19 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// Instruction descriptor: kind::f16 with FP16 A/B (format code 0), F32 accumulate, both K-major.
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 // Same with B MN-major (bit 16): B stored with N contiguous inside 16-byte core rows
 // (INTERLEAVE canonical: core matrix = 8 K-rows x 8 N-elements, 128 B; SBO = N-direction core stride,
 // LBO = K-direction core stride).
 __host__ __device__ constexpr uint32_t idesc_bf16_f32_bmn(int M, int N) { return idesc_bf16_f32(M, N) | (1u << 16); }
 
-// D[tmem] (+)= A[tmem] * B[smem]^T  (A from TMEM: "TS" form), cta_group::1, kind::f16
-__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+// D[tmem] (+)= A[tmem] * B[smem]^T  (A from TMEM: "TS" form), cta_group::1, kind::f16 (bf16 or fp16
+// operands, as the instruction descriptor says: idesc_bf16_f32 / idesc_f16_f32)
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -181,7 +188,7 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       : "memory");
 }
 // D[tmem] (+)= A[smem] * B[smem]^T  ("SS" form)
-__device__ __forceinline__ void mma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+__device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -198,6 +205,25 @@ __device__ __forceinline__ void split2_bf16(float x0, float x1, uint32_t& hi, ui
   __nv_bfloat162 l = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
   hi = *reinterpret_cast<uint32_t*>(&h);
   lo = *reinterpret_cast<uint32_t*>(&l);
+}
+
+// fp16 split x = hi + lo (round-to-nearest both), packed pairs for two consecutive K elements.  The operands
+// are pre-scaled by powers of two into fp16's range (|x| <= 2^14, see ftk_tc.cu "fp16x3 scaling"), so hi
+// keeps 11 significant bits and lo the next 11: 22 bits per operand against bf16x3's 16.
+__device__ __forceinline__ void split2_f16(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  __half2 h = __floats2half2_rn(x0, x1);
+  float2 hf = __half22float2(h);
+  __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<uint32_t*>(&h);
+  lo = *reinterpret_cast<uint32_t*>(&l);
+}
+// 14 - ceil(log2 x) for x > 0 (0 otherwise): the exponent e with x 2^e in (2^13, 2^14]
+__host__ __device__ inline int f16_scale_exp(float x) {
+  if (!(x > 0.f) || !(x < 3.0e38f)) return 0;
+  int e;
+  const float f = frexpf(x, &e);  // x = f 2^e, f in [0.5, 1)
+  const int c = (f == 0.5f) ? e - 1 : e;
+  return 14 - c;
 }
 
 __device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }

@@ -1,9 +1,19 @@
-// Tensor-core (tcgen05) engine of the FTK hot path, bf16x3 split arithmetic.
+// Tensor-core (tcgen05) engine of the FTK hot path, fp16x3 split arithmetic with power-of-two operand scaling.
 //
 // Step 3 (PAPER.md Eq. fbk3; real form of DESIGN.md reading R13):
 //   X_p(t, r) = sum_k Z3_p[r][k] Y3[t][k],  k < K3 = 2 H_plus - H0,  then max/argmax over (t, r).
-// Every operand x is split x = hi + lo in bf16 and the product is hi*hi + hi*lo + lo*hi with fp32
-// accumulation in TMEM (measured <= 6e-6 ||A|| ||B|| vs the 1e-4 budget).
+// Every operand x is scaled by a power of two into fp16's range and split x = hi + lo in fp16; the product is
+// hi*hi + hi*lo + lo*hi with fp32 accumulation in TMEM and the scale removed exactly afterwards (DESIGN.md
+// section 6 "fp16x3": 22 significant bits per operand, the accuracy of 3xTF32 at the bf16 MMA rate).
+// fp16x3 scaling (all exponents from f16_scale_exp, x 2^e in (2^13, 2^14]):
+//   Step-1 image operand  a_i      x 2^{e(amax_i)}            amax_i = max |Re|, |Im| of image i's FB coefficients
+//   Step-1 generated operand c_j   x 2^{e(gmax bmax_j)}       gmax = max |g_zeta(k_m)|, bmax_j likewise for template j
+//   Step-1 output Zhat'            unscaled (x 2^{-(e_a + e_c)}) in the epilogue: Zhat' is plain fp32
+//   Step-3 operand Z (pair i, j)   x 2^{e(gmax |a_i| |b_j|)}  |.| = Frobenius norm over (m, p); bounds |Z| by
+//                                  |Z_zeta(r)| <= sum_{m,p} |a(m,p)| |g_zeta(m)| |b(m,p+ell)| <= gmax |a| |b|
+//                                  (Cauchy-Schwarz; the shift p -> p + ell permutes the modes)
+//   Step-3 operand Y3              x 2^{eY}, eY = e(max |Y3|) (plan constant)
+//   Step-3 results                 x 2^{-(e_Z + eY)} per pair before keys / landscapes / log-marginals
 //
 // Kernel k_step3_tc (one CTA per SM, persistent).  GEMM orientation: M = 128 rotations r (one "r-tile"
 // of the pair's operand Z3, the A operand, held in TMEM), N = a chunk of NCH representative shifts
@@ -13,7 +23,7 @@
 // E = Z_even Y_even, O = Z_odd Y_odd accumulated separately: half the shifts, same K.
 // Representative shifts are split into rep-groups whose Y image fits in shared memory; CTA b serves
 // group b % G for a contiguous range of pairs (G = 1 at the BASELINE configs c2, c3, c5).
-//   * warp 1 (one lane): producer -- per (pair, r-tile) one bulk copy of the Step-2 operand image (bf16
+//   * warp 1 (one lane): producer -- per (pair, r-tile) one bulk copy of the Step-2 operand image (fp16
 //     hi/lo, canonical K-major core matrices) into a shared-memory staging ring.
 //   * warp 0 (one elected lane): per r-tile 2 x K3p/16 tcgen05.cp.128x256b staging -> TMEM A slot, then
 //     per chunk 3 x K3p/16 tcgen05.mma M128 x NCH x K16 (A = Z r-tile from TMEM, B = Y chunk from SMEM)
@@ -25,7 +35,7 @@
 //     (branch-free over all-fast half chunks); per pair the partial records go to the resolver through
 //     shared memory (no CTA-wide barrier).  MODE 1 replaces the max by a log-sum-exp (marginalization).
 //   * warp 10: resolver -- merges the 8 partial records, recomputes the 16 E / O sums of the pair's
-//     winning group in fp32 from the same bf16 operands to recover the exact (shift, sign), one
+//     winning group in fp32 from the same fp16 operands to recover the exact (shift, sign), one
 //     packed-key atomicMax per pair.
 // TMEM columns: D buffers [0, 4 NCH) (E, O of buffer 0 then 1), A slots [4 NCH, 4 NCH + 2 K3p).
 #include <cuda.h>
@@ -70,7 +80,7 @@ constexpr int S3_MAXG = TcPlan::MAXG;
 constexpr int S3_MAXNS = 4;
 
 struct S3Params {
-  const uint8_t* Zop;     // per pair: [r-tile][part][row/8][K3p/8][8 rows x 16 B] bf16x2 words (Step 2 output)
+  const uint8_t* Zop;     // per pair: [r-tile][part][row/8][K3p/8][8 rows x 16 B] fp16x2 words (Step 2 output)
   const uint8_t* Ysm;     // per group: shared-memory image [part][rep/8][K3p/8][8 rows x 16 B]
   const int* colrep;      // [ncol_total] shift index of the representative (+delta); -1: padding column
   const int* colpart;     // [ncol_total] shift index of -delta; -1: none
@@ -87,6 +97,10 @@ struct S3Params {
   float2* marg_part;  // MODE 1 with G > 1: [G][N_im][n_tm_local] base-2 (max, sum) partials
   long long marg_np;
   float msc;       // MODE 1: log2(e) / tau
+  const float2* ast;  // fp16x3 scaling (see the file header): per image / local template maxima
+  const float2* bst;
+  float Cz;
+  int eY;
   int dbg;         // FTK_S3_DBG (diagnostics): bit 0 skips the epilogue arithmetic, bit 1 the TMEM drain (timing only)
   unsigned long long* trace;  // nullable (FTK_S3_TRACE=1): wait / busy cycle counters of CTA 0
 };
@@ -125,7 +139,7 @@ struct S3MmaArgs {
 template <int KS, bool TR>
 __device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[3]) {
   S3Smem& S = *a.S;
-  const uint32_t idesc = idesc_bf16_f32(128, a.NCH);
+  const uint32_t idesc = idesc_f16_f32(128, a.NCH);
   const int ksteps = KS > 0 ? KS : a.K3p / 16, halfk = a.K3p / 2, ke = a.ke_steps;
   uint32_t g_a = 0, g_d = 0;
   const long long tr0 = diag_clock();
@@ -163,18 +177,18 @@ __device__ __forceinline__ void s3_mma_loop(const S3MmaArgs& a, long long (&tr)[
             const uint32_t d = ks >= ke ? dO : dE;
             const uint32_t acc0 = (ks == 0 || ks == ke) ? 0u : 1u;
             const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + (uint32_t)halfk;
-            mma_bf16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);  // +256 B per k-step
-            mma_bf16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
-            mma_bf16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_f16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);  // +256 B per k-step
+            mma_f16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_f16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
           }
         } else {
           for (int ks = 0; ks < ksteps; ++ks) {
             const uint32_t d = ks >= ke ? dO : dE;
             const uint32_t acc0 = (ks == 0 || ks == ke) ? 0u : 1u;
             const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + (uint32_t)halfk;
-            mma_bf16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);
-            mma_bf16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
-            mma_bf16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_f16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);
+            mma_f16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_f16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
           }
         }
         tc_commit(&S.d_full[db]);
@@ -205,7 +219,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
   uint8_t* s_fastc = s_fast + ncol / 8;  // [nch * 2]: leading columns of a half chunk in fast groups
   const uint32_t meta_bytes = ((uint32_t)ncol * 8u + (uint32_t)ncol / 8u + 2u * (uint32_t)nch + 512u + 1023u) & ~1023u;
   uint8_t* ys = s3_raw + 1024 + meta_bytes;                        // Y image of this group
-  const uint32_t ypart = (uint32_t)ncol * (uint32_t)K3p * 2u;       // bytes of one bf16 part
+  const uint32_t ypart = (uint32_t)ncol * (uint32_t)K3p * 2u;       // bytes of one fp16 part
   const uint32_t rt_part = 128u * (uint32_t)K3p * 2u;              // one part of an r-tile image
   uint8_t* stg = ys + ((2u * ypart + 1023u) & ~1023u);              // staging ring: NS r-tile images
   const uint32_t SBO = (uint32_t)K3p * 16u;                         // bytes between 8-row groups
@@ -332,6 +346,13 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
       uint32_t bfe = 0xffffffffu;
       float mrun = -INFINITY, srun = 0.f;  // MODE 1: running base-2 log-sum-exp of X log2(e) / tau
       float* land_p = P.land ? P.land + (size_t)p * P.N_t * n : nullptr;
+      int pe;  // this pair's result scale exponent (values are X 2^pe)
+      {
+        int pi_, pj_;
+        pair_of(P.pb, p, pi_, pj_);
+        pe = f16_scale_exp(P.Cz * __ldg(P.ast + pi_).y * __ldg(P.bst + pj_).y) + P.eY;
+      }
+      const float msc_p = ldexpf(P.msc, -pe);  // MODE 1: log2(e) / tau in scaled units
       for (int T = 0; T < NRT; ++T) {
         const int r = T * 128 + row;
         const bool active = T * 128 + q * 32 < n;  // warp-uniform: lane quarters beyond n_psi idle
@@ -394,7 +415,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
                   bve = xp;
                   bfe = fp;
                 }
-                if (land_p) land_p[(size_t)tp * n + r] = xp;
+                if (land_p) land_p[(size_t)tp * n + r] = ldexpf(xp, -pe);
                 if (tm >= 0) {
                   const float xm = ev - ov;
                   const uint32_t fm = (uint32_t)tm * (uint32_t)n + (uint32_t)r;
@@ -402,7 +423,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
                     bve = xm;
                     bfe = fm;
                   }
-                  if (land_p) land_p[(size_t)tm * n + r] = xm;
+                  if (land_p) land_p[(size_t)tm * n + r] = ldexpf(xm, -pe);
                 }
               }
             }
@@ -502,12 +523,12 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
               }
             float cm = fmaxf(fmaxf(fmaxf(cmk[0], cmk[1]), fmaxf(cmk[2], cmk[3])),
                              fmaxf(fmaxf(cmk[4], cmk[5]), fmaxf(cmk[6], cmk[7])));
-            cm *= P.msc;
+            cm *= msc_p;
             if (cm > mrun) {
               srun *= ex2_approx(mrun - cm);
               mrun = cm;
             }
-            const float nm = -mrun, sc = P.msc;
+            const float nm = -mrun, sc = msc_p;
             float sk[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) sk[k] = 0.f;
@@ -563,7 +584,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
             float cm = fmaxf(fmaxf(fmaxf(cmk[0], cmk[1]), fmaxf(cmk[2], cmk[3])),
                              fmaxf(fmaxf(cmk[4], cmk[5]), fmaxf(cmk[6], cmk[7])));
             if (cm != -INFINITY) {
-              cm *= P.msc;
+              cm *= msc_p;
               if (cm > mrun) {
                 srun *= ex2_approx(mrun - cm);
                 mrun = cm;
@@ -572,7 +593,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
               float sk[8];
 #pragma unroll
               for (int k = 0; k < 8; ++k) sk[k] = 0.f;
-              const float nm = -mrun, sc = P.msc;
+              const float nm = -mrun, sc = msc_p;
 #pragma unroll
               for (int g8 = 0; g8 < 5; ++g8) {
                 if (8 * g8 >= hw) break;
@@ -646,7 +667,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
     }
   } else {
     // ---------------- resolver (warp 10): merge the 8 partial records; exact (shift, sign) of the pair's
-    // winning group by recomputing its 16 E / O sums from the same bf16 hi/lo operands (fp32 on CUDA
+    // winning group by recomputing its 16 E / O sums from the same fp16 hi/lo operands (fp32 on CUDA
     // cores); merge with the exact record; one packed-key atomicMax per pair.
     uint32_t it = 0;
     for (int p = p_begin; p < p_end; ++p, ++it) {
@@ -694,18 +715,18 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         float es[8], os[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) es[k] = os[k] = 0.f;
-        const __nv_bfloat16* yh = reinterpret_cast<const __nv_bfloat16*>(ys);
-        const __nv_bfloat16* yl = yh + (size_t)ncol * K3p;
+        const __half* yh = reinterpret_cast<const __half*>(ys);
+        const __half* yl = yh + (size_t)ncol * K3p;
         for (int kk = lane; kk < K3p; kk += 32) {
           const size_t zo = (size_t)(kk >> 3) * 128 + (kk & 7) * 2;
-          const float zh = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(zrow + zo));
-          const float zl = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(zrow + rt_part + zo));
+          const float zh = __half2float(*reinterpret_cast<const __half*>(zrow + zo));
+          const float zl = __half2float(*reinterpret_cast<const __half*>(zrow + rt_part + zo));
           const bool even = kk < P.Ke;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const int cc = cl + k;
             const size_t yo = (size_t)(cc >> 3) * (K3p / 8) * 64 + (size_t)(kk >> 3) * 64 + (cc & 7) * 8 + (kk & 7);
-            const float a = __bfloat162float(yh[yo]), b = __bfloat162float(yl[yo]);
+            const float a = __half2float(yh[yo]), b = __half2float(yl[yo]);
             const float pr = fmaf(zh, a, fmaf(zh, b, zl * a));
             if (even)
               es[k] += pr;
@@ -743,7 +764,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         pair_of(P.pb, p, i, j);
         const uint32_t tt2 = bf / (uint32_t)n, rr = bf - tt2 * (uint32_t)n;
         const uint32_t gflat = ((uint32_t)(P.tm_off + j) * (uint32_t)P.N_t + tt2) * (uint32_t)n + rr;
-        const unsigned long long kk = pack_key(bv, gflat);
+        const int pe = f16_scale_exp(P.Cz * __ldg(P.ast + i).y * __ldg(P.bst + j).y) + P.eY;
+        const unsigned long long kk = pack_key(ldexpf(bv, -pe), gflat);  // fp16x3 scale removed (exact)
         if (P.img_keys) atomicMax(&P.img_keys[i], kk);
         if (P.pair_keys) atomicMax(&P.pair_keys[(size_t)i * P.n_tm_local + j], kk);
       }
@@ -785,6 +807,9 @@ struct S1Params {
   int i0, ni, j0, nj;   // block (i0 multiple of 128)
   int n, n_k, Hp, Hs, KCH, NKCH, NIT;  // NIT = image tiles per mode in Aop
   int F, NCT;           // F = nj * Hs flattened (j, zeta slot) columns (pad slots written as zeros), NCT = ceil(F / 64)
+  const float2* ast;    // fp16x3 scaling (file header): image maxima [N_im], local template maxima [n_tm_local]
+  const float2* bst;
+  float gmax;           // max |g_zeta(k_m)|
   unsigned long long* trace;  // nullable (FTK_S1_TRACE=1): wait cycle counters of CTA 0
 };
 
@@ -815,14 +840,14 @@ struct S1MmaArgs {
 };
 
 // Step-1 MMA issue loop (one thread): per unit the generated A operand (TMEM) against every image tile,
-// per stage KS = KCH / 16 k-steps x 3 bf16 products (compile-time unrolled: a runtime loop around
+// per stage KS = KCH / 16 k-steps x 3 fp16 products (compile-time unrolled: a runtime loop around
 // tcgen05.mma costs ~500 cycles per stage, scripts/micro_s3.cu).  tr: total, A-wait, acc-wait, stage-wait.
 // NK = NKCH at compile time (1, 2, 4; 0 = runtime): the k-chunk loop is then unrolled, which avoids the
 // per-iteration cost of a runtime loop around tcgen05.mma (see the Step-3 note in DESIGN.md)
 template <int KS, int NK>
 __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&tr)[4]) {
   S1Smem& S = *a.S;
-  const uint32_t idesc = idesc_bf16_f32(128, 128);
+  const uint32_t idesc = idesc_f16_f32(128, 128);
   uint32_t g_st = 0, g_acc = 0, g_u = 0;
   const long long tr0 = diag_clock();
   // generation rounds: R = 2 when the K' chunks split by radial halves (NKCH % 4 == 0): round r fills the
@@ -863,9 +888,9 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
             const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8);
             const uint32_t a_lo = a_hi + (uint32_t)a.nk;
             const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
-            mma_bf16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc);  // +256 B per k-step
-            mma_bf16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
-            mma_bf16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_f16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc);  // +256 B per k-step
+            mma_f16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_f16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
           }
           tc_commit(&S.st_empty[s]);
           // last tile: a round's chunks are free once its last stage has been read
@@ -993,6 +1018,7 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
       // DRAM read-modify-write (that made Step 1 2x slower whenever Hs > Hp)
       const bool valid = f < P.F && z < P.Hp;
       const int qt = valid ? ((p + __ldg(P.ell + z)) & (n - 1)) : 0;
+      const int ec = valid ? f16_scale_exp(P.gmax * __ldg(P.bst + P.j0 + jl).x) : 0;  // fp16x3 operand scale
       const float2* brow = P.B + ((size_t)(P.j0 + jl) * n + qt) * nk;
       const float* grow = P.g + (size_t)z * nk;
       for (int rnd = 0; rnd < R; ++rnd) {
@@ -1027,11 +1053,11 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
           uint32_t h1[8], l1[8], h2[8], l2[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float cr0 = gg[s2][e].x * bb[s2][e].x, ci0 = -gg[s2][e].x * bb[s2][e].y;
-            const float cr1 = gg[s2][e].y * bb[s2][e].z, ci1 = -gg[s2][e].y * bb[s2][e].w;
+            const float cr0 = ldexpf(gg[s2][e].x * bb[s2][e].x, ec), ci0 = ldexpf(-gg[s2][e].x * bb[s2][e].y, ec);
+            const float cr1 = ldexpf(gg[s2][e].y * bb[s2][e].z, ec), ci1 = ldexpf(-gg[s2][e].y * bb[s2][e].w, ec);
             // Re-row: [c_r | -c_i],  Im-row: [c_i | c_r]  (branch-free)
-            split2_bf16(part ? ci0 : cr0, part ? ci1 : cr1, h1[e], l1[e]);
-            split2_bf16(part ? cr0 : -ci0, part ? cr1 : -ci1, h2[e], l2[e]);
+            split2_f16(part ? ci0 : cr0, part ? ci1 : cr1, h1[e], l1[e]);
+            split2_f16(part ? cr0 : -ci0, part ? cr1 : -ci1, h2[e], l2[e]);
           }
           const uint32_t col = (uint32_t)((m0 + 16 * s2) / 2);
           tmem_st8(base + col, h1);
@@ -1061,6 +1087,7 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
       // this lane's two complex columns cc = lane, lane + 32 -> offsets (template jl, term z) in Zhat'
       long long coff[2];
       bool cval[2];
+      int cexp[2];  // fp16x3 scale exponent of the generated operand of this lane's columns
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int cc = lane + 32 * h;
@@ -1068,6 +1095,7 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
         const int jl = f / P.Hs, z = f - jl * P.Hs;
         cval[h] = 2 * cc < nvalid;  // pad slots included (zeros)
         coff[h] = (long long)jl * n * P.Hs + z;
+        cexp[h] = cval[h] ? f16_scale_exp(P.gmax * __ldg(P.bst + P.j0 + min(jl, P.nj - 1)).x) : 0;
       }
       for (int t = 0; t < nit; ++t, ++g_acc) {
         const int ab = g_acc & 1;
@@ -1090,10 +1118,13 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
           const int il = t * 128 + ii;  // local image index within the block
           if (il >= P.ni) continue;
           float2* dst = P.Zhat + ((size_t)il * P.nj * n + p) * P.Hs;
+          const int ea = f16_scale_exp(__ldg(P.ast + P.i0 + il).x);
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             if (cval[h]) {
-              const float2 v = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
+              float2 v = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
+              v.x = ldexpf(v.x, -(ea + cexp[h]));  // remove the fp16x3 operand scales (exact)
+              v.y = ldexpf(v.y, -(ea + cexp[h]));
               if constexpr ((kS1Hint & 1) != 0)
                 st_f2_hint(dst + coff[h], v, pol_st);
               else
@@ -1116,9 +1147,9 @@ static size_t s1_smem_bytes(const TcPlan& tc) {
   return 1024 + (size_t)S1_STAGES * 128 * tc.KCH * 4 + (size_t)128 * 128 * 4;
 }
 
-// Image operand prep: FB a[i][q][m] -> split bf16 canonical K-major tiles (B operand of Step 1).
+// Image operand prep: FB a[i][q][m] -> scaled fp16 hi/lo canonical K-major tiles (B operand of Step 1).
 __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restrict__ Aop, int NI, int NIT, int n,
-                                int nk, int KCH, int NKCH) {
+                                int nk, int KCH, int NKCH, const float2* __restrict__ ast) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int groups = (2 * nk) / 8;  // 8-element k' groups per row
   const int64_t total = (int64_t)NIT * 128 * n * groups;
@@ -1129,21 +1160,22 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
   const int p = (int)(rest / (NIT * 128));
   const int k0 = gk * 8;
   float v[8];
+  const int ea = i < NI ? f16_scale_exp(ast[i].x) : 0;  // fp16x3 operand scale of image i
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int kp = k0 + e;
     float x = 0.f;
     if (i < NI) {
       const float2 a = fb[((size_t)i * n + p) * nk + (kp < nk ? kp : kp - nk)];
-      x = kp < nk ? a.x : a.y;
+      x = ldexpf(kp < nk ? a.x : a.y, ea);
     }
     v[e] = x;
   }
   uint4 h, l;
-  split2_bf16(v[0], v[1], h.x, l.x);
-  split2_bf16(v[2], v[3], h.y, l.y);
-  split2_bf16(v[4], v[5], h.z, l.z);
-  split2_bf16(v[6], v[7], h.w, l.w);
+  split2_f16(v[0], v[1], h.x, l.x);
+  split2_f16(v[2], v[3], h.y, l.y);
+  split2_f16(v[4], v[5], h.z, l.z);
+  split2_f16(v[6], v[7], h.w, l.w);
   const int it = i / 128, ii = i % 128, kch = k0 / KCH, kk = k0 % KCH;
   const size_t stage_bytes = 128u * KCH * 4u;
   uint8_t* st = Aop + (((size_t)p * NIT + it) * NKCH + kch) * stage_bytes;
@@ -1155,7 +1187,7 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 // Step 2 for the tensor-core engine (Eq. fbk3 Step 2, Form B):
 //   Z_zeta(r) = e^{-2 pi i ell r / n} sum_p Zhat'_zeta(p) e^{-2 pi i p r / n},   (q = p + ell)
 // read from Zhat' [pair][p][Hs] (Form B, written by k_step1_tc); written as the Step-3 A operand rows
-// (real columns of reading R13), bf16 hi/lo packed in 32-bit words (two K columns per word), per (pair,
+// (real columns of reading R13), scaled fp16 hi/lo packed in 32-bit words (two K columns per word), per (pair,
 // r-tile, part) the canonical K-major core-matrix image [row/8][word group][8 rows x 16 B] that k_step3_tc
 // bulk-copies and tcgen05.cp-s into TMEM.
 // Work item = (pair, Step-2 block of <= 8 terms in one aligned 8-term window); persistent CTAs; the item's
@@ -1168,7 +1200,9 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 using S2Blocks = S2BlockTable;
 template <int E>
 __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* __restrict__ Zop,
-                                                      int npair, DevPlan P, S2Blocks B,
+                                                      int npair, DevPlan P, S2Blocks B, PairBlock pb,
+                                                      const float2* __restrict__ ast, const float2* __restrict__ bst,
+                                                      float Cz,
                                                       const float2* __restrict__ twtab,
                                                       const __grid_constant__ CUtensorMap zmap) {
   extern __shared__ __align__(1024) uint8_t s2raw[];
@@ -1314,6 +1348,9 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
       // the neighbouring ell = 0 term (a term without a neighbour writes the whole word, upper half 0)
       const int kl = col - 8 * g0;  // 0..15 within the block
       const int grp = kl >> 3, w = (kl & 7) >> 1;
+      int pi_, pj_;
+      pair_of(pb, pr, pi_, pj_);
+      const int ez = f16_scale_exp(Cz * __ldg(ast + pi_).y * __ldg(bst + pj_).y);  // fp16x3 scale of this pair's Z
       const bool lone = (B.lone[b] >> zz) & 1;
       uint32_t* shi = stg + (size_t)((grp * 2 + 0) * 4 + w) * RS;
       uint32_t* slo = stg + (size_t)((grp * 2 + 1) * 4 + w) * RS;
@@ -1321,22 +1358,22 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
 #pragma unroll
       for (int dd = 0; dd < E; ++dd) {
         const int pi = pbase + (E + 1) * dd;
-        const float2 a0 = x[rv(dd)];
+        const float2 a0 = make_float2(ldexpf(x[rv(dd)].x, ez), ldexpf(x[rv(dd)].y, ez));
         if (l > 0) {
           uint32_t hh, ll;
-          split2_bf16(a0.x, a0.y, hh, ll);
+          split2_f16(a0.x, a0.y, hh, ll);
           shi[pi] = hh;
           slo[pi] = ll;
         } else if (lone) {
           uint32_t hh, ll;
-          split2_bf16(a0.x, 0.f, hh, ll);
+          split2_f16(a0.x, 0.f, hh, ll);
           shi[pi] = hh;
           slo[pi] = ll;
         } else {
-          const __nv_bfloat16 hb = __float2bfloat16_rn(a0.x);
-          const __nv_bfloat16 lb = __float2bfloat16_rn(a0.x - __bfloat162float(hb));
-          reinterpret_cast<__nv_bfloat16*>(shi + pi)[kl & 1] = hb;
-          reinterpret_cast<__nv_bfloat16*>(slo + pi)[kl & 1] = lb;
+          const __half hb = __float2half_rn(a0.x);
+          const __half lb = __float2half_rn(a0.x - __half2float(hb));
+          reinterpret_cast<__half*>(shi + pi)[kl & 1] = hb;
+          reinterpret_cast<__half*>(slo + pi)[kl & 1] = lb;
         }
       }
     }
@@ -1399,8 +1436,8 @@ static int make_zmap(CUtensorMap* m, const float2* Zhat, int npair, const DevPla
   return r == CUDA_SUCCESS ? FTK_OK : FTK_ECUDA;
 }
 
-static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, const DevPlan& P,
-                            cudaStream_t s) {
+static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, const PairBlock& pb,
+                            const DevPlan& P, cudaStream_t s) {
   S2Blocks B;
   std::memcpy(&B, &tc.s2_blocks, sizeof B);
   alignas(64) CUtensorMap zmap;
@@ -1417,7 +1454,7 @@ static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
     occ = std::max(1, std::min(occ, 4));
     dim3 grid(items < occ * tc.num_sms ? items : occ * tc.num_sms);
-    kern<<<grid, 256, smem, s>>>(Zop, npair, P, B, tc.d_s2tw, zmap);
+    kern<<<grid, 256, smem, s>>>(Zop, npair, P, B, pb, tc.d_ast, tc.d_bst, tc.Cz, tc.d_s2tw, zmap);
   };
   switch (P.n_gamma) {
     case 64: run(k_step2_fft<2>); break;
@@ -1484,9 +1521,9 @@ __global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const fl
       const uint64_t bd = smem_desc_kmajor_noswz(smem_u32(sb) + ks * 256, 128, SBO);
       const uint64_t ad = smem_desc_kmajor_noswz(smem_u32(sa) + ks * 256, 128, SBO);
       const uint64_t bm = smem_desc_kmajor_noswz(smem_u32(sbm) + ks * 256, 128, SBO);
-      mma_bf16_ts(tm + 64, tm + ks * 8, bd, idesc, ks > 0);
-      mma_bf16_ss(tm + 128, ad, bd, idesc, ks > 0);
-      mma_bf16_ts(tm + 192, tm + ks * 8, bm, idesc_bf16_f32_bmn(128, 64), ks > 0);
+      mma_f16_ts(tm + 64, tm + ks * 8, bd, idesc, ks > 0);
+      mma_f16_ss(tm + 128, ad, bd, idesc, ks > 0);
+      mma_f16_ts(tm + 192, tm + ks * 8, bm, idesc_bf16_f32_bmn(128, 64), ks > 0);
     }
     tc_commit(&bar);
   }
@@ -1655,7 +1692,7 @@ int tc_term_order(const std::vector<int>& ell, const std::vector<int>& col, int 
   return FTK_OK;
 }
 
-int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, const std::vector<int>& ell,
+int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, const std::vector<int>& ell,
                  const std::vector<int>& col, const std::vector<float>& Y3, int K3p, int Ke, int n_gamma,
                  std::string& msg) {
   tc_plan_free(tc);
@@ -1744,6 +1781,15 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
   std::vector<uint8_t> colfast(tc.ncol / 8, 0);
   const size_t ygroup = (size_t)4 * ncol_g * K3p;
   std::vector<uint16_t> yimg(ygroup / 2 * tc.G, 0);
+  {  // fp16x3 scale constants (file header)
+    float ym = 0.f;
+    for (float y : Y3) ym = std::max(ym, std::fabs(y));
+    tc.eY = f16_scale_exp(ym);
+    float gm = 0.f;
+    for (float x : g) gm = std::max(gm, std::fabs(x));
+    tc.gmax = gm;
+    tc.Cz = gm;  // |Z| <= gmax |a| |b| (file header)
+  }
   for (int g = 0; g < tc.G; ++g) {
     tc.g_col0[g] = g * ncol_g;
     tc.g_yoff[g] = (long long)(g * ygroup);
@@ -1754,9 +1800,9 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>&, cons
       colpart[g * ncol_g + c] = partner[rr];
       const int t = rep[rr];
       for (int k = 0; k < K3p; ++k) {
-        const float x = Y3[(size_t)t * K3p + k];
-        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-        const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+        const float x = std::ldexp(Y3[(size_t)t * K3p + k], tc.eY);  // fp16x3: scaled, split in fp16
+        const __half hi = __float2half_rn(x);
+        const __half lo = __float2half_rn(x - __half2float(hi));
         const size_t off = (size_t)(c / 8) * (K3p / 8) * 64 + (size_t)(k / 8) * 64 + (c % 8) * 8 + (k % 8);
         std::memcpy(&yimg[g * ygroup / 2 + off], &hi, 2);
         std::memcpy(&yimg[g * ygroup / 2 + (size_t)ncol_g * K3p + off], &lo, 2);
@@ -1848,12 +1894,64 @@ void tc_plan_free(TcPlan& tc) {
   cudaFree(tc.d_colpart);
   cudaFree(tc.d_colfast);
   cudaFree(tc.d_Aop);
+  cudaFree(tc.d_ast);
+  cudaFree(tc.d_bst);
+  tc.d_ast = tc.d_bst = nullptr;
+  tc.ast_cap = tc.bst_cap = 0;
   tc.d_Ysm = nullptr;
   tc.d_colrep = tc.d_colpart = nullptr;
   tc.d_colfast = nullptr;
   tc.d_Aop = nullptr;
   tc.aop_bytes = 0;
   tc.ready = false;
+}
+
+// fp16x3 scaling: out[i] = (max over item i's FB coefficients of max(|Re|, |Im|), Frobenius norm of item i's
+// coefficients, rounded up by 2^-20 so that it bounds the exact norm), one CTA of 256 threads per item
+__global__ void k_item_stats(const float2* __restrict__ fb, int64_t per_item, float2* __restrict__ out) {
+  const float2* x = fb + (size_t)blockIdx.x * per_item;
+  float m = 0.f, q = 0.f;
+  for (int64_t k = threadIdx.x; k < per_item; k += blockDim.x) {
+    const float2 v = x[k];
+    m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    q = fmaf(v.x, v.x, fmaf(v.y, v.y, q));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    q += __shfl_xor_sync(0xffffffffu, q, o);
+  }
+  __shared__ float wm[8], wq[8];
+  if ((threadIdx.x & 31) == 0) {
+    wm[threadIdx.x >> 5] = m;
+    wq[threadIdx.x >> 5] = q;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    m = wm[0];
+    double qq = wq[0];
+    for (int w = 1; w < 8; ++w) {
+      m = fmaxf(m, wm[w]);
+      qq += wq[w];
+    }
+    out[blockIdx.x] = make_float2(m, (float)(sqrt(qq) * (1.0 + 0x1p-20)));
+  }
+}
+
+static int item_stats(const float2* fb, int64_t n, int64_t per_item, float2*& d_out, int64_t& cap, cudaStream_t s,
+                      std::string& msg) {
+  if (n > cap) {
+    cudaFree(d_out);
+    d_out = nullptr;
+    cap = 0;
+    if (cudaMalloc(&d_out, (size_t)n * sizeof(float2)) != cudaSuccess) {
+      cudaGetLastError();
+      msg = "tensor-core engine: scale table allocation failed";
+      return FTK_ENOMEM;
+    }
+    cap = n;
+  }
+  if (n > 0) k_item_stats<<<(unsigned)n, 256, 0, s>>>(fb, per_item, d_out);
+  return FTK_OK;
 }
 
 int tc_prepare_images(TcPlan& tc, const float2* fb, int64_t n_im, const DevPlan& P, cudaStream_t s, std::string& msg) {
@@ -1870,13 +1968,16 @@ int tc_prepare_images(TcPlan& tc, const float2* fb, int64_t n_im, const DevPlan&
     }
     tc.aop_bytes = bytes;
   }
+  if (item_stats(fb, n_im, (int64_t)P.n_k * P.n_psi, tc.d_ast, tc.ast_cap, s, msg) != FTK_OK) return FTK_ENOMEM;
   const int64_t total = (int64_t)tc.NIT * 128 * P.n_psi * (2 * P.n_k / 8);
   k_prep_image_op<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(fb, tc.d_Aop, (int)n_im, tc.NIT, P.n_psi, P.n_k,
-                                                                   tc.KCH, tc.NKCH);
+                                                                   tc.KCH, tc.NKCH, tc.d_ast);
   return cudaGetLastError() == cudaSuccess ? FTK_OK : FTK_ECUDA;
 }
-int tc_prepare_templates(TcPlan&, const float2*, int64_t, const DevPlan&, cudaStream_t, std::string&) {
-  return FTK_OK;
+int tc_prepare_templates(TcPlan& tc, const float2* fb, int64_t n_tm, const DevPlan& P, cudaStream_t s,
+                         std::string& msg) {
+  if (item_stats(fb, n_tm, (int64_t)P.n_k * P.n_psi, tc.d_bst, tc.bst_cap, s, msg) != FTK_OK) return FTK_ENOMEM;
+  return cudaGetLastError() == cudaSuccess ? FTK_OK : FTK_ECUDA;
 }
 
 size_t tc_bytes_per_pair(const TcPlan& tc, const DevPlan& P) {
@@ -1952,6 +2053,10 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
   prm.marg_part = tc.marg_part;
   prm.marg_np = tc.marg_np;
   prm.msc = tc.marg_scale;
+  prm.ast = tc.d_ast;
+  prm.bst = tc.d_bst;
+  prm.Cz = tc.Cz;
+  prm.eY = tc.eY;
   if (tc.marg)
     k_step3_tc<1><<<cpg * tc.G, S3_THREADS, tc.s3_smem, s>>>(prm);
   else
@@ -2010,6 +2115,9 @@ void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const Pair
   prm.NIT = tc.NIT;
   prm.F = pb.nj * P.Hs;  // (template, slot) columns, pad slots included
   prm.NCT = (prm.F + 63) / 64;
+  prm.ast = tc.d_ast;
+  prm.bst = tc.d_bst;
+  prm.gmax = tc.gmax;
   const int units = P.n_psi * prm.NCT;
   const int grid = units < tc.num_sms ? units : tc.num_sms;
   static unsigned long long* d_trace = nullptr;  // diagnostics: FTK_S1_TRACE=1 prints CTA 0's counters
@@ -2075,7 +2183,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
       return FTK_OK;
     }
     if (prof) prof(plan, 2, 0, s);
-    if (launch_step2_fft(tc, Zhat, Zop, pb.count, P, s) != FTK_OK) {
+    if (launch_step2_fft(tc, Zhat, Zop, pb.count, pb, P, s) != FTK_OK) {
       msg = "Step 2: tensor map encoding failed";
       return FTK_ECUDA;
     }
@@ -2158,10 +2266,6 @@ int tc_landscape_pairs(TcPlan& tc, const DevPlan& P, const float2* B, const int3
         }
         continue;
       }
-      if (launch_step2_fft(tc, zp, Zop, 1, P, s) != FTK_OK) {
-        msg = "Step 2: tensor map encoding failed";
-        return FTK_ECUDA;
-      }
       PairBlock pb3;
       pb3.i0 = i;
       pb3.ni = 1;
@@ -2169,6 +2273,10 @@ int tc_landscape_pairs(TcPlan& tc, const DevPlan& P, const float2* B, const int3
       pb3.nj = 1;
       pb3.li = pb3.lj = nullptr;
       pb3.count = 1;
+      if (launch_step2_fft(tc, zp, Zop, 1, pb3, P, s) != FTK_OK) {
+        msg = "Step 2: tensor map encoding failed";
+        return FTK_ECUDA;
+      }
       if (tc_s3v2_eligible(tc, P)) {
         if (launch_step3_cg2(tc, Zop, pb3, P, tm_off, nullptr, nullptr, n_tm_local, out + (size_t)k * land_pp, s) !=
             FTK_OK) {

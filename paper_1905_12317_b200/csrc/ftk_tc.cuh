@@ -1,4 +1,4 @@
-// Tensor-core (tcgen05, bf16x3 split) engine of the FTK hot path.
+// Tensor-core (tcgen05, fp16x3 split with power-of-two scaling) engine of the FTK hot path.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -35,12 +35,20 @@ struct TcPlan {
   uint8_t* d_Ysm = nullptr;   // per group: shared-memory image of Y3 hi/lo (B operand)
   size_t s3_smem = 0;
   // Step 1 operands
-  uint8_t* d_Aop = nullptr;    // images, bf16 hi/lo split, Step-1 K-major tiles [p][tile][kchunk][part]...
+  uint8_t* d_Aop = nullptr;    // images, fp16 hi/lo split (scaled), Step-1 K-major tiles [p][tile][kchunk][part]...
   size_t aop_bytes = 0;
   int NIT = 0, KCH = 64, NKCH = 0;
   S2BlockTable s2_blocks;     // Step-2 work blocks
   float2* d_s2tw = nullptr;  // Step-2 four-step twiddle tables
   int64_t n_tm = 0;
+  // fp16x3 power-of-two operand scaling (ftk_tc.cu header): per-item maxima of the loaded images / local templates
+  // (x = max |Re|, |Im| of the FB coefficients, y = their Frobenius norm), gmax = max |g_zeta(k_m)|, Cz = gmax (the
+  // Z bound's constant), eY = the exponent of the Step-3 Y3 operand
+  float2* d_ast = nullptr;  // images: (max |Re|, |Im|, ||a||_F) per item
+  float2* d_bst = nullptr;  // local templates, likewise
+  int64_t ast_cap = 0, bst_cap = 0;
+  float gmax = 0.f, Cz = 0.f;
+  int eY = 0;
   int num_sms = 148;
   bool sync_debug = false;
   // Step-3 epilogue of the next tc_run_block calls: marg == nullptr -> max / argmax (MODE 0); else the

@@ -189,7 +189,7 @@ __device__ __forceinline__ void tmem_dealloc_cg2(uint32_t taddr) {
 }
 // D[tmem] (+)= A[tmem] * B[smem]^T over the CTA pair: M = 256 (128 rows of A / D in each CTA's TMEM), B's N
 // columns split N/2 per CTA (same shared-memory offset).  Issued by one thread of the even CTA.
-__device__ __forceinline__ void mma_bf16_ts_cg2(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+__device__ __forceinline__ void mma_f16_ts_cg2(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                                 uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"

@@ -33,8 +33,8 @@ __global__ void __launch_bounds__(288, 1) k(int mma_iters, int ld_iters, unsigne
       const uint32_t idesc = idesc_bf16_f32(128 * CG, 80);
       const uint64_t bd = smem_desc_kmajor_noswz(smem_u32(sb), 128, 256);
       for (int i = 0; i < mma_iters; ++i) {
-        if (CG == 2) mma_bf16_ts_cg2(tm, tm + 400, bd, idesc, 1u);
-        else mma_bf16_ts(tm, tm + 400, bd, idesc, 1u);
+        if (CG == 2) mma_f16_ts_cg2(tm, tm + 400, bd, idesc, 1u);
+        else mma_f16_ts(tm, tm + 400, bd, idesc, 1u);
       }
       if (CG == 2) tc_commit_cg2(&bar); else tc_commit(&bar);
     }

@@ -140,11 +140,11 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, int N, int layoutA, i
           const uint64_t bd = make_desc(layoutB, smem_u32(sb), NB, KK, ks);
           const uint32_t acc = (it > 0 || ks > 0) ? 1u : 0u;
           if (ts) {
-            if (CG == 1) mma_bf16_ts(tm, tm + 256 + ks * 8, bd, idesc, acc);
+            if (CG == 1) mma_f16_ts(tm, tm + 256 + ks * 8, bd, idesc, acc);
             else mma_ts2(tm, tm + 256 + ks * 8, bd, idesc, acc);
           } else {
             const uint64_t ad = make_desc(layoutA, smem_u32(sa), 128, KK, ks);
-            if (CG == 1) mma_bf16_ss(tm, ad, bd, idesc, acc);
+            if (CG == 1) mma_f16_ss(tm, ad, bd, idesc, acc);
             else mma_ss2(tm, ad, bd, idesc, acc);
           }
         }
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(288, 1) k_cp(int iters, int ncp, int nmma, int
       for (int it = 0; it < iters; ++it) {
         for (int c = 0; c < ncp; ++c)
           tc_cp_128x256b(tm + 160 + (uint32_t)((c & 7) * 8), smem_desc_kmajor_noswz(smem_u32(sm) + (c & 7) * 4096, 128, 256));
-        for (int m = 0; m < nmma; ++m) mma_bf16_ts(tm, tm + 160 + (uint32_t)((m & 3) * 8), bd, idesc, 1u);
+        for (int m = 0; m < nmma; ++m) mma_f16_ts(tm, tm + 160 + (uint32_t)((m & 3) * 8), bd, idesc, 1u);
       }
       tc_commit(&bar);
     }

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(288, 1) k_s3(int chunks, int N, int K3p, int K
           const uint64_t bb = bd + ((v == 2) ? (uint64_t)(alt * 16) : 0ull);
           const uint32_t ac = (v == 3) ? alt : (c > 0 ? 1u : 0u);
           const uint32_t aa = a_hi0 + ((v == 4) ? alt * 8u : 0u);
-          mma_bf16_ts(dd, aa, bb, idesc, ac);
+          mma_f16_ts(dd, aa, bb, idesc, ac);
         }
         tc_commit(&bar[0]);
       }
@@ -132,9 +132,9 @@ __global__ void __launch_bounds__(288, 1) k_s3(int chunks, int N, int K3p, int K
             const uint32_t d = ks >= kev ? dO : dE;
             const uint32_t acc0 = (ks == 0 || ks == kev) ? 0u : 1u;
             const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + 48u;
-            mma_bf16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);
-            mma_bf16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
-            mma_bf16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_f16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc0);
+            mma_f16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma_f16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
           }
           tc_commit(&bar[db]);
         }
@@ -165,10 +165,10 @@ __global__ void __launch_bounds__(288, 1) k_s3(int chunks, int N, int K3p, int K
             if (dm == 3) { acc0 = 1u; }
             const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + (uint32_t)halfk;
             const uint64_t b_hi = bh0 + (uint64_t)(ks * 16), b_lo = bl0 + (uint64_t)(ks * 16);
-            mma_bf16_ts(d, a_hi, b_hi, idesc, acc0);
+            mma_f16_ts(d, a_hi, b_hi, idesc, acc0);
             if (prods > 1) {
-              mma_bf16_ts(d, a_hi, b_lo, idesc, 1u);
-              mma_bf16_ts(d, a_lo, b_hi, idesc, 1u);
+              mma_f16_ts(d, a_hi, b_lo, idesc, 1u);
+              mma_f16_ts(d, a_lo, b_hi, idesc, 1u);
             }
           }
           if (!(flags & 2) || c >= chunks - NB) tc_commit(&bar[db]);
@@ -199,10 +199,10 @@ __global__ void __launch_bounds__(288, 1) k_s3(int chunks, int N, int K3p, int K
         if (dm == 3) { acc0 = 1u; }
         const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8), a_lo = a_hi + (uint32_t)halfk;
         const uint64_t b_hi = bh0 + (uint64_t)(bfixed ? 0 : ks * 16), b_lo = bl0 + (uint64_t)(bfixed ? 0 : ks * 16);
-        mma_bf16_ts(d, a_hi, b_hi, idesc, acc0);
+        mma_f16_ts(d, a_hi, b_hi, idesc, acc0);
         if (prods > 1) {
-          mma_bf16_ts(d, a_hi, b_lo, idesc, 1u);
-          mma_bf16_ts(d, a_lo, b_hi, idesc, 1u);
+          mma_f16_ts(d, a_hi, b_lo, idesc, 1u);
+          mma_f16_ts(d, a_lo, b_hi, idesc, 1u);
         }
       }
       if (!(flags & 2) || c >= chunks - NB) tc_commit(&bar[db]);

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int N, int mode, unsigned
           bd = smem_desc_kmajor_noswz(base + st * stage + ks * 256, 128, (64 / 8) * 128);
         else            // 128B swizzle: row r at r * 128 (+ XOR), K16 step = +32 B
           bd = desc_sw128(base + st * stage + ks * 32);
-        mma_bf16_ts(tm, tm + 256, bd, idesc, c > 0 ? 1u : 0u);
+        mma_f16_ts(tm, tm + 256, bd, idesc, c > 0 ? 1u : 0u);
       }
       tc_commit(&bar);
     }

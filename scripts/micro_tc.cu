@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(544, 1) k_tmem(int iters, int mma_iters, int N
     if (lane == 0 && mma_iters > 0) {
       const uint32_t idesc = idesc_bf16_f32(128, N);
       const uint64_t bd = smem_desc_kmajor_noswz(smem_u32(sb), 128, 256);
-      for (int i = 0; i < mma_iters; ++i) mma_bf16_ts(tm + 0, tm + 384, bd, idesc, i > 0 ? 1u : 0u);
+      for (int i = 0; i < mma_iters; ++i) mma_f16_ts(tm + 0, tm + 384, bd, idesc, i > 0 ? 1u : 0u);
       tc_commit(&bar);
       mbar_wait(&bar, 0);
       cyc[blockIdx.x * 2 + 1] = clock64() - t0;

@@ -5,7 +5,9 @@ formats, against the float64 oracle FTK (oracle.ftk.ftk_landscapes) on config-sh
   fp32     operands and accumulation in float32
   tf32x1   operands rounded to TF32 (10-bit mantissa), one product
   tf32x3   x = hi + lo in TF32, hi*hi + hi*lo + lo*hi
-  bf16x3   x = hi + lo in bf16 (8-bit mantissa), hi*hi + hi*lo + lo*hi   (the library's engine 0)
+  fp16x3   x scaled by a power of two into (2^13, 2^14] (the operand's bound), x = hi + lo in fp16
+           (11-bit significand, subnormals below 2^-14), hi*hi + hi*lo + lo*hi   (the library's engine 0, round 2)
+  bf16x3   x = hi + lo in bf16 (8-bit mantissa), hi*hi + hi*lo + lo*hi   (engine 0 in round 1)
   bf16x1   operands rounded to bf16, one product
 
 Products are exact (float64) and summed in float32 per contraction, as the tensor core accumulates in fp32.
@@ -37,8 +39,23 @@ def round_mant(x, bits):
     return np.ldexp(np.round(m * scale) / scale, e)
 
 
-def split(x, fmt):
-    """Operand terms of a format: list of (component) arrays whose products are formed pairwise."""
+def f16_scale_exp(bound):
+    """The exponent e with bound 2^e in (2^13, 2^14] (0 for a zero bound), as the kernels compute it."""
+    if not bound > 0:
+        return 0
+    m, e = math.frexp(bound)
+    return 14 - (e - 1 if m == 0.5 else e)
+
+
+def split(x, fmt, bound=None):
+    """Operand terms of a format: list of (component) arrays whose products are formed pairwise.  fp16x3 takes
+    the operand's bound (scale) and returns the terms unscaled (power-of-two scaling is exact)."""
+    if fmt == "fp16x3":
+        e = f16_scale_exp(float(np.max(np.abs(x))) if bound is None else bound)
+        xs = np.ldexp(np.asarray(x, np.float32).astype(np.float64), e)
+        hi = xs.astype(np.float16).astype(np.float64)
+        lo = (xs - hi).astype(np.float32).astype(np.float16).astype(np.float64)
+        return [np.ldexp(hi, -e), np.ldexp(lo, -e)]
     if fmt == "fp32":
         return [np.asarray(x, np.float32).astype(np.float64)]
     bits = {"tf32x1": 10, "tf32x3": 10, "bf16x3": 7, "bf16x1": 7}[fmt]
@@ -53,16 +70,16 @@ def _pairs(n):
     return [(0, 0)] if n == 1 else [(0, 0), (0, 1), (1, 0)]
 
 
-def dot_rows(A, B, fmt):
+def dot_rows(A, B, fmt, ba=None, bb=None):
     """out[p] = sum_k A[p, k] B[p, k] with the format's products; float32 result (fp32 accumulation)."""
-    As, Bs = split(A, fmt), split(B, fmt)
+    As, Bs = split(A, fmt, ba), split(B, fmt, bb)
     acc = sum((As[i] * Bs[j]).sum(-1) for i, j in _pairs(len(As)))
     return acc.astype(np.float32).astype(np.float64)
 
 
-def matmul(A, B, fmt):
+def matmul(A, B, fmt, ba=None, bb=None):
     """A @ B with the format's products; float32 result."""
-    As, Bs = split(A, fmt), split(B, fmt)
+    As, Bs = split(A, fmt, ba), split(B, fmt, bb)
     acc = sum(As[i] @ Bs[j] for i, j in _pairs(len(As)))
     return acc.astype(np.float32).astype(np.float64)
 
@@ -73,14 +90,21 @@ def chain(a, b, plan, fmt):
     zp = [z for z, t in enumerate(plan.terms) if t.ell >= 0]          # ell >= 0 terms (reading R13)
     ells = np.array([plan.terms[z].ell for z in zp])
     g = (2.0 * math.pi * plan.w[None, :] * plan.G[zp]).astype(np.float32).astype(np.float64)  # [Hp, n_k]
+    # fp16x3 bounds, as the kernels form them (ftk_tc.cu header): image max, template max x max |g|, and the
+    # a-priori bound of Z: |Z_zeta(r)| <= sum_{m,p} |a(m,p)| |g_zeta(m)| |b(m,p+ell)| <= gmax ||a||_F ||b||_F
+    amax = float(max(np.abs(a.real).max(), np.abs(a.imag).max()))
+    bmax = float(max(np.abs(b.real).max(), np.abs(b.imag).max()))
+    gabs = np.abs(g)
+    cbound = float(gabs.max()) * bmax
+    zbound = float(gabs.max()) * float(np.linalg.norm(a)) * float(np.linalg.norm(b))  # Cauchy-Schwarz over (m, p)
     # Step 1, Form B: Zhat'_z(p) = sum_m a(m, p) g_z(m) conj b(m, p + ell_z)   (real GEMM over [re | im])
     Zh = np.empty((len(zp), n), dtype=np.complex128)
     for zi, l in enumerate(ells):
         c = (g[zi][:, None] * np.conj(np.roll(b, -l, axis=1))).astype(np.complex64).astype(np.complex128)  # [m, p]
         ar, ai, cr, ci = a.real.T, a.imag.T, c.real.T, c.imag.T   # [p, m]
         arow = np.concatenate([ar, ai], 1)                        # image operand rows [p, 2 n_k]
-        re = dot_rows(arow, np.concatenate([cr, -ci], 1), fmt)   # Re-row of the generated operand
-        im = dot_rows(arow, np.concatenate([ci, cr], 1), fmt)    # Im-row
+        re = dot_rows(arow, np.concatenate([cr, -ci], 1), fmt, amax, cbound)   # Re-row of the generated operand
+        im = dot_rows(arow, np.concatenate([ci, cr], 1), fmt, amax, cbound)    # Im-row
         Zh[zi] = re + 1j * im
     # Step 2 in fp32: Z_z(r) = e^{-2 pi i ell r / n} FFT(Zhat'_z)(r)
     Z = np.fft.fft(Zh.astype(np.complex64), axis=1).astype(np.complex64).astype(np.complex128)
@@ -98,7 +122,7 @@ def chain(a, b, plan, fmt):
             cols_Z += [Z[zi].real, Z[zi].imag]
     Y3 = np.stack(cols_Y, 1).astype(np.float32).astype(np.float64)      # [N_t, K3]
     Z3 = np.stack(cols_Z, 0)                                            # [K3, n]
-    return matmul(Y3, Z3, fmt)
+    return matmul(Y3, Z3, fmt, None, zbound)
 
 
 def main():
@@ -107,7 +131,7 @@ def main():
     ap.add_argument("--configs", default="tiny,c2,c3,c5")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
-    fmts = ["fp32", "tf32x3", "bf16x3", "tf32x1", "bf16x1"]
+    fmts = ["fp32", "tf32x3", "fp16x3", "bf16x3", "tf32x1", "bf16x1"]
     lines = ["| config | pairs | " + " | ".join(fmts) + " |", "|---|---|" + "---|" * len(fmts)]
     for name in args.configs.split(","):
         cfg = synth.config(name)

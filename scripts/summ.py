@@ -1,3 +1,5 @@
+"""Summarise bench.py JSON lines: value, ms/step, per-kernel ms, roofline fraction, clock reasons.
+Usage: python scripts/summ.py gpurun_out/*.json (used by full_bench.sh / gpu_round.sh / ctf_bench.sh)."""
 import json, sys
 for f in sys.argv[1:]:
     try:

@@ -5,7 +5,9 @@ Eq. fbk3, P:1324 consistency check).
 Which kernels each test runs (engine 0):
   * test_landscape_pairs_32       k_step1_tc over each pair's 128-image tile, k_step2_fft (Form B),
                                   k_step3_tc with landscape output (exact epilogue) -- 32 random pairs per
-                                  config, element-wise |dX| <= 1e-4 ||A|| ||B||.
+                                  config, element-wise |dX| <= 1e-4 ||A|| ||B|| (north star) and the
+                                  engine's own precision claim |dX| <= 2.5e-6 ||A|| ||B|| (DESIGN.md
+                                  section 6, fp16x3: emulated worst case 3.9e-7 at tiny).
   * test_pair_best_every_pair     ftk_align as bench.py runs it (k_step1_tc, k_step2_fft, k_step3_tc with the
                                   fast E + |O| epilogue and the resolver): value AND (shift, rot) of every
                                   pair of a >= 2-image-tile subset vs the oracle (argmax: gap rule).
@@ -32,6 +34,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-4
+PREC = 2.5e-6  # fp16x3 precision bar, 40x inside the north-star tolerance
 _OPLANS = {}
 _STATS = {}
 
@@ -99,7 +102,7 @@ def test_landscape_pairs_32(pkg, name):
     ni, nj = min(cfg.N_im, 300), min(cfg.N_tm, 300)
     p, w, imgs, tpls = load_gpu(pkg, cfg, ni, nj)
     rng = np.random.default_rng(7)
-    n = 32 if name != "tiny" else 16
+    n = 32
     ii = rng.integers(0, ni, n)
     jj = rng.integers(0, nj, n)
     Lp = p.landscape_pairs(ii, jj).cpu().numpy()
@@ -113,6 +116,7 @@ def test_landscape_pairs_32(pkg, name):
         worst = max(worst, np.max(np.abs(Lp[s] - X)) / (na[s] * nb[s]))
     note(f"landscape_pairs_{name}", worst)
     assert worst <= TOL, worst
+    assert worst <= PREC, worst
 
 
 @pytest.mark.parametrize("name,ni,nj", [("c5", 130, 40), ("c4", 130, 8), ("c3", 160, 24)])
