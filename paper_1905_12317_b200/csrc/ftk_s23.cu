@@ -143,9 +143,9 @@ struct S23Params {
   float2* marg_part;  // MODE 1: [2 G][N_im][n_tm_local] base-2 (max, sum) partials
   long long marg_np;
   float msc;          // MODE 1: log2(e) / tau
-  const float2* ast;  // fp16x3 scaling (ftk_tc.cu header): image / local template maxima, Z bound constant,
+  const float2* ast;  // fp16x3 scaling (ftk_tc.cu header): image / local template maxima, 
   const float2* bst;  // Y3 exponent
-  float Cz;
+  float gmax;
   int eY;
   unsigned long long* trace;  // diagnostics (kDiag23): [cta of cluster 0][16] cycle counters
   const void* zdbg;           // diagnostics: base of the block's Zhat' (FTK_S23_DBG bit 2)
@@ -416,8 +416,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
           mbar_arrive(&S.red_empty[rb]);
           if (f != 0xffffffffu) {
             // f: global flat index (template, shift, rot); v is in pair p's fp16x3 units (exact rescale)
-            const int pe = f16_scale_exp(P.Cz * __ldg(P.ast + i).y * __ldg(P.bst + j).y) + P.eY;
-            const unsigned long long key = pack_key(ldexpf(v, -pe), f);
+            const int pe = z_exp(P.ast, P.bst, P.gmax, i, j) + P.eY;
+            const unsigned long long key = pack_key(v * pow2f_wide(-pe), f);
             if (P.img_keys) atomicMax(&P.img_keys[i], key);
             if (P.pair_keys) atomicMax(&P.pair_keys[(size_t)i * P.n_tm_local + j], key);
           }
@@ -519,12 +519,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
       pair_of(P.pb, p, pi_img, pj_tm);
       // fp16x3: this pair's results are X 2^pe; a MODE-0 record carried over from the previous pair of the same
       // image is rescaled (exactly) into this pair's units
-      const int pe = f16_scale_exp(P.Cz * __ldg(P.ast + pi_img).y * __ldg(P.bst + pj_tm).y) + P.eY;
+      const int pe = z_exp(P.ast, P.bst, P.gmax, pi_img, pj_tm) + P.eY;
       if (s == 0) {
-        if (MODE == 0 && bv != -INFINITY) bv = ldexpf(bv, pe - pe_prev);
+        if (MODE == 0 && bv != -INFINITY) bv *= pow2f_wide(pe - pe_prev);
         pe_prev = pe;
       }
-      const float msc_p = ldexpf(P.msc, -pe);
+      const float unsc = pow2f_wide(-pe);
+      const float msc_p = P.msc * unsc;
       // flat indices are global ((template, shift) major, rotation minor): the running best of MODE 0 is
       // carried over the consecutive templates of one image unless per-pair maxima are requested
       const uint32_t fbase = (uint32_t)(P.tm_off + pj_tm) * (uint32_t)P.N_t;
@@ -616,7 +617,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
                     bv = xp;
                     bf = fp;
                   }
-                  if (land_p && row < F) land_p[(size_t)tp * n + r] = ldexpf(xp, -pe);
+                  if (land_p && row < F) land_p[(size_t)tp * n + r] = xp * unsc;
                   if (tm >= 0) {
                     const float xm = ev - ov;
                     const uint32_t fm = (fbase + (uint32_t)tm) * (uint32_t)n + r;
@@ -624,7 +625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
                       bv = xm;
                       bf = fm;
                     }
-                    if (land_p && row < F) land_p[(size_t)tm * n + r] = ldexpf(xm, -pe);
+                    if (land_p && row < F) land_p[(size_t)tm * n + r] = xm * unsc;
                   }
                 }
               }
@@ -768,11 +769,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
     for (int u = 0; u < U; ++u) {
       const int s = u % NT;
       const int crot = 2 * s + (int)h;
-      int ez;  // fp16x3 scale exponent of this pair's Z
+      float zsc;  // fp16x3: this pair's Zhat' scale -> its Z scale
       {
         int pi_, pj_;
         pair_of(P.pb, p_begin + u / NT, pi_, pj_);
-        ez = f16_scale_exp(P.Cz * __ldg(P.ast + pi_).y * __ldg(P.bst + pj_).y);
+        zsc = zhat_to_z_scale(P.ast, P.bst, P.gmax, pi_, pj_);  // Zhat' arrives in Step 1's scale
       }
       // per unit: w_n^{q1 c} for this lane's q1 = a + 16 b, and the radix-D combination constants
       float2 tu[V];
@@ -869,7 +870,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
           for (int m = 0; m < V; ++m) {
             const int i = k1g + V * m + V * V * m2;
             const int pi = i + V * m2;
-            const float2 a0v = make_float2(ldexpf(x[rv(m)].x, ez), ldexpf(x[rv(m)].y, ez));
+            const float2 a0v = make_float2(x[rv(m)].x * zsc, x[rv(m)].y * zsc);
             if (l > 0) {
               uint32_t hh2, ll2;
               split2_f16(a0v.x, a0v.y, hh2, ll2);
@@ -1103,7 +1104,7 @@ static int launch_cg2(const TcPlan& tc, bool zs, const float2* Zhat, const uint8
   prm.msc = tc.marg_scale;
   prm.ast = tc.d_ast;
   prm.bst = tc.d_bst;
-  prm.Cz = tc.Cz;
+  prm.gmax = tc.gmax;
   prm.eY = tc.eY;
   if (kDiag23) {
     const char* e = std::getenv("FTK_S23_DBG");

@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+
+#include <cstring>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -217,13 +219,29 @@ __device__ __forceinline__ void split2_f16(float x0, float x1, uint32_t& hi, uin
   hi = *reinterpret_cast<uint32_t*>(&h);
   lo = *reinterpret_cast<uint32_t*>(&l);
 }
-// 14 - ceil(log2 x) for x > 0 (0 otherwise): the exponent e with x 2^e in (2^13, 2^14]
-__host__ __device__ inline int f16_scale_exp(float x) {
-  if (!(x > 0.f) || !(x < 3.0e38f)) return 0;
-  int e;
-  const float f = frexpf(x, &e);  // x = f 2^e, f in [0.5, 1)
-  const int c = (f == 0.5f) ? e - 1 : e;
-  return 14 - c;
+// fp16x3 operand scaling.  f16_scale_exp(x) = 14 - ceil(log2 x): the exponent e with x 2^e in (2^13, 2^14],
+// for normal positive finite x (0 for zero, subnormal, negative, inf, NaN), clamped to [-126, 127] so that
+// pow2f(e) is a normal float.  Integer bit arithmetic only (cheap on the device, identical on the host).
+__host__ __device__ __forceinline__ int f16_scale_exp(float x) {
+  uint32_t b;
+  memcpy(&b, &x, 4);
+  const int eb = (int)((b >> 23) & 255u);
+  if ((b >> 31) || eb == 0 || eb == 255) return 0;
+  const int e = ((b & 0x7fffffu) ? 13 : 14) - (eb - 127);
+  return e < -126 ? -126 : (e > 127 ? 127 : e);
+}
+// 2^e as a float for e in [-126, 127] (exact; multiplying by it scales exactly unless the result leaves the
+// normal range)
+__host__ __device__ __forceinline__ float pow2f(int e) {
+  const uint32_t b = (uint32_t)(127 + e) << 23;
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
+}
+// 2^e for e in [-252, 254] as the product of two normal factors (per-pair unscale factors)
+__host__ __device__ __forceinline__ float pow2f_wide(int e) {
+  const int h = e / 2;
+  return pow2f(h) * pow2f(e - h);
 }
 
 __device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }

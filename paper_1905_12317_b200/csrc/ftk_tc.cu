@@ -8,7 +8,8 @@
 // fp16x3 scaling (all exponents from f16_scale_exp, x 2^e in (2^13, 2^14]):
 //   Step-1 image operand  a_i      x 2^{e(amax_i)}            amax_i = max |Re|, |Im| of image i's FB coefficients
 //   Step-1 generated operand c_j   x 2^{e(gmax bmax_j)}       gmax = max |g_zeta(k_m)|, bmax_j likewise for template j
-//   Step-1 output Zhat'            unscaled (x 2^{-(e_a + e_c)}) in the epilogue: Zhat' is plain fp32
+//   Step-1 output Zhat'            left scaled: pair (i, j)'s block is Zhat' 2^{e_a(i) + e_c(j)} (one factor per
+//                                  pair), which Step 2 folds into its own Z scale (no epilogue work)
 //   Step-3 operand Z (pair i, j)   x 2^{e(gmax |a_i| |b_j|)}  |.| = Frobenius norm over (m, p); bounds |Z| by
 //                                  |Z_zeta(r)| <= sum_{m,p} |a(m,p)| |g_zeta(m)| |b(m,p+ell)| <= gmax |a| |b|
 //                                  (Cauchy-Schwarz; the shift p -> p + ell permutes the modes)
@@ -99,7 +100,7 @@ struct S3Params {
   float msc;       // MODE 1: log2(e) / tau
   const float2* ast;  // fp16x3 scaling (see the file header): per image / local template maxima
   const float2* bst;
-  float Cz;
+  float gmax;
   int eY;
   int dbg;         // FTK_S3_DBG (diagnostics): bit 0 skips the epilogue arithmetic, bit 1 the TMEM drain (timing only)
   unsigned long long* trace;  // nullable (FTK_S3_TRACE=1): wait / busy cycle counters of CTA 0
@@ -346,13 +347,13 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
       uint32_t bfe = 0xffffffffu;
       float mrun = -INFINITY, srun = 0.f;  // MODE 1: running base-2 log-sum-exp of X log2(e) / tau
       float* land_p = P.land ? P.land + (size_t)p * P.N_t * n : nullptr;
-      int pe;  // this pair's result scale exponent (values are X 2^pe)
+      float unsc;  // this pair's fp16x3 unscale factor (values are X 2^pe, unsc = 2^-pe)
       {
         int pi_, pj_;
         pair_of(P.pb, p, pi_, pj_);
-        pe = f16_scale_exp(P.Cz * __ldg(P.ast + pi_).y * __ldg(P.bst + pj_).y) + P.eY;
+        unsc = pow2f_wide(-(z_exp(P.ast, P.bst, P.gmax, pi_, pj_) + P.eY));
       }
-      const float msc_p = ldexpf(P.msc, -pe);  // MODE 1: log2(e) / tau in scaled units
+      const float msc_p = P.msc * unsc;  // MODE 1: log2(e) / tau in scaled units
       for (int T = 0; T < NRT; ++T) {
         const int r = T * 128 + row;
         const bool active = T * 128 + q * 32 < n;  // warp-uniform: lane quarters beyond n_psi idle
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
                   bve = xp;
                   bfe = fp;
                 }
-                if (land_p) land_p[(size_t)tp * n + r] = ldexpf(xp, -pe);
+                if (land_p) land_p[(size_t)tp * n + r] = xp * unsc;
                 if (tm >= 0) {
                   const float xm = ev - ov;
                   const uint32_t fm = (uint32_t)tm * (uint32_t)n + (uint32_t)r;
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
                     bve = xm;
                     bfe = fm;
                   }
-                  if (land_p) land_p[(size_t)tm * n + r] = ldexpf(xm, -pe);
+                  if (land_p) land_p[(size_t)tm * n + r] = xm * unsc;
                 }
               }
             }
@@ -764,8 +765,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         pair_of(P.pb, p, i, j);
         const uint32_t tt2 = bf / (uint32_t)n, rr = bf - tt2 * (uint32_t)n;
         const uint32_t gflat = ((uint32_t)(P.tm_off + j) * (uint32_t)P.N_t + tt2) * (uint32_t)n + rr;
-        const int pe = f16_scale_exp(P.Cz * __ldg(P.ast + i).y * __ldg(P.bst + j).y) + P.eY;
-        const unsigned long long kk = pack_key(ldexpf(bv, -pe), gflat);  // fp16x3 scale removed (exact)
+        const int pe = z_exp(P.ast, P.bst, P.gmax, i, j) + P.eY;
+        const unsigned long long kk = pack_key(bv * pow2f_wide(-pe), gflat);  // fp16x3 scale removed (exact)
         if (P.img_keys) atomicMax(&P.img_keys[i], kk);
         if (P.pair_keys) atomicMax(&P.pair_keys[(size_t)i * P.n_tm_local + j], kk);
       }
@@ -1018,7 +1019,8 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
       // DRAM read-modify-write (that made Step 1 2x slower whenever Hs > Hp)
       const bool valid = f < P.F && z < P.Hp;
       const int qt = valid ? ((p + __ldg(P.ell + z)) & (n - 1)) : 0;
-      const int ec = valid ? f16_scale_exp(P.gmax * __ldg(P.bst + P.j0 + jl).x) : 0;  // fp16x3 operand scale
+      // fp16x3 operand scale of this row's template (folded into g: (g 2^e) b = (g b) 2^e exactly)
+      const float gsc = pow2f(valid ? s1_gen_exp(P.bst, P.gmax, P.j0 + jl) : 0);
       const float2* brow = P.B + ((size_t)(P.j0 + jl) * n + qt) * nk;
       const float* grow = P.g + (size_t)z * nk;
       for (int rnd = 0; rnd < R; ++rnd) {
@@ -1046,6 +1048,8 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
             else
               bb[s2][e] = ok ? __ldg(reinterpret_cast<const float4*>(brow + m)) : make_float4(0.f, 0.f, 0.f, 0.f);
             gg[s2][e] = ok ? __ldg(reinterpret_cast<const float2*>(grow + m)) : make_float2(0.f, 0.f);
+            gg[s2][e].x *= gsc;
+            gg[s2][e].y *= gsc;
           }
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
@@ -1053,8 +1057,8 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
           uint32_t h1[8], l1[8], h2[8], l2[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float cr0 = ldexpf(gg[s2][e].x * bb[s2][e].x, ec), ci0 = ldexpf(-gg[s2][e].x * bb[s2][e].y, ec);
-            const float cr1 = ldexpf(gg[s2][e].y * bb[s2][e].z, ec), ci1 = ldexpf(-gg[s2][e].y * bb[s2][e].w, ec);
+            const float cr0 = gg[s2][e].x * bb[s2][e].x, ci0 = -gg[s2][e].x * bb[s2][e].y;
+            const float cr1 = gg[s2][e].y * bb[s2][e].z, ci1 = -gg[s2][e].y * bb[s2][e].w;
             // Re-row: [c_r | -c_i],  Im-row: [c_i | c_r]  (branch-free)
             split2_f16(part ? ci0 : cr0, part ? ci1 : cr1, h1[e], l1[e]);
             split2_f16(part ? cr0 : -ci0, part ? cr1 : -ci1, h2[e], l2[e]);
@@ -1087,7 +1091,6 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
       // this lane's two complex columns cc = lane, lane + 32 -> offsets (template jl, term z) in Zhat'
       long long coff[2];
       bool cval[2];
-      int cexp[2];  // fp16x3 scale exponent of the generated operand of this lane's columns
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int cc = lane + 32 * h;
@@ -1095,7 +1098,6 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
         const int jl = f / P.Hs, z = f - jl * P.Hs;
         cval[h] = 2 * cc < nvalid;  // pad slots included (zeros)
         coff[h] = (long long)jl * n * P.Hs + z;
-        cexp[h] = cval[h] ? f16_scale_exp(P.gmax * __ldg(P.bst + P.j0 + min(jl, P.nj - 1)).x) : 0;
       }
       for (int t = 0; t < nit; ++t, ++g_acc) {
         const int ab = g_acc & 1;
@@ -1118,13 +1120,10 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
           const int il = t * 128 + ii;  // local image index within the block
           if (il >= P.ni) continue;
           float2* dst = P.Zhat + ((size_t)il * P.nj * n + p) * P.Hs;
-          const int ea = f16_scale_exp(__ldg(P.ast + P.i0 + il).x);
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             if (cval[h]) {
-              float2 v = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
-              v.x = ldexpf(v.x, -(ea + cexp[h]));  // remove the fp16x3 operand scales (exact)
-              v.y = ldexpf(v.y, -(ea + cexp[h]));
+              const float2 v = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
               if constexpr ((kS1Hint & 1) != 0)
                 st_f2_hint(dst + coff[h], v, pol_st);
               else
@@ -1160,14 +1159,14 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
   const int p = (int)(rest / (NIT * 128));
   const int k0 = gk * 8;
   float v[8];
-  const int ea = i < NI ? f16_scale_exp(ast[i].x) : 0;  // fp16x3 operand scale of image i
+  const float asc = pow2f(i < NI ? s1_img_exp(ast, i) : 0);  // fp16x3 operand scale of image i
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int kp = k0 + e;
     float x = 0.f;
     if (i < NI) {
       const float2 a = fb[((size_t)i * n + p) * nk + (kp < nk ? kp : kp - nk)];
-      x = ldexpf(kp < nk ? a.x : a.y, ea);
+      x = (kp < nk ? a.x : a.y) * asc;
     }
     v[e] = x;
   }
@@ -1202,7 +1201,7 @@ template <int E>
 __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* __restrict__ Zop,
                                                       int npair, DevPlan P, S2Blocks B, PairBlock pb,
                                                       const float2* __restrict__ ast, const float2* __restrict__ bst,
-                                                      float Cz,
+                                                      float gmax,
                                                       const float2* __restrict__ twtab,
                                                       const __grid_constant__ CUtensorMap zmap) {
   extern __shared__ __align__(1024) uint8_t s2raw[];
@@ -1350,7 +1349,7 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
       const int grp = kl >> 3, w = (kl & 7) >> 1;
       int pi_, pj_;
       pair_of(pb, pr, pi_, pj_);
-      const int ez = f16_scale_exp(Cz * __ldg(ast + pi_).y * __ldg(bst + pj_).y);  // fp16x3 scale of this pair's Z
+      const float zsc = zhat_to_z_scale(ast, bst, gmax, pi_, pj_);  // fp16x3: Zhat' scale -> Z scale
       const bool lone = (B.lone[b] >> zz) & 1;
       uint32_t* shi = stg + (size_t)((grp * 2 + 0) * 4 + w) * RS;
       uint32_t* slo = stg + (size_t)((grp * 2 + 1) * 4 + w) * RS;
@@ -1358,7 +1357,7 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
 #pragma unroll
       for (int dd = 0; dd < E; ++dd) {
         const int pi = pbase + (E + 1) * dd;
-        const float2 a0 = make_float2(ldexpf(x[rv(dd)].x, ez), ldexpf(x[rv(dd)].y, ez));
+        const float2 a0 = make_float2(x[rv(dd)].x * zsc, x[rv(dd)].y * zsc);
         if (l > 0) {
           uint32_t hh, ll;
           split2_f16(a0.x, a0.y, hh, ll);
@@ -1454,7 +1453,7 @@ static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
     occ = std::max(1, std::min(occ, 4));
     dim3 grid(items < occ * tc.num_sms ? items : occ * tc.num_sms);
-    kern<<<grid, 256, smem, s>>>(Zop, npair, P, B, pb, tc.d_ast, tc.d_bst, tc.Cz, tc.d_s2tw, zmap);
+    kern<<<grid, 256, smem, s>>>(Zop, npair, P, B, pb, tc.d_ast, tc.d_bst, tc.gmax, tc.d_s2tw, zmap);
   };
   switch (P.n_gamma) {
     case 64: run(k_step2_fft<2>); break;
@@ -1788,7 +1787,6 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, co
     float gm = 0.f;
     for (float x : g) gm = std::max(gm, std::fabs(x));
     tc.gmax = gm;
-    tc.Cz = gm;  // |Z| <= gmax |a| |b| (file header)
   }
   for (int g = 0; g < tc.G; ++g) {
     tc.g_col0[g] = g * ncol_g;
@@ -2055,7 +2053,7 @@ void launch_step3_tc(const TcPlan& tc, const uint8_t* Zop, const PairBlock& pb, 
   prm.msc = tc.marg_scale;
   prm.ast = tc.d_ast;
   prm.bst = tc.d_bst;
-  prm.Cz = tc.Cz;
+  prm.gmax = tc.gmax;
   prm.eY = tc.eY;
   if (tc.marg)
     k_step3_tc<1><<<cpg * tc.G, S3_THREADS, tc.s3_smem, s>>>(prm);

@@ -42,12 +42,12 @@ struct TcPlan {
   float2* d_s2tw = nullptr;  // Step-2 four-step twiddle tables
   int64_t n_tm = 0;
   // fp16x3 power-of-two operand scaling (ftk_tc.cu header): per-item maxima of the loaded images / local templates
-  // (x = max |Re|, |Im| of the FB coefficients, y = their Frobenius norm), gmax = max |g_zeta(k_m)|, Cz = gmax (the
-  // Z bound's constant), eY = the exponent of the Step-3 Y3 operand
+  // (x = max |Re|, |Im| of the FB coefficients, y = their Frobenius norm), gmax = max |g_zeta(k_m)|, eY = the
+  // exponent of the Step-3 Y3 operand
   float2* d_ast = nullptr;  // images: (max |Re|, |Im|, ||a||_F) per item
   float2* d_bst = nullptr;  // local templates, likewise
   int64_t ast_cap = 0, bst_cap = 0;
-  float gmax = 0.f, Cz = 0.f;
+  float gmax = 0.f;
   int eY = 0;
   int num_sms = 148;
   bool sync_debug = false;

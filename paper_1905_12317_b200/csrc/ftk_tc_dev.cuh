@@ -13,6 +13,23 @@
 namespace ftk {
 using namespace sm100;
 
+// fp16x3 operand scales of the tensor-core engine (ftk_tc.cu header).  ast / bst: per image / local template
+// (x = max |Re|, |Im| of the FB coefficients, y = Frobenius norm); gmax = max |g_zeta(k_m)|.
+// Step-1 image operand exponent and generated-operand exponent:
+__device__ __forceinline__ int s1_img_exp(const float2* ast, int i) { return f16_scale_exp(__ldg(ast + i).x); }
+__device__ __forceinline__ int s1_gen_exp(const float2* bst, float gmax, int j) {
+  return f16_scale_exp(gmax * __ldg(bst + j).x);
+}
+// Step-3 Z operand exponent of pair (i, j): |Z| <= gmax |a_i| |b_j| (Cauchy-Schwarz over (m, p))
+__device__ __forceinline__ int z_exp(const float2* ast, const float2* bst, float gmax, int i, int j) {
+  return f16_scale_exp(gmax * __ldg(ast + i).y * __ldg(bst + j).y);
+}
+// Step 1 stores pair (i, j)'s Zhat' block x 2^{s1_img_exp + s1_gen_exp}; Step 2 (and the fused kernel) move it to
+// Z's scale with one exact factor
+__device__ __forceinline__ float zhat_to_z_scale(const float2* ast, const float2* bst, float gmax, int i, int j) {
+  return pow2f_wide(z_exp(ast, bst, gmax, i, j) - s1_img_exp(ast, i) - s1_gen_exp(bst, gmax, j));
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {  // 2^x, one MUFU op (2^-inf = 0)
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
