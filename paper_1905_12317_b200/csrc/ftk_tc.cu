@@ -826,6 +826,16 @@ __device__ __forceinline__ void s1_unit(int u, int NCT, int& p, int& ct) {
   ct = rest % NCT;
   p = (rest / NCT) * PLO + p_lo;
 }
+// Processing order of the K' chunks of one image tile: with two generation rounds (NKCH % 4 == 0) all chunks
+// of round 0 first, then round 1, so that round 0 of the next unit can be generated during the last tile's
+// round-1 MMAs (and round 1 during the first tile's round-0 MMAs)
+__host__ __device__ __forceinline__ int s1_chunk_of(int i, int nkch) {
+  if (nkch % 4 != 0) return i;
+  const int hq = nkch / 2, qq = nkch / 4;
+  const int j = i < hq ? i : i - hq;
+  return (j / qq) * hq + (i < hq ? 0 : qq) + (j % qq);
+}
+
 
 struct S1Smem {
   uint64_t st_full[S1_STAGES], st_empty[S1_STAGES];
@@ -866,7 +876,8 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
       tr[2] += diag_clock() - t1;
       tc_fence_after();
       const uint32_t d = a.tmem + 256 + (uint32_t)(ab * 128);
-      auto chunk = [&](const int kc) {
+      auto chunk = [&](const int i) {  // i: processing index, kc: the K' chunk
+        const int kc = s1_chunk_of(i, nkch);
         const int s = g_st % S1_STAGES;
           const int rr = round_of(kc);
           if (rr == 0 ? !got0 : !got1) {  // the generated operand chunk of this round (first tile of a unit)
@@ -888,15 +899,15 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
           for (int ks = 0; ks < KS; ++ks) {
             const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8);
             const uint32_t a_lo = a_hi + (uint32_t)a.nk;
-            const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+            const uint32_t acc = (i > 0 || ks > 0) ? 1u : 0u;
             mma_f16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc);  // +256 B per k-step
             mma_f16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
             mma_f16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
           }
           tc_commit(&S.st_empty[s]);
           // last tile: a round's chunks are free once its last stage has been read
-          if (t == a.nit - 1 && (R == 1 ? kc == nkch - 1 : (kc == nkch - 1 || kc == hq + qq - 1)))
-            tc_commit(&S.a_empty[R == 1 ? 0 : (kc == nkch - 1 ? 1 : 0)]);
+          if (t == a.nit - 1 && (i == nkch - 1 || (R == 2 && i == hq - 1)))
+            tc_commit(&S.a_empty[R == 1 ? 0 : (i == nkch - 1 ? 1 : 0)]);
           ++g_st;
       };
       if constexpr (NK > 0) {
@@ -920,7 +931,6 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
   S1Smem& S = *reinterpret_cast<S1Smem*>(s1_raw);
   uint8_t* stages = s1_raw + 1024;                                   // S1_STAGES x stage_bytes
   const uint32_t stage_bytes = 128u * P.KCH * 4u;                    // hi + lo
-  float* stg = reinterpret_cast<float*>(stages + S1_STAGES * stage_bytes);  // [128 img][128 rows]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = P.n, nk = P.n_k;
   if (threadIdx.x == 0) {
@@ -955,15 +965,17 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
         int p, ct_unused;
         s1_unit(u, P.NCT, p, ct_unused);
         for (int t = 0; t < nit; ++t) {
-          for (int kc = 0; kc < P.NKCH; ++kc, ++g_st) {
+          for (int ci = 0; ci < P.NKCH; ++ci, ++g_st) {
+            const int kc = s1_chunk_of(ci, P.NKCH);
             const int s = g_st % S1_STAGES;
             mbar_wait(&S.st_empty[s], ((g_st / S1_STAGES) & 1) ^ 1);
-            mbar_arrive_expect_tx(&S.st_full[s], stage_bytes);
             const uint8_t* src = P.Aop + (((size_t)p * P.NIT + it0 + t) * P.NKCH + kc) * stage_bytes;
-            if constexpr ((kS1Hint & 2) != 0)
+            mbar_arrive_expect_tx(&S.st_full[s], stage_bytes);
+            if constexpr ((kS1Hint & 2) != 0) {
               bulk_g2s_hint(stages + s * stage_bytes, src, stage_bytes, &S.st_full[s], l2_policy_evict_last());
-            else
+            } else {
               bulk_g2s(stages + s * stage_bytes, src, stage_bytes, &S.st_full[s]);
+            }
           }
         }
       }
@@ -1077,60 +1089,52 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
       }
     }
   } else {
-    // ---------------- epilogue: accumulator [128 rows (j,zeta,part)] x [128 images] -> Zhat'
+    // ---------------- epilogue: accumulator [128 rows (j,zeta,part)] x [128 images] -> Zhat', straight from
+    // TMEM to global memory (no shared-memory staging: shared-memory bandwidth is taken by the MMA operand
+    // reads and the stage copies).  Lane pairs (2c, 2c + 1) hold the Re / Im rows of complex column c: one
+    // shuffle per two images turns them into an (Re, Im) float2 for image e (even lane) and e + 1 (odd lane),
+    // so each store instruction writes two 128-byte row segments.
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int ew = warp - 10;  // 0..7
     const int eh = ew >> 2;    // image half of the TMEM columns this warp drains
-    const uint64_t pol_st = (kS1Hint & 1) ? l2_policy_evict_first() : 0;
+    const bool odd = lane & 1;
     uint32_t g_acc = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int p, ct;
       s1_unit(u, P.NCT, p, ct);
-      const int nvalid = min(128, 2 * (P.F - ct * 64));
-      // this lane's two complex columns cc = lane, lane + 32 -> offsets (template jl, term z) in Zhat'
-      long long coff[2];
-      bool cval[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int cc = lane + 32 * h;
-        const int f = ct * 64 + cc;
-        const int jl = f / P.Hs, z = f - jl * P.Hs;
-        cval[h] = 2 * cc < nvalid;  // pad slots included (zeros)
-        coff[h] = (long long)jl * n * P.Hs + z;
-      }
+      const int f = ct * 64 + (row >> 1);  // this lane's complex column (template jl, slot z)
+      const bool cval = f < P.F;           // pad slots included (zero rows)
+      const int jl = cval ? f / P.Hs : 0, z = f - jl * P.Hs;
+      // Zhat'[pair (il, jl)][p][z] = Zhat + (il nj + jl) n Hs + p Hs + z
+      const size_t coff = ((size_t)jl * n + p) * P.Hs + z;
+      const size_t istride = (size_t)P.nj * n * P.Hs;
       for (int t = 0; t < nit; ++t, ++g_acc) {
         const int ab = g_acc & 1;
         mbar_wait(&S.acc_full[ab], (g_acc >> 1) & 1);
         tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + 256 + (uint32_t)(ab * 128);
-        for (int c0 = 64 * eh; c0 < 64 * eh + 64; c0 += 16) {
-          uint32_t r16[16];
-          tmem_ld16(base + c0, r16);
+#pragma unroll 1
+        for (int c0 = 64 * eh; c0 < 64 * eh + 64; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld16(base + c0, *reinterpret_cast<uint32_t(*)[16]>(r));
+          tmem_ld16(base + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
           tmem_wait_ld();
+          if (c0 + 32 == 64 * eh + 64) {  // this warp's last columns are in registers: release the buffer
+            tc_fence_before();
+            mbar_arrive(&S.acc_empty[ab]);
+          }
+          const int ibase = t * 128 + c0;  // local image index of r[0]
 #pragma unroll
-          for (int e = 0; e < 16; ++e) stg[(c0 + e) * 128 + row] = __uint_as_float(r16[e]);
+          for (int e = 0; e < 32; e += 2) {
+            // even lane: (Re, Im) of image e; odd lane: (Re, Im) of image e + 1
+            const float send = __uint_as_float(odd ? r[e] : r[e + 1]);
+            const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+            const float2 v = odd ? make_float2(recv, __uint_as_float(r[e + 1])) : make_float2(__uint_as_float(r[e]), recv);
+            const int il = ibase + e + (odd ? 1 : 0);
+            if (cval && il < P.ni) P.Zhat[(size_t)il * istride + coff] = v;
+          }
         }
-        tc_fence_before();
-        mbar_arrive(&S.acc_empty[ab]);
-        named_bar(2, 256);
-        // write-out: image ii, complex column cc = (template jl, term z) -> Zhat'[pair (il, jl)][p][z]
-        // (runs of consecutive terms of one pair row)
-        for (int ii = ew; ii < 128; ii += 8) {
-          const int il = t * 128 + ii;  // local image index within the block
-          if (il >= P.ni) continue;
-          float2* dst = P.Zhat + ((size_t)il * P.nj * n + p) * P.Hs;
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (cval[h]) {
-              const float2 v = *reinterpret_cast<const float2*>(stg + ii * 128 + 2 * (lane + 32 * h));
-              if constexpr ((kS1Hint & 1) != 0)
-                st_f2_hint(dst + coff[h], v, pol_st);
-              else
-                dst[coff[h]] = v;
-            }
-        }
-        named_bar(2, 256);
       }
     }
   }
@@ -1142,9 +1146,7 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
   }
 }
 
-static size_t s1_smem_bytes(const TcPlan& tc) {
-  return 1024 + (size_t)S1_STAGES * 128 * tc.KCH * 4 + (size_t)128 * 128 * 4;
-}
+static size_t s1_smem_bytes(const TcPlan& tc) { return 1024 + (size_t)S1_STAGES * 128 * tc.KCH * 4; }
 
 // Image operand prep: FB a[i][q][m] -> scaled fp16 hi/lo canonical K-major tiles (B operand of Step 1).
 __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restrict__ Aop, int NI, int NIT, int n,
