@@ -50,6 +50,9 @@ def check_best(best, X, na, nb, j_offset=0):
         assert abs(best["value"][i] - v[i]) <= tol, (i, best["value"][i], v[i])
         if gap[i] > 2 * tol:
             assert (best["template_idx"][i], best["shift_idx"][i], best["rot_idx"][i]) == (j[i] + j_offset, t[i], r[i])
+        # R25: inside the gap rule the GPU's location must still be a near-maximum of the oracle landscape
+        xg = np.real(X[i, best["template_idx"][i] - j_offset, best["shift_idx"][i], best["rot_idx"][i]])
+        assert xg >= v[i] - 2 * tol, (i, xg, v[i])
 
 
 @pytest.mark.parametrize("engine", ENGINES)
