@@ -416,7 +416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
           mbar_arrive(&S.red_empty[rb]);
           if (f != 0xffffffffu) {
             // f: global flat index (template, shift, rot); v is in pair p's fp16x3 units (exact rescale)
-            const int pe = z_exp(P.ast, P.bst, P.gmax, i, j) + P.eY;
+            const int pe = z_exp(__ldg(P.ast + i), __ldg(P.bst + j), P.gmax) + P.eY;
             const unsigned long long key = pack_key(v * pow2f_wide(-pe), f);
             if (P.img_keys) atomicMax(&P.img_keys[i], key);
             if (P.pair_keys) atomicMax(&P.pair_keys[(size_t)i * P.n_tm_local + j], key);
@@ -519,7 +519,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
       pair_of(P.pb, p, pi_img, pj_tm);
       // fp16x3: this pair's results are X 2^pe; a MODE-0 record carried over from the previous pair of the same
       // image is rescaled (exactly) into this pair's units
-      const int pe = z_exp(P.ast, P.bst, P.gmax, pi_img, pj_tm) + P.eY;
+      const int pe = z_exp(__ldg(P.ast + pi_img), __ldg(P.bst + pj_tm), P.gmax) + P.eY;
       if (s == 0) {
         if (MODE == 0 && bv != -INFINITY) bv *= pow2f_wide(pe - pe_prev);
         pe_prev = pe;
@@ -773,7 +773,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
       {
         int pi_, pj_;
         pair_of(P.pb, p_begin + u / NT, pi_, pj_);
-        zsc = zhat_to_z_scale(P.ast, P.bst, P.gmax, pi_, pj_);  // Zhat' arrives in Step 1's scale
+        zsc = zhat_to_z_scale(__ldg(P.ast + pi_), __ldg(P.bst + pj_), P.gmax);  // Zhat' arrives in Step 1's scale
       }
       // per unit: w_n^{q1 c} for this lane's q1 = a + 16 b, and the radix-D combination constants
       float2 tu[V];

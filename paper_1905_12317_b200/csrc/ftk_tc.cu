@@ -347,11 +347,11 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
       uint32_t bfe = 0xffffffffu;
       float mrun = -INFINITY, srun = 0.f;  // MODE 1: running base-2 log-sum-exp of X log2(e) / tau
       float* land_p = P.land ? P.land + (size_t)p * P.N_t * n : nullptr;
-      float unsc;  // this pair's fp16x3 unscale factor (values are X 2^pe, unsc = 2^-pe)
-      {
+      float unsc = 1.f;  // this pair's fp16x3 unscale factor (values are X 2^pe, unsc = 2^-pe); MODE 0 needs it
+      if (MODE == 1 || land_p) {  // only for landscapes (the resolver unscales the keys)
         int pi_, pj_;
         pair_of(P.pb, p, pi_, pj_);
-        unsc = pow2f_wide(-(z_exp(P.ast, P.bst, P.gmax, pi_, pj_) + P.eY));
+        unsc = pow2f_wide(-(z_exp(__ldg(P.ast + pi_), __ldg(P.bst + pj_), P.gmax) + P.eY));
       }
       const float msc_p = P.msc * unsc;  // MODE 1: log2(e) / tau in scaled units
       for (int T = 0; T < NRT; ++T) {
@@ -673,6 +673,9 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
     uint32_t it = 0;
     for (int p = p_begin; p < p_end; ++p, ++it) {
       const int rb = it & 1;
+      int pi_r, pj_r;
+      pair_of(P.pb, p, pi_r, pj_r);
+      const float2 st_a = __ldg(P.ast + pi_r), st_b = __ldg(P.bst + pj_r);  // fp16x3 stats, loaded early
       mbar_wait_lazy(&S.red_full[rb], (it >> 1) & 1, 200);
       if (MODE == 1) {
         float m = S.red_v[rb][0], sm = S.red_ve[rb][0];
@@ -765,7 +768,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1) k_step3_tc(S3Params P) {
         pair_of(P.pb, p, i, j);
         const uint32_t tt2 = bf / (uint32_t)n, rr = bf - tt2 * (uint32_t)n;
         const uint32_t gflat = ((uint32_t)(P.tm_off + j) * (uint32_t)P.N_t + tt2) * (uint32_t)n + rr;
-        const int pe = z_exp(P.ast, P.bst, P.gmax, i, j) + P.eY;
+        const int pe = z_exp(st_a, st_b, P.gmax) + P.eY;
         const unsigned long long kk = pack_key(bv * pow2f_wide(-pe), gflat);  // fp16x3 scale removed (exact)
         if (P.img_keys) atomicMax(&P.img_keys[i], kk);
         if (P.pair_keys) atomicMax(&P.pair_keys[(size_t)i * P.n_tm_local + j], kk);
@@ -1276,6 +1279,14 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
   for (int item = i_beg; item < i_end; ++item) {
     const int b = item % B.nb, pr = item / B.nb;
     const int zs = B.zs[b], nz = B.ze[b] - zs, g0 = B.g0[b];
+    // fp16x3 statistics of the item's pair, loaded now (used after the FFT: the latency overlaps it)
+    float2 st_a, st_b;
+    {
+      int pi_, pj_;
+      pair_of(pb, pr, pi_, pj_);
+      st_a = __ldg(ast + pi_);
+      st_b = __ldg(bst + pj_);
+    }
     mbar_wait(bar, phase);
     phase ^= 1u;
     // ---- each warp takes one term: load its row (cyclic shift by ell, zero padding to n)
@@ -1349,9 +1360,7 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
       // the neighbouring ell = 0 term (a term without a neighbour writes the whole word, upper half 0)
       const int kl = col - 8 * g0;  // 0..15 within the block
       const int grp = kl >> 3, w = (kl & 7) >> 1;
-      int pi_, pj_;
-      pair_of(pb, pr, pi_, pj_);
-      const float zsc = zhat_to_z_scale(ast, bst, gmax, pi_, pj_);  // fp16x3: Zhat' scale -> Z scale
+      const float zsc = zhat_to_z_scale(st_a, st_b, gmax);  // fp16x3: Zhat' scale -> Z scale
       const bool lone = (B.lone[b] >> zz) & 1;
       uint32_t* shi = stg + (size_t)((grp * 2 + 0) * 4 + w) * RS;
       uint32_t* slo = stg + (size_t)((grp * 2 + 1) * 4 + w) * RS;

@@ -20,14 +20,13 @@ __device__ __forceinline__ int s1_img_exp(const float2* ast, int i) { return f16
 __device__ __forceinline__ int s1_gen_exp(const float2* bst, float gmax, int j) {
   return f16_scale_exp(gmax * __ldg(bst + j).x);
 }
-// Step-3 Z operand exponent of pair (i, j): |Z| <= gmax |a_i| |b_j| (Cauchy-Schwarz over (m, p))
-__device__ __forceinline__ int z_exp(const float2* ast, const float2* bst, float gmax, int i, int j) {
-  return f16_scale_exp(gmax * __ldg(ast + i).y * __ldg(bst + j).y);
-}
+// Step-3 Z operand exponent of pair (i, j) from its statistics a = ast[i], b = bst[j]: |Z| <= gmax |a_i| |b_j|
+// (Cauchy-Schwarz over (m, p))
+__device__ __forceinline__ int z_exp(float2 a, float2 b, float gmax) { return f16_scale_exp(gmax * a.y * b.y); }
 // Step 1 stores pair (i, j)'s Zhat' block x 2^{s1_img_exp + s1_gen_exp}; Step 2 (and the fused kernel) move it to
 // Z's scale with one exact factor
-__device__ __forceinline__ float zhat_to_z_scale(const float2* ast, const float2* bst, float gmax, int i, int j) {
-  return pow2f_wide(z_exp(ast, bst, gmax, i, j) - s1_img_exp(ast, i) - s1_gen_exp(bst, gmax, j));
+__device__ __forceinline__ float zhat_to_z_scale(float2 a, float2 b, float gmax) {
+  return pow2f_wide(z_exp(a, b, gmax) - f16_scale_exp(a.x) - f16_scale_exp(gmax * b.x));
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {  // 2^x, one MUFU op (2^-inf = 0)
