@@ -324,3 +324,36 @@ def test_deterministic_across_runs_and_block_shapes(pkg, name, ni, nj, ws_small)
     for other in runs[1:]:
         for x, y in zip(runs[0], other):
             assert np.array_equal(x, y)
+
+
+def test_fp16x3_extreme_and_mixed_scales(pkg):
+    """The fp16x3 arithmetic relies on per-item power-of-two scales.  Images and
+    templates spanning 36 decades (1e-18 .. 1e18), an all-zero image and an all-zero template must keep the
+    engine's precision bar relative to ||A|| ||B|| in every pair (full landscapes, all pairs), and the zero
+    pairs must be exactly zero with the tie rule's (0, 0, 0) best."""
+    cfg = synth.config("tiny")
+    p = make(pkg, cfg)
+    k, w = p.radial()
+    imgs, _ = synth.draw_items(cfg, "images", range(6), k, "planted")
+    tpls, _ = synth.draw_items(cfg, "templates", range(4), k)
+    si = np.array([1e-18, 1e-6, 1.0, 1e6, 1e18, 0.0])
+    sj = np.array([1e-15, 1.0, 1e15, 0.0])
+    imgs = (imgs * si[:, None, None]).astype(np.complex64)
+    tpls = (tpls * sj[:, None, None]).astype(np.complex64)
+    p.load_images(torch.from_numpy(imgs).cuda())
+    p.load_templates(torch.from_numpy(tpls).cuda())
+    ii, jj = np.meshgrid(np.arange(6), np.arange(4), indexing="ij")
+    Lp = p.landscape_pairs(ii.ravel(), jj.ravel()).cpu().numpy().reshape(6, 4, p.info["N_t"], p.info["n_gamma"])
+    a, b = fb.fb_coeffs(imgs.astype(np.complex128)), fb.fb_coeffs(tpls.astype(np.complex128))
+    na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+    X = np.real(ftk.ftk_landscapes(a, b, oracle_plan(cfg)))
+    for i in range(6):
+        for j in range(4):
+            if na[i] * nb[j] == 0.0:
+                assert np.all(Lp[i, j] == 0.0), (i, j)
+                continue
+            err = np.max(np.abs(Lp[i, j] - X[i, j])) / (na[i] * nb[j])
+            assert err <= PREC, (i, j, err)
+    best = pkg.best_to_numpy(p.align()["best"])
+    assert best["value"][5] == 0.0
+    assert (best["template_idx"][5], best["shift_idx"][5], best["rot_idx"][5]) == (0, 0, 0)
