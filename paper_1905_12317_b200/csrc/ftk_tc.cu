@@ -1202,6 +1202,9 @@ __global__ void k_prep_image_op(const float2* __restrict__ fb, uint8_t* __restri
 // Output words are staged per (group, part, word) in padded rows (index r + r / E: conflict-free) and
 // written out as contiguous 2 KB row blocks.
 using S2Blocks = S2BlockTable;
+// w_32^k = e^{-2 pi i k / 32}, k < 32 (Step 2's (B2) twiddles for L = 2, read with compile-time indices)
+__constant__ float2 c_w32[32];
+
 template <int E>
 __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* __restrict__ Zop,
                                                       int npair, DevPlan P, S2Blocks B, PairBlock pb,
@@ -1279,7 +1282,8 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
   for (int item = i_beg; item < i_end; ++item) {
     const int b = item % B.nb, pr = item / B.nb;
     const int zs = B.zs[b], nz = B.ze[b] - zs, g0 = B.g0[b];
-    // fp16x3 statistics of the item's pair, loaded now (used after the FFT: the latency overlaps it)
+    // fp16x3 statistics of the item's pair and this warp's term (ell, Step-3 column), loaded before the
+    // row wait so that their latency overlaps it
     float2 st_a, st_b;
     {
       int pi_, pj_;
@@ -1287,17 +1291,18 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
       st_a = __ldg(ast + pi_);
       st_b = __ldg(bst + pj_);
     }
+    const int zz = warp;
+    const bool act = zz < nz;
+    int l = 0, col = 0;
+    if (act) {
+      l = __ldg(P.ell + zs + zz);
+      col = __ldg(P.col + zs + zz);
+    }
     mbar_wait(bar, phase);
     phase ^= 1u;
     // ---- each warp takes one term: load its row (cyclic shift by ell, zero padding to n)
-    const int zz = warp;
-    const bool act = zz < nz;
     float2 x[E];
-    int l = 0, col = 0;
     if (act) {
-      const int z = zs + zz;
-      l = P.ell[z];
-      col = P.col[z];
       const int e = (zs & 1) + zz;  // window column of this term
       auto at = [&](int p) { return rows[s2_slot(p, e)]; };
       // Form B: Z(r) w^{ell r} = DFT of the cyclically shifted row Zhat'(q - ell) (reading R5)
@@ -1338,8 +1343,17 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
       }
       dft_regs<E>(x);  // (A2): natural order in x[rv(d')]
       if constexpr (L > 1) {
+        if constexpr (L == 2) {  // (B2) w_32^{(lane % 2) d'}: 1 on even lanes, a constant-bank value on odd lanes
+          const bool oddl = lane & 1;
 #pragma unroll
-        for (int dd = 1; dd < E; ++dd) x[rv(dd)] = cmulf(x[rv(dd)], __ldg(twC + dd * 32 + lane));  // (B2)
+          for (int dd = 1; dd < E; ++dd) {
+            const float2 t = cmulf(x[rv(dd)], c_w32[dd]);
+            x[rv(dd)] = oddl ? t : x[rv(dd)];
+          }
+        } else {
+#pragma unroll
+          for (int dd = 1; dd < E; ++dd) x[rv(dd)] = cmulf(x[rv(dd)], __ldg(twC + dd * 32 + lane));  // (B2)
+        }
 #pragma unroll
         for (int s = 0; s < LL; ++s) {  // (C2) L-point DIF across lanes (branch-free butterfly)
           const int h = (L / 2) >> s;
@@ -1875,6 +1889,12 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, co
         return FTK_ENOMEM;
       }
       cudaMemcpy(tc.d_s2tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice);
+      float2 w32[32];
+      for (int k = 0; k < 32; ++k) {
+        const double ph = -2.0 * M_PI * k / 32.0;
+        w32[k] = make_float2((float)std::cos(ph), (float)std::sin(ph));
+      }
+      cudaMemcpyToSymbol(c_w32, w32, sizeof w32);  // (per device: plan creation runs on the plan's device)
     }
     const int sm2 = (int)step2_smem(pm.n_psi, n_gamma);
     FTK_SMEM_OPTIN((k_step2_fft<2>));
