@@ -68,7 +68,7 @@ class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.limit")
 
     def __init__(self, index: int):
         self.index = index
@@ -111,8 +111,20 @@ class ClockSampler:
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k].lower() == "active"})
+        def num(k):
+            v = []
+            for r in self.rows:
+                try:
+                    v.append(float(r[k]))
+                except (ValueError, IndexError):
+                    pass
+            return v
+        pw, pl = num(2), num(8)
+        capped = sum(1 for r in self.rows if r[7].lower() == "active")
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w": statistics.median(pw) if pw else None, "power_limit_w": max(pl) if pl else None,
+                "power_cap_frac": capped / len(self.rows)}
 
 
 def measured_peaks():
