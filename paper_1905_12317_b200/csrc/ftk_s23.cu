@@ -870,7 +870,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(S23_THREADS, 1)
           for (int m = 0; m < V; ++m) {
             const int i = k1g + V * m + V * V * m2;
             const int pi = i + V * m2;
-            const float2 a0v = make_float2(x[rv(m)].x * zsc, x[rv(m)].y * zsc);
+            const float2 a0v = mul2(make_float2(zsc, zsc), x[rv(m)]);
             if (l > 0) {
               uint32_t hh2, ll2;
               split2_f16(a0v.x, a0v.y, hh2, ll2);

@@ -1062,9 +1062,8 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
               bb[s2][e] = ok ? ldg_f4_hint(reinterpret_cast<const float4*>(brow + m), pol_b) : make_float4(0.f, 0.f, 0.f, 0.f);
             else
               bb[s2][e] = ok ? __ldg(reinterpret_cast<const float4*>(brow + m)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            gg[s2][e] = ok ? __ldg(reinterpret_cast<const float2*>(grow + m)) : make_float2(0.f, 0.f);
-            gg[s2][e].x *= gsc;
-            gg[s2][e].y *= gsc;
+            gg[s2][e] = ok ? mul2(make_float2(gsc, gsc), __ldg(reinterpret_cast<const float2*>(grow + m)))
+                           : make_float2(0.f, 0.f);
           }
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
@@ -1072,8 +1071,10 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
           uint32_t h1[8], l1[8], h2[8], l2[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float cr0 = gg[s2][e].x * bb[s2][e].x, ci0 = -gg[s2][e].x * bb[s2][e].y;
-            const float cr1 = gg[s2][e].y * bb[s2][e].z, ci1 = -gg[s2][e].y * bb[s2][e].w;
+            // c = g conj(b) for nodes m, m + 1: one packed multiply each
+            const float2 c0 = mul2(make_float2(gg[s2][e].x, gg[s2][e].x), make_float2(bb[s2][e].x, -bb[s2][e].y));
+            const float2 c1 = mul2(make_float2(gg[s2][e].y, gg[s2][e].y), make_float2(bb[s2][e].z, -bb[s2][e].w));
+            const float cr0 = c0.x, ci0 = c0.y, cr1 = c1.x, ci1 = c1.y;
             // Re-row: [c_r | -c_i],  Im-row: [c_i | c_r]  (branch-free)
             split2_f16(part ? ci0 : cr0, part ? ci1 : cr1, h1[e], l1[e]);
             split2_f16(part ? cr0 : -ci0, part ? cr1 : -ci1, h2[e], l2[e]);
@@ -1320,7 +1321,7 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
           const float wgt = (qp < Qh || qp > n - Qh) ? 1.f : ((qp == Qh || qp == n - Qh) ? 0.5f : 0.f);
           const int src = (qc - l) & (n_in - 1);
           const float2 v = at(src);
-          x[bb] = make_float2(wgt * v.x, wgt * v.y);
+          x[bb] = mul2(make_float2(wgt, wgt), v);
         }
       }
     }
@@ -1382,7 +1383,7 @@ __global__ void __launch_bounds__(256, (E >= 16 ? 3 : 4)) k_step2_fft(uint8_t* _
 #pragma unroll
       for (int dd = 0; dd < E; ++dd) {
         const int pi = pbase + (E + 1) * dd;
-        const float2 a0 = make_float2(x[rv(dd)].x * zsc, x[rv(dd)].y * zsc);
+        const float2 a0 = mul2(make_float2(zsc, zsc), x[rv(dd)]);
         if (l > 0) {
           uint32_t hh, ll;
           split2_f16(a0.x, a0.y, hh, ll);
