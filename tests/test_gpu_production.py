@@ -357,3 +357,29 @@ def test_fp16x3_extreme_and_mixed_scales(pkg):
     best = pkg.best_to_numpy(p.align()["best"])
     assert best["value"][5] == 0.0
     assert (best["template_idx"][5], best["shift_idx"][5], best["rot_idx"][5]) == (0, 0, 0)
+
+
+@pytest.mark.parametrize("name,ni,nj", [("c3", 200, 24), ("c5", 260, 12)])
+def test_cta_pair_variants_match_default(pkg, name, ni, nj, monkeypatch):
+    """The opt-in CTA-pair kernels: the fused Steps 2 + 3 (FTK_S23=1) and the
+    Step-3-only CTA-pair kernel (FTK_S3V2=1) against the default k_step2_fft + k_step3_tc on the same inputs:
+    the Step-3-only variant bitwise (same operands, same accumulation order), the fused one's per-pair maxima
+    within the precision bar of the default ones (its F-point FFT rounds differently)."""
+    cfg = synth.config(name)
+
+    def run(s23, s3v2):
+        monkeypatch.setenv("FTK_S23", s23)
+        monkeypatch.setenv("FTK_S3V2", s3v2)
+        p, w, imgs, tpls = load_gpu(pkg, cfg, ni, nj)
+        pb = pkg.best_to_numpy(p.align(pair_best=True)["pair_best"].reshape(-1, 4)).reshape(ni, nj)
+        na = fb.discrete_norm(imgs.cpu().numpy(), w)
+        nb = fb.discrete_norm(tpls.cpu().numpy(), w)
+        del p
+        return pb, na, nb
+
+    ref, na, nb = run("0", "0")
+    v2, _, _ = run("0", "1")
+    assert np.array_equal(ref.view(np.int32), v2.view(np.int32))
+    fused, _, _ = run("1", "0")
+    scale = na[:, None] * nb[None, :]
+    assert np.max(np.abs(fused["value"] - ref["value"]) / scale) <= PREC
