@@ -1906,6 +1906,8 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, co
   }
   const char* sdbg = std::getenv("FTK_SYNC_DEBUG");
   tc.sync_debug = sdbg && sdbg[0] == '1';
+  const char* pz = std::getenv("FTK_POISON");
+  tc.poison = (pz && pz[0]) ? (int)(std::strtol(pz, nullptr, 0) & 0xFF) : -1;
   if (tc.sync_debug)
     for (int bi = 0; bi < tc.s2_blocks.nb; ++bi)
       fprintf(stderr, "s2 block %d: terms [%d,%d) groups %d+%d used %x lone %x\n", bi, tc.s2_blocks.zs[bi],
@@ -2171,8 +2173,49 @@ void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const Pair
   }
 }
 
+// FTK_POISON (tests): one CTA per SM takes all of the SM's dynamic shared memory and all 512 TMEM columns and
+// fills both with the byte pattern, so that a later kernel that reads shared memory or TMEM it did not write
+// (a missing accumulate-reset, a stale stage, a race on a buffer hand-off) sees the pattern instead of zeros or a
+// previous launch's values.  With 0x7B the pattern is a large finite value in fp32 (1.3e36) and fp16 (61280),
+// so a stray read cannot hide inside a max as a NaN would; 0xFF gives NaNs.
+__global__ void __launch_bounds__(128, 1) k_poison_onchip(uint32_t word, int smem_bytes) {
+  extern __shared__ __align__(16) uint8_t praw[];
+  __shared__ uint32_t taddr;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(&taddr);
+  uint4* p4 = reinterpret_cast<uint4*>(praw);
+  for (int i = threadIdx.x; i < smem_bytes / 16; i += blockDim.x) p4[i] = make_uint4(word, word, word, word);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = word;
+  const uint32_t base = taddr + ((uint32_t)(warp * 32) << 16);
+  for (int c = 0; c < 512; c += 16) tmem_st16(base + c, v);
+  tmem_wait_st();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(taddr);
+  }
+}
+
+void tc_poison(const TcPlan& tc, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (tc.poison < 0) return;
+  const uint32_t b = (uint32_t)tc.poison & 0xFFu;
+  if (ws && ws_bytes) cudaMemsetAsync(ws, (int)b, ws_bytes, s);
+  FTK_SMEM_OPTIN(k_poison_onchip);
+  int dev = 0, mx = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int smem = (mx - 1024) / 16 * 16;  // the static taddr word + reserve; one CTA per SM
+  k_poison_onchip<<<tc.num_sms, 128, smem, s>>>(b * 0x01010101u, smem);
+}
+
 int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2* A, const float2* B, void* ws,
-                 size_t, int tm_off, unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local,
+                 size_t ws_bytes, int tm_off, unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local,
                  float* land, cudaStream_t s, prof_cb_t prof, void* plan, std::string& msg) {
   if (!tc.ready) {
     msg = "tensor-core engine not initialized";
@@ -2184,6 +2227,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     msg = "tensor-core engine: explicit pair lists go through tc_landscape_pairs";
     return FTK_EINVAL;
   }
+  tc_poison(tc, ws, ws_bytes, s);
   {
     if (prof) prof(plan, 1, 0, s);
     launch_step1_tc(tc, B, Zhat, pb, P, s);
@@ -2195,6 +2239,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
         return FTK_ECUDA;
       }
     }
+    tc_poison(tc, nullptr, 0, s);
     if (tc_s23_eligible(tc, P)) {  // fused Steps 2 + 3: Zhat' -> keys
       if (prof) prof(plan, 3, 0, s);
       const int st = launch_step23(tc, Zhat, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s);
@@ -2226,6 +2271,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
       return FTK_ECUDA;
     }
   }
+  tc_poison(tc, nullptr, 0, s);
   if (prof) prof(plan, 3, 0, s);
   if (tc_s3v2_eligible(tc, P)) {
     if (launch_step3_cg2(tc, Zop, pb, P, tm_off, img_keys, pair_keys, n_tm_local, land, s) != FTK_OK) {
@@ -2278,6 +2324,7 @@ int tc_landscape_pairs(TcPlan& tc, const DevPlan& P, const float2* B, const int3
     pb1.nj = 1;
     pb1.li = pb1.lj = nullptr;
     pb1.count = pb1.ni;
+    tc_poison(tc, ws, (size_t)128 * P.Hs * P.n_psi * sizeof(float2) + (size_t)tc_bytes_per_pair(tc, P), s);
     launch_step1_tc(tc, B, Zhat, pb1, P, s);
     for (int c = a; c < b; ++c) {
       const int k = order[c], i = h_img[k];
@@ -2303,10 +2350,12 @@ int tc_landscape_pairs(TcPlan& tc, const DevPlan& P, const float2* B, const int3
       pb3.nj = 1;
       pb3.li = pb3.lj = nullptr;
       pb3.count = 1;
+      tc_poison(tc, Zop, (size_t)tc_bytes_per_pair(tc, P) - (size_t)P.Hs * P.n_psi * sizeof(float2), s);
       if (launch_step2_fft(tc, zp, Zop, 1, pb3, P, s) != FTK_OK) {
         msg = "Step 2: tensor map encoding failed";
         return FTK_ECUDA;
       }
+      tc_poison(tc, nullptr, 0, s);
       if (tc_s3v2_eligible(tc, P)) {
         if (launch_step3_cg2(tc, Zop, pb3, P, tm_off, nullptr, nullptr, n_tm_local, out + (size_t)k * land_pp, s) !=
             FTK_OK) {

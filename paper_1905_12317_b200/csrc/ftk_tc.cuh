@@ -51,6 +51,9 @@ struct TcPlan {
   int eY = 0;
   int num_sms = 148;
   bool sync_debug = false;
+  // FTK_POISON=<byte> (tests, an initcheck / racecheck stand-in): before every pair block the workspace, and before
+  // every Steps 1-3 launch the shared memory and TMEM of every SM, are filled with this byte (-1: off)
+  int poison = -1;
   // Step-3 epilogue of the next tc_run_block calls: marg == nullptr -> max / argmax (MODE 0); else the
   // marginalization epilogue (MODE 1) writes log sum exp(X / tau) per pair to marg[i][j], marg_scale =
   // log2(e) / tau
@@ -124,6 +127,9 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
                  size_t ws_size, int tm_off,
                  unsigned long long* img_keys, unsigned long long* pair_keys, int n_tm_local, float* land,
                  cudaStream_t s, prof_cb_t prof, void* plan, std::string& msg);
+
+// fill ws (if non-null) and every SM's shared memory and TMEM with the byte tc.poison (no-op when off)
+void tc_poison(const TcPlan& tc, void* ws, size_t ws_bytes, cudaStream_t s);
 
 }  // namespace ftk
 

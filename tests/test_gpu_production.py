@@ -326,6 +326,48 @@ def test_deterministic_across_runs_and_block_shapes(pkg, name, ni, nj, ws_small)
             assert np.array_equal(x, y)
 
 
+@pytest.mark.parametrize("name,ni,nj,ws", [("tiny", 4, 5, 0), ("c3", 260, 6, 0), ("c5", 140, 4, 64 << 20)])
+def test_poisoned_onchip_state_and_workspace(pkg, name, ni, nj, ws):
+    """initcheck / racecheck stand-in (compute-sanitizer is closed on the GPU pool): with FTK_POISON the
+    library fills the pair-block workspace (Zhat', the Step-3 operand) before every block, and every SM's
+    shared memory and all 512 TMEM columns before every Step 1 / 2 / 3 launch, with a byte pattern -- 0x7B
+    (a large finite fp32 / fp16 value that a max cannot ignore) and 0xFF (NaN).  Per-image bests, per-pair
+    maxima, landscapes of explicit pairs and log-marginals must be BITWISE equal to the unpoisoned run: a
+    read of shared memory, TMEM or workspace that the same launch did not write first (a missing
+    accumulate reset, a stale pipeline stage, a hand-off race) would change them."""
+    cfg = synth.config(name)
+    rng = np.random.default_rng(7)
+    ii = rng.integers(0, ni, 6)
+    jj = rng.integers(0, nj, 6)
+    runs = []
+    for pat in (None, "0x7B", "0xFF"):
+        if pat is None:
+            os.environ.pop("FTK_POISON", None)
+        else:
+            os.environ["FTK_POISON"] = pat
+        try:
+            p, w, imgs, tpls = load_gpu(pkg, cfg, ni, nj, workspace_bytes=ws)
+        finally:
+            os.environ.pop("FTK_POISON", None)
+        res = p.align(pair_best=True)
+        L = p.landscape_pairs(ii, jj)
+        tau = 0.1 * float(np.median(fb.discrete_norm(imgs[:4].cpu().numpy(), w)) *
+                          np.median(fb.discrete_norm(tpls[:4].cpu().numpy(), w)))
+        lm = p.align_marginal(tau)
+        torch.cuda.synchronize()
+        out = [pkg.best_to_numpy(res["best"]).view(np.int32).copy(),
+               pkg.best_to_numpy(res["pair_best"].reshape(-1, 4)).view(np.int32).copy(),
+               L.cpu().numpy().view(np.int32).copy(), lm.cpu().numpy().view(np.int32).copy()]
+        if name == "tiny":
+            out.append(p.align(landscape=True)["landscape"].cpu().numpy().view(np.int32).copy())
+        assert all(np.all(np.isfinite(x.view(np.float32))) for x in out[2:]), pat
+        runs.append(out)
+        del p
+    for other in runs[1:]:
+        for x, y in zip(runs[0], other):
+            assert np.array_equal(x, y)
+
+
 def test_fp16x3_extreme_and_mixed_scales(pkg):
     """The fp16x3 arithmetic relies on per-item power-of-two scales.  Images and
     templates spanning 36 decades (1e-18 .. 1e18), an all-zero image and an all-zero template must keep the
