@@ -41,6 +41,7 @@
 // TMEM columns: D buffers [0, 4 NCH) (E, O of buffer 0 then 1), A slots [4 NCH, 4 NCH + 2 K3p).
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -1491,6 +1492,379 @@ static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, 
   return FTK_OK;
 }
 
+// ---------------------------------------------------------------- Step 2 on the tensor cores (n_gamma = n_psi = 512)
+// The same Z as k_step2_fft (Eq. fbk3 Step 2, Form B: x(q) = Zhat'(q - ell), reading R5), by the
+// four-step split q = a + 64 b (a < 64, b < 8), r = c + 8 d (c < 8, d < 64):
+//   Z(c + 8 d) = sum_a w64^{a d} T(a, c),   T(a, c) = w512^{a c} sum_b x(a + 64 b) w8^{b c}     (w_n = e^{-2 pi i / n})
+// * T on the CUDA cores: per (slot, a) an 8-point register DFT and 7 twiddles, scaled into Z's fp16x3 range (the
+//   bound of the file header holds for every partial sum of the DFT), split into fp16 hi / lo and stored as the B
+//   operand: MN-major (N = (slot, c), K = (Re | Im, a)), canonical core matrices, one 32 KB stage per block.
+// * The DFT-64 over a as ONE GEMM D[(d, Re|Im)][(slot, c)] = F64 . T, F64 = the real 128 x 128 form of
+//   [w64^{a d}] (rows m = 2 d + Re|Im, columns k = Re|Im * 64 + a) as fp16 hi / lo, resident in TMEM as the A
+//   operand for the whole kernel: 3 x 8 tcgen05.mma M128 N64 K16 per block (fp16x3).
+// * Epilogue straight from TMEM: lane (d, Re) writes the hi words, lane (d, Im) the lo words of rows 8 d + c of
+//   the Step-3 operand (one shuffle per two values exchanges the halves); slot s of a block is Step-3 word s
+//   (group s / 4, word s % 4): an ell > 0 term (Re Z, Im Z), or two ell = 0 terms transformed together as
+//   x_1 + i x_2 (their Z are real for real images, reading R13: Re -> low half, Im -> high half).
+// Warps: 0 TMA producer (8-term Zhat' windows, NR-deep ring), 1 MMA issuer, 2-9 builders (T -> B operand,
+// NB-deep ring), 10-17 epilogue (two TMEM accumulators).
+constexpr int S2T_THREADS = 18 * 32;
+constexpr int S2T_NR = 3, S2T_NB = 2, S2T_NO = 2;  // rows ring, B-operand ring, output staging buffers
+constexpr uint32_t S2T_ROWS_BYTES = 512u * 8u * 8u;  // one block window: 512 rows x 8 terms, complex fp32
+constexpr uint32_t S2T_BOP_PART = 8u * 2048u;        // one part (hi or lo) of a B stage: 8 slots x 16 K-cores x 128 B
+constexpr uint32_t S2T_BOP_BYTES = 2u * S2T_BOP_PART;
+constexpr uint32_t S2T_OUT_BYTES = 2u * 16384u;       // epilogue staging of one block: <= 2 word groups x 16 KB
+constexpr size_t S2T_SMEM = (size_t)S2T_NR * S2T_ROWS_BYTES + (size_t)S2T_NB * S2T_BOP_BYTES + S2T_NO * S2T_OUT_BYTES + 512;
+
+struct S2TParams {
+  uint8_t* Zop;
+  int npair, NWG, K3p, dbg;
+  PairBlock pb;
+  const float2* ast;
+  const float2* bst;
+  float gmax;
+  const uint32_t* F;  // [128 rows][64 hi words, 64 lo words]
+  const float2* tw;   // [64 a][8 c] w512^{a c}
+  S2BlockTable B;
+  S2TSlotTable sl;
+};
+struct S2TMeta {  // per rows stage, written by the producer before the TMA is armed
+  float zsc;
+  int bi;
+};
+
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+__global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_constant__ S2TParams P,
+                                                            const __grid_constant__ CUtensorMap zmap,
+                                                            const __grid_constant__ CUtensorMap omap) {
+  extern __shared__ __align__(1024) uint8_t s2traw[];
+  uint8_t* rows_base = s2traw;
+  uint8_t* bop_base = s2traw + S2T_NR * S2T_ROWS_BYTES;
+  uint8_t* out_base = bop_base + S2T_NB * S2T_BOP_BYTES;  // NO x (2 groups x [T 4][part 2][row group 16][128 B])
+  uint64_t* bars = reinterpret_cast<uint64_t*>(out_base + S2T_NO * S2T_OUT_BYTES);
+  uint64_t* rows_full = bars;
+  uint64_t* rows_empty = bars + S2T_NR;
+  uint64_t* bop_full = bars + 2 * S2T_NR;
+  uint64_t* bop_empty = bop_full + S2T_NB;
+  uint64_t* d_full = bop_empty + S2T_NB;
+  uint64_t* d_empty = d_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
+  S2TMeta* meta = reinterpret_cast<S2TMeta*>(tmem_slot + 2);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int nb = P.B.nb;
+  const int total = P.npair * nb;
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int i_beg = blockIdx.x * per;
+  const int nit = max(0, min(total, i_beg + per) - i_beg);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S2T_NR; ++i) {
+      mbar_init(rows_full + i, 1);
+      mbar_init(rows_empty + i, 8);
+    }
+    for (int i = 0; i < S2T_NB; ++i) {
+      mbar_init(bop_full + i, 8);
+      mbar_init(bop_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(d_full + i, 1);
+      mbar_init(d_empty + i, 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // columns [0, 128): two accumulators; [128, 192): F hi; [192, 256): F lo
+  if (warp >= 2 && warp <= 9) {      // F64 into TMEM: two builder warps per lane quarter, 64 columns each
+    const int q = warp & 3, hh = (warp - 2) >> 2;
+    const uint32_t* src = P.F + (size_t)(q * 32 + lane) * 128 + hh * 64;
+    const uint32_t dst = tmem + ((uint32_t)(q * 32) << 16) + 128u + (uint32_t)hh * 64u;
+#pragma unroll 1
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      uint32_t v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = __ldg(src + c0 + k);
+      tmem_st16(dst + c0, v);
+    }
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == 0) {
+    // ---------------- TMA producer: the block's aligned 8-term window of the pair's 512 Zhat' rows, plus the
+    // item's metadata (block, Zhat' -> Z scale) for the builders
+    if (lane == 0) {
+      int bi = i_beg % nb, pr = i_beg / nb;
+      for (int k = 0; k < nit; ++k) {
+        const int st = k % S2T_NR;
+        int pi_, pj_;
+        pair_of(P.pb, pr, pi_, pj_);
+        const float zsc = zhat_to_z_scale(__ldg(P.ast + pi_), __ldg(P.bst + pj_), P.gmax);
+        mbar_wait(rows_empty + st, ((k / S2T_NR) & 1) ^ 1);
+        meta[st].zsc = zsc;
+        meta[st].bi = bi;
+        uint8_t* dst = rows_base + st * S2T_ROWS_BYTES;
+        mbar_arrive_expect_tx(rows_full + st, S2T_ROWS_BYTES);
+        tma_load_2d(dst, &zmap, P.B.zs[bi] & ~1, pr * 512, rows_full + st);
+        tma_load_2d(dst + S2T_ROWS_BYTES / 2, &zmap, P.B.zs[bi] & ~1, pr * 512 + 256, rows_full + st);
+        if (++bi == nb) {
+          bi = 0;
+          ++pr;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: D[db] = F64 . T (fp16x3: Fhi Thi + Fhi Tlo + Flo Thi), 8 k-steps
+    if (lane == 0) {
+      const uint32_t idesc = idesc_f16_f32(128, 64) | (1u << 16);  // B MN-major
+      for (int k = 0; k < nit; ++k) {
+        const int sb = k % S2T_NB, db = k & 1;
+        mbar_wait(bop_full + sb, (k / S2T_NB) & 1);
+        mbar_wait(d_empty + db, ((k >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t bh = smem_u32(bop_base + sb * S2T_BOP_BYTES), bl = bh + S2T_BOP_PART;
+        const uint32_t d = tmem + (uint32_t)db * 64u, fh = tmem + 128u, fl = tmem + 192u;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint64_t dh = smem_desc_kmajor_noswz(bh + ks * 256, 128, 2048);
+          const uint64_t dl = smem_desc_kmajor_noswz(bl + ks * 256, 128, 2048);
+          mma_f16_ts(d, fh + ks * 8, dh, idesc, ks > 0 ? 1u : 0u);
+          mma_f16_ts(d, fh + ks * 8, dl, idesc, 1u);
+          mma_f16_ts(d, fl + ks * 8, dh, idesc, 1u);
+        }
+        tc_commit(bop_empty + sb);
+        tc_commit(d_full + db);
+      }
+    }
+    __syncwarp();
+  } else if (warp <= 9) {
+    // ---------------- builders: thread (a, slots s0 and s0 + 4) -> T(a, c), c < 8, as B-operand rows
+    const int bt = threadIdx.x - 64;
+    const int a = bt & 63, s0 = bt >> 6;  // warp-uniform slot pair
+    float2 tw[8];
+#pragma unroll
+    for (int c = 1; c < 8; ++c) tw[c] = __ldg(P.tw + a * 8 + c);
+    auto rv = [](int i) { return ((i & 1) << 2) | (i & 2) | ((i >> 2) & 1); };
+    const int swa = (a >> 1) & 3;  // the row swizzle term of rows a + 64 b (independent of b)
+    for (int k = 0; k < nit; ++k) {
+      const int st = k % S2T_NR, sb = k % S2T_NB;
+      mbar_wait(rows_full + st, (k / S2T_NR) & 1);
+      const float zsc = meta[st].zsc;
+      const int bi = meta[st].bi;
+      uint32_t info[2];
+      info[0] = P.sl.info[bi][s0];
+      info[1] = P.sl.info[bi][s0 + 4];
+      const float2* rows = reinterpret_cast<const float2*>(rows_base + st * S2T_ROWS_BYTES);
+      float2 x[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int kind = info[u] & 3, e1 = (info[u] >> 4) & 15, e2 = (info[u] >> 8) & 15, el = (int)(info[u] >> 16);
+        if (kind == 1) {
+          // complex index of (row q0 + 64 b mod 512, column e1): ((q0 + 64 b) * 8 + swizzled column) mod 4096
+          const int q0 = (a - el) & 511;
+          const int base = q0 * 8 + ((((e1 >> 1) ^ (q0 >> 1)) & 3) << 1) + (e1 & 1);
+#pragma unroll
+          for (int b = 0; b < 8; ++b) x[u][b] = rows[(base + 512 * b) & 4095];
+        } else if (kind == 2) {
+          const int c1 = a * 8 + ((((e1 >> 1) ^ swa) & 3) << 1) + (e1 & 1);
+          const int c2 = a * 8 + ((((e2 >> 1) ^ swa) & 3) << 1) + (e2 & 1);
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            const float2 r1 = e1 < 15 ? rows[c1 + 512 * b] : make_float2(0.f, 0.f);
+            const float2 r2 = e2 < 15 ? rows[c2 + 512 * b] : make_float2(0.f, 0.f);
+            x[u][b] = make_float2(r1.x - r2.y, r1.y + r2.x);  // x_1 + i x_2
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(rows_empty + st);
+      // the pair's Zhat' -> Z scale folded into the twiddles
+      float2 tz[8];
+      tz[0] = make_float2(zsc, zsc);
+#pragma unroll
+      for (int c = 1; c < 8; ++c) tz[c] = mul2(make_float2(zsc, zsc), tw[c]);
+      mbar_wait(bop_empty + sb, ((k / S2T_NB) & 1) ^ 1);
+      uint8_t* bop = bop_base + sb * S2T_BOP_BYTES;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t off = (uint32_t)(s0 + 4 * u) * 2048u + (uint32_t)a * 16u;
+        uint4 hr, lr, hi_, li_;
+        if ((info[u] & 3) == 0 || (P.dbg & 1)) {  // no term: a zero column block (the word stays zero)
+          hr = lr = hi_ = li_ = make_uint4(0u, 0u, 0u, 0u);
+        } else {
+          dft_regs<8>(x[u]);  // natural order in x[rv(c)]
+          float2 T[8];
+          T[0] = mul2(tz[0], x[u][rv(0)]);
+#pragma unroll
+          for (int c = 1; c < 8; ++c) T[c] = cmulf(x[u][rv(c)], tz[c]);
+          split2_f16(T[0].x, T[1].x, hr.x, lr.x);
+          split2_f16(T[2].x, T[3].x, hr.y, lr.y);
+          split2_f16(T[4].x, T[5].x, hr.z, lr.z);
+          split2_f16(T[6].x, T[7].x, hr.w, lr.w);
+          split2_f16(T[0].y, T[1].y, hi_.x, li_.x);
+          split2_f16(T[2].y, T[3].y, hi_.y, li_.y);
+          split2_f16(T[4].y, T[5].y, hi_.z, li_.z);
+          split2_f16(T[6].y, T[7].y, hi_.w, li_.w);
+        }
+        // MN-major core (n / 8 = slot, k / 8), row k % 8, element n % 8 = c; K = a (Re), 64 + a (Im)
+        *reinterpret_cast<uint4*>(bop + off) = hr;
+        *reinterpret_cast<uint4*>(bop + off + 1024u) = hi_;
+        *reinterpret_cast<uint4*>(bop + S2T_BOP_PART + off) = lr;
+        *reinterpret_cast<uint4*>(bop + S2T_BOP_PART + off + 1024u) = li_;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bop_full + sb);
+    }
+  } else {
+    // ---------------- epilogue: lane quarter q, columns c in [4h, 4h + 4) of every slot
+    const int ew = warp - 10, q = warp & 3, h = ew >> 2;
+    const int ri = lane & 1;  // 0: the Re row of this d (writes hi words), 1: the Im row (lo words)
+    // word (c) = (Re, Im) halves: Re lane keeps its hi halves and receives the Im lane's hi halves; the Im
+    // lane keeps its lo halves and receives the Re lane's lo halves
+    const uint32_t sel0 = ri ? 0x1054u : 0x5410u, sel1 = ri ? 0x3276u : 0x7632u;
+    // staging row of this lane: [T = q][part = ri][row group = lane / 2] (128 B, 128B-swizzled as the TMA store
+    // reads it: 16-byte chunk c at c ^ (row group & 7))
+    const uint32_t srow = (uint32_t)(((q * 2 + ri) * 16 + (lane >> 1)) * 128);
+    const int swz = (lane >> 1) & 7;
+    const bool issuer = (warp == 10 && lane == 0);
+    int bi = i_beg % nb, pr = i_beg / nb;
+    for (int k = 0; k < nit; ++k) {
+      const int db = k & 1;
+      mbar_wait(d_full + db, (k >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[8][4];
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)db * 64u + 4u * (uint32_t)h;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) tmem_ld4(base + 8u * s, v[s]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d_empty + db);
+      const int ng = P.B.ng[bi];
+      uint32_t w[8][4];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        uint32_t h01, l01, h23, l23;
+        split2_f16(__uint_as_float(v[s][0]), __uint_as_float(v[s][1]), h01, l01);
+        split2_f16(__uint_as_float(v[s][2]), __uint_as_float(v[s][3]), h23, l23);
+        const uint32_t k01 = ri ? l01 : h01, k23 = ri ? l23 : h23;
+        const uint32_t r01 = __shfl_xor_sync(0xffffffffu, ri ? h01 : l01, 1);
+        const uint32_t r23 = __shfl_xor_sync(0xffffffffu, ri ? h23 : l23, 1);
+        w[s][0] = prmt(k01, r01, sel0);
+        w[s][1] = prmt(k01, r01, sel1);
+        w[s][2] = prmt(k23, r23, sel0);
+        w[s][3] = prmt(k23, r23, sel1);
+      }
+      if (P.sl.needmask[bi]) {
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const uint32_t m = P.sl.mask[bi][s];
+#pragma unroll
+          for (int ci = 0; ci < 4; ++ci) w[s][ci] &= m;
+        }
+      }
+      // the staging buffer of item k - NO must have been read by its TMA store
+      if (issuer) bulk_wait_group_read<S2T_NO - 1>();
+      named_bar(1, 256);
+      uint8_t* stg = out_base + (k % S2T_NO) * S2T_OUT_BYTES + srow;
+#pragma unroll
+      for (int grp = 0; grp < 2; ++grp) {
+        if (grp >= ng) break;
+#pragma unroll
+        for (int ci = 0; ci < 4; ++ci)
+          *reinterpret_cast<uint4*>(stg + grp * 16384 + (((4 * h + ci) ^ swz) << 4)) =
+              make_uint4(w[4 * grp][ci], w[4 * grp + 1][ci], w[4 * grp + 2][ci], w[4 * grp + 3][ci]);
+      }
+      fence_proxy_async_smem();
+      named_bar(1, 256);
+      if (issuer && !(P.dbg & 2)) {
+        for (int grp = 0; grp < ng; ++grp)
+          tma_store_5d(&omap, out_base + (k % S2T_NO) * S2T_OUT_BYTES + grp * 16384, 0, P.B.g0[bi] + grp, 0, 0, pr * 4);
+        bulk_commit_group();
+      }
+      if (++bi == nb) {
+        bi = 0;
+        ++pr;
+      }
+    }
+    if (issuer) bulk_wait_group<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+static int launch_step2_tc(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, const PairBlock& pb,
+                           const DevPlan& P, cudaStream_t s) {
+  S2TParams prm;
+  std::memset(&prm, 0, sizeof prm);
+  prm.Zop = Zop;
+  prm.npair = npair;
+  prm.NWG = P.K3p / 8;
+  prm.K3p = P.K3p;
+  prm.pb = pb;
+  prm.ast = tc.d_ast;
+  prm.bst = tc.d_bst;
+  prm.gmax = tc.gmax;
+  prm.F = tc.d_s2F;
+  prm.tw = tc.d_s2w;
+  {
+    const char* dg = std::getenv("FTK_S2TC_DBG");  // (timing experiments: 1 skips the builders' arithmetic, 2 the epilogue's)
+    prm.dbg = dg ? std::atoi(dg) : 0;
+  }
+  std::memcpy(&prm.B, &tc.s2_blocks, sizeof prm.B);
+  std::memcpy(&prm.sl, &tc.s2t, sizeof prm.sl);
+  alignas(64) CUtensorMap zmap;
+  std::memset(&zmap, 0, sizeof zmap);
+  if (make_zmap(&zmap, Zhat, npair, P) != FTK_OK) return FTK_ECUDA;
+  // Step-3 operand as a 5-D tensor of 32-bit words: (word in a 128-byte core row group, word group, row group
+  // of the r-tile, part, pair x r-tile); one 16 KB box per (item, word group), 128-byte swizzle
+  alignas(64) CUtensorMap omap;
+  std::memset(&omap, 0, sizeof omap);
+  {
+    PFN_encodeTiled enc = get_encode_tiled();
+    if (!enc) return FTK_ECUDA;
+    const cuuint64_t NWG = (cuuint64_t)(P.K3p / 8);
+    const cuuint64_t dims[5] = {32, NWG, 16, 2, (cuuint64_t)npair * 4};
+    const cuuint64_t strides[4] = {128, NWG * 128, NWG * 2048, NWG * 4096};
+    const cuuint32_t box[5] = {32, 1, 16, 2, 4};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (enc(&omap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, Zop, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return FTK_ECUDA;
+  }
+  const int items = tc.s2_blocks.nb * npair;
+  const int grid = items < tc.num_sms ? items : tc.num_sms;
+  k_step2_tc<<<grid, S2T_THREADS, S2T_SMEM, s>>>(prm, zmap, omap);
+  return FTK_OK;
+}
+
+// Step 2 dispatch: the tensor-core kernel where the plan enabled it (n_gamma = n_psi = 512), else the CUDA-core FFT
+static int launch_step2(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, int npair, const PairBlock& pb,
+                        const DevPlan& P, cudaStream_t s) {
+  if (tc.s2tc) return launch_step2_tc(tc, Zhat, Zop, npair, pb, P, s);
+  return launch_step2_fft(tc, Zhat, Zop, npair, pb, P, s);
+}
+
 // ---------------------------------------------------------------- single-MMA self-test
 // D = A * B^T with A [128 x 32] (TS: from TMEM; SS: from SMEM), B [N=64 x 32] from SMEM, bf16 inputs.
 __global__ void __launch_bounds__(128, 1) k_tc_selftest(const float* A, const float* B, float* D_ts, float* D_ss,
@@ -1898,6 +2272,76 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, co
       cudaMemcpyToSymbol(c_w32, w32, sizeof w32);  // (per device: plan creation runs on the plan's device)
     }
     const int sm2 = (int)step2_smem(pm.n_psi, n_gamma);
+    // k_step2_tc tables (n_gamma = n_psi = 512): F64 real form, radix-8 twiddles, per-block word slots
+    tc.s2tc = 0;
+    if (pm.n_psi == 512 && n_gamma == 512) {
+      const char* e2 = std::getenv("FTK_S2TC");
+      const int want = e2 ? std::atoi(e2) : 1;  // default on; FTK_S2TC=0 selects k_step2_fft
+      std::memset(&tc.s2t, 0, sizeof tc.s2t);
+      for (int bi = 0; bi < tc.s2_blocks.nb; ++bi) {
+        int kind[8] = {0}, e1[8], e2[8], el[8] = {0};
+        for (int sl = 0; sl < 8; ++sl) e1[sl] = e2[sl] = 15;
+        const int zs = tc.s2_blocks.zs[bi], g0 = tc.s2_blocks.g0[bi];
+        for (int z = zs; z < tc.s2_blocks.ze[bi]; ++z) {
+          const int kl = col[z] - 8 * g0, sl = kl >> 1, e = (zs & 1) + (z - zs);
+          if (kl < 0 || kl >= 16 || e > 7) {
+            msg = "tensor-core engine: Step-2 slot table";
+            return FTK_EINVAL;
+          }
+          if (ell[z] > 0) {
+            kind[sl] = 1;
+            e1[sl] = e;
+            el[sl] = ell[z];
+          } else {
+            kind[sl] = 2;
+            if (kl & 1)
+              e2[sl] = e;
+            else
+              e1[sl] = e;
+          }
+        }
+        for (int sl = 0; sl < 8; ++sl) {
+          tc.s2t.info[bi][sl] = (uint32_t)kind[sl] | ((uint32_t)e1[sl] << 4) | ((uint32_t)e2[sl] << 8) |
+                                ((uint32_t)el[sl] << 16);
+          const uint32_t m = kind[sl] == 2 ? ((e1[sl] < 15 ? 0x0000FFFFu : 0u) | (e2[sl] < 15 ? 0xFFFF0000u : 0u))
+                                           : 0xFFFFFFFFu;
+          tc.s2t.mask[bi][sl] = m;
+          if (m != 0xFFFFFFFFu) tc.s2t.needmask[bi] = 1;
+        }
+      }
+      std::vector<uint32_t> F((size_t)128 * 128);
+      for (int m = 0; m < 128; ++m) {
+        const int d = m >> 1, ro = m & 1;
+        for (int kk = 0; kk < 128; kk += 2) {
+          uint16_t hw[2], lw[2];
+          for (int u = 0; u < 2; ++u) {
+            const int k = kk + u, ri = k >> 6, a = k & 63;
+            const double ph = 2.0 * M_PI * (double)((a * d) % 64) / 64.0;
+            const double v = ro == 0 ? (ri == 0 ? std::cos(ph) : std::sin(ph)) : (ri == 0 ? -std::sin(ph) : std::cos(ph));
+            const __half hh = __float2half_rn((float)v);
+            const __half ll = __float2half_rn((float)(v - (double)__half2float(hh)));
+            hw[u] = *reinterpret_cast<const uint16_t*>(&hh);
+            lw[u] = *reinterpret_cast<const uint16_t*>(&ll);
+          }
+          F[(size_t)m * 128 + kk / 2] = (uint32_t)hw[0] | ((uint32_t)hw[1] << 16);
+          F[(size_t)m * 128 + 64 + kk / 2] = (uint32_t)lw[0] | ((uint32_t)lw[1] << 16);
+        }
+      }
+      std::vector<float2> w8((size_t)64 * 8);
+      for (int a = 0; a < 64; ++a)
+        for (int c = 0; c < 8; ++c) {
+          const double ph = -2.0 * M_PI * (double)((a * c) % 512) / 512.0;
+          w8[(size_t)a * 8 + c] = make_float2((float)std::cos(ph), (float)std::sin(ph));
+        }
+      if (cudaMalloc(&tc.d_s2F, F.size() * 4) != cudaSuccess || cudaMalloc(&tc.d_s2w, w8.size() * 8) != cudaSuccess) {
+        msg = "tensor-core engine: allocation failed";
+        return FTK_ENOMEM;
+      }
+      cudaMemcpy(tc.d_s2F, F.data(), F.size() * 4, cudaMemcpyHostToDevice);
+      cudaMemcpy(tc.d_s2w, w8.data(), w8.size() * 8, cudaMemcpyHostToDevice);
+      FTK_SMEM_OPTIN(k_step2_tc);
+      tc.s2tc = want != 0 ? 1 : 0;
+    }
     FTK_SMEM_OPTIN((k_step2_fft<2>));
     FTK_SMEM_OPTIN((k_step2_fft<4>));
     FTK_SMEM_OPTIN((k_step2_fft<8>));
@@ -1921,6 +2365,10 @@ void tc_plan_free(TcPlan& tc) {
   tc_s23_free(tc);
   cudaFree(tc.d_s2tw);
   tc.d_s2tw = nullptr;
+  cudaFree(tc.d_s2F);
+  tc.d_s2F = nullptr;
+  cudaFree(tc.d_s2w);
+  tc.d_s2w = nullptr;
   cudaFree(tc.d_Ysm);
   cudaFree(tc.d_colrep);
   cudaFree(tc.d_colpart);
@@ -2258,7 +2706,7 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
       return FTK_OK;
     }
     if (prof) prof(plan, 2, 0, s);
-    if (launch_step2_fft(tc, Zhat, Zop, pb.count, pb, P, s) != FTK_OK) {
+    if (launch_step2(tc, Zhat, Zop, pb.count, pb, P, s) != FTK_OK) {
       msg = "Step 2: tensor map encoding failed";
       return FTK_ECUDA;
     }
@@ -2351,7 +2799,7 @@ int tc_landscape_pairs(TcPlan& tc, const DevPlan& P, const float2* B, const int3
       pb3.li = pb3.lj = nullptr;
       pb3.count = 1;
       tc_poison(tc, Zop, (size_t)tc_bytes_per_pair(tc, P) - (size_t)P.Hs * P.n_psi * sizeof(float2), s);
-      if (launch_step2_fft(tc, zp, Zop, 1, pb3, P, s) != FTK_OK) {
+      if (launch_step2(tc, zp, Zop, 1, pb3, P, s) != FTK_OK) {
         msg = "Step 2: tensor map encoding failed";
         return FTK_ECUDA;
       }

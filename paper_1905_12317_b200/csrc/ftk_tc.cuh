@@ -19,6 +19,18 @@ struct S2BlockTable {
   int lone[16];        // terms (bit z - zs) with ell = 0 and no neighbour in their word
 };
 
+// Step 2 on the tensor cores (k_step2_tc, n_gamma = n_psi = 512): per Step-2 block, one slot per Step-3 operand
+// word (word group grp, word w -> slot 4 grp + w).  kind 0: no term (the word is zero); kind 1: an ell > 0 term at
+// window column e1, cyclic shift ell (word = (Re Z, Im Z)); kind 2: ell = 0 terms at window columns e1 (low half)
+// and e2 (high half), either may be absent (-1), transformed together as x_e1 + i x_e2 (both Z are real).
+// info = kind | e1 << 4 | e2 << 8 | ell << 16 (window columns 0..7, 15 = absent); mask: bits of the word kept;
+// needmask[b]: some word of block b keeps only one half (a lone ell = 0 term)
+struct S2TSlotTable {
+  uint32_t info[16][8];
+  uint32_t mask[16][8];
+  int needmask[16];
+};
+
 struct TcPlan {
   static constexpr int MAXG = 16;  // max rep-groups (Y slices) of Step 3
   bool ready = false;
@@ -40,6 +52,12 @@ struct TcPlan {
   int NIT = 0, KCH = 64, NKCH = 0;
   S2BlockTable s2_blocks;     // Step-2 work blocks
   float2* d_s2tw = nullptr;  // Step-2 four-step twiddle tables
+  // k_step2_tc (tensor-core Step 2, n = 512): DFT-64 matrix as the TMEM A operand ([128 rows][64 hi + 64 lo words]),
+  // radix-8 twiddles [64 a][8 c], per-block slot table; s2tc: 1 when this plan runs it (FTK_S2TC != 0, n = 512)
+  uint32_t* d_s2F = nullptr;
+  float2* d_s2w = nullptr;
+  S2TSlotTable s2t;
+  int s2tc = 0;
   int64_t n_tm = 0;
   // fp16x3 power-of-two operand scaling (ftk_tc.cu header): per-item maxima of the loaded images / local templates
   // (x = max |Re|, |Im| of the FB coefficients, y = their Frobenius norm), gmax = max |g_zeta(k_m)|, eY = the
