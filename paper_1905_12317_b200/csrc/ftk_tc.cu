@@ -1630,9 +1630,13 @@ __global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_consta
   } else if (warp == 1) {
     // ---------------- MMA issuer: D[db] = F64 . T (fp16x3: Fhi Thi + Fhi Tlo + Flo Thi), 8 k-steps
     if (lane == 0) {
-      const uint32_t idesc = idesc_f16_f32(128, 64) | (1u << 16);  // B MN-major
+      // B MN-major; blocks of one word group (slots 0-3) run N = 32
+      const uint32_t idesc64 = idesc_f16_f32(128, 64) | (1u << 16), idesc32 = idesc_f16_f32(128, 32) | (1u << 16);
+      int bi = i_beg % nb;
       for (int k = 0; k < nit; ++k) {
         const int sb = k % S2T_NB, db = k & 1;
+        const uint32_t idesc = P.B.ng[bi] > 1 ? idesc64 : idesc32;
+        if (++bi == nb) bi = 0;
         mbar_wait(bop_full + sb, (k / S2T_NB) & 1);
         mbar_wait(d_empty + db, ((k >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -1703,6 +1707,7 @@ __global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_consta
       for (int u = 0; u < 2; ++u) {
         const uint32_t off = (uint32_t)(s0 + 4 * u) * 2048u + (uint32_t)a * 16u;
         uint4 hr, lr, hi_, li_;
+        if (u == 1 && P.B.ng[bi] == 1) continue;  // N = 32 block: slots 4-7 are not read
         if ((info[u] & 3) == 0 || (P.dbg & 1)) {  // no term: a zero column block (the word stays zero)
           hr = lr = hi_ = li_ = make_uint4(0u, 0u, 0u, 0u);
         } else {
@@ -1749,13 +1754,17 @@ __global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_consta
       tc_fence_after();
       uint32_t v[8][4];
       const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)db * 64u + 4u * (uint32_t)h;
+      const int ng = P.B.ng[bi];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) tmem_ld4(base + 8u * s, v[s]);
+      for (int s = 0; s < 4; ++s) tmem_ld4(base + 8u * s, v[s]);
+      if (ng > 1) {
+#pragma unroll
+        for (int s = 4; s < 8; ++s) tmem_ld4(base + 8u * s, v[s]);
+      }
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(d_empty + db);
-      const int ng = P.B.ng[bi];
       uint32_t w[8][4];
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
