@@ -1492,26 +1492,28 @@ static int launch_step2_fft(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, 
   return FTK_OK;
 }
 
-// ---------------------------------------------------------------- Step 2 on the tensor cores (n_gamma = n_psi = 512)
+// ---------------------------------------------------------------- Step 2 on the tensor cores (n_gamma = n_psi = 64 R)
 // The same Z as k_step2_fft (Eq. fbk3 Step 2, Form B: x(q) = Zhat'(q - ell), reading R5), by the
-// four-step split q = a + 64 b (a < 64, b < 8), r = c + 8 d (c < 8, d < 64):
-//   Z(c + 8 d) = sum_a w64^{a d} T(a, c),   T(a, c) = w512^{a c} sum_b x(a + 64 b) w8^{b c}     (w_n = e^{-2 pi i / n})
-// * T on the CUDA cores: per (slot, a) an 8-point register DFT and 7 twiddles, scaled into Z's fp16x3 range (the
+// four-step split q = a + 64 b (a < 64, b < R), r = c + R d (c < R, d < 64), n = 64 R, R = 2, 4, 8:
+//   Z(c + R d) = sum_a w64^{a d} T(a, c),   T(a, c) = w_n^{a c} sum_b x(a + 64 b) w_R^{b c}     (w_m = e^{-2 pi i / m})
+// * T on the CUDA cores: per (slot, a) an R-point register DFT and R - 1 twiddles, scaled into Z's fp16x3 range (the
 //   bound of the file header holds for every partial sum of the DFT), split into fp16 hi / lo and stored as the B
-//   operand: MN-major (N = (slot, c), K = (Re | Im, a)), canonical core matrices, one 32 KB stage per block.
+//   operand: MN-major (N = (slot, c), K = (Re | Im, a)), canonical core matrices, one stage per block.
 // * The DFT-64 over a as ONE GEMM D[(d, Re|Im)][(slot, c)] = F64 . T, F64 = the real 128 x 128 form of
 //   [w64^{a d}] (rows m = 2 d + Re|Im, columns k = Re|Im * 64 + a) as fp16 hi / lo, resident in TMEM as the A
-//   operand for the whole kernel: 3 x 8 tcgen05.mma M128 N64 K16 per block (fp16x3).
-// * Epilogue straight from TMEM: lane (d, Re) writes the hi words, lane (d, Im) the lo words of rows 8 d + c of
-//   the Step-3 operand (one shuffle per two values exchanges the halves); slot s of a block is Step-3 word s
-//   (group s / 4, word s % 4): an ell > 0 term (Re Z, Im Z), or two ell = 0 terms transformed together as
-//   x_1 + i x_2 (their Z are real for real images, reading R13: Re -> low half, Im -> high half).
+//   operand for the whole kernel: 3 x 8 tcgen05.mma M128 N(8 R) K16 per block (fp16x3; N = 4 R for blocks of
+//   one word group when 4 R >= 16).
+// * Epilogue from TMEM: lane (d, Re) forms the hi words, lane (d, Im) the lo words of rows R d + c of the Step-3
+//   operand (one shuffle per two values exchanges the halves), staged 128B-swizzled in shared memory and written
+//   by one 5-D TMA store per word group.  Slot s of a block is Step-3 word s (group s / 4, word s % 4): an ell > 0
+//   term (Re Z, Im Z), or two ell = 0 terms transformed together as x_1 + i x_2 (their Z are real for real images,
+//   reading R13: Re -> low half, Im -> high half).
 // Warps: 0 TMA producer (8-term Zhat' windows, NR-deep ring), 1 MMA issuer, 2-9 builders (T -> B operand,
-// NB-deep ring), 10-17 epilogue (two TMEM accumulators).
+// NB-deep ring), 10-17 epilogue (two TMEM accumulators).  Buffers are sized for R = 8.
 constexpr int S2T_THREADS = 18 * 32;
 constexpr int S2T_NR = 3, S2T_NB = 2, S2T_NO = 2;  // rows ring, B-operand ring, output staging buffers
-constexpr uint32_t S2T_ROWS_BYTES = 512u * 8u * 8u;  // one block window: 512 rows x 8 terms, complex fp32
-constexpr uint32_t S2T_BOP_PART = 8u * 2048u;        // one part (hi or lo) of a B stage: 8 slots x 16 K-cores x 128 B
+constexpr uint32_t S2T_ROWS_BYTES = 512u * 8u * 8u;  // one block window: n <= 512 rows x 8 terms, complex fp32
+constexpr uint32_t S2T_BOP_PART = 8u * 2048u;        // one part (hi or lo) of a B stage: <= 8 N-cores x 16 K-cores x 128 B
 constexpr uint32_t S2T_BOP_BYTES = 2u * S2T_BOP_PART;
 constexpr uint32_t S2T_OUT_BYTES = 2u * 16384u;       // epilogue staging of one block: <= 2 word groups x 16 KB
 constexpr size_t S2T_SMEM = (size_t)S2T_NR * S2T_ROWS_BYTES + (size_t)S2T_NB * S2T_BOP_BYTES + S2T_NO * S2T_OUT_BYTES + 512;
@@ -1524,7 +1526,7 @@ struct S2TParams {
   const float2* bst;
   float gmax;
   const uint32_t* F;  // [128 rows][64 hi words, 64 lo words]
-  const float2* tw;   // [64 a][8 c] w512^{a c}
+  const float2* tw;   // [64 a][8] w_n^{a c}, c < R
   S2BlockTable B;
   S2TSlotTable sl;
 };
@@ -1533,24 +1535,42 @@ struct S2TMeta {  // per rows stage, written by the producer before the TMA is a
   int bi;
 };
 
-__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(taddr));
+template <int NC>
+__device__ __forceinline__ void tmem_ld_x(uint32_t taddr, uint32_t (&r)[NC]) {  // 32 lanes x NC columns
+  if constexpr (NC == 4)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+  else if constexpr (NC == 2)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
+  else
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r[0]) : "r"(taddr));
 }
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t d;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
   return d;
 }
+template <int R>
+__device__ __forceinline__ void sts_bytes(uint8_t* p, const uint32_t (&w)[R / 2]) {  // 2 R bytes
+  if constexpr (R == 8)
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  else if constexpr (R == 4)
+    *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+  else
+    *reinterpret_cast<uint32_t*>(p) = w[0];
+}
 
+template <int R>
 __global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_constant__ S2TParams P,
                                                             const __grid_constant__ CUtensorMap zmap,
                                                             const __grid_constant__ CUtensorMap omap) {
+  constexpr int n = 64 * R, NRT = n / 128, H = R / 2;  // H: c values per epilogue warp half
+  constexpr int LOGR = R == 8 ? 3 : (R == 4 ? 2 : 1);
   extern __shared__ __align__(1024) uint8_t s2traw[];
   uint8_t* rows_base = s2traw;
   uint8_t* bop_base = s2traw + S2T_NR * S2T_ROWS_BYTES;
-  uint8_t* out_base = bop_base + S2T_NB * S2T_BOP_BYTES;  // NO x (2 groups x [T 4][part 2][row group 16][128 B])
+  uint8_t* out_base = bop_base + S2T_NB * S2T_BOP_BYTES;  // NO x (2 groups x [T][part 2][row group 16][128 B])
   uint64_t* bars = reinterpret_cast<uint64_t*>(out_base + S2T_NO * S2T_OUT_BYTES);
   uint64_t* rows_full = bars;
   uint64_t* rows_empty = bars + S2T_NR;
@@ -1604,7 +1624,7 @@ __global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_consta
   tc_fence_after();
 
   if (warp == 0) {
-    // ---------------- TMA producer: the block's aligned 8-term window of the pair's 512 Zhat' rows, plus the
+    // ---------------- TMA producer: the block's aligned 8-term window of the pair's n Zhat' rows, plus the
     // item's metadata (block, Zhat' -> Z scale) for the builders
     if (lane == 0) {
       int bi = i_beg % nb, pr = i_beg / nb;
@@ -1617,9 +1637,10 @@ __global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_consta
         meta[st].zsc = zsc;
         meta[st].bi = bi;
         uint8_t* dst = rows_base + st * S2T_ROWS_BYTES;
-        mbar_arrive_expect_tx(rows_full + st, S2T_ROWS_BYTES);
-        tma_load_2d(dst, &zmap, P.B.zs[bi] & ~1, pr * 512, rows_full + st);
-        tma_load_2d(dst + S2T_ROWS_BYTES / 2, &zmap, P.B.zs[bi] & ~1, pr * 512 + 256, rows_full + st);
+        mbar_arrive_expect_tx(rows_full + st, (uint32_t)n * 64u);
+#pragma unroll
+        for (int r0 = 0; r0 < n; r0 += 256)
+          tma_load_2d(dst + r0 * 64, &zmap, P.B.zs[bi] & ~1, pr * n + r0, rows_full + st);
         if (++bi == nb) {
           bi = 0;
           ++pr;
@@ -1630,12 +1651,13 @@ __global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_consta
   } else if (warp == 1) {
     // ---------------- MMA issuer: D[db] = F64 . T (fp16x3: Fhi Thi + Fhi Tlo + Flo Thi), 8 k-steps
     if (lane == 0) {
-      // B MN-major; blocks of one word group (slots 0-3) run N = 32
-      const uint32_t idesc64 = idesc_f16_f32(128, 64) | (1u << 16), idesc32 = idesc_f16_f32(128, 32) | (1u << 16);
+      // B MN-major; blocks of one word group (slots 0-3) run N = 4 R where that is a valid MMA width
+      constexpr int NF = 8 * R, NH = 4 * R >= 16 ? 4 * R : 8 * R;
+      const uint32_t idescF = idesc_f16_f32(128, NF) | (1u << 16), idescH = idesc_f16_f32(128, NH) | (1u << 16);
       int bi = i_beg % nb;
       for (int k = 0; k < nit; ++k) {
         const int sb = k % S2T_NB, db = k & 1;
-        const uint32_t idesc = P.B.ng[bi] > 1 ? idesc64 : idesc32;
+        const uint32_t idesc = P.B.ng[bi] > 1 ? idescF : idescH;
         if (++bi == nb) bi = 0;
         mbar_wait(bop_full + sb, (k / S2T_NB) & 1);
         mbar_wait(d_empty + db, ((k >> 1) & 1) ^ 1);
@@ -1656,38 +1678,44 @@ __global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_consta
     }
     __syncwarp();
   } else if (warp <= 9) {
-    // ---------------- builders: thread (a, slots s0 and s0 + 4) -> T(a, c), c < 8, as B-operand rows
+    // ---------------- builders: thread (a, slots 2 s0 and 2 s0 + 1) -> T(a, c), c < R, as B-operand rows
     const int bt = threadIdx.x - 64;
     const int a = bt & 63, s0 = bt >> 6;  // warp-uniform slot pair
-    float2 tw[8];
+    float2 tw[R];
 #pragma unroll
-    for (int c = 1; c < 8; ++c) tw[c] = __ldg(P.tw + a * 8 + c);
-    auto rv = [](int i) { return ((i & 1) << 2) | (i & 2) | ((i >> 2) & 1); };
+    for (int c = 1; c < R; ++c) tw[c] = __ldg(P.tw + a * 8 + c);
+    auto rv = [](int i) {
+      int r = 0;
+#pragma unroll
+      for (int bb = 0; bb < LOGR; ++bb) r |= ((i >> bb) & 1) << (LOGR - 1 - bb);
+      return r;
+    };
     const int swa = (a >> 1) & 3;  // the row swizzle term of rows a + 64 b (independent of b)
     for (int k = 0; k < nit; ++k) {
       const int st = k % S2T_NR, sb = k % S2T_NB;
       mbar_wait(rows_full + st, (k / S2T_NR) & 1);
       const float zsc = meta[st].zsc;
       const int bi = meta[st].bi;
+      const bool half = P.B.ng[bi] == 1 && 4 * R >= 16;  // N = 4 R block: slots 4-7 are not read
       uint32_t info[2];
-      info[0] = P.sl.info[bi][s0];
-      info[1] = P.sl.info[bi][s0 + 4];
+      info[0] = P.sl.info[bi][2 * s0];
+      info[1] = P.sl.info[bi][2 * s0 + 1];
       const float2* rows = reinterpret_cast<const float2*>(rows_base + st * S2T_ROWS_BYTES);
-      float2 x[2][8];
+      float2 x[2][R];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int kind = info[u] & 3, e1 = (info[u] >> 4) & 15, e2 = (info[u] >> 8) & 15, el = (int)(info[u] >> 16);
         if (kind == 1) {
-          // complex index of (row q0 + 64 b mod 512, column e1): ((q0 + 64 b) * 8 + swizzled column) mod 4096
-          const int q0 = (a - el) & 511;
+          // complex index of (row q0 + 64 b mod n, column e1): ((q0 + 64 b) * 8 + swizzled column) mod 8 n
+          const int q0 = (a - el) & (n - 1);
           const int base = q0 * 8 + ((((e1 >> 1) ^ (q0 >> 1)) & 3) << 1) + (e1 & 1);
 #pragma unroll
-          for (int b = 0; b < 8; ++b) x[u][b] = rows[(base + 512 * b) & 4095];
+          for (int b = 0; b < R; ++b) x[u][b] = rows[(base + 512 * b) & (8 * n - 1)];
         } else if (kind == 2) {
           const int c1 = a * 8 + ((((e1 >> 1) ^ swa) & 3) << 1) + (e1 & 1);
           const int c2 = a * 8 + ((((e2 >> 1) ^ swa) & 3) << 1) + (e2 & 1);
 #pragma unroll
-          for (int b = 0; b < 8; ++b) {
+          for (int b = 0; b < R; ++b) {
             const float2 r1 = e1 < 15 ? rows[c1 + 512 * b] : make_float2(0.f, 0.f);
             const float2 r2 = e2 < 15 ? rows[c2 + 512 * b] : make_float2(0.f, 0.f);
             x[u][b] = make_float2(r1.x - r2.y, r1.y + r2.x);  // x_1 + i x_2
@@ -1697,113 +1725,115 @@ __global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_consta
       __syncwarp();
       if (lane == 0) mbar_arrive(rows_empty + st);
       // the pair's Zhat' -> Z scale folded into the twiddles
-      float2 tz[8];
+      float2 tz[R];
       tz[0] = make_float2(zsc, zsc);
 #pragma unroll
-      for (int c = 1; c < 8; ++c) tz[c] = mul2(make_float2(zsc, zsc), tw[c]);
+      for (int c = 1; c < R; ++c) tz[c] = mul2(make_float2(zsc, zsc), tw[c]);
       mbar_wait(bop_empty + sb, ((k / S2T_NB) & 1) ^ 1);
       uint8_t* bop = bop_base + sb * S2T_BOP_BYTES;
+      if (!(half && s0 >= 2)) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const uint32_t off = (uint32_t)(s0 + 4 * u) * 2048u + (uint32_t)a * 16u;
-        uint4 hr, lr, hi_, li_;
-        if (u == 1 && P.B.ng[bi] == 1) continue;  // N = 32 block: slots 4-7 are not read
-        if ((info[u] & 3) == 0 || (P.dbg & 1)) {  // no term: a zero column block (the word stays zero)
-          hr = lr = hi_ = li_ = make_uint4(0u, 0u, 0u, 0u);
-        } else {
-          dft_regs<8>(x[u]);  // natural order in x[rv(c)]
-          float2 T[8];
-          T[0] = mul2(tz[0], x[u][rv(0)]);
+        for (int u = 0; u < 2; ++u) {
+          // MN-major core (n / 8, k / 8), row k % 8, element n % 8; N index = slot R + c, K = a (Re), 64 + a (Im)
+          const int nn = (2 * s0 + u) * R;
+          const uint32_t off = (uint32_t)(nn >> 3) * 2048u + (uint32_t)a * 16u + (uint32_t)(nn & 7) * 2u;
+          uint32_t hr[H], lr[H], hi_[H], li_[H];
+          if ((info[u] & 3) == 0 || (P.dbg & 1)) {  // no term: a zero column block (the word stays zero)
 #pragma unroll
-          for (int c = 1; c < 8; ++c) T[c] = cmulf(x[u][rv(c)], tz[c]);
-          split2_f16(T[0].x, T[1].x, hr.x, lr.x);
-          split2_f16(T[2].x, T[3].x, hr.y, lr.y);
-          split2_f16(T[4].x, T[5].x, hr.z, lr.z);
-          split2_f16(T[6].x, T[7].x, hr.w, lr.w);
-          split2_f16(T[0].y, T[1].y, hi_.x, li_.x);
-          split2_f16(T[2].y, T[3].y, hi_.y, li_.y);
-          split2_f16(T[4].y, T[5].y, hi_.z, li_.z);
-          split2_f16(T[6].y, T[7].y, hi_.w, li_.w);
+            for (int j = 0; j < H; ++j) hr[j] = lr[j] = hi_[j] = li_[j] = 0u;
+          } else {
+            dft_regs<R>(x[u]);  // natural order in x[rv(c)]
+            float2 T[R];
+            T[0] = mul2(tz[0], x[u][rv(0)]);
+#pragma unroll
+            for (int c = 1; c < R; ++c) T[c] = cmulf(x[u][rv(c)], tz[c]);
+#pragma unroll
+            for (int j = 0; j < H; ++j) {
+              split2_f16(T[2 * j].x, T[2 * j + 1].x, hr[j], lr[j]);
+              split2_f16(T[2 * j].y, T[2 * j + 1].y, hi_[j], li_[j]);
+            }
+          }
+          sts_bytes<R>(bop + off, hr);
+          sts_bytes<R>(bop + off + 1024u, hi_);
+          sts_bytes<R>(bop + S2T_BOP_PART + off, lr);
+          sts_bytes<R>(bop + S2T_BOP_PART + off + 1024u, li_);
         }
-        // MN-major core (n / 8 = slot, k / 8), row k % 8, element n % 8 = c; K = a (Re), 64 + a (Im)
-        *reinterpret_cast<uint4*>(bop + off) = hr;
-        *reinterpret_cast<uint4*>(bop + off + 1024u) = hi_;
-        *reinterpret_cast<uint4*>(bop + S2T_BOP_PART + off) = lr;
-        *reinterpret_cast<uint4*>(bop + S2T_BOP_PART + off + 1024u) = li_;
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(bop_full + sb);
     }
   } else {
-    // ---------------- epilogue: lane quarter q, columns c in [4h, 4h + 4) of every slot
+    // ---------------- epilogue: lane quarter q, columns c in [H h, H h + H) of every slot
     const int ew = warp - 10, q = warp & 3, h = ew >> 2;
     const int ri = lane & 1;  // 0: the Re row of this d (writes hi words), 1: the Im row (lo words)
+    const int dd = q * 16 + (lane >> 1);
     // word (c) = (Re, Im) halves: Re lane keeps its hi halves and receives the Im lane's hi halves; the Im
     // lane keeps its lo halves and receives the Re lane's lo halves
     const uint32_t sel0 = ri ? 0x1054u : 0x5410u, sel1 = ri ? 0x3276u : 0x7632u;
-    // staging row of this lane: [T = q][part = ri][row group = lane / 2] (128 B, 128B-swizzled as the TMA store
-    // reads it: 16-byte chunk c at c ^ (row group & 7))
-    const uint32_t srow = (uint32_t)(((q * 2 + ri) * 16 + (lane >> 1)) * 128);
-    const int swz = (lane >> 1) & 7;
     const bool issuer = (warp == 10 && lane == 0);
     int bi = i_beg % nb, pr = i_beg / nb;
     for (int k = 0; k < nit; ++k) {
       const int db = k & 1;
       mbar_wait(d_full + db, (k >> 1) & 1);
       tc_fence_after();
-      uint32_t v[8][4];
-      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)db * 64u + 4u * (uint32_t)h;
+      uint32_t v[8][H];
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)db * 64u + (uint32_t)(H * h);
       const int ng = P.B.ng[bi];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) tmem_ld4(base + 8u * s, v[s]);
+      for (int s = 0; s < 4; ++s) tmem_ld_x<H>(base + (uint32_t)(R * s), v[s]);
       if (ng > 1) {
 #pragma unroll
-        for (int s = 4; s < 8; ++s) tmem_ld4(base + 8u * s, v[s]);
+        for (int s = 4; s < 8; ++s) tmem_ld_x<H>(base + (uint32_t)(R * s), v[s]);
       }
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(d_empty + db);
-      uint32_t w[8][4];
+      uint32_t w[8][H];
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
-        uint32_t h01, l01, h23, l23;
-        split2_f16(__uint_as_float(v[s][0]), __uint_as_float(v[s][1]), h01, l01);
-        split2_f16(__uint_as_float(v[s][2]), __uint_as_float(v[s][3]), h23, l23);
-        const uint32_t k01 = ri ? l01 : h01, k23 = ri ? l23 : h23;
-        const uint32_t r01 = __shfl_xor_sync(0xffffffffu, ri ? h01 : l01, 1);
-        const uint32_t r23 = __shfl_xor_sync(0xffffffffu, ri ? h23 : l23, 1);
-        w[s][0] = prmt(k01, r01, sel0);
-        w[s][1] = prmt(k01, r01, sel1);
-        w[s][2] = prmt(k23, r23, sel0);
-        w[s][3] = prmt(k23, r23, sel1);
+#pragma unroll
+        for (int j = 0; j < H; j += 2) {
+          uint32_t hh, ll;
+          split2_f16(__uint_as_float(v[s][j]), H > 1 ? __uint_as_float(v[s][H > 1 ? j + 1 : j]) : 0.f, hh, ll);
+          const uint32_t kk = ri ? ll : hh;
+          const uint32_t rr = __shfl_xor_sync(0xffffffffu, ri ? hh : ll, 1);
+          w[s][j] = prmt(kk, rr, sel0);
+          if constexpr (H > 1) w[s][j + 1] = prmt(kk, rr, sel1);
+        }
       }
       if (P.sl.needmask[bi]) {
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
           const uint32_t m = P.sl.mask[bi][s];
 #pragma unroll
-          for (int ci = 0; ci < 4; ++ci) w[s][ci] &= m;
+          for (int ci = 0; ci < H; ++ci) w[s][ci] &= m;
         }
       }
       // the staging buffer of item k - NO must have been read by its TMA store
       if (issuer) bulk_wait_group_read<S2T_NO - 1>();
       named_bar(1, 256);
-      uint8_t* stg = out_base + (k % S2T_NO) * S2T_OUT_BYTES + srow;
+      uint8_t* stg = out_base + (k % S2T_NO) * S2T_OUT_BYTES;
 #pragma unroll
       for (int grp = 0; grp < 2; ++grp) {
         if (grp >= ng) break;
 #pragma unroll
-        for (int ci = 0; ci < 4; ++ci)
-          *reinterpret_cast<uint4*>(stg + grp * 16384 + (((4 * h + ci) ^ swz) << 4)) =
+        for (int ci = 0; ci < H; ++ci) {
+          // row r = R d + c of the pair's n rows: r-tile r / 128, row group (r / 8) % 16, row r % 8; staging
+          // [T][part][row group][128 B] with the 16-byte chunk index XOR (row group & 7) (TMA 128B swizzle)
+          const int r = R * dd + H * h + ci, rg = (r >> 3) & 15;
+          *reinterpret_cast<uint4*>(stg + grp * 16384 + ((((r >> 7) * 2 + ri) * 16 + rg) << 7) +
+                                    (((r & 7) ^ (rg & 7)) << 4)) =
               make_uint4(w[4 * grp][ci], w[4 * grp + 1][ci], w[4 * grp + 2][ci], w[4 * grp + 3][ci]);
+        }
       }
       fence_proxy_async_smem();
       named_bar(1, 256);
       if (issuer && !(P.dbg & 2)) {
         for (int grp = 0; grp < ng; ++grp)
-          tma_store_5d(&omap, out_base + (k % S2T_NO) * S2T_OUT_BYTES + grp * 16384, 0, P.B.g0[bi] + grp, 0, 0, pr * 4);
+          tma_store_5d(&omap, out_base + (k % S2T_NO) * S2T_OUT_BYTES + grp * 16384, 0, P.B.g0[bi] + grp, 0, 0,
+                       pr * NRT);
         bulk_commit_group();
       }
       if (++bi == nb) {
@@ -1836,7 +1866,7 @@ static int launch_step2_tc(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, i
   prm.F = tc.d_s2F;
   prm.tw = tc.d_s2w;
   {
-    const char* dg = std::getenv("FTK_S2TC_DBG");  // (timing experiments: 1 skips the builders' arithmetic, 2 the epilogue's)
+    const char* dg = std::getenv("FTK_S2TC_DBG");  // (timing experiments: 1 skips the builders' arithmetic, 2 the stores)
     prm.dbg = dg ? std::atoi(dg) : 0;
   }
   std::memcpy(&prm.B, &tc.s2_blocks, sizeof prm.B);
@@ -1844,17 +1874,18 @@ static int launch_step2_tc(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, i
   alignas(64) CUtensorMap zmap;
   std::memset(&zmap, 0, sizeof zmap);
   if (make_zmap(&zmap, Zhat, npair, P) != FTK_OK) return FTK_ECUDA;
+  const int NRT = P.n_psi / 128;
   // Step-3 operand as a 5-D tensor of 32-bit words: (word in a 128-byte core row group, word group, row group
-  // of the r-tile, part, pair x r-tile); one 16 KB box per (item, word group), 128-byte swizzle
+  // of the r-tile, part, pair x r-tile); one (NRT x 4 KB) box per (item, word group), 128-byte swizzle
   alignas(64) CUtensorMap omap;
   std::memset(&omap, 0, sizeof omap);
   {
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) return FTK_ECUDA;
     const cuuint64_t NWG = (cuuint64_t)(P.K3p / 8);
-    const cuuint64_t dims[5] = {32, NWG, 16, 2, (cuuint64_t)npair * 4};
+    const cuuint64_t dims[5] = {32, NWG, 16, 2, (cuuint64_t)npair * NRT};
     const cuuint64_t strides[4] = {128, NWG * 128, NWG * 2048, NWG * 4096};
-    const cuuint32_t box[5] = {32, 1, 16, 2, 4};
+    const cuuint32_t box[5] = {32, 1, 16, 2, (cuuint32_t)NRT};
     const cuuint32_t es[5] = {1, 1, 1, 1, 1};
     if (enc(&omap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, Zop, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
@@ -1863,7 +1894,11 @@ static int launch_step2_tc(const TcPlan& tc, const float2* Zhat, uint8_t* Zop, i
   }
   const int items = tc.s2_blocks.nb * npair;
   const int grid = items < tc.num_sms ? items : tc.num_sms;
-  k_step2_tc<<<grid, S2T_THREADS, S2T_SMEM, s>>>(prm, zmap, omap);
+  switch (P.n_psi) {
+    case 128: k_step2_tc<2><<<grid, S2T_THREADS, S2T_SMEM, s>>>(prm, zmap, omap); break;
+    case 256: k_step2_tc<4><<<grid, S2T_THREADS, S2T_SMEM, s>>>(prm, zmap, omap); break;
+    default: k_step2_tc<8><<<grid, S2T_THREADS, S2T_SMEM, s>>>(prm, zmap, omap); break;
+  }
   return FTK_OK;
 }
 
@@ -2281,11 +2316,13 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, co
       cudaMemcpyToSymbol(c_w32, w32, sizeof w32);  // (per device: plan creation runs on the plan's device)
     }
     const int sm2 = (int)step2_smem(pm.n_psi, n_gamma);
-    // k_step2_tc tables (n_gamma = n_psi = 512): F64 real form, radix-8 twiddles, per-block word slots
+    // k_step2_tc tables (n_gamma = n_psi = 64 R, R = 2, 4, 8): F64 real form, radix-R twiddles, per-block word slots
     tc.s2tc = 0;
-    if (pm.n_psi == 512 && n_gamma == 512) {
+    if ((pm.n_psi == 128 || pm.n_psi == 256 || pm.n_psi == 512) && n_gamma == pm.n_psi) {
       const char* e2 = std::getenv("FTK_S2TC");
-      const int want = e2 ? std::atoi(e2) : 1;  // default on; FTK_S2TC=0 selects k_step2_fft
+      // default: on at n = 512 (c5: Step 2 -23 %), off below (at n = 256 / 128 the N = 32 / 16 MMAs leave it slower
+      // than k_step2_fft: c3 Step 2 41.7 vs 37.4 ms); FTK_S2TC=1 forces it on, FTK_S2TC=0 off
+      const int want = e2 ? std::atoi(e2) : (pm.n_psi == 512 ? 1 : 0);
       std::memset(&tc.s2t, 0, sizeof tc.s2t);
       for (int bi = 0; bi < tc.s2_blocks.nb; ++bi) {
         int kind[8] = {0}, e1[8], e2[8], el[8] = {0};
@@ -2337,9 +2374,10 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, co
         }
       }
       std::vector<float2> w8((size_t)64 * 8);
+      const int nn = pm.n_psi;
       for (int a = 0; a < 64; ++a)
         for (int c = 0; c < 8; ++c) {
-          const double ph = -2.0 * M_PI * (double)((a * c) % 512) / 512.0;
+          const double ph = -2.0 * M_PI * (double)((a * c) % nn) / (double)nn;
           w8[(size_t)a * 8 + c] = make_float2((float)std::cos(ph), (float)std::sin(ph));
         }
       if (cudaMalloc(&tc.d_s2F, F.size() * 4) != cudaSuccess || cudaMalloc(&tc.d_s2w, w8.size() * 8) != cudaSuccess) {
@@ -2348,7 +2386,9 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, co
       }
       cudaMemcpy(tc.d_s2F, F.data(), F.size() * 4, cudaMemcpyHostToDevice);
       cudaMemcpy(tc.d_s2w, w8.data(), w8.size() * 8, cudaMemcpyHostToDevice);
-      FTK_SMEM_OPTIN(k_step2_tc);
+      FTK_SMEM_OPTIN(k_step2_tc<2>);
+      FTK_SMEM_OPTIN(k_step2_tc<4>);
+      FTK_SMEM_OPTIN(k_step2_tc<8>);
       tc.s2tc = want != 0 ? 1 : 0;
     }
     FTK_SMEM_OPTIN((k_step2_fft<2>));

@@ -32,12 +32,12 @@ def run(cfg, ni, nj, s2tc):
     return pb, dt, L
 
 
-cfg = synth.config("c5")
-for ni, nj in [(4, 3), (140, 12), (600, 40)]:
+for name, ni, nj in [("c5", 4, 3), ("c5", 140, 12), ("c5", 600, 40), ("c3", 300, 20), ("c4", 130, 9), ("c2", 200, 30)]:
+    cfg = synth.config(name)
     a, ta, La = run(cfg, ni, nj, False)
     b, tb, Lb = run(cfg, ni, nj, True)
     dv = np.abs(a["value"] - b["value"]).max() / np.abs(a["value"]).max()
     same = np.mean((a["shift_idx"] == b["shift_idx"]) & (a["rot_idx"] == b["rot_idx"]))
     dl = np.abs(La - Lb).max() / np.abs(La).max()
-    print(f"c5 {ni}x{nj}: pair max |dv|/max|v| = {dv:.2e}, argmax agreement {same:.4f}, landscapes "
+    print(f"{name} {ni}x{nj}: pair max |dv|/max|v| = {dv:.2e}, argmax agreement {same:.4f}, landscapes "
           f"max |dL|/max|L| = {dl:.2e}; time fft {ta*1e3:.1f} ms tc {tb*1e3:.1f} ms", flush=True)

@@ -368,6 +368,43 @@ def test_poisoned_onchip_state_and_workspace(pkg, name, ni, nj, ws):
             assert np.array_equal(x, y)
 
 
+@pytest.mark.parametrize("name,ni,nj", [("c2", 140, 6), ("c3", 140, 5), ("c4", 130, 4), ("c5", 130, 3)])
+def test_step2_tensor_core_all_sizes(pkg, name, ni, nj):
+    """k_step2_tc (the DFT-64 GEMM form of Step 2) at every n it supports -- n = 128, 256 (forced with
+    FTK_S2TC=1; the default there is k_step2_fft) and 512 (its default) -- against the oracle: 12 sampled
+    landscapes through ftk_landscape_pairs at the engine's precision bar, and every pair's maximum and
+    (shift, rotation) through ftk_align (gap rule R25), with 2-image-tile subsets."""
+    cfg = synth.config(name)
+    os.environ["FTK_S2TC"] = "1"
+    try:
+        p, w, imgs, tpls = load_gpu(pkg, cfg, ni, nj)
+    finally:
+        os.environ.pop("FTK_S2TC", None)
+    rng = np.random.default_rng(11)
+    ii, jj = rng.integers(0, ni, 12), rng.integers(0, nj, 12)
+    L = p.landscape_pairs(ii, jj).cpu().numpy()
+    pb = pkg.best_to_numpy(p.align(pair_best=True)["pair_best"].reshape(-1, 4)).reshape(ni, nj)
+    a = fb.fb_coeffs(imgs.cpu().numpy().astype(np.complex128))
+    b = fb.fb_coeffs(tpls.cpu().numpy().astype(np.complex128))
+    na, nb = fb.discrete_norm(imgs.cpu().numpy(), w), fb.discrete_norm(tpls.cpu().numpy(), w)
+    plan = oracle_plan(cfg)
+    for k in range(12):
+        X = np.real(ftk.ftk_landscapes(a[ii[k]:ii[k] + 1], b[jj[k]:jj[k] + 1], plan))[0, 0]
+        assert np.max(np.abs(L[k] - X)) / (na[ii[k]] * nb[jj[k]]) <= PREC, (name, k)
+    for i in rng.integers(0, ni, 6):
+        X = np.real(ftk.ftk_landscapes(a[i:i + 1], b, plan))[0]
+        for j in range(nj):
+            scale = na[i] * nb[j]
+            v = X[j].max()
+            assert abs(pb["value"][i, j] - v) <= PREC * scale, (name, i, j)
+            t, r = pb["shift_idx"][i, j], pb["rot_idx"][i, j]
+            flat = np.sort(X[j].ravel())
+            if flat[-1] - flat[-2] > 2 * TOL * scale:
+                assert (t, r) == np.unravel_index(np.argmax(X[j]), X[j].shape), (name, i, j)
+            else:
+                assert X[j][t, r] >= v - TOL * scale, (name, i, j)
+
+
 def test_fp16x3_extreme_and_mixed_scales(pkg):
     """The fp16x3 arithmetic relies on per-item power-of-two scales.  Images and
     templates spanning 36 decades (1e-18 .. 1e18), an all-zero image and an all-zero template must keep the
