@@ -1,4 +1,5 @@
 #!/usr/bin/env bash
+# ncu --set full of one k_step1_tc launch at c5 shapes (2048 x 64 reduced job).  Usage: scripts/prof_s1.sh TAG
 set -u
 TAG=${1:-r2q}
 OUT=gpurun_out

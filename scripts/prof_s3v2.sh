@@ -1,4 +1,5 @@
 #!/usr/bin/env bash
+# A/B of the CTA-pair Step-3 kernel (FTK_S3V2=1) against k_step3_tc at c5 shapes, after scripts/s23_check.py.  Usage: scripts/prof_s3v2.sh TAG
 set -u
 TAG=${1:-r2r}
 OUT=gpurun_out
