@@ -72,6 +72,8 @@ struct TcPlan {
   // FTK_POISON=<byte> (tests, an initcheck / racecheck stand-in): before every pair block the workspace, and before
   // every Steps 1-3 launch the shared memory and TMEM of every SM, are filled with this byte (-1: off)
   int poison = -1;
+  // FTK_ONLY_STEP=1|2|3 (power / clock experiments only; results are garbage): run just that step's kernel
+  int only_step = 0;
   // Step-3 epilogue of the next tc_run_block calls: marg == nullptr -> max / argmax (MODE 0); else the
   // marginalization epilogue (MODE 1) writes log sum exp(X / tau) per pair to marg[i][j], marg_scale =
   // log2(e) / tau
