@@ -73,8 +73,9 @@ typedef struct {
   int rank, world;      /* template shard of this process; world <= 0 is treated as 1 */
   int engine;           /* 0 = tcgen05 fp16x3 tensor-core path (default; each operand scaled by a power of two
                            and split into two fp16 halves, three products, fp32 accumulation: measured
-                           |dX| <= 6.2e-7 ||A|| ||B|| against the float64 oracle),
-                           1 = SIMT fp32 reference kernels.
+                           |dX| <= 6.2e-7 ||A|| ||B|| against the float64 oracle; Step 2 at
+                           n_gamma = n_psi = 512 as a radix-8 register stage plus a DFT-64 fp16x3 GEMM, else a
+                           shared-memory FFT), 1 = SIMT fp32 reference kernels.
                            Engine 0 needs n_k a multiple of 16 (<= 128), n_psi a multiple of 64 and a Step-3
                            width K3p <= 224 (K3 = 2 H_plus - H0 plus block padding; plain configs <= 128, wide
                            CTF plans up to 224), else ftk_plan_create returns FTK_EINVAL (use engine 1) */
@@ -224,7 +225,7 @@ ftk_status_t ftk_align_marginal(ftk_plan_t plan, double tau, float* log_marginal
  * for the pairs (img_idx[k], tpl_idx[k]).  img_idx / tpl_idx: int32 [n_pairs], host or device
  * (template index LOCAL to this rank); out: device float [n_pairs][N_t][n_gamma], out_capacity = its
  * element count (FTK_ECAPACITY if < n_pairs * N_t * n_gamma).  Engine 0 runs the production kernels
- * (k_step1_tc over the pair's 128-image tile, k_step2_fft, k_step3_tc with landscape output).  Errors:
+ * (k_step1_tc over the pair's 128-image tile, the plan's Step-2 kernel, k_step3_tc with landscape output).  Errors:
  * FTK_EINVAL (null pointer, n_pairs <= 0, an index out of range), FTK_ESTATE, FTK_ECAPACITY, FTK_ECUDA.
  * Synchronizes `stream` once (index validation); the kernels are asynchronous on it. */
 ftk_status_t ftk_landscape_pairs(ftk_plan_t plan, const int32_t* img_idx, const int32_t* tpl_idx, int n_pairs,
