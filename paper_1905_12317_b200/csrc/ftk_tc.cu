@@ -841,8 +841,9 @@ __host__ __device__ __forceinline__ int s1_chunk_of(int i, int nkch) {
 }
 
 
+constexpr int S1_MAXST = 8;  // stage barriers (CTA pair: 8 half-size stages)
 struct S1Smem {
-  uint64_t st_full[S1_STAGES], st_empty[S1_STAGES];
+  uint64_t st_full[S1_MAXST], st_empty[S1_MAXST];
   uint64_t a_full[2], a_empty[2];  // per generation round (see s1_rounds)
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
@@ -850,7 +851,7 @@ struct S1Smem {
 
 struct S1MmaArgs {
   uint32_t tmem, sbase, stage_bytes, part_bytes, SBO;
-  int KCH, NKCH, nk, units, nit;
+  int KCH, NKCH, nk, units, nit, ubeg, ustep;
   S1Smem* S;
 };
 
@@ -858,11 +859,26 @@ struct S1MmaArgs {
 // per stage KS = KCH / 16 k-steps x 3 fp16 products (compile-time unrolled: a runtime loop around
 // tcgen05.mma costs ~500 cycles per stage, scripts/micro_s3.cu).  tr: total, A-wait, acc-wait, stage-wait.
 // NK = NKCH at compile time (1, 2, 4; 0 = runtime): the k-chunk loop is then unrolled, which avoids the
-// per-iteration cost of a runtime loop around tcgen05.mma (see the Step-3 note in DESIGN.md)
-template <int KS, int NK>
+// per-iteration cost of a runtime loop around tcgen05.mma (see the Step-3 note in DESIGN.md).
+// CG2: the CTA pair's MMAs (M = 256: this CTA's 128 generated rows and the peer's; each CTA holds half of the
+// 128-image stage), issued by the even CTA, committed to both CTAs' barriers.
+template <int KS, int NK, bool CG2>
 __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&tr)[4]) {
+  constexpr int NST = CG2 ? 8 : S1_STAGES;
   S1Smem& S = *a.S;
-  const uint32_t idesc = idesc_f16_f32(128, 128);
+  const uint32_t idesc = idesc_f16_f32(CG2 ? 256 : 128, 128);
+  auto mma = [&](uint32_t d, uint32_t at, uint64_t bd, uint32_t acc) {
+    if constexpr (CG2)
+      mma_f16_ts_cg2(d, at, bd, idesc, acc);
+    else
+      mma_f16_ts(d, at, bd, idesc, acc);
+  };
+  auto commit = [&](uint64_t* bar) {
+    if constexpr (CG2)
+      tc_commit_cg2(bar);
+    else
+      tc_commit(bar);
+  };
   uint32_t g_st = 0, g_acc = 0, g_u = 0;
   const long long tr0 = diag_clock();
   // generation rounds: R = 2 when the K' chunks split by radial halves (NKCH % 4 == 0): round r fills the
@@ -871,7 +887,7 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
   const int R = (nkch % 4 == 0) ? 2 : 1;
   const int hq = nkch / 2, qq = nkch / 4;
   auto round_of = [&](int kc) { return R == 2 ? ((kc % hq) >= qq ? 1 : 0) : 0; };
-  for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++g_u) {
+  for (int u = a.ubeg; u < a.units; u += a.ustep, ++g_u) {
     bool got0 = false, got1 = false;
     for (int t = 0; t < a.nit; ++t, ++g_acc) {
       const int ab = g_acc & 1;
@@ -882,7 +898,7 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
       const uint32_t d = a.tmem + 256 + (uint32_t)(ab * 128);
       auto chunk = [&](const int i) {  // i: processing index, kc: the K' chunk
         const int kc = s1_chunk_of(i, nkch);
-        const int s = g_st % S1_STAGES;
+        const int s = g_st % NST;
           const int rr = round_of(kc);
           if (rr == 0 ? !got0 : !got1) {  // the generated operand chunk of this round (first tile of a unit)
             t1 = diag_clock();
@@ -892,7 +908,7 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
             if (rr == 0) got0 = true; else got1 = true;
           }
           t1 = diag_clock();
-          mbar_wait(&S.st_full[s], (g_st / S1_STAGES) & 1);
+          mbar_wait(&S.st_full[s], (g_st / NST) & 1);
           tr[3] += diag_clock() - t1;
           tc_fence_after();
           const uint32_t st = a.sbase + s * a.stage_bytes;
@@ -904,14 +920,14 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
             const uint32_t a_hi = a_hi0 + (uint32_t)(ks * 8);
             const uint32_t a_lo = a_hi + (uint32_t)a.nk;
             const uint32_t acc = (i > 0 || ks > 0) ? 1u : 0u;
-            mma_f16_ts(d, a_hi, bh0 + (uint64_t)(ks * 16), idesc, acc);  // +256 B per k-step
-            mma_f16_ts(d, a_hi, bl0 + (uint64_t)(ks * 16), idesc, 1u);
-            mma_f16_ts(d, a_lo, bh0 + (uint64_t)(ks * 16), idesc, 1u);
+            mma(d, a_hi, bh0 + (uint64_t)(ks * 16), acc);  // +256 B per k-step
+            mma(d, a_hi, bl0 + (uint64_t)(ks * 16), 1u);
+            mma(d, a_lo, bh0 + (uint64_t)(ks * 16), 1u);
           }
-          tc_commit(&S.st_empty[s]);
+          commit(&S.st_empty[s]);
           // last tile: a round's chunks are free once its last stage has been read
           if (t == a.nit - 1 && (i == nkch - 1 || (R == 2 && i == hq - 1)))
-            tc_commit(&S.a_empty[R == 1 ? 0 : (i == nkch - 1 ? 1 : 0)]);
+            commit(&S.a_empty[R == 1 ? 0 : (i == nkch - 1 ? 1 : 0)]);
           ++g_st;
       };
       if constexpr (NK > 0) {
@@ -920,7 +936,7 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
       } else {
         for (int kc = 0; kc < nkch; ++kc) chunk(kc);
       }
-      tc_commit(&S.acc_full[ab]);
+      commit(&S.acc_full[ab]);
     }
   }
   tr[0] = diag_clock() - tr0;
@@ -928,54 +944,82 @@ __device__ __forceinline__ uint32_t s1_mma_loop(const S1MmaArgs& a, long long (&
 }
 
 // NKC: the k-chunk count at compile time (4: n_k = 128, the c5 shape; 0: runtime), a separate instance so
-// that the unrolled MMA loop does not change the register allocation of the other shapes
-template <int NKC>
-__global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
+// that the unrolled MMA loop does not change the register allocation of the other shapes.
+// CG2 (k_step1_cg2, opt-in FTK_S1CG2=1): a CTA pair (cluster of 2, cta_group::2) runs two adjacent column tiles
+// of one mode as one M = 256 GEMM: each CTA generates its 128 rows into its own TMEM and loads HALF of every
+// 128-image stage (64 images, 16 KB), so the image bytes each SM receives per tile halve; the even CTA issues
+// the MMAs, a relay thread of the odd CTA forwards its stage completions, and the generators / epilogues of
+// both CTAs arrive on the even CTA's barriers.
+template <int NKC, bool CG2>
+__device__ __forceinline__ void s1_body(const S1Params& P) {
+  constexpr int NST = CG2 ? 8 : S1_STAGES;
   extern __shared__ __align__(1024) uint8_t s1_raw[];
   S1Smem& S = *reinterpret_cast<S1Smem*>(s1_raw);
-  uint8_t* stages = s1_raw + 1024;                                   // S1_STAGES x stage_bytes
-  const uint32_t stage_bytes = 128u * P.KCH * 4u;                    // hi + lo
+  uint8_t* stages = s1_raw + 1024;                                   // NST x stage_bytes
+  const uint32_t stage_bytes = (CG2 ? 64u : 128u) * P.KCH * 4u;      // hi + lo (this CTA's images)
+  const uint32_t part_bytes = stage_bytes / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = P.n, nk = P.n_k;
+  const uint32_t h = CG2 ? cluster_rank() : 0u;
+  // units: (mode p, column tile ct); CTA pair: unit pairs (p, 2 ctp + h)
+  const int NCTu = CG2 ? (P.NCT + 1) / 2 : P.NCT;
+  const int units = n * NCTu;
+  const int ubeg = CG2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ustep = CG2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  auto unit_of = [&](int u, int& p, int& ct) {
+    s1_unit(u, NCTu, p, ct);
+    if constexpr (CG2) ct = 2 * ct + (int)h;
+  };
   if (threadIdx.x == 0) {
-    for (int i = 0; i < S1_STAGES; ++i) {
-      mbar_init(&S.st_full[i], 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&S.st_full[i], (CG2 && h == 0) ? 2 : 1);  // CTA pair: + the odd CTA's relayed completion
       mbar_init(&S.st_empty[i], 1);
     }
     for (int r = 0; r < 2; ++r) {
-      mbar_init(&S.a_full[r], 8);
+      mbar_init(&S.a_full[r], CG2 ? 16 : 8);
       mbar_init(&S.a_empty[r], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.acc_full[i], 1);
-      mbar_init(&S.acc_empty[i], 256);
+      mbar_init(&S.acc_empty[i], CG2 ? 16 : 256);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(&S.tmem_base);
+  if (warp == 1) {
+    if constexpr (CG2)
+      tmem_alloc_cg2<512>(&S.tmem_base);
+    else
+      tmem_alloc<512>(&S.tmem_base);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG2) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
-  const int units = n * P.NCT;
   const int it0 = P.i0 / 128;
   const int nit = (P.ni + 127) / 128;
 
   if (warp == 0) {
-    // ---------------- bulk-copy producer of image operand stages
+    // ---------------- bulk-copy producer of image operand stages (CTA pair: this CTA's 64 images of each)
     if (lane == 0) {
       uint32_t g_st = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = ubeg; u < units; u += ustep) {
         int p, ct_unused;
-        s1_unit(u, P.NCT, p, ct_unused);
+        unit_of(u, p, ct_unused);
         for (int t = 0; t < nit; ++t) {
           for (int ci = 0; ci < P.NKCH; ++ci, ++g_st) {
             const int kc = s1_chunk_of(ci, P.NKCH);
-            const int s = g_st % S1_STAGES;
-            mbar_wait(&S.st_empty[s], ((g_st / S1_STAGES) & 1) ^ 1);
-            const uint8_t* src = P.Aop + (((size_t)p * P.NIT + it0 + t) * P.NKCH + kc) * stage_bytes;
+            const int s = g_st % NST;
+            mbar_wait(&S.st_empty[s], ((g_st / NST) & 1) ^ 1);
+            const uint8_t* src = P.Aop + (((size_t)p * P.NIT + it0 + t) * P.NKCH + kc) * (size_t)(128u * P.KCH * 4u);
             mbar_arrive_expect_tx(&S.st_full[s], stage_bytes);
-            if constexpr ((kS1Hint & 2) != 0) {
+            if constexpr (CG2) {
+              // the stage's [part][16 row groups][KCH/8][128 B]: this CTA's row groups [8 h, 8 h + 8) of each part
+              for (int pt = 0; pt < 2; ++pt)
+                bulk_g2s_hint(stages + s * stage_bytes + pt * part_bytes,
+                              src + (size_t)pt * (128u * P.KCH * 2u) + (size_t)h * part_bytes, part_bytes,
+                              &S.st_full[s], l2_policy_evict_last());
+            } else if constexpr ((kS1Hint & 2) != 0) {
               bulk_g2s_hint(stages + s * stage_bytes, src, stage_bytes, &S.st_full[s], l2_policy_evict_last());
             } else {
               bulk_g2s(stages + s * stage_bytes, src, stage_bytes, &S.st_full[s]);
@@ -986,24 +1030,36 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one elected lane; the k-steps of a stage unrolled at compile time)
-    if (elect_one()) {
-      S1MmaArgs a{tmem, smem_u32(stages), stage_bytes, 128u * P.KCH * 2u, (uint32_t)(P.KCH / 8) * 128u, P.KCH,
-                  P.NKCH, nk, units, nit, &S};
-      long long tr[4] = {0, 0, 0, 0};
-      uint32_t g_u = 0;
-      if (P.KCH == 64) {
-        g_u = s1_mma_loop<4, NKC>(a, tr);
-      } else {
-        g_u = s1_mma_loop<2, 0>(a, tr);
+    if (h == 0) {
+      // ---------------- MMA issuer (one elected lane; the k-steps of a stage unrolled at compile time)
+      if (elect_one()) {
+        S1MmaArgs a{tmem, smem_u32(stages), stage_bytes, part_bytes, (uint32_t)(P.KCH / 8) * 128u, P.KCH,
+                    P.NKCH, nk, units, nit, ubeg, ustep, &S};
+        long long tr[4] = {0, 0, 0, 0};
+        uint32_t g_u = 0;
+        if (P.KCH == 64) {
+          g_u = s1_mma_loop<4, NKC, CG2>(a, tr);
+        } else {
+          g_u = s1_mma_loop<2, 0, CG2>(a, tr);
+        }
+        if (P.trace && blockIdx.x == 0) {
+          P.trace[0] = tr[0];
+          P.trace[1] = tr[1];
+          P.trace[2] = tr[2];
+          P.trace[3] = tr[3];
+          P.trace[4] = g_u;
+        }
       }
-      if (P.trace && blockIdx.x == 0) {
-        P.trace[0] = tr[0];
-        P.trace[1] = tr[1];
-        P.trace[2] = tr[2];
-        P.trace[3] = tr[3];
-        P.trace[4] = g_u;
-      }
+    } else if (CG2 && lane == 0) {
+      // ---------------- relay (odd CTA): this CTA's stage completions -> the even CTA's stage barriers
+      uint32_t g_st = 0;
+      const int per_unit = nit * P.NKCH;
+      for (int u = ubeg; u < units; u += ustep)
+        for (int i = 0; i < per_unit; ++i, ++g_st) {
+          const int s = g_st % NST;
+          mbar_wait(&S.st_full[s], (g_st / NST) & 1);
+          mbar_arrive_cluster(mapa_shared(&S.st_full[s], 0));
+        }
     }
     __syncwarp();
   } else if (warp < 10) {
@@ -1020,10 +1076,15 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
     // narrower than one 16-node STTM step; the first-half warps do all nodes)
     const int R = (P.NKCH % 4 == 0) ? 2 : 1;
     const uint64_t pol_b = (kS1Hint & 4) ? l2_policy_evict_last() : 0;
+    uint32_t a_full_cl[2] = {0u, 0u};
+    if constexpr (CG2) {
+      a_full_cl[0] = mapa_shared(&S.a_full[0], 0);
+      a_full_cl[1] = mapa_shared(&S.a_full[1], 0);
+    }
     uint32_t g_u = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++g_u) {
+    for (int u = ubeg; u < units; u += ustep, ++g_u) {
       int p, ct;
-      s1_unit(u, P.NCT, p, ct);
+      unit_of(u, p, ct);
       const int f = ct * 64 + c;
       int jl = 0, z = 0;
       if (f < P.F) {
@@ -1090,7 +1151,12 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.a_full[rnd]);
+      if (lane == 0) {
+        if constexpr (CG2)
+          mbar_arrive_cluster(a_full_cl[rnd]);
+        else
+          mbar_arrive(&S.a_full[rnd]);
+      }
       }
     }
   } else {
@@ -1104,10 +1170,15 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
     const int ew = warp - 10;  // 0..7
     const int eh = ew >> 2;    // image half of the TMEM columns this warp drains
     const bool odd = lane & 1;
+    uint32_t acc_empty_cl[2] = {0u, 0u};
+    if constexpr (CG2) {
+      acc_empty_cl[0] = mapa_shared(&S.acc_empty[0], 0);
+      acc_empty_cl[1] = mapa_shared(&S.acc_empty[1], 0);
+    }
     uint32_t g_acc = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = ubeg; u < units; u += ustep) {
       int p, ct;
-      s1_unit(u, P.NCT, p, ct);
+      unit_of(u, p, ct);
       const int f = ct * 64 + (row >> 1);  // this lane's complex column (template jl, slot z)
       const bool cval = f < P.F;           // pad slots included (zero rows)
       const int jl = cval ? f / P.Hs : 0, z = f - jl * P.Hs;
@@ -1127,7 +1198,12 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
           tmem_wait_ld();
           if (c0 + 32 == 64 * eh + 64) {  // this warp's last columns are in registers: release the buffer
             tc_fence_before();
-            mbar_arrive(&S.acc_empty[ab]);
+            if constexpr (CG2) {
+              __syncwarp();
+              if (lane == 0) mbar_arrive_cluster(acc_empty_cl[ab]);
+            } else {
+              mbar_arrive(&S.acc_empty[ab]);
+            }
           }
           const int ibase = t * 128 + c0;  // local image index of r[0]
 #pragma unroll
@@ -1145,10 +1221,23 @@ __global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG2) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    if constexpr (CG2)
+      tmem_dealloc_cg2<512>(tmem);
+    else
+      tmem_dealloc<512>(tmem);
   }
+}
+
+template <int NKC>
+__global__ void __maxnreg__(96) k_step1_tc(S1Params P) {
+  s1_body<NKC, false>(P);
+}
+template <int NKC>
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96) k_step1_cg2(S1Params P) {
+  s1_body<NKC, true>(P);
 }
 
 static size_t s1_smem_bytes(const TcPlan& tc) { return 1024 + (size_t)S1_STAGES * 128 * tc.KCH * 4; }
@@ -2284,6 +2373,12 @@ int tc_plan_init(TcPlan& tc, const PlanMath& pm, const std::vector<float>& g, co
   tc.NKCH = 2 * pm.n_k / tc.KCH;
   FTK_SMEM_OPTIN((k_step1_tc<0>));
   FTK_SMEM_OPTIN((k_step1_tc<4>));
+  FTK_SMEM_OPTIN((k_step1_cg2<0>));
+  FTK_SMEM_OPTIN((k_step1_cg2<4>));
+  {
+    const char* e1 = std::getenv("FTK_S1CG2");  // (opt-in) the CTA-pair Step 1
+    tc.s1cg2 = (e1 && std::atoi(e1) != 0) ? 1 : 0;
+  }
   // Step-2 blocks (s2_block_table); the device term order (tc_term_order, applied in ftk_capi.cu) puts
   // every block's terms in one aligned 8-term window of a Zhat' row (one TMA box)
   {
@@ -2660,7 +2755,14 @@ void launch_step1_tc(const TcPlan& tc, const float2* B, float2* Zhat, const Pair
     cudaMemsetAsync(d_trace, 0, 16 * sizeof(unsigned long long), s);
     prm.trace = d_trace;
   }
-  if (tc.KCH == 64 && tc.NKCH == 4)
+  if (tc.s1cg2) {  // CTA pairs over unit pairs (opt-in FTK_S1CG2=1)
+    const int upairs = P.n_psi * ((prm.NCT + 1) / 2);
+    const int ncl = std::max(1, std::min(upairs, tc.num_sms / 2));
+    if (tc.KCH == 64 && tc.NKCH == 4)
+      k_step1_cg2<4><<<2 * ncl, S1_THREADS, s1_smem_bytes(tc), s>>>(prm);
+    else
+      k_step1_cg2<0><<<2 * ncl, S1_THREADS, s1_smem_bytes(tc), s>>>(prm);
+  } else if (tc.KCH == 64 && tc.NKCH == 4)
     k_step1_tc<4><<<grid, S1_THREADS, s1_smem_bytes(tc), s>>>(prm);
   else
     k_step1_tc<0><<<grid, S1_THREADS, s1_smem_bytes(tc), s>>>(prm);

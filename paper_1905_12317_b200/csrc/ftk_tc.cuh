@@ -58,6 +58,7 @@ struct TcPlan {
   float2* d_s2w = nullptr;
   S2TSlotTable s2t;
   int s2tc = 0;
+  int s1cg2 = 0;  // (opt-in FTK_S1CG2=1) k_step1_cg2: CTA pairs, half of every image stage per SM
   int64_t n_tm = 0;
   // fp16x3 power-of-two operand scaling (ftk_tc.cu header): per-item maxima of the loaded images / local templates
   // (x = max |Re|, |Im| of the FB coefficients, y = their Frobenius norm), gmax = max |g_zeta(k_m)|, eY = the

@@ -1,5 +1,6 @@
-"""A/B of the tensor-core Step 2 (k_step2_tc, FTK_S2TC=1) against the CUDA-core k_step2_fft on the same inputs:
-per-pair maxima and argmax, and explicit-pair landscapes (debug script; the oracle parity is in tests/)."""
+"""A/B of a kernel option on the same inputs: per-pair maxima and argmax, and explicit-pair landscapes (debug script;
+the oracle parity is in tests/).  Default: the tensor-core Step 2 (FTK_S2TC=1) against k_step2_fft (FTK_S2TC=0);
+`python scripts/s2tc_check.py FTK_S1CG2 c5` compares FTK_S1CG2=1 against 0 on the listed configs."""
 import os
 import sys
 import time
@@ -12,8 +13,12 @@ import synth  # noqa: E402
 import paper_1905_12317_b200 as pkg  # noqa: E402
 
 
+VAR = sys.argv[1] if len(sys.argv) > 1 else "FTK_S2TC"
+ONLY = sys.argv[2].split(",") if len(sys.argv) > 2 else None
+
+
 def run(cfg, ni, nj, s2tc):
-    os.environ["FTK_S2TC"] = "1" if s2tc else "0"
+    os.environ[VAR] = "1" if s2tc else "0"
     p = pkg.FTKPlan(cfg.n, cfg.K, synth.delta_max(cfg), synth.shift_list(cfg), cfg.eps, n_k=cfg.n_k,
                     n_psi=cfg.n_psi, device=0)
     k, w = p.radial()
@@ -33,6 +38,8 @@ def run(cfg, ni, nj, s2tc):
 
 
 for name, ni, nj in [("c5", 4, 3), ("c5", 140, 12), ("c5", 600, 40), ("c3", 300, 20), ("c4", 130, 9), ("c2", 200, 30)]:
+    if ONLY and name not in ONLY:
+        continue
     cfg = synth.config(name)
     a, ta, La = run(cfg, ni, nj, False)
     b, tb, Lb = run(cfg, ni, nj, True)
