@@ -17,6 +17,11 @@ Which kernels each test runs (engine 0):
                                   bench's block) plus a ragged one; sampled pair maxima vs the oracle.
   * test_nccl_single_rank         ftk_align with a 1-rank NCCL communicator (the library's all-gather +
                                   device merge): bests equal the oracle's and, bitwise, the plain call.
+  * test_poisoned_onchip_state_and_workspace  FTK_POISON: workspace, shared memory and TMEM filled with
+                                  0x7B / 0xFF before every block / launch; results bitwise equal (the
+                                  initcheck / racecheck stand-in: compute-sanitizer is closed on the pool).
+  * test_step2_tensor_core_all_sizes  k_step2_tc<R> (the default Step 2 at n = 512) forced at c2 / c3 / c4
+                                  and at c5: sampled landscapes and every pair's max + argmax vs the oracle.
 Argmax rule (reading R25): GPU and oracle argmax must agree unless the oracle's top-2 gap is
 within 2 x the tolerance (each side may be off by one tolerance).
 Set FTK_PARITY_LOG=path to write the max |dX| / (||A|| ||B||) per config as JSON.
