@@ -181,9 +181,25 @@ def cpu_baseline(cfg, imgs_cpu, tpls_cpu, k_nodes, seconds_budget=15.0):
         thr = max((d.get("num_threads", 1) for d in threadpoolctl.threadpool_info()), default=1)
     except Exception:  # noqa: BLE001
         thr = os.cpu_count()
+    # the brute-force definition (oracle/brute.py, Eq. Xdg discretized: no Bessel / SVD / FFT) at sampled
+    # (pair, shift, rotation) points, time-bounded (the brute-force rate beside the FTK rate)
+    from oracle import brute, quadrature
+    kq, wq = quadrature.radial_rule(cfg.n_k, cfg.k_max)
+    shifts = synth.shift_list(cfg)
+    rng = np.random.default_rng(1)
+    nbf, tb0 = 0, time.perf_counter()
+    while time.perf_counter() - tb0 < 3.0:
+        i, j = int(rng.integers(0, ni)), int(rng.integers(0, nj))
+        tt, rr = rng.integers(0, n_t, 50), rng.integers(0, n_psi, 50)
+        brute.brute_points(imgs_cpu[i], tpls_cpu[j], kq, wq, shifts, tt, rr)
+        nbf += 50
+    dtb = time.perf_counter() - tb0
     return {"value": ips, "unit": "inner products/s", "cores": int(thr), "kind": "oracle",
             "sample": f"{cfg.name}: {done_pairs} (image, template) pairs x {n_t} shifts x {n_psi} rotations, "
                       f"float64 numpy oracle (FB coeffs + plan excluded), {dt:.1f} s",
+            "brute_force": {"value": nbf / dtb, "unit": "inner products/s",
+                            "sample": f"{nbf} random (pair, shift, rotation) points of the same sample, "
+                                      f"oracle/brute.py (8 n_k n_psi flop per inner product), {dtb:.1f} s"},
             "host": host_description()}
 
 
