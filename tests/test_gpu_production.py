@@ -410,6 +410,32 @@ def test_step2_tensor_core_all_sizes(pkg, name, ni, nj):
                 assert X[j][t, r] >= v - TOL * scale, (name, i, j)
 
 
+@pytest.mark.parametrize("name,ni,nj", [("c3", 260, 7), ("c5", 140, 5)])
+def test_step1_cta_pair_bitwise(pkg, name, ni, nj):
+    """The opt-in CTA-pair Step 1 (k_step1_cg2, FTK_S1CG2=1: cta_group::2 M = 256, half of every image stage per
+    SM) computes the same products in the same order as k_step1_tc: per-pair maxima, per-image bests and explicit-
+    pair landscapes must be bitwise equal to the default path (ragged image tiles, odd column-tile counts)."""
+    cfg = synth.config(name)
+    rng = np.random.default_rng(5)
+    ii, jj = rng.integers(0, ni, 6), rng.integers(0, nj, 6)
+    outs = []
+    for v in ("0", "1"):
+        os.environ["FTK_S1CG2"] = v
+        try:
+            p, w, imgs, tpls = load_gpu(pkg, cfg, ni, nj)
+        finally:
+            os.environ.pop("FTK_S1CG2", None)
+        res = p.align(pair_best=True)
+        L = p.landscape_pairs(ii, jj)
+        torch.cuda.synchronize()
+        outs.append([pkg.best_to_numpy(res["best"]).view(np.int32).copy(),
+                     pkg.best_to_numpy(res["pair_best"].reshape(-1, 4)).view(np.int32).copy(),
+                     L.cpu().numpy().view(np.int32).copy()])
+        del p
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
+
+
 def test_fp16x3_extreme_and_mixed_scales(pkg):
     """The fp16x3 arithmetic relies on per-item power-of-two scales.  Images and
     templates spanning 36 decades (1e-18 .. 1e18), an all-zero image and an all-zero template must keep the
