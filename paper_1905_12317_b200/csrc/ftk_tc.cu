@@ -2830,8 +2830,9 @@ int tc_run_block(TcPlan& tc, const PairBlock& pb, const DevPlan& P, const float2
     return FTK_EINVAL;
   }
   tc_poison(tc, ws, ws_bytes, s);
-  static int primed = 0;  // (experiment) the first block runs all steps so the workspace holds real Zhat' / Zop
-  if (tc.only_step && primed++ > 0) {  // (experiment) one step's kernel alone, on the workspace's data
+  // (experiment) the plan's first block runs all steps so the workspace holds real Zhat' / Zop; later blocks run
+  // only FTK_ONLY_STEP's kernel on that data
+  if (tc.only_step && tc.only_primed++ > 0) {
     if (prof) prof(plan, tc.only_step, 0, s);
     if (tc.only_step == 1) launch_step1_tc(tc, B, Zhat, pb, P, s);
     if (tc.only_step == 2) launch_step2(tc, Zhat, Zop, pb.count, pb, P, s);

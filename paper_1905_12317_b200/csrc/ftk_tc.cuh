@@ -75,6 +75,7 @@ struct TcPlan {
   int poison = -1;
   // FTK_ONLY_STEP=1|2|3 (power / clock experiments only; results are garbage): run just that step's kernel
   int only_step = 0;
+  int only_primed = 0;  // blocks run so far under FTK_ONLY_STEP (the first one runs every step)
   // Step-3 epilogue of the next tc_run_block calls: marg == nullptr -> max / argmax (MODE 0); else the
   // marginalization epilogue (MODE 1) writes log sum exp(X / tau) per pair to marg[i][j], marg_scale =
   // log2(e) / tau
