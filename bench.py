@@ -401,7 +401,12 @@ def main():
                              "time; tensor_issued_tflops counts the MMAs actually issued (fp16x3 = 3 products, +-delta "
                              "symmetry halves the rows, tile padding)")
             elif kern == "step1":
-                r["note"] = "achieved = algorithmic flops 8 n_psi H_plus n_k per pair (complex Step-1 GEMM) / launch time"
+                if engine == pkg.ENGINE_TC:
+                    s1_rows = ((info["H_plus"] + 1) // 2 * 2) * 2   # generated rows per template (Re/Im per slot)
+                    issued = 3.0 * 2.0 * s1_rows * 2 * cfg.n_k * cfg.n_psi * per_launch
+                    r["tensor_issued_tflops"] = issued / avg_s / 1e12 if avg_s > 0 else None
+                r["note"] = ("achieved = algorithmic flops 8 n_psi H_plus n_k per pair (complex Step-1 GEMM) / launch time; "
+                             "tensor_issued_tflops counts the fp16x3 MMAs issued (3 products, Re/Im rows of the padded slots)")
         r["frac"] = (r["achieved"] / r["peak"]) if r.get("achieved") else None
         return r
 
