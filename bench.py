@@ -414,7 +414,8 @@ def main():
     dom = max(kerns, key=lambda c: kt_acc[c][0]) if kerns else "step3"
     roofline = roof(dom)
     roofline["all_kernels"] = {k2: {f: roof(k2).get(f) for f in ("bound", "achieved", "peak", "unit", "frac",
-                                                                   "avg_launch_ms")} for k2 in kerns}
+                                                                   "avg_launch_ms", "tensor_issued_tflops")
+                                    if roof(k2).get(f) is not None} for k2 in kerns}
     launches = sum(v[1] for v in kt_acc.values())
     # whole-step tensor floor: the step's tensor work at the measured sustained bf16 (= fp16) peak, in the minimal
     # (algorithmic) and in the issued (fp16x3, padded tiles) form, against the measured step time
