@@ -1885,7 +1885,9 @@ __global__ void __launch_bounds__(S2T_THREADS, 1) k_step2_tc(const __grid_consta
 #pragma unroll
         for (int j = 0; j < H; j += 2) {
           uint32_t hh, ll;
-          split2_f16(__uint_as_float(v[s][j]), H > 1 ? __uint_as_float(v[s][H > 1 ? j + 1 : j]) : 0.f, hh, ll);
+          // values c and c + 1 packed in one f16x2 word (H = 1: one value, the high half unused)
+          const float v1 = H > 1 ? __uint_as_float(v[s][(j + 1) % H]) : 0.f;
+          split2_f16(__uint_as_float(v[s][j]), v1, hh, ll);
           const uint32_t kk = ri ? ll : hh;
           const uint32_t rr = __shfl_xor_sync(0xffffffffu, ri ? hh : ll, 1);
           w[s][j] = prmt(kk, rr, sel0);
