@@ -154,3 +154,37 @@ def test_nccl_unique_id_and_status(ftk):
     assert L.ftk_nccl_unique_id(None) == 1          # FTK_EINVAL
     h = C.c_void_p()
     assert L.ftk_nccl_comm_create(buf, 2, 5, -1, C.byref(h)) == 1   # rank >= world
+
+
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=12, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(dmax=st.floats(0.3, 3.0), eps=st.sampled_from([1e-1, 3e-2, 1e-2, 3e-3]), n_k=st.sampled_from([16, 32]),
+       seed=st.integers(0, 10_000))
+def test_host_plan_matches_oracle_random(ftk, dmax, eps, n_k, seed):
+    """Property test: for random shift radii, tolerances, radial orders and shift lists the C++
+    host plan (Nystrom + one-sided Jacobi SVD, truncation Sigma > eps, zeta relabel, G / Y) reproduces the
+    float64 oracle's terms, singular values and rank-1 factors Y_zeta G_zeta^T, and its kernel certificate
+    stays within the factorization's own error scale."""
+    n, K = 32, 16.0
+    rng = np.random.default_rng(seed)
+    r = dmax * np.sqrt(rng.uniform(0.0, 1.0, 9))
+    th = rng.uniform(0.0, 2.0 * math.pi, 9)
+    sh = np.concatenate([[[0.0, 0.0]], np.stack([r * np.cos(th), r * np.sin(th)], 1)])
+    p = ftk.FTKPlan(n, K, dmax, sh, eps, n_k=n_k, n_psi=64, device=-1)
+    op = ks.build_plan(n, K, dmax, sh, eps, n_k, 64, n_nodes=96)
+    ell, eta, sig = p.terms()
+    ref = np.array([t.sigma for t in op.terms])
+    # a singular value within 1e-9 of eps may legitimately fall on either side of the cut (reading R6)
+    if np.any(np.abs(ref - eps) < 1e-9) or p.info["H"] != len(op.terms):
+        assert abs(p.info["H"] - len(op.terms)) <= 2 and np.min(np.abs(ref - eps)) < 1e-6
+        return
+    assert list(ell) == [t.ell for t in op.terms] and list(eta) == [t.eta for t in op.terms]
+    assert np.max(np.abs(sig - ref)) < 1e-10
+    G, Y = p.factors()
+    for z in range(len(ref)):
+        P1 = np.outer(Y[:, z], G[z])
+        P2 = np.outer(op.Y[:, z], op.G[z])
+        assert np.max(np.abs(P1 - P2)) < 1e-8 * max(1.0, np.max(np.abs(P2)))
+    assert p.info["certificate"] < 13 * eps
