@@ -436,6 +436,52 @@ def test_step1_cta_pair_bitwise(pkg, name, ni, nj):
         assert np.array_equal(x, y)
 
 
+def test_random_shapes_vs_oracle(pkg):
+    """Property test over random small problems on the production engine: random radial order,
+    angular grid, shift radius, shift list (1-40 arbitrary off-lattice shifts), tolerance and image / template
+    counts (ragged 128-image tiles, single templates).  Per-image bests vs the oracle (value within the
+    tolerance, location by the gap rule R25) and sampled landscapes at the engine's precision bar."""
+    import dataclasses
+    import math
+    from hypothesis import HealthCheck, given, settings, strategies as st
+
+    @settings(max_examples=16, deadline=None, suppress_health_check=list(HealthCheck))
+    @given(n_k=st.sampled_from([16, 32]), n_psi=st.sampled_from([64, 128, 256, 512]), dmax=st.floats(0.3, 2.0),
+           nt=st.integers(1, 40), eps=st.sampled_from([1e-1, 1e-2]), ni=st.integers(1, 150),
+           nj=st.integers(1, 5), seed=st.integers(0, 10_000))
+    def case(n_k, n_psi, dmax, nt, eps, ni, nj, seed):
+        cfg = dataclasses.replace(synth.config("tiny"), n_k=n_k, n_psi=n_psi, eps=eps, seed=seed % 97)
+        rng = np.random.default_rng(seed)
+        r = dmax * np.sqrt(rng.uniform(0.0, 1.0, nt))
+        th = rng.uniform(0.0, 2.0 * math.pi, nt)
+        sh = np.stack([r * np.cos(th), r * np.sin(th)], 1)
+        p = pkg.FTKPlan(cfg.n, cfg.K, dmax, sh, eps, n_k=n_k, n_psi=n_psi, device=0, engine=0)
+        k, w = p.radial()
+        imgs, _ = synth.draw_items(cfg, "images", range(ni), k, "planted")
+        tpls, _ = synth.draw_items(cfg, "templates", range(nj), k)
+        p.load_images(torch.from_numpy(imgs).cuda())
+        p.load_templates(torch.from_numpy(tpls).cuda())
+        best = pkg.best_to_numpy(p.align()["best"])
+        op = ks.build_plan(cfg.n, cfg.K, dmax, sh, eps, n_k, n_psi, n_nodes=64)
+        X = np.real(ftk.ftk_landscapes(fb.fb_coeffs(imgs), fb.fb_coeffs(tpls), op))
+        na, nb = fb.discrete_norm(imgs, w), fb.discrete_norm(tpls, w)
+        v, j, t, rr, gap = ftk.best_per_image(X)
+        for i in range(ni):
+            scale = na[i] * np.max(nb)
+            assert abs(best["value"][i] - v[i]) <= TOL * scale, (i, best["value"][i], v[i])
+            if gap[i] > 2 * TOL * scale:
+                assert (best["template_idx"][i], best["shift_idx"][i], best["rot_idx"][i]) == (j[i], t[i], rr[i]), i
+            else:
+                bj, bt, br = best["template_idx"][i], best["shift_idx"][i], best["rot_idx"][i]
+                assert X[i, bj, bt, br] >= v[i] - TOL * scale, i
+        ii, jj = rng.integers(0, ni, 4), rng.integers(0, nj, 4)
+        L = p.landscape_pairs(ii, jj).cpu().numpy()
+        for q in range(4):
+            assert np.max(np.abs(L[q] - X[ii[q], jj[q]])) <= PREC * na[ii[q]] * nb[jj[q]], q
+
+    case()
+
+
 def test_fp16x3_extreme_and_mixed_scales(pkg):
     """The fp16x3 arithmetic relies on per-item power-of-two scales.  Images and
     templates spanning 36 decades (1e-18 .. 1e18), an all-zero image and an all-zero template must keep the
