@@ -22,6 +22,8 @@ if os.environ.get("FTK_S1_PLO"):  # (experiment) Step-1 modes interleaved in the
     FLAGS += ["-DFTK_S1_PLO=" + os.environ["FTK_S1_PLO"]]
 if os.environ.get("FTK_S1_HINT"):  # (experiment) Step-1 L2 cache hints
     FLAGS += ["-DFTK_S1_HINT=" + os.environ["FTK_S1_HINT"]]
+if os.environ.get("FTK_S1_GEN16"):  # (experiment) Step-1 generator nodes per step: 16 (1) or 32 (0)
+    FLAGS += ["-DFTK_S1_GEN16=" + os.environ["FTK_S1_GEN16"]]
 if os.environ.get("FTK_DIAG") == "1":  # wait-cycle counters / trace / FTK_S3_DBG (remove _build/ to switch)
     FLAGS += ["-DFTK_DIAG=1"]
 

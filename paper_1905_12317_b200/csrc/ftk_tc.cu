@@ -1111,11 +1111,17 @@ __device__ __forceinline__ void s1_body(const S1Params& P) {
       }
       mbar_wait(&S.a_empty[rnd], (g_u & 1) ^ 1);
       tc_fence_after();
-      for (int m0 = m_beg; m0 < m_end; m0 += 32) {
-        float4 bb[2][8];
-        float2 gg[2][8];
+#ifndef FTK_S1_GEN16
+#define FTK_S1_GEN16 1
+#endif
+      // 16 radial nodes per step (one STTM group each): fewer loads in flight than two steps at a time, no
+      // register spills at the 96-register cap
+      for (int m0 = m_beg; m0 < m_end; m0 += FTK_S1_GEN16 ? 16 : 32) {
+        constexpr int NS2 = FTK_S1_GEN16 ? 1 : 2;
+        float4 bb[NS2][8];
+        float2 gg[NS2][8];
 #pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2)
+        for (int s2 = 0; s2 < NS2; ++s2)
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int m = m0 + 16 * s2 + 2 * e;
@@ -1128,7 +1134,7 @@ __device__ __forceinline__ void s1_body(const S1Params& P) {
                            : make_float2(0.f, 0.f);
           }
 #pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2) {
+        for (int s2 = 0; s2 < NS2; ++s2) {
           if (m0 + 16 * s2 >= m_end) break;
           uint32_t h1[8], l1[8], h2[8], l2[8];
 #pragma unroll
